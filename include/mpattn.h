@@ -1,0 +1,138 @@
+/*
+ * libmpattn -- B200 (sm_100a) kernels for the Multipole Attention decode path.
+ *
+ * C ABI: plain device pointers, sizes and a cudaStream_t passed as void*.  Every entry
+ * point is stream-ordered, graph-capturable, allocates nothing, and returns 0 on
+ * success or a nonzero code (see MPA_ERR_*; CUDA errors are returned as their
+ * cudaError_t value) with a message available from mpa_last_error().
+ *
+ * Data layout ("ledger" l = seq * n_kv_heads + kv_head, L ledgers, head_dim d):
+ *   KV cache      k_rot / k_raw / v : [L, tcap, d]  (dtype MPA_F32 or MPA_BF16)
+ *   fine level    kc / vc           : [L, kcap, d]  (serving dtype), size [L, kcap],
+ *                 count [L], mem_off [L, kcap + 1] (CSR into mem), mem [L, tcap]
+ *   coarse level  kc / vc           : [L, ccap, d], size [L, ccap], count [L],
+ *                 child_off [L, ccap + 1] (CSR into child), child [L, kcap]
+ *
+ * Each entry point names the reference function it replaces
+ * (/root/reference/pkg/src/multipole_attn/<file>:<line>).
+ */
+#ifndef MPATTN_H
+#define MPATTN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { MPA_F32 = 0, MPA_BF16 = 1, MPA_F64 = 2 /* centroid levels only */ };
+
+enum {
+    MPA_OK = 0,
+    MPA_ERR_ARG = 1001,       /* bad argument (shape, dtype, null pointer) */
+    MPA_ERR_UNSUPPORTED = 1002 /* configuration the kernels do not implement */
+};
+
+/* Last error message of the calling thread ("" if none). */
+const char* mpa_last_error(void);
+/* Library version string and the sm architecture it was compiled for. */
+const char* mpa_version(void);
+
+typedef struct mpa_cache {
+    void* k_rot;      /* keys rotated at their true positions (exact-attention view) */
+    void* k_raw;      /* pre-rotation keys (clustering / windowed lookup view)       */
+    void* v;
+    int32_t dtype;
+    int32_t n_ledgers;
+    int32_t tcap;
+    int32_t head_dim;
+} mpa_cache;
+
+typedef struct mpa_level {
+    const void* kc;          /* [L, cap, d] key centroids: serving dtype, or fp64 (MPA_F64) */
+    const void* vc;          /* [L, cap, d] value centroids               */
+    const int32_t* size;     /* [L, cap]                                   */
+    const int32_t* count;    /* [L]                                        */
+    const int32_t* off;      /* [L, cap + 1] CSR offsets (members or children) */
+    const int32_t* idx;      /* [L, idx_cap] member token ids or child fine ids */
+    int32_t cap;
+    int32_t idx_cap;
+    int32_t dtype;           /* dtype of kc; vc always has the KV-cache dtype */
+    int32_t n_ledgers;
+} mpa_level;
+
+/* K1/K14 -- write n_tok new tokens per ledger at positions pos0[l] .. pos0[l]+n_tok-1:
+ * k_raw = k, v = v, k_rot = rotate(k, pos) with fp64 angles pos * inv_freq[i]
+ * (replaces rope.py:37-53 applied at attention.py:84-85, and pipeline.py:38-44, 156-159).
+ * k_src / v_src: fp32 [L, n_tok, d] (device). inv_freq: fp64 [d/2] (device). */
+int mpa_kv_write(const mpa_cache* cache, const float* k_src, const float* v_src,
+                 const int32_t* pos0, int n_tok, const double* inv_freq, void* stream);
+
+/* K1 -- rotate queries: q_rot = rotate(q, qpos[seq]) * scale (fp32, exact view) and
+ * q_lk = rotate(q, delta) (fp64, lookup view; rope.py:66-68).  q: fp32 [n_seq, n_qh, d]. */
+int mpa_rotate_queries(const float* q, int n_seq, int n_qh, int d, const int32_t* qpos,
+                       int delta, const double* inv_freq, float scale,
+                       float* q_rot, double* q_lk, void* stream);
+
+/* K9 -- centroid lookup logits, fp64: logits[l, g, i] = q_lk[seq, h*G+g] . kc[l, id_i] / sqrt(d)
+ * for candidates i < n_cand[l]; id_i = cand[l, i] (cand may be NULL: id_i = i, n = lv->count)
+ * (attention.py:267-276 `_scores_per_group` logits). */
+int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group, int d,
+                        const mpa_level* lv, const int32_t* cand, const int32_t* n_cand,
+                        int cand_cap, double* logits, void* stream);
+
+/* K10 -- Eq. 1 scores and budgeted greedy selection (attention.py:192-207, 267-290).
+ * Scores: e_g,i = exp(l_g,i - max_g), Z_g = sum over candidates AND live extras of N * e,
+ * score_i = mean_g e_g,i / Z_g.  Selection: visit candidates by (score desc, tie key asc),
+ * take while the running size sum < budget[l] (the crossing cluster is included).
+ * sizes: lv_size[l, id_i]; tie key: id_i.  Extras (may be NULL): logits [L, G, ecap] with sizes
+ * esize[l, j] that enter only the denominators when eflag[l, j] == 0 (hierarchical union,
+ * attention.py:331-334).  Writes flag[l, i] = 1 selected / 0 rejected, sel_tokens[l]. */
+int mpa_select(const double* logits, int group, const int32_t* cand, const int32_t* n_cand,
+               int cand_cap, const int32_t* lv_size, int lv_cap,
+               const double* elogits, const int32_t* esize, const uint8_t* eflag,
+               const int32_t* n_extra, int ecap,
+               const int64_t* budget, int n_ledgers, uint8_t* flag, int32_t* sel_tokens,
+               void* stream);
+
+/* Hierarchy stage glue (attention.py:321-329): cand[l] = children of coarse clusters with
+ * cflag == 1, promoted in coarse-id order, children ascending; n_cand[l]. */
+int mpa_hier_candidates(const mpa_level* coarse, const uint8_t* cflag, int n_ledgers,
+                        int32_t* cand, int32_t* n_cand, int cand_cap, void* stream);
+
+/* Work lists for the fused kernel (attention.py:469-496):
+ *   tok[l, :]  = sinks [0, min(sink_end, cache_len)) ++ buffer [buffer_start, cache_len)
+ *                ++ members of selected fine candidates;  n_tok[l]
+ *   rej[l, :]  = rejected centroids as value-row codes (>= 0 fine row, < 0: coarse row -1-code)
+ *                with w[l, j, g] = logit + ln(size) (fp32);  n_rej[l]
+ * Fine candidates: (cand, n_cand, flag, logits); coarse rejected (hier only, may be NULL):
+ * (clogits, cflag) over the coarse level.  replacement == 0 drops every centroid term
+ * ("flat-no-replacement", attention.py:441).  stats is [4, L]: rows n_tok, n_rej, sel_tokens,
+ * n_selected_clusters (rows 0 and 1 feed mpa_sparse_decode directly).  sink_end / buffer_start / cache_len are per sequence [n_seq]. */
+int mpa_build_worklist(const mpa_level* fine, const mpa_level* coarse, int group,
+                       const int32_t* cand, const int32_t* n_cand, int cand_cap,
+                       const uint8_t* flag, const double* logits,
+                       const uint8_t* cflag, const double* clogits,
+                       const int32_t* sink_end, const int32_t* buffer_start, const int32_t* cache_len,
+                       int n_kv_heads, int n_ledgers, int replacement,
+                       int32_t* tok, int tok_cap, int32_t* rej, float* rej_w, int rej_cap,
+                       int32_t* stats, void* stream);
+
+/* K11 + K12 -- fused sparse decode: one online softmax over the exact tokens (K_rot/V gathered
+ * by index, logits q_rot . k) and the rejected-centroid pseudo-tokens (logit + ln N, value
+ * centroid), split over n_split CTAs per ledger, LSE-merged by the last CTA of each ledger
+ * (attention.py:58-87, 120-137, 210-239, 473-498).  tok == NULL: dense decode over
+ * [0, n_tok[l]) (the "oracle" comparator, attention.py:90-102).  part_* / ticket are
+ * workspace: part_ml [L, n_split, G, 2], part_acc [L, n_split, G, d] fp32, ticket [L] int32
+ * (zero-initialised once; the kernel leaves it zeroed).  out: fp32 [n_seq, Hq, d]. */
+int mpa_sparse_decode(const mpa_cache* cache, const float* q_rot, int n_kv_heads, int group,
+                      const int32_t* tok, const int32_t* n_tok, int tok_cap,
+                      const int32_t* rej, const float* rej_w, const int32_t* n_rej, int rej_cap,
+                      const void* fine_vc, int fine_cap, const void* coarse_vc, int coarse_cap,
+                      int n_split, float* part_ml, float* part_acc, int32_t* ticket,
+                      float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPATTN_H */

@@ -1,0 +1,116 @@
+// Shared helpers for the libmpattn sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "mpattn.h"
+
+namespace mpa {
+
+// ---- error plumbing: every C-ABI entry point returns 0 or an error code and
+// stores a message readable through mpa_last_error().
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+
+#define MPA_REQUIRE(cond, code, ...)        \
+    do {                                    \
+        if (!(cond)) {                      \
+            ::mpa::set_error(__VA_ARGS__);  \
+            return (code);                  \
+        }                                   \
+    } while (0)
+
+// ---- element types ---------------------------------------------------------
+template <typename T> struct elem;
+template <> struct elem<float> {
+    static __device__ __forceinline__ float to_f(float x) { return x; }
+    static __device__ __forceinline__ double to_d(float x) { return (double)x; }
+    static __device__ __forceinline__ float from_d(double x) { return (float)x; }
+};
+template <> struct elem<double> {
+    static __device__ __forceinline__ float to_f(double x) { return (float)x; }
+    static __device__ __forceinline__ double to_d(double x) { return x; }
+    static __device__ __forceinline__ double from_d(double x) { return x; }
+};
+template <> struct elem<__nv_bfloat16> {
+    static __device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+    static __device__ __forceinline__ double to_d(__nv_bfloat16 x) { return (double)__bfloat162float(x); }
+    static __device__ __forceinline__ __nv_bfloat16 from_d(double x) { return __double2bfloat16(x); }
+};
+
+// ---- warp / block reductions -----------------------------------------------
+template <typename T> __device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+template <typename T> __device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-wide reduction of one value per thread; result broadcast to all threads.
+// `scratch` needs blockDim.x/32 entries. Callers must __syncthreads() before reusing scratch.
+template <typename T, typename Op>
+__device__ __forceinline__ T block_reduce(T v, T* scratch, Op op) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    T r = scratch[0];
+    for (int i = 1; i < nw; ++i) r = op(r, scratch[i]);
+    __syncthreads();
+    return r;
+}
+
+// Exclusive block-wide prefix sum of one int per thread (blockDim.x <= 1024).
+// Returns the exclusive prefix; *total receives the block total. scratch: 33 ints.
+__device__ __forceinline__ int block_exclusive_scan(int v, int* scratch, int* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) scratch[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        int s = lane < nw ? scratch[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < nw) scratch[lane] = s;  // inclusive warp totals
+        if (lane == 31) scratch[32] = s;
+    }
+    __syncthreads();
+    const int base = wid ? scratch[wid - 1] : 0;
+    *total = scratch[32];
+    __syncthreads();
+    return base + incl - v;
+}
+
+__host__ __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+}  // namespace mpa
+
+// Runtime GQA group size -> compile-time kG (1..8).
+#define MPA_DISPATCH_G(G, ...)                                                                      \
+    switch (G) {                                                                                    \
+        case 1: { constexpr int kG = 1; __VA_ARGS__; } break;                                      \
+        case 2: { constexpr int kG = 2; __VA_ARGS__; } break;                                      \
+        case 3: { constexpr int kG = 3; __VA_ARGS__; } break;                                      \
+        case 4: { constexpr int kG = 4; __VA_ARGS__; } break;                                      \
+        case 5: { constexpr int kG = 5; __VA_ARGS__; } break;                                      \
+        case 6: { constexpr int kG = 6; __VA_ARGS__; } break;                                      \
+        case 7: { constexpr int kG = 7; __VA_ARGS__; } break;                                      \
+        case 8: { constexpr int kG = 8; __VA_ARGS__; } break;                                      \
+        default: ::mpa::set_error("group size %d not supported (1..8)", (int)(G));                \
+                 return MPA_ERR_UNSUPPORTED;                                                        \
+    }

@@ -1,0 +1,121 @@
+// K1 / K14: rotary views and KV-cache writes.
+//
+// Reference: rope.py:37-53 (`rotate`: interleaved pairs (2i, 2i+1) rotated by
+// pos * theta^(-2i/d), computed in fp64), rope.py:66-68 (lookup query at the fixed
+// offset Delta), attention.py:84-85 (exact view: both q and keys at true positions),
+// pipeline.py:38-44 + 156-159 (append the step's key/value after attending).
+//
+// The rotated key is materialised ONCE per token at write time (K_rot cache), so the
+// fused decode kernel reads exactly 2*d*sizeof(T) bytes per exact token. Angles are
+// fp64 (pos * inv_freq with inv_freq computed by numpy on the host, identical bits to
+// the reference), sincos in fp64, result rounded once to the cache dtype.
+#include <cstdarg>
+#include <cstdio>
+
+#include "mpa_common.cuh"
+
+namespace mpa {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("%s: %s", what, cudaGetErrorString(e));
+        return (int)e;
+    }
+    return 0;
+}
+
+template <typename T>
+__global__ void kv_write_kernel(T* __restrict__ k_rot, T* __restrict__ k_raw, T* __restrict__ v,
+                                const float* __restrict__ k_src, const float* __restrict__ v_src,
+                                const int32_t* __restrict__ pos0, int n_tok, int tcap, int d,
+                                const double* __restrict__ inv_freq) {
+    const int l = blockIdx.y;
+    const int t = blockIdx.x;                      // token within this write
+    const int pos = pos0[l] + t;
+    const size_t src = ((size_t)l * n_tok + t) * d;
+    const size_t dst = ((size_t)l * tcap + pos) * d;
+    for (int i = threadIdx.x; i < d / 2; i += blockDim.x) {
+        const double x = (double)k_src[src + 2 * i];
+        const double y = (double)k_src[src + 2 * i + 1];
+        double sn, cs;
+        sincos((double)pos * inv_freq[i], &sn, &cs);
+        // no FMA contraction: same rounding sequence as numpy's ev*cos - od*sin
+        k_rot[dst + 2 * i] = elem<T>::from_d(__dsub_rn(__dmul_rn(x, cs), __dmul_rn(y, sn)));
+        k_rot[dst + 2 * i + 1] = elem<T>::from_d(__dadd_rn(__dmul_rn(x, sn), __dmul_rn(y, cs)));
+        k_raw[dst + 2 * i] = elem<T>::from_d(x);
+        k_raw[dst + 2 * i + 1] = elem<T>::from_d(y);
+        v[dst + 2 * i] = elem<T>::from_d((double)v_src[src + 2 * i]);
+        v[dst + 2 * i + 1] = elem<T>::from_d((double)v_src[src + 2 * i + 1]);
+    }
+}
+
+__global__ void rotate_queries_kernel(const float* __restrict__ q, int n_qh, int d,
+                                      const int32_t* __restrict__ qpos, int delta,
+                                      const double* __restrict__ inv_freq, float scale,
+                                      float* __restrict__ q_rot, double* __restrict__ q_lk) {
+    const int s = blockIdx.y, h = blockIdx.x;
+    const size_t base = ((size_t)s * n_qh + h) * d;
+    const double p = (double)qpos[s];
+    for (int i = threadIdx.x; i < d / 2; i += blockDim.x) {
+        const double x = (double)q[base + 2 * i], y = (double)q[base + 2 * i + 1];
+        double sn, cs;
+        sincos(p * inv_freq[i], &sn, &cs);
+        if (q_rot) {
+            q_rot[base + 2 * i] = (float)(__dsub_rn(__dmul_rn(x, cs), __dmul_rn(y, sn)) * (double)scale);
+            q_rot[base + 2 * i + 1] = (float)(__dadd_rn(__dmul_rn(x, sn), __dmul_rn(y, cs)) * (double)scale);
+        }
+        sincos((double)delta * inv_freq[i], &sn, &cs);
+        if (q_lk) {
+            q_lk[base + 2 * i] = __dsub_rn(__dmul_rn(x, cs), __dmul_rn(y, sn));
+            q_lk[base + 2 * i + 1] = __dadd_rn(__dmul_rn(x, sn), __dmul_rn(y, cs));
+        }
+    }
+}
+
+}  // namespace mpa
+
+using namespace mpa;
+
+extern "C" const char* mpa_last_error(void) { return g_err; }
+
+extern "C" const char* mpa_version(void) { return "libmpattn 0.1 (sm_100a)"; }
+
+extern "C" int mpa_kv_write(const mpa_cache* c, const float* k_src, const float* v_src,
+                            const int32_t* pos0, int n_tok, const double* inv_freq, void* stream) {
+    MPA_REQUIRE(c && k_src && v_src && pos0 && inv_freq, MPA_ERR_ARG, "mpa_kv_write: null argument");
+    MPA_REQUIRE(c->head_dim >= 2 && c->head_dim % 2 == 0, MPA_ERR_ARG, "mpa_kv_write: bad head_dim %d", c->head_dim);
+    if (n_tok <= 0 || c->n_ledgers <= 0) return 0;
+    dim3 grid(n_tok, c->n_ledgers);
+    const int threads = c->head_dim / 2 < 64 ? 32 : 64;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (c->dtype == MPA_F32)
+        kv_write_kernel<float><<<grid, threads, 0, st>>>((float*)c->k_rot, (float*)c->k_raw, (float*)c->v, k_src,
+                                                         v_src, pos0, n_tok, c->tcap, c->head_dim, inv_freq);
+    else if (c->dtype == MPA_BF16)
+        kv_write_kernel<__nv_bfloat16><<<grid, threads, 0, st>>>(
+            (__nv_bfloat16*)c->k_rot, (__nv_bfloat16*)c->k_raw, (__nv_bfloat16*)c->v, k_src, v_src, pos0, n_tok,
+            c->tcap, c->head_dim, inv_freq);
+    else
+        MPA_REQUIRE(false, MPA_ERR_ARG, "mpa_kv_write: bad dtype %d", c->dtype);
+    return check_launch("mpa_kv_write");
+}
+
+extern "C" int mpa_rotate_queries(const float* q, int n_seq, int n_qh, int d, const int32_t* qpos, int delta,
+                                  const double* inv_freq, float scale, float* q_rot, double* q_lk, void* stream) {
+    MPA_REQUIRE(q && qpos && inv_freq, MPA_ERR_ARG, "mpa_rotate_queries: null argument");
+    MPA_REQUIRE(d >= 2 && d % 2 == 0, MPA_ERR_ARG, "mpa_rotate_queries: bad head_dim %d", d);
+    if (n_seq <= 0 || n_qh <= 0) return 0;
+    rotate_queries_kernel<<<dim3(n_qh, n_seq), 64, 0, (cudaStream_t)stream>>>(q, n_qh, d, qpos, delta, inv_freq,
+                                                                             scale, q_rot, q_lk);
+    return check_launch("mpa_rotate_queries");
+}

@@ -1,0 +1,226 @@
+"""Device-resident Multipole Attention decode engine (one attention layer, a batch of sequences).
+
+This is the B200 replacement for the per-kv-head Python loops of the reference
+(attention.py:410-552 `decode_step_attention`, pipeline.py:124-191 `step`).  All state lives
+in HBM; one decode step is a short, graph-capturable chain of libmpattn kernels on one stream:
+
+    mpa_rotate_queries   q -> q_rot (true position, fp32) and q_lookup (Delta, fp64)     K1
+    mpa_centroid_logits  fp64 logits of the fine (or coarse) centroids                   K9
+    mpa_select           Eq. 1 scores + size-weighted radix select to the budget         K10
+    [hierarchy: mpa_hier_candidates, mpa_centroid_logits (fine children), mpa_select with
+     the coarse-rejected union denominator]
+    mpa_build_worklist   sinks ++ buffer ++ selected members; rejected centroids + ln N
+    mpa_sparse_decode    gather + exact attention + centroid replacement, split-KV merge K11+K12
+
+Attention happens before the step's token is appended (pipeline.py:137-159); the online
+cluster update runs when the buffer reaches 2L (pipeline.py:161) -- see clustering.py.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import MpaCache, call, dtype_code, ptr, stream_ptr
+from .core import ConfigError, EngineConfig, HeadLayout, inv_freq
+from .ledger import DeviceLedgers, HostLedger
+
+NUM_SMS = 148
+MAX_SPLITS = 64
+
+
+class DecodeEngine:
+    def __init__(self, cfg: EngineConfig, layout: HeadLayout, n_seq: int, tcap: int,
+                 dtype: torch.dtype = torch.bfloat16, device="cuda", kcap: int | None = None,
+                 ccap: int | None = None, mode: str = "multipole"):
+        if not torch.cuda.is_available():
+            raise RuntimeError("DecodeEngine needs a CUDA device (B200); there is no CPU fallback")
+        _lib.lib()  # fail loudly if libmpattn.so is missing
+        self.cfg, self.layout, self.mode = cfg, layout, mode
+        self.n_seq, self.d, self.G = n_seq, layout.head_dim, layout.group_size
+        self.Hkv, self.Hq = layout.num_kv_heads, layout.num_q_heads
+        self.L = n_seq * self.Hkv
+        self.tcap, self.dtype = tcap, dtype
+        self.device = torch.device(device)
+        r = cfg.fine_ratio
+        self.kcap = kcap or max(64, 2 * (tcap // r) + 64)
+        hier = cfg.hierarchy is not None
+        self.ccap = ccap or (max(16, 2 * (tcap // cfg.hierarchy.r1) + 64) if hier else 0)
+        L, d, G, dev = self.L, self.d, self.G, self.device
+        z = dict(device=dev)
+        self.k_rot = torch.zeros(L, tcap, d, dtype=dtype, **z)
+        self.k_raw = torch.zeros(L, tcap, d, dtype=dtype, **z)
+        self.v = torch.zeros(L, tcap, d, dtype=dtype, **z)
+        self.led = DeviceLedgers(L, d, tcap, self.kcap, self.ccap, dtype, hier, dev)
+        self.inv_freq = torch.as_tensor(inv_freq(d, cfg.rope_theta), dtype=torch.float64, device=dev)
+        # per-sequence scalars (host mirror + device copy)
+        self.cache_len = np.zeros(n_seq, np.int64)
+        self.sink_end = np.zeros(n_seq, np.int64)
+        self.buffer_start = np.zeros(n_seq, np.int64)
+        self.splits = np.zeros(L, np.int64)
+        self.cache_len_d = torch.zeros(n_seq, dtype=torch.int32, **z)
+        self.sink_end_d = torch.zeros(n_seq, dtype=torch.int32, **z)
+        self.buffer_start_d = torch.zeros(n_seq, dtype=torch.int32, **z)
+        self.ntok_dense_d = torch.zeros(L, dtype=torch.int32, **z)
+        # workspace
+        self.q_rot = torch.zeros(n_seq, self.Hq, d, dtype=torch.float32, **z)
+        self.q_lk = torch.zeros(n_seq, self.Hq, d, dtype=torch.float64, **z)
+        self.logits = torch.zeros(L, G, self.kcap, dtype=torch.float64, **z)
+        self.flag = torch.zeros(L, self.kcap, dtype=torch.uint8, **z)
+        self.sel_tokens = torch.zeros(L, dtype=torch.int32, **z)
+        self.budget = torch.full((L,), cfg.token_budget, dtype=torch.int64, **z)
+        if hier:
+            self.clogits = torch.zeros(L, G, self.ccap, dtype=torch.float64, **z)
+            self.cflag = torch.zeros(L, self.ccap, dtype=torch.uint8, **z)
+            self.cbudget = torch.zeros(L, dtype=torch.int64, **z)
+            self.cand = torch.zeros(L, self.kcap, dtype=torch.int32, **z)
+            self.n_cand = torch.zeros(L, dtype=torch.int32, **z)
+            self.csel_tokens = torch.zeros(L, dtype=torch.int32, **z)
+        self.tok_cap = tcap
+        self.rej_cap = self.kcap + self.ccap
+        self.tok = torch.zeros(L, self.tok_cap, dtype=torch.int32, **z)
+        self.rej = torch.zeros(L, self.rej_cap, dtype=torch.int32, **z)
+        self.rej_w = torch.zeros(L, self.rej_cap, G, dtype=torch.float32, **z)
+        self.stats = torch.zeros(4, L, dtype=torch.int32, **z)
+        self.part_ml = torch.zeros(L, MAX_SPLITS, G, 2, dtype=torch.float32, **z)
+        self.part_acc = torch.zeros(L, MAX_SPLITS, G, d, dtype=torch.float32, **z)
+        self.ticket = torch.zeros(L, dtype=torch.int32, **z)
+        self.out = torch.zeros(n_seq, self.Hq, d, dtype=torch.float32, **z)
+        self.cache_struct = MpaCache(ptr(self.k_rot), ptr(self.k_raw), ptr(self.v), dtype_code(dtype), L, tcap, d)
+        self.last_split = 1
+
+    # ------------------------------------------------------------------ KV cache
+    def write_tokens(self, k: torch.Tensor, v: torch.Tensor, pos0: torch.Tensor | None = None) -> None:
+        """Write n new tokens per ledger: k, v fp32 [n_seq, Hkv, n, d] (device) at cache_len."""
+        n = k.shape[2]
+        if pos0 is None:
+            if int(self.cache_len.max()) + n > self.tcap:
+                raise RuntimeError(f"KV cache capacity {self.tcap} exceeded")
+            pos0 = self.cache_len_d.repeat_interleave(self.Hkv)
+        k = k.reshape(self.L, n, self.d).float().contiguous()
+        v = v.reshape(self.L, n, self.d).float().contiguous()
+        call("mpa_kv_write", self.cache_struct, ptr(k), ptr(v), ptr(pos0), n, ptr(self.inv_freq), stream_ptr())
+        self.cache_len += n
+        self.cache_len_d += n
+        self.ntok_dense_d += n
+
+    def set_prompt_layout(self) -> None:
+        """Sinks / buffer split of the prompt (clustering.py:295-299)."""
+        cfg = self.cfg
+        for s in range(self.n_seq):
+            P = int(self.cache_len[s])
+            if P <= cfg.sink_tokens:
+                raise ConfigError(f"prompt_len {P} must exceed sink_tokens {cfg.sink_tokens}")
+            self.sink_end[s] = cfg.sink_tokens
+            self.buffer_start[s] = P - min(cfg.local_buffer, P - cfg.sink_tokens)
+        self._sync_scalars()
+
+    def _sync_scalars(self) -> None:
+        self.sink_end_d.copy_(torch.as_tensor(self.sink_end, dtype=torch.int32))
+        self.buffer_start_d.copy_(torch.as_tensor(self.buffer_start, dtype=torch.int32))
+        self.cache_len_d.copy_(torch.as_tensor(self.cache_len, dtype=torch.int32))
+        self.ntok_dense_d.copy_(torch.as_tensor(np.repeat(self.cache_len, self.Hkv), dtype=torch.int32))
+        if self.cfg.hierarchy is not None:
+            p = self.cfg.hierarchy.promote_fraction
+            clustered = np.repeat(self.buffer_start - self.sink_end, self.Hkv)
+            self.cbudget.copy_(torch.as_tensor([int(np.ceil(p * int(c))) for c in clustered], dtype=torch.int64))
+
+    def load_ledgers(self, ledgers: list[HostLedger]) -> None:
+        for l, h in enumerate(ledgers):
+            self.led.load(l, h)
+            s = l // self.Hkv
+            self.sink_end[s], self.buffer_start[s] = h.sink_end, h.buffer_start
+            self.splits[l] = h.splits
+        self._sync_scalars()
+
+    # ------------------------------------------------------------------ decode
+    def _n_split(self, units_per_ledger: float) -> int:
+        target_ctas = 2 * NUM_SMS
+        s = max(1, round(target_ctas / self.L))
+        s = min(s, max(1, int(units_per_ledger // 96)), MAX_SPLITS)
+        return int(s)
+
+    def _sparse_units(self) -> float:
+        cfg = self.cfg
+        buf = float(np.max(self.cache_len - self.buffer_start))
+        sel = min(cfg.token_budget + float(self.led.max_size.max(initial=0)), float(np.max(self.cache_len)))
+        rej = float(self.led.n_fine.max(initial=0) + self.led.n_coarse.max(initial=0))
+        return 2.0 * (cfg.sink_tokens + buf + sel) + rej
+
+    def rotate(self, q: torch.Tensor) -> None:
+        q = q.float().contiguous()
+        call("mpa_rotate_queries", ptr(q), self.n_seq, self.Hq, self.d, ptr(self.cache_len_d), self.cfg.window_offset,
+             ptr(self.inv_freq), 1.0 / math.sqrt(self.d), ptr(self.q_rot), ptr(self.q_lk), stream_ptr())
+
+    def lookup(self) -> None:
+        """K9 + K10 + work lists for the current q_lk (flat or hierarchical)."""
+        st = stream_ptr()
+        G, L = self.G, self.L
+        fine = self.led.fine_level()
+        replacement = 0 if self.mode == "flat-no-replacement" else 1
+        if self.cfg.hierarchy is None:
+            if int(self.led.n_fine.min(initial=0)) == 0:
+                raise ConfigError("ledger has no clusters")
+            call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, None, None, self.kcap,
+                 ptr(self.logits), st)
+            call("mpa_select", ptr(self.logits), G, None, ptr(self.led.count), self.kcap, ptr(self.led.size),
+                 self.kcap, None, None, None, None, 0, ptr(self.budget), L, ptr(self.flag), ptr(self.sel_tokens), st)
+            call("mpa_build_worklist", fine, None, G, None, None, self.kcap, ptr(self.flag), ptr(self.logits), None,
+                 None, ptr(self.sink_end_d), ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv, L,
+                 replacement, ptr(self.tok), self.tok_cap, ptr(self.rej), ptr(self.rej_w), self.rej_cap,
+                 ptr(self.stats), st)
+        else:
+            if int(self.led.n_coarse.min(initial=0)) == 0:
+                raise ConfigError("ledger has no coarse clusters")
+            coarse = self.led.coarse_level()
+            call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, coarse, None, None, self.ccap,
+                 ptr(self.clogits), st)
+            call("mpa_select", ptr(self.clogits), G, None, ptr(self.led.ccount), self.ccap, ptr(self.led.csize),
+                 self.ccap, None, None, None, None, 0, ptr(self.cbudget), L, ptr(self.cflag),
+                 ptr(self.csel_tokens), st)
+            call("mpa_hier_candidates", coarse, ptr(self.cflag), L, ptr(self.cand), ptr(self.n_cand), self.kcap, st)
+            call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, ptr(self.cand), ptr(self.n_cand),
+                 self.kcap, ptr(self.logits), st)
+            call("mpa_select", ptr(self.logits), G, ptr(self.cand), ptr(self.n_cand), self.kcap, ptr(self.led.size),
+                 self.kcap, ptr(self.clogits), ptr(self.led.csize), ptr(self.cflag), ptr(self.led.ccount),
+                 self.ccap, ptr(self.budget), L, ptr(self.flag), ptr(self.sel_tokens), st)
+            call("mpa_build_worklist", fine, coarse, G, ptr(self.cand), ptr(self.n_cand), self.kcap, ptr(self.flag),
+                 ptr(self.logits), ptr(self.cflag), ptr(self.clogits), ptr(self.sink_end_d),
+                 ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv, L, replacement, ptr(self.tok),
+                 self.tok_cap, ptr(self.rej), ptr(self.rej_w), self.rej_cap, ptr(self.stats), st)
+
+    def fused(self, n_split: int | None = None) -> torch.Tensor:
+        S = n_split or self._n_split(self._sparse_units())
+        self.last_split = S
+        st = stream_ptr()
+        rej = None if self.mode == "flat-no-replacement" else self.rej
+        ckc = self.led.cvc if self.led.hierarchy else None
+        call("mpa_sparse_decode", self.cache_struct, ptr(self.q_rot), self.Hkv, self.G, ptr(self.tok),
+             ptr(self.stats[0]), self.tok_cap, ptr(rej), ptr(self.rej_w), ptr(self.stats[1]), self.rej_cap,
+             ptr(self.led.vc), self.kcap, ptr(ckc), self.ccap, S, ptr(self.part_ml), ptr(self.part_acc),
+             ptr(self.ticket), ptr(self.out), st)
+        return self.out
+
+    def attend(self, q: torch.Tensor, n_split: int | None = None) -> torch.Tensor:
+        """One multipole decode step over the current cache; q fp32 [n_seq, Hq, d] (device)."""
+        if self.mode == "oracle":
+            return self.attend_dense(q, n_split)
+        self.rotate(q)
+        self.lookup()
+        return self.fused(n_split)
+
+    def attend_dense(self, q: torch.Tensor, n_split: int | None = None) -> torch.Tensor:
+        """Dense exact attention over [0, cache_len) with the same kernel (K13 comparator)."""
+        self.rotate(q)
+        S = n_split or self._n_split(2.0 * float(self.cache_len.max()))
+        call("mpa_sparse_decode", self.cache_struct, ptr(self.q_rot), self.Hkv, self.G, None, ptr(self.ntok_dense_d),
+             0, None, None, None, 0, None, 0, None, 0, S, ptr(self.part_ml), ptr(self.part_acc), ptr(self.ticket),
+             ptr(self.out), stream_ptr())
+        return self.out
+
+    def head_stats(self) -> np.ndarray:
+        """[L, 4]: n_tok, n_rej, selected tokens, selected clusters (host copy)."""
+        return self.stats.cpu().numpy().T

@@ -1,0 +1,55 @@
+"""CPU checks of the C-ABI boundary: libmpattn.so loads, exports every function that
+include/mpattn.h declares, and reports argument errors through mpa_last_error without a GPU."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mpattn.h")
+LIB = os.path.join(ROOT, "paper_2506_13059_b200", "libmpattn.so")
+
+
+def declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mpa_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(LIB):
+        from paper_2506_13059_b200.build import build
+        build(verbose=False)
+    return ctypes.CDLL(LIB)
+
+
+def test_header_declares_entry_points():
+    names = declared()
+    for must in ("mpa_kv_write", "mpa_rotate_queries", "mpa_centroid_logits", "mpa_select",
+                 "mpa_build_worklist", "mpa_sparse_decode", "mpa_last_error"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    missing = [n for n in declared() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_python_binding_covers_header():
+    from paper_2506_13059_b200 import _lib
+    assert sorted(_lib.EXPORTED) == declared()
+
+
+def test_argument_errors_without_gpu(lib):
+    lib.mpa_last_error.restype = ctypes.c_char_p
+    lib.mpa_version.restype = ctypes.c_char_p
+    assert b"sm_100a" in lib.mpa_version()
+    rc = lib.mpa_select(None, 4, None, None, 0, None, 0, None, None, None, None, 0, None, 1, None, None, None)
+    assert rc == 1001
+    assert b"null argument" in lib.mpa_last_error()
+    rc = lib.mpa_sparse_decode(None, None, 8, 4, None, None, 0, None, None, None, 0, None, 0, None, 0, 1,
+                               None, None, None, None, None)
+    assert rc == 1001
