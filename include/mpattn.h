@@ -132,6 +132,86 @@ int mpa_sparse_decode(const mpa_cache* cache, const float* q_rot, int n_kv_heads
                       int n_split, float* part_ml, float* part_acc, int32_t* ticket,
                       float* out, void* stream);
 
+/* ------------------------------------------------------------------------------------------
+ * Clustering (K2-K8).  A batch of independent k-means "problems" p, each over a contiguous run
+ * of points: rows prob_start[p] .. +prob_n[p] of ledger prob_l[p] -- either pre-rotation keys
+ * (pts: [L, tcap, d] in pts_dtype) or fp64 rows (pts64: [L, rows64_cap, d], the fine centroids,
+ * with integer weights wts [L, rows64_cap] for the hierarchy's size-weighted k-means).
+ * Per-point arrays are indexed pt_off[p] + i, per-centroid arrays c_off[p] + j.
+ * (clustering.py:84-184 Lloyd, :210-264 hierarchy, :343-472 online update / split / settle.) */
+typedef struct mpa_km {
+    int32_t n_prob;
+    int32_t d;
+    const void* pts;
+    int32_t pts_dtype;
+    int32_t tcap;
+    const double* pts64;
+    const int32_t* wts;
+    int32_t rows64_cap;
+    int32_t n_max;           /* max prob_n (grid sizing) */
+    int32_t k_max;           /* max prob_k */
+    int32_t min_iters;       /* Lloyd minimum update rounds (clustering.py:123-143) */
+    const int32_t* prob_l;
+    const int32_t* prob_start;
+    const int32_t* prob_n;
+    const int32_t* prob_k;
+    const int32_t* pt_off;
+    const int32_t* c_off;
+    int32_t* assign;         /* [sum n] current assignment                 */
+    int32_t* prev;           /* [sum n] previous round's assignment         */
+    double* p2;              /* [sum n] squared point norms                 */
+    double* cent;            /* [sum k, d] fp64 centroids (in: init; out: final) */
+    double* c2;              /* [sum k]                                      */
+    int32_t* count;          /* [sum k]                                      */
+    int32_t* order;          /* [sum n] point ids grouped by cluster, ascending within */
+    int32_t* cstart;         /* [sum k] first position of each cluster in order */
+    int32_t* state;          /* [n_prob, 4] active, rounds, changed, has_empty */
+    int32_t* flag;           /* [2] device scratch for the Lloyd driver loop (any active, max rounds) */
+} mpa_km;
+
+/* Lloyd to a fixed point for every problem (assign -> repair empties -> converged? -> means),
+ * at least min_iters update rounds and at most min_iters + 100 (clustering.py:30, 123-143).
+ * The assignment is the fp64 argmin of ||p||^2 + ||c||^2 - 2 p.c (first minimum); means are
+ * sequential fp64 member sums in ascending point order (bit-equal to np.add.at / np.mean).
+ * Weighted mode (wts != NULL) keeps the centroid of an empty cluster (clustering.py:236-242).
+ * Host-driven loop: one 8-byte readback per round.  *rounds_out = max rounds over problems. */
+int mpa_km_lloyd(const mpa_km* km, int32_t* rounds_out, void* stream);
+
+/* Means / counts / grouping for the assignment already in km->assign (no iteration): used to
+ * seed the two sides of a sliding-window split (clustering.py:368-383). */
+int mpa_km_means(const mpa_km* km, void* stream);
+
+/* nk[p] = number of non-empty clusters of problem p after Lloyd. */
+int mpa_km_count_nonempty(const mpa_km* km, int32_t* nk, void* stream);
+
+/* Compaction into a ledger level (clustering.py:146-167, 187-192): non-empty clusters of problem
+ * p, in centroid order, become clusters f0[p] .. f0[p]+nk[p]-1 of ledger prob_l[p]:
+ *   kc64 = centroid, vc64 = sequential mean of the members' value rows (vals: [L, tcap, d] in
+ *   pts_dtype; NULL for the hierarchy), serving copies kc / vc in the cache dtype, size,
+ *   CSR off[f0 + j] = mbase[p] + prefix, idx[mbase[p] + ...] = member ids (token ids
+ *   prob_start + i for key problems, fine ids for the hierarchy -- "children").
+ * Hierarchy (pts64 != NULL): kc64 / vc64 are the size-weighted means of the children's fine
+ * centroids (fine_vc64 supplies the value side) -- clustering.py:249-255. */
+int mpa_km_write_level(const mpa_km* km, const void* vals, const double* fine_vc64,
+                       const int32_t* f0, const int32_t* mbase,
+                       double* kc64, double* vc64, void* kc, void* vc, int32_t serve_dtype,
+                       int32_t* size, int32_t* off, int32_t* idx, int32_t level_cap, int32_t idx_cap,
+                       void* stream);
+
+/* Initial assignment of a problem from an existing ledger level: point i (token prob_start + i)
+ * gets the LOCAL id (cluster - first[p]) of the cluster of ledger prob_l[p] containing it
+ * (first[p] .. first[p] + nclus[p] - 1 are searched).  Used by splits and settles. */
+int mpa_km_assign_from_level(const mpa_km* km, const int32_t* off, const int32_t* idx, int32_t level_cap,
+                             int32_t idx_cap, const int32_t* first, const int32_t* nclus,
+                             const int32_t* mbase, void* stream);
+
+/* K6 -- single-pass sequential assignment of the L appended tokens with running-mean updates
+ * (clustering.py:439-444): for t in order: c = argmin_j ||cent_j - x_t||^2 (direct form, first
+ * min); count[c] += 1; cent[c] += (x_t - cent[c]) / count[c].  One CTA per ledger; cent / count
+ * are per-problem arrays at c_off[p] with k = prob_k[p]; tokens prob_start[p] + tail_start[p] ..
+ * +n_new.  dist is [n_prob, n_new, k_max] fp64 workspace. */
+int mpa_km_seq_assign(const mpa_km* km, const int32_t* tail_start, int n_new, double* dist, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -611,7 +611,9 @@ class StepReport:
 
 
 def decode_step(queries, ledgers, keys, values, cache_len, step, cfg: EngineConfig,
-                layout: HeadLayout, mode="multipole"):
+                layout: HeadLayout, mode="multipole", rot_keys=None):
+    """`rot_keys` (test hook, per head (T, d)): use these already-rotated keys for the exact
+    logits instead of rotating `keys` -- emulates a cache that stores K_rot in a lower precision."""
     d = layout.head_dim
     th = cfg.rope_theta
     out = np.empty((layout.num_q_heads, d))
@@ -626,7 +628,12 @@ def decode_step(queries, ledgers, keys, values, cache_len, step, cfg: EngineConf
         K, V = keys[h], values[h]
         for gi, g in enumerate(grp):
             q = queries[g]
-            parts = [exact_part(q, cache_len, K[ix], V[ix], ix, d, th) for ix in (sinks, buf, lk.sel_idx)]
+            if rot_keys is None:
+                parts = [exact_part(q, cache_len, K[ix], V[ix], ix, d, th) for ix in (sinks, buf, lk.sel_idx)]
+            else:
+                qr = rotate(q, cache_len, d, th)
+                parts = [partial_of(np.asarray(rot_keys[h][ix], np.float64) @ qr / np.sqrt(d), V[ix]) if ix.size
+                         else Partial.empty(d) for ix in (sinks, buf, lk.sel_idx)]
             if use_rep:
                 parts += [replacement(gi, r, d) for r in (lk.fine_rej, lk.coarse_rej) if r]
             out[g] = merge(parts).out()

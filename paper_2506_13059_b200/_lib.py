@@ -37,6 +37,16 @@ class MpaLevel(C.Structure):
                 ("cap", _i32), ("idx_cap", _i32), ("dtype", _i32), ("n_ledgers", _i32)]
 
 
+class MpaKm(C.Structure):
+    _fields_ = [("n_prob", _i32), ("d", _i32), ("pts", _vp), ("pts_dtype", _i32), ("tcap", _i32), ("pts64", _vp),
+                ("wts", _vp), ("rows64_cap", _i32), ("n_max", _i32), ("k_max", _i32), ("min_iters", _i32),
+                ("prob_l", _vp), ("prob_start", _vp), ("prob_n", _vp), ("prob_k", _vp), ("pt_off", _vp),
+                ("c_off", _vp), ("assign", _vp), ("prev", _vp), ("p2", _vp), ("cent", _vp), ("c2", _vp),
+                ("count", _vp), ("order", _vp), ("cstart", _vp), ("state", _vp), ("flag", _vp)]
+
+
+_KM = C.POINTER(MpaKm)
+
 _SIGS = {
     "mpa_kv_write": [C.POINTER(MpaCache), _vp, _vp, _vp, C.c_int, _vp, _vp],
     "mpa_rotate_queries": [_vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int, _vp, _f32, _vp, _vp, _vp],
@@ -47,6 +57,12 @@ _SIGS = {
     "mpa_build_worklist": [C.POINTER(MpaLevel), C.POINTER(MpaLevel), C.c_int, _vp, _vp, C.c_int, _vp, _vp,
                            _vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int, _vp, _vp,
                            C.c_int, _vp, _vp],
+    "mpa_km_lloyd": [_KM, C.POINTER(_i32), _vp],
+    "mpa_km_means": [_KM, _vp],
+    "mpa_km_count_nonempty": [_KM, _vp, _vp],
+    "mpa_km_write_level": [_KM, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i32, _i32, _vp],
+    "mpa_km_assign_from_level": [_KM, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp],
+    "mpa_km_seq_assign": [_KM, _vp, C.c_int, _vp, _vp],
     "mpa_sparse_decode": [C.POINTER(MpaCache), _vp, C.c_int, C.c_int, _vp, _vp, C.c_int, _vp, _vp, _vp,
                           C.c_int, _vp, C.c_int, _vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp],
 }

@@ -1,0 +1,423 @@
+"""GPU key clustering: blockwise prefill index, online update, sliding-window split/settle and
+the two-level hierarchy, driving the batched k-means kernels of libmpattn (csrc/mpa_cluster.cu).
+
+Reference (pkg/src/multipole_attn/clustering.py):
+  build_prefill_index_head  :288-326   -> prefill_ledgers()
+  append_tokens             :404-472   -> online_update()
+  _split_final / _settle    :343-401   -> _split()
+  build_hierarchy           :210-264   -> _hierarchy()
+  kmeans / lloyd            :123-184   -> KMeansBatch (all problems of a call in one batch)
+
+Everything numerical runs on the GPU.  The host only draws the reference's RNG indices
+(numpy PCG64 with the same seeds: block k-means init, update samples, hierarchy init), keeps
+the per-ledger block table (spans and cluster counts) and sizes the problem batches.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from ._lib import MpaKm, call, dtype_code, ptr, stream_ptr
+from .core import ConfigError, block_seed, update_rng
+from .ledger import BlockRow
+
+MAX_POINTS = 16384  # per problem (csrc/mpa_cluster.cu kMaxPoints)
+
+
+class KMeansBatch:
+    """One batch of independent Lloyd problems (l, start, n, k) on a shared point source."""
+
+    def __init__(self, device, d: int, probs, init: torch.Tensor, *, pts=None, tcap: int = 0, pts64=None, wts=None,
+                 rows64_cap: int = 0, min_iters: int = 0, count_init: torch.Tensor | None = None):
+        arr = np.asarray(probs, np.int64).reshape(-1, 4)
+        self.probs = arr
+        self.P = arr.shape[0]
+        n, k = arr[:, 2], arr[:, 3]
+        if self.P and int(n.max()) > MAX_POINTS:
+            raise ConfigError(f"k-means problem with {int(n.max())} points > {MAX_POINTS} per problem")
+        self.pt_off = np.concatenate([[0], np.cumsum(n)[:-1]]).astype(np.int64)
+        self.c_off = np.concatenate([[0], np.cumsum(k)[:-1]]).astype(np.int64)
+        i32 = dict(dtype=torch.int32, device=device)
+        N, K = int(n.sum()), int(k.sum())
+        self.d = d
+        self.t = {name: torch.as_tensor(v, **i32) for name, v in
+                  (("l", arr[:, 0]), ("start", arr[:, 1]), ("n", n), ("k", k), ("pt_off", self.pt_off),
+                   ("c_off", self.c_off))}
+        self.assign = torch.zeros(max(N, 1), **i32)
+        self.prev = torch.zeros(max(N, 1), **i32)
+        self.p2 = torch.zeros(max(N, 1), dtype=torch.float64, device=device)
+        self.order = torch.zeros(max(N, 1), **i32)
+        self.cent = init.to(torch.float64).contiguous().reshape(-1, d)
+        assert self.cent.shape[0] == K, (self.cent.shape, K)
+        self.c2 = torch.zeros(max(K, 1), dtype=torch.float64, device=device)
+        self.count = (count_init.to(torch.int32).contiguous() if count_init is not None
+                      else torch.zeros(max(K, 1), **i32))
+        self.cstart = torch.zeros(max(K, 1), **i32)
+        self.state = torch.zeros(max(self.P, 1), 4, **i32)
+        self.flag = torch.zeros(2, **i32)
+        self.src = (pts, tcap, pts64, wts, rows64_cap)
+        self.min_iters = min_iters
+        self.n_max = int(n.max()) if self.P else 0
+        self.k_max = int(k.max()) if self.P else 0
+
+    def struct(self) -> MpaKm:
+        pts, tcap, pts64, wts, rcap = self.src
+        t = self.t
+        return MpaKm(self.P, self.d, ptr(pts), dtype_code(pts.dtype) if pts is not None else 0, tcap, ptr(pts64),
+                     ptr(wts), rcap, self.n_max, self.k_max, self.min_iters, ptr(t["l"]), ptr(t["start"]),
+                     ptr(t["n"]), ptr(t["k"]), ptr(t["pt_off"]), ptr(t["c_off"]), ptr(self.assign), ptr(self.prev),
+                     ptr(self.p2), ptr(self.cent), ptr(self.c2), ptr(self.count), ptr(self.order), ptr(self.cstart),
+                     ptr(self.state), ptr(self.flag))
+
+    def lloyd(self) -> int:
+        import ctypes
+
+        r = ctypes.c_int32(0)
+        call("mpa_km_lloyd", self.struct(), ctypes.byref(r), stream_ptr())
+        return int(r.value)
+
+    def means(self) -> None:
+        call("mpa_km_means", self.struct(), stream_ptr())
+
+    def nonempty(self) -> np.ndarray:
+        nk = torch.zeros(max(self.P, 1), dtype=torch.int32, device=self.assign.device)
+        call("mpa_km_count_nonempty", self.struct(), ptr(nk), stream_ptr())
+        return nk[: self.P].cpu().numpy().astype(np.int64)
+
+    def counts(self, p: int) -> torch.Tensor:
+        c0, k = int(self.c_off[p]), int(self.probs[p, 3])
+        return self.count[c0:c0 + k]
+
+    def centroids(self, p: int) -> torch.Tensor:
+        c0, k = int(self.c_off[p]), int(self.probs[p, 3])
+        return self.cent[c0:c0 + k]
+
+
+def _write_fine(eng, km: KMeansBatch, f0: np.ndarray, mbase: np.ndarray) -> None:
+    led, dev = eng.led, eng.device
+    call("mpa_km_write_level", km.struct(), ptr(eng.v), None,
+         ptr(torch.as_tensor(f0, dtype=torch.int32, device=dev)), ptr(torch.as_tensor(mbase, dtype=torch.int32, device=dev)),
+         ptr(led.kc64), ptr(led.vc64), ptr(led.kc), ptr(led.vc), dtype_code(led.dtype), ptr(led.size), ptr(led.off),
+         ptr(led.mem), led.kcap, led.tcap, stream_ptr())
+
+
+def _write_coarse(eng, km: KMeansBatch, c0: np.ndarray, mbase: np.ndarray) -> None:
+    led, dev = eng.led, eng.device
+    call("mpa_km_write_level", km.struct(), None, ptr(led.vc64),
+         ptr(torch.as_tensor(c0, dtype=torch.int32, device=dev)), ptr(torch.as_tensor(mbase, dtype=torch.int32, device=dev)),
+         ptr(led.ckc64), ptr(led.cvc64), ptr(led.ckc), ptr(led.cvc), dtype_code(led.dtype), ptr(led.csize),
+         ptr(led.coff), ptr(led.child), led.ccap, led.kcap, stream_ptr())
+
+
+def _refresh_counts(eng, ledgers) -> None:
+    led = eng.led
+    for l in ledgers:
+        rows = led.blocks[l]
+        led.n_fine[l] = rows[-1].f0 + rows[-1].fk if rows else 0
+        led.n_coarse[l] = rows[-1].c0 + rows[-1].ck if rows else 0
+        if led.n_fine[l] > led.kcap or led.n_coarse[l] > max(led.ccap, 0) and led.hierarchy:
+            raise ConfigError(f"ledger {l}: cluster capacity exceeded (fine {led.n_fine[l]}/{led.kcap}, "
+                              f"coarse {led.n_coarse[l]}/{led.ccap})")
+    led.count.copy_(torch.as_tensor(led.n_fine, dtype=torch.int32))
+    if led.hierarchy:
+        led.ccount.copy_(torch.as_tensor(led.n_coarse, dtype=torch.int32))
+    K = int(led.n_fine.max()) if led.L else 0
+    if K:
+        mask = torch.arange(K, device=eng.device)[None, :] < led.count[:, None]
+        led.max_size[:] = (led.size[:, :K] * mask).amax(dim=1).cpu().numpy()
+
+
+def _head(eng, l: int) -> int:
+    return l % eng.Hkv
+
+
+# ---------------------------------------------------------------------------- prefill
+
+
+def prefill_ledgers(eng) -> None:
+    """Blockwise k-means of every ledger's prompt (clustering.py:288-326); k = ceil(n / r),
+    init = default_rng(block_seed(seed, head, b)).choice(n, k, replace=False)."""
+    cfg, led = eng.cfg, eng.led
+    W = cfg.block_size
+    eng.set_prompt_layout()
+    probs, inits, owners = [], [], []
+    tables = []
+    for l in range(eng.L):
+        s = l // eng.Hkv
+        s0, b0 = int(eng.sink_end[s]), int(eng.buffer_start[s])
+        nsealed = (b0 - s0) // W
+        spans = [(s0 + b * W, s0 + b * W + W) for b in range(nsealed)] + [(s0 + nsealed * W, b0)]
+        tables.append(spans)
+        for b, (lo, hi) in enumerate(spans):
+            n = hi - lo
+            if n <= 0:
+                continue
+            k = min(max(1, -(-n // cfg.fine_ratio)), n)
+            pick = np.random.default_rng(block_seed(cfg.seed, _head(eng, l), b)).choice(n, size=k, replace=False)
+            probs.append((l, lo, n, k))
+            inits.append(eng.k_raw[l, lo + torch.as_tensor(pick, device=eng.device)].double())
+            owners.append((l, b))
+    km = KMeansBatch(eng.device, eng.d, probs, torch.cat(inits) if inits else torch.zeros(0, eng.d),
+                     pts=eng.k_raw, tcap=eng.tcap, min_iters=cfg.prefill_kmeans_iters)
+    eng.last_lloyd_rounds = km.lloyd() if probs else 0
+    nk = km.nonempty()
+    f0 = np.zeros(len(probs), np.int64)
+    mbase = np.zeros(len(probs), np.int64)
+    per = {o: i for i, o in enumerate(owners)}
+    for l in range(eng.L):
+        s0 = int(eng.sink_end[l // eng.Hkv])
+        rows, acc = [], 0
+        for b, (lo, hi) in enumerate(tables[l]):
+            i = per.get((l, b))
+            fk = int(nk[i]) if i is not None else 0
+            if i is not None:
+                f0[i], mbase[i] = acc, lo - s0
+            rows.append(BlockRow(lo, hi, acc, fk))
+            acc += fk
+        led.blocks[l] = rows
+        eng.splits[l] = 0
+    if probs:
+        _write_fine(eng, km, f0, mbase)
+    _refresh_counts(eng, range(eng.L))
+    if cfg.hierarchy is not None:
+        _hierarchy(eng, [(l, b, block_seed(cfg.seed, _head(eng, l), b, 1)) for l in range(eng.L)
+                         for b in range(len(led.blocks[l]))])
+
+
+# ---------------------------------------------------------------------------- hierarchy
+
+
+def _hierarchy(eng, jobs) -> None:
+    """Coarse level of the given (ledger, block, seed) jobs (clustering.py:210-264).  Jobs of
+    one ledger must be its LAST blocks in ascending order (coarse clusters are laid out in
+    block order, so rebuilding the tail keeps every earlier block's coarse ids)."""
+    cfg, led = eng.cfg, eng.led
+    probs, inits, meta = [], [], []
+    for (l, b, seed) in jobs:
+        r = led.blocks[l][b]
+        if r.fk == 0:
+            meta.append(None)
+            continue
+        k1 = min(r.fk, max(1, -(-(r.end - r.start) // cfg.hierarchy.r1)))
+        pick = np.random.default_rng(seed).choice(r.fk, size=k1, replace=False)
+        probs.append((l, r.f0, r.fk, k1))
+        inits.append(led.kc64[l, r.f0 + torch.as_tensor(pick, device=eng.device)])
+        meta.append(len(probs) - 1)
+    nk = np.zeros(0, np.int64)
+    km = None
+    if probs:
+        km = KMeansBatch(eng.device, eng.d, probs, torch.cat(inits), pts64=led.kc64, wts=led.size,
+                         rows64_cap=led.kcap, min_iters=cfg.refine_kmeans_iters)
+        km.lloyd()
+        nk = km.nonempty()
+    c0 = np.zeros(len(probs), np.int64)
+    mbase = np.zeros(len(probs), np.int64)
+    for (l, b, _), pi in zip(jobs, meta):
+        rows = led.blocks[l]
+        start = rows[b - 1].c0 + rows[b - 1].ck if b > 0 else 0
+        rows[b].c0 = start
+        rows[b].ck = int(nk[pi]) if pi is not None else 0
+        if pi is not None:
+            c0[pi], mbase[pi] = start, rows[b].f0
+    if probs:
+        _write_coarse(eng, km, c0, mbase)
+    _refresh_counts(eng, sorted({j[0] for j in jobs}))
+
+
+# ---------------------------------------------------------------------------- online update
+
+
+def online_update(eng, seqs, cursor: int) -> dict:
+    """Absorb the oldest L buffered tokens of every kv-head of `seqs` into the final block
+    (clustering.py:404-472), then split / settle (:359-401) and refresh the final block's
+    hierarchy (:465-471).  Returns timing-free counters (rounds, splits)."""
+    cfg, led = eng.cfg, eng.led
+    L = cfg.local_buffer
+    n_new = -(-L // cfg.fine_ratio)
+    ledgers = [s * eng.Hkv + h for s in seqs for h in range(eng.Hkv)]
+    for s in seqs:
+        if eng.cache_len[s] - eng.buffer_start[s] < 2 * L:
+            raise RuntimeError(f"buffer underflow: have {eng.cache_len[s] - eng.buffer_start[s]} tokens, need {2 * L}")
+    probs, inits, counts, tails = [], [], [], []
+    for l in ledgers:
+        s = l // eng.Hkv
+        F = led.blocks[l][-1]
+        bs = int(eng.buffer_start[s])
+        rng = update_rng(cfg.seed, cursor, _head(eng, l))
+        samp = rng.choice(L, size=n_new, replace=False)
+        old = led.kc64[l, F.f0:F.f0 + F.fk]
+        inits.append(torch.cat([old, eng.k_raw[l, bs + torch.as_tensor(samp, device=eng.device)].double()]))
+        counts.append(torch.cat([led.size[l, F.f0:F.f0 + F.fk],
+                                 torch.zeros(n_new, dtype=torch.int32, device=eng.device)]))
+        probs.append((l, F.start, bs + L - F.start, F.fk + n_new))
+        tails.append(bs - F.start)
+    km = KMeansBatch(eng.device, eng.d, probs, torch.cat(inits), pts=eng.k_raw, tcap=eng.tcap,
+                     min_iters=cfg.refine_kmeans_iters, count_init=torch.cat(counts))
+    dist = torch.empty(len(probs), L, km.k_max, dtype=torch.float64, device=eng.device)
+    call("mpa_km_seq_assign", km.struct(), ptr(torch.as_tensor(tails, dtype=torch.int32, device=eng.device)), L,
+         ptr(dist), stream_ptr())
+    rounds = km.lloyd()
+    nk = km.nonempty()
+    f0 = np.zeros(len(probs), np.int64)
+    mbase = np.zeros(len(probs), np.int64)
+    for i, l in enumerate(ledgers):
+        s = l // eng.Hkv
+        F = led.blocks[l][-1]
+        f0[i], mbase[i] = F.f0, F.start - int(eng.sink_end[s])
+        F.end = int(eng.buffer_start[s]) + L
+        F.fk = int(nk[i])
+    _write_fine(eng, km, f0, mbase)
+    for s in seqs:
+        eng.buffer_start[s] += L
+    eng._sync_scalars()
+    _refresh_counts(eng, ledgers)
+    n_splits = _split(eng, ledgers)
+    if cfg.hierarchy is not None:
+        _hierarchy(eng, [(l, len(led.blocks[l]) - 1,
+                          block_seed(cfg.seed, _head(eng, l), int(eng.buffer_start[l // eng.Hkv]), 3))
+                         for l in ledgers])
+    return {"rounds": rounds, "splits": n_splits}
+
+
+def _split(eng, ledgers, settle: bool = True) -> int:
+    """Seal the first W tokens of every final block with |final| >= W + alpha; both sides are
+    seeded with their members' means and (settle=True) settled with Lloyd(min_iters=0)."""
+    cfg, led = eng.cfg, eng.led
+    W, A = cfg.block_size, cfg.alpha
+    total = 0
+    while True:
+        todo = [l for l in ledgers if led.blocks[l][-1].end - led.blocks[l][-1].start >= W + A]
+        if not todo:
+            return total
+        total += len(todo)
+        # (1) side means from the current membership
+        probs, firsts, ncl = [], [], []
+        for l in todo:
+            F = led.blocks[l][-1]
+            cut = F.start + W
+            probs += [(l, F.start, W, F.fk), (l, cut, F.end - cut, F.fk)]
+            firsts += [F.f0, F.f0]
+            ncl += [F.fk, F.fk]
+        dev = eng.device
+        km = KMeansBatch(dev, eng.d, probs, torch.zeros(sum(p[3] for p in probs), eng.d, dtype=torch.float64,
+                                                         device=dev), pts=eng.k_raw, tcap=eng.tcap)
+        call("mpa_km_assign_from_level", km.struct(), ptr(led.off), ptr(led.mem), led.kcap, led.tcap,
+             ptr(torch.as_tensor(firsts, dtype=torch.int32, device=dev)),
+             ptr(torch.as_tensor(ncl, dtype=torch.int32, device=dev)), None, stream_ptr())
+        km.means()
+        if settle:
+            # (2) settle each side from its non-empty side means (clustering.py:384-394)
+            sprobs, sinit = [], []
+            for i, (l, lo, n, k) in enumerate(probs):
+                live = km.counts(i) > 0
+                c = km.centroids(i)[live]
+                sprobs.append((l, lo, n, int(c.shape[0])))
+                sinit.append(c)
+            st = KMeansBatch(dev, eng.d, sprobs, torch.cat(sinit), pts=eng.k_raw, tcap=eng.tcap, min_iters=0)
+            st.lloyd()
+        else:
+            st = km  # positional pages: straddlers split, no settle (clustering.py:540)
+        nk = st.nonempty()
+        f0 = np.zeros(len(sprobs), np.int64)
+        mbase = np.zeros(len(sprobs), np.int64)
+        for j, l in enumerate(todo):
+            s0 = int(eng.sink_end[l // eng.Hkv])
+            F = led.blocks[l][-1]
+            cut = F.start + W
+            left = BlockRow(F.start, cut, F.f0, int(nk[2 * j]), F.c0, 0)
+            right = BlockRow(cut, F.end, F.f0 + int(nk[2 * j]), int(nk[2 * j + 1]), F.c0, 0)
+            f0[2 * j], mbase[2 * j] = left.f0, left.start - s0
+            f0[2 * j + 1], mbase[2 * j + 1] = right.f0, right.start - s0
+            led.blocks[l][-1:] = [left, right]
+            eng.splits[l] += 1
+        _write_fine(eng, st, f0, mbase)
+        _refresh_counts(eng, todo)
+        if cfg.hierarchy is not None:
+            _hierarchy(eng, [(l, len(led.blocks[l]) - 2, block_seed(cfg.seed, _head(eng, l), len(led.blocks[l]) - 2, 2))
+                             for l in todo])
+
+
+# ---------------------------------------------------------------------------- positional pages
+
+
+def _page_batch(eng, spans):
+    """KMeansBatch whose assignment is the contiguous r-token page of each point, with means."""
+    r = eng.cfg.fine_ratio
+    probs = [(l, lo, hi - lo, -(-(hi - lo) // r)) for (l, lo, hi) in spans]
+    km = KMeansBatch(eng.device, eng.d, probs, torch.zeros(sum(p[3] for p in probs), eng.d, dtype=torch.float64,
+                                                          device=eng.device), pts=eng.k_raw, tcap=eng.tcap)
+    asg = [torch.arange(p[2], device=eng.device, dtype=torch.int32) // r for p in probs]
+    if asg:
+        flat = torch.cat(asg)
+        km.assign[: flat.numel()].copy_(flat)
+        km.means()
+    return km
+
+
+def prefill_positional(eng) -> None:
+    """Positional comparator: contiguous r-token pages with mean centroids (clustering.py:497-526)."""
+    cfg, led = eng.cfg, eng.led
+    W = cfg.block_size
+    eng.set_prompt_layout()
+    spans, owners = [], []
+    for l in range(eng.L):
+        s = l // eng.Hkv
+        s0, b0 = int(eng.sink_end[s]), int(eng.buffer_start[s])
+        nsealed = (b0 - s0) // W
+        rows = []
+        for b in range(nsealed + 1):
+            lo = s0 + b * W
+            hi = lo + W if b < nsealed else b0
+            rows.append(BlockRow(lo, hi, 0, 0))
+            if hi > lo:
+                spans.append((l, lo, hi))
+                owners.append((l, b))
+        led.blocks[l] = rows
+    km = _page_batch(eng, spans)
+    nk = km.nonempty()
+    f0 = np.zeros(len(spans), np.int64)
+    mbase = np.zeros(len(spans), np.int64)
+    per = {o: i for i, o in enumerate(owners)}
+    for l in range(eng.L):
+        acc = 0
+        s0 = int(eng.sink_end[l // eng.Hkv])
+        for b, row in enumerate(led.blocks[l]):
+            row.f0 = acc
+            i = per.get((l, b))
+            if i is not None:
+                row.fk = int(nk[i])
+                f0[i], mbase[i] = acc, row.start - s0
+            acc += row.fk
+    if spans:
+        _write_fine(eng, km, f0, mbase)
+    _refresh_counts(eng, range(eng.L))
+
+
+def positional_update(eng, seqs) -> dict:
+    """Rebuild the final block's pages over the absorbed tokens, then split without settling
+    (clustering.py:529-541)."""
+    cfg, led = eng.cfg, eng.led
+    L = cfg.local_buffer
+    ledgers = [s * eng.Hkv + h for s in seqs for h in range(eng.Hkv)]
+    spans = []
+    for l in ledgers:
+        s = l // eng.Hkv
+        if eng.cache_len[s] - eng.buffer_start[s] < 2 * L:
+            raise RuntimeError("buffer underflow")
+        F = led.blocks[l][-1]
+        spans.append((l, F.start, int(eng.buffer_start[s]) + L))
+    km = _page_batch(eng, spans)
+    nk = km.nonempty()
+    f0 = np.zeros(len(spans), np.int64)
+    mbase = np.zeros(len(spans), np.int64)
+    for i, l in enumerate(ledgers):
+        F = led.blocks[l][-1]
+        f0[i], mbase[i] = F.f0, F.start - int(eng.sink_end[l // eng.Hkv])
+        F.end, F.fk = spans[i][2], int(nk[i])
+    _write_fine(eng, km, f0, mbase)
+    for s in seqs:
+        eng.buffer_start[s] += L
+    eng._sync_scalars()
+    _refresh_counts(eng, ledgers)
+    return {"rounds": 0, "splits": _split(eng, ledgers, settle=False)}

@@ -91,6 +91,9 @@ class DecodeEngine:
         self.out = torch.zeros(n_seq, self.Hq, d, dtype=torch.float32, **z)
         self.cache_struct = MpaCache(ptr(self.k_rot), ptr(self.k_raw), ptr(self.v), dtype_code(dtype), L, tcap, d)
         self.last_split = 1
+        self.cursor = 0
+        self.last_lloyd_rounds = 0
+        self.last_update: dict | None = None
 
     # ------------------------------------------------------------------ KV cache
     def write_tokens(self, k: torch.Tensor, v: torch.Tensor, pos0: torch.Tensor | None = None) -> None:
@@ -162,7 +165,7 @@ class DecodeEngine:
         fine = self.led.fine_level()
         replacement = 0 if self.mode == "flat-no-replacement" else 1
         if self.cfg.hierarchy is None:
-            if int(self.led.n_fine.min(initial=0)) == 0:
+            if int(self.led.n_fine.min()) == 0:
                 raise ConfigError("ledger has no clusters")
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, None, None, self.kcap,
                  ptr(self.logits), st)
@@ -173,7 +176,7 @@ class DecodeEngine:
                  replacement, ptr(self.tok), self.tok_cap, ptr(self.rej), ptr(self.rej_w), self.rej_cap,
                  ptr(self.stats), st)
         else:
-            if int(self.led.n_coarse.min(initial=0)) == 0:
+            if int(self.led.n_coarse.min()) == 0:
                 raise ConfigError("ledger has no coarse clusters")
             coarse = self.led.coarse_level()
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, coarse, None, None, self.ccap,
@@ -220,6 +223,47 @@ class DecodeEngine:
              0, None, None, None, 0, None, 0, None, 0, S, ptr(self.part_ml), ptr(self.part_acc), ptr(self.ticket),
              ptr(self.out), stream_ptr())
         return self.out
+
+    # ------------------------------------------------------------------ pipeline
+    def prefill(self) -> None:
+        """Index the prompt already written with write_tokens (pipeline.py:69-94)."""
+        from . import clustering
+
+        if self.mode == "oracle":
+            self.set_prompt_layout()
+        elif self.mode == "positional-baseline":
+            clustering.prefill_positional(self)
+        else:
+            clustering.prefill_ledgers(self)
+        self.cursor = 0
+
+    def needs_update(self) -> list[int]:
+        if self.mode == "oracle":
+            return []
+        L = self.cfg.local_buffer
+        return [s for s in range(self.n_seq) if self.cache_len[s] - self.buffer_start[s] >= 2 * L]
+
+    def step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor) -> torch.Tensor:
+        """Attend, append the step's token, then run the online update when a buffer holds 2L
+        tokens (pipeline.py:124-191).  q [n_seq, Hq, d], k_new / v_new [n_seq, Hkv, d] (fp32)."""
+        from . import clustering
+
+        out = self.attend(q)
+        self.write_tokens(k_new[:, :, None], v_new[:, :, None])
+        todo = self.needs_update()
+        self.last_update = None
+        if todo:
+            if self.mode == "positional-baseline":
+                self.last_update = clustering.positional_update(self, todo)
+            else:
+                self.last_update = clustering.online_update(self, todo, self.cursor)
+        self.cursor += 1
+        return out
+
+    def export_ledger(self, l: int) -> HostLedger:
+        s = l // self.Hkv
+        return self.led.export(l, int(self.sink_end[s]), int(self.buffer_start[s]), int(self.cache_len[s]),
+                               int(self.splits[l]))
 
     def head_stats(self) -> np.ndarray:
         """[L, 4]: n_tok, n_rej, selected tokens, selected clusters (host copy)."""

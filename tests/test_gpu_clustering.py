@@ -1,0 +1,172 @@
+"""GPU clustering (K2-K8) and the end-to-end pipeline against the pinned oracle.
+
+* prefill ledgers (blockwise k-means, hierarchy) equal the oracle's bit-for-bit: spans,
+  cluster order, sizes, members, fp64 key/value centroids, coarse children;
+* online updates (sequential assignment + Lloyd refinement + split/settle + hierarchy rebuild)
+  over long replays equal the oracle's ledgers after every update;
+* `pipeline.run` reproduces the oracle's outputs (fp32: 1e-5) and selections on the reference's
+  own test scenarios (test_pipeline.py, test_clustering.py:179-194, acceptance criterion 6).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import mpa_oracle as O
+from paper_2506_13059_b200.core import EngineConfig, HeadLayout, HierarchyConfig, KvTrace, gen_synthetic
+from tests.bridge import rel_err, to_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _bf16(a):
+    return torch.as_tensor(a).to(torch.bfloat16).float().numpy()
+
+
+def _engine_prefill(trace, cfg, dtype, mode="multipole"):
+    from paper_2506_13059_b200.engine import DecodeEngine
+
+    P = trace.prompt_len
+    eng = DecodeEngine(cfg, trace.layout, 1, tcap=trace.total_len + 8, dtype=dtype, mode=mode)
+    eng.write_tokens(torch.as_tensor(trace.keys[:, :P]).cuda()[None], torch.as_tensor(trace.values[:, :P]).cuda()[None])
+    eng.prefill()
+    return eng
+
+
+def _assert_same_ledger(got: O.LedgerO, want: O.LedgerO, where=""):
+    a, b = O.ledger_arrays(got), O.ledger_arrays(want)
+    assert sorted(a) == sorted(b), where
+    for k in a:
+        assert np.array_equal(a[k], b[k]), (where, k)
+
+
+def _as_dtype_trace(trace, dtype):
+    if dtype == torch.float32:
+        return trace
+    return KvTrace(trace.layout, trace.prompt_len, _bf16(trace.keys), _bf16(trace.values), trace.queries)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("hier", [None, HierarchyConfig(32, 8, 0.5)])
+def test_prefill_ledgers_bitexact(dtype, hier):
+    tr = _as_dtype_trace(gen_synthetic(6, 500, HeadLayout(2, 2, 8), 0.05, seed=5, decode_steps=200), dtype)
+    cfg = EngineConfig(block_size=128, alpha=64, local_buffer=16, sink_tokens=8, token_budget=32,
+                       tokens_per_centroid=8, hierarchy=hier, seed=5)
+    eng = _engine_prefill(tr, cfg, dtype)
+    for h in range(2):
+        want = O.prefill_ledger(tr.keys[h, :500], tr.values[h, :500], 500, cfg, h)
+        _assert_same_ledger(to_oracle(eng.export_ledger(h)), want, f"head {h}")
+
+
+def test_kmeans_degenerate_duplicates_and_empty_repair():
+    # duplicate-heavy points exercise _repair_empty and the sizes[big] <= 1 stop (test_clustering.py:69-72)
+    lay = HeadLayout(1, 1, 4)
+    keys = np.zeros((1, 60, 4), np.float32)
+    keys[0, 30:] = 1.0
+    vals = np.random.default_rng(0).standard_normal((1, 60, 4)).astype(np.float32)
+    tr = KvTrace(lay, 60, keys, vals, np.zeros((1, 0, 4), np.float32))
+    cfg = EngineConfig(block_size=64, local_buffer=2, sink_tokens=2, tokens_per_centroid=4, seed=1)
+    eng = _engine_prefill(tr, cfg, torch.float32)
+    want = O.prefill_ledger(keys[0], vals[0], 60, cfg, 0)
+    _assert_same_ledger(to_oracle(eng.export_ledger(0)), want)
+
+
+def test_c1_prefill_bitexact():
+    tr = gen_synthetic(256, 8192, HeadLayout(32, 8, 128), 0.05, seed=0, decode_steps=32)
+    cfg = EngineConfig(tokens_per_centroid=32, token_budget=819, seed=0)
+    eng = _engine_prefill(tr, cfg, torch.float32)
+    for h in range(8):
+        want = O.prefill_ledger(tr.keys[h, :8192], tr.values[h, :8192], 8192, cfg, h)
+        _assert_same_ledger(to_oracle(eng.export_ledger(h)), want, f"head {h}")
+
+
+def _run_both(tr, cfg, steps, dtype=torch.float32, mode="multipole", check_ledgers_every_update=True):
+    from paper_2506_13059_b200 import pipeline as G
+
+    st_g = G.prefill(tr, cfg, mode=mode, dtype=dtype)
+    st_o = O.prefill(tr, cfg, mode)
+    worst = 0.0
+    n_upd = 0
+    for t in range(steps):
+        pos = tr.prompt_len + t
+        args = (tr.queries[:, t], tr.keys[:, pos], tr.values[:, pos])
+        out_g, rep_g = G.step(st_g, *args)
+        out_o, rep_o = O.step(st_o, *args)
+        worst = max(worst, float(rel_err(out_g, out_o).max()))
+        assert rep_g.update_occurred == rep_o.update_occurred, t
+        if mode != "oracle":
+            for h in range(tr.layout.num_kv_heads):
+                assert np.array_equal(rep_g.selected_indices[h], rep_o.selected_indices[h]), (t, h)
+                assert rep_g.per_head[h].selected_tokens == rep_o.per_head[h].selected_tokens
+                assert rep_g.per_head[h].scored_centroids == rep_o.per_head[h].scored_centroids, (t, h)
+                assert rep_g.per_head[h].rejected_centroids == rep_o.per_head[h].rejected_centroids
+        if rep_o.update_occurred:
+            n_upd += 1
+            if check_ledgers_every_update:
+                for h in range(tr.layout.num_kv_heads):
+                    _assert_same_ledger(to_oracle(st_g.engine.export_ledger(h)), st_o.ledgers[h], f"t={t} h={h}")
+    return worst, n_upd, st_g, st_o
+
+
+@pytest.mark.parametrize("mode", ["multipole", "flat-no-replacement", "positional-baseline", "oracle"])
+def test_pipeline_small_trace(mode):
+    tr = gen_synthetic(8, 600, HeadLayout(8, 2, 16), 0.05, seed=11, decode_steps=20)
+    cfg = EngineConfig(block_size=256, alpha=128, local_buffer=16, sink_tokens=5, token_budget=64, seed=11)
+    worst, n_upd, _, _ = _run_both(tr, cfg, 20, mode=mode)
+    assert worst < 1e-5, worst
+    if mode != "oracle":
+        assert n_upd == 1
+
+
+def test_pipeline_long_trajectory_with_splits():
+    # online updates every L steps with two sliding-window splits (C4 analogue at desk scale)
+    tr = gen_synthetic(8, 1000, HeadLayout(4, 1, 16), 0.1, seed=3, decode_steps=400)
+    cfg = EngineConfig(block_size=256, alpha=128, local_buffer=16, sink_tokens=5, token_budget=64, seed=3)
+    worst, n_upd, st_g, _ = _run_both(tr, cfg, 400)
+    assert worst < 1e-5, worst
+    assert n_upd == 25
+    assert st_g.engine.splits[0] >= 1
+
+
+def test_pipeline_hierarchical_updates():
+    tr = gen_synthetic(8, 600, HeadLayout(8, 2, 16), 0.05, seed=13, decode_steps=40)
+    cfg = EngineConfig(block_size=256, alpha=128, local_buffer=16, sink_tokens=5, token_budget=64,
+                       hierarchy=HierarchyConfig(32, 8, 0.5), seed=13)
+    worst, n_upd, _, _ = _run_both(tr, cfg, 40)
+    assert worst < 1e-5, worst
+    assert n_upd >= 2
+
+
+def test_pipeline_hierarchical_splits():
+    tr = gen_synthetic(8, 700, HeadLayout(4, 1, 16), 0.1, seed=21, decode_steps=300)
+    cfg = EngineConfig(block_size=256, alpha=128, local_buffer=16, sink_tokens=5, token_budget=64,
+                       hierarchy=HierarchyConfig(32, 8, 0.25), seed=21)
+    worst, n_upd, st_g, _ = _run_both(tr, cfg, 300)
+    assert worst < 1e-5, worst
+    assert st_g.engine.splits[0] >= 1
+
+
+def test_audit_after_updates():
+    from paper_2506_13059_b200 import pipeline as G
+
+    tr = gen_synthetic(8, 1000, HeadLayout(4, 1, 16), 0.1, seed=3, decode_steps=200)
+    cfg = EngineConfig(block_size=256, alpha=128, local_buffer=16, sink_tokens=5, token_budget=64, seed=3)
+    reps = G.run(tr, cfg, audit=True, max_steps=200)
+    assert sum(r.update_occurred for r in reps) == 12
+
+
+def test_update_cadence_and_attend_before_append():
+    # test_pipeline.py:44-53 and :71-81
+    from paper_2506_13059_b200 import pipeline as G
+
+    tr = gen_synthetic(8, 600, HeadLayout(8, 2, 16), 0.05, seed=11, decode_steps=20)
+    cfg = EngineConfig(block_size=256, alpha=128, local_buffer=16, sink_tokens=5, token_budget=64, seed=11)
+    reps = G.run(tr, cfg, max_steps=20)
+    ups = [r.step for r in reps if r.update_occurred]
+    assert ups and ups[0] == cfg.local_buffer - 1
+    a = G.prefill(tr, cfg)
+    b = G.prefill(tr, cfg)
+    q, pos = tr.queries[:, 0], tr.prompt_len
+    oa, _ = G.step(a, q, tr.keys[:, pos], tr.values[:, pos])
+    ob, _ = G.step(b, q, -tr.keys[:, pos], -tr.values[:, pos])
+    assert np.array_equal(oa, ob)

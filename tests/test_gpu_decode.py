@@ -19,6 +19,16 @@ from tests.bridge import rel_err, rounded, to_host
 pytestmark = pytest.mark.gpu
 
 TOL = {torch.float32: 1e-5, torch.bfloat16: 1e-2}
+# bf16 kernel error against the oracle fed the SAME stored cache (bf16 K_rot / V): the only
+# remaining error is the kernel's own fp32 math, far below the storage effect.
+KERNEL_TOL_BF16 = 2e-3
+# bf16 K_rot storage vs the fp32 reference on gen_synthetic's deliberately peaked queries
+# (query_gain = 12 sqrt(d)): SURVEY 7.3-5 measured up to 1.8e-2 from storage alone.
+PEAKED_TOL_BF16 = 3e-2
+
+
+def _stored(arr, dtype):
+    return torch.as_tensor(arr, dtype=torch.float64).to(dtype).to(torch.float64).numpy()
 
 
 def _engine(trace, cfg, dtype, ledgers, mode="multipole", n_seq=1):
@@ -37,7 +47,7 @@ def _engine(trace, cfg, dtype, ledgers, mode="multipole", n_seq=1):
     return eng
 
 
-def _replay(trace, cfg, dtype, steps, mode="multipole", check_sel=True):
+def _replay(trace, cfg, dtype, steps, mode="multipole", check_sel=True, e2e_tol=None):
     lay, P = trace.layout, trace.prompt_len
     ledgers = [O.prefill_ledger(trace.keys[h, :P], trace.values[h, :P], P, cfg, h) for h in range(lay.num_kv_heads)]
     eng = _engine(trace, cfg, dtype, ledgers, mode)
@@ -46,13 +56,20 @@ def _replay(trace, cfg, dtype, steps, mode="multipole", check_sel=True):
         ref_ledgers = [rounded(x, dtype, keys_too=False) for x in ledgers]
     keys = [trace.keys[h, :P].copy() for h in range(lay.num_kv_heads)]
     vals = [trace.values[h, :P].copy() for h in range(lay.num_kv_heads)]
-    worst = 0.0
+    worst = worst_k = 0.0
     for t in range(steps):
         n = P + t
         q = trace.queries[:, t]
         out = eng.attend(torch.as_tensor(q).cuda()[None]).cpu().numpy()[0]
         want, rep = O.decode_step(q, ref_ledgers, keys, vals, n, t, cfg, lay, mode)
         worst = max(worst, float(rel_err(out, want).max()))
+        if dtype != torch.float32:
+            # the same step on exactly what the GPU stores (bf16 K_rot and V)
+            rk = [_stored(O.rotate(keys[h], np.arange(n), lay.head_dim, cfg.rope_theta), dtype)
+                  for h in range(lay.num_kv_heads)]
+            sv = [_stored(vals[h], dtype) for h in range(lay.num_kv_heads)]
+            want_k, _ = O.decode_step(q, ref_ledgers, keys, sv, n, t, cfg, lay, mode, rot_keys=rk)
+            worst_k = max(worst_k, float(rel_err(out, want_k).max()))
         st = eng.head_stats()
         for h, led in enumerate(ref_ledgers):
             ns = min(led.sink_end, n)
@@ -70,7 +87,9 @@ def _replay(trace, cfg, dtype, steps, mode="multipole", check_sel=True):
             keys[h] = np.concatenate([keys[h], trace.keys[h, n][None]])
             vals[h] = np.concatenate([vals[h], trace.values[h, n][None]])
             ref_ledgers[h].total += 1
-    assert worst <= TOL[dtype], worst
+    assert worst <= (e2e_tol or TOL[dtype]), worst
+    if dtype != torch.float32:
+        assert worst_k <= KERNEL_TOL_BF16, worst_k
     return worst
 
 
@@ -80,7 +99,7 @@ SMALL_CFG = EngineConfig(block_size=256, alpha=128, local_buffer=16, sink_tokens
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 def test_small_trace_flat(dtype):
     tr = gen_synthetic(8, 600, HeadLayout(8, 2, 16), 0.05, seed=11, decode_steps=20)
-    _replay(tr, SMALL_CFG, dtype, steps=12)
+    _replay(tr, SMALL_CFG, dtype, steps=12, e2e_tol=PEAKED_TOL_BF16 if dtype == torch.bfloat16 else None)
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
@@ -88,13 +107,14 @@ def test_small_trace_hierarchical(dtype):
     tr = gen_synthetic(8, 600, HeadLayout(8, 2, 16), 0.05, seed=13, decode_steps=40)
     cfg = EngineConfig(block_size=256, alpha=128, local_buffer=16, sink_tokens=5, token_budget=64,
                        hierarchy=HierarchyConfig(32, 8, 0.5), seed=13)
-    _replay(tr, cfg, dtype, steps=12)
+    _replay(tr, cfg, dtype, steps=12, e2e_tol=PEAKED_TOL_BF16 if dtype == torch.bfloat16 else None)
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 def test_flat_no_replacement(dtype):
     tr = gen_synthetic(8, 600, HeadLayout(8, 2, 16), 0.05, seed=11, decode_steps=20)
-    _replay(tr, SMALL_CFG, dtype, steps=6, mode="flat-no-replacement")
+    _replay(tr, SMALL_CFG, dtype, steps=6, mode="flat-no-replacement",
+            e2e_tol=PEAKED_TOL_BF16 if dtype == torch.bfloat16 else None)
 
 
 @pytest.mark.parametrize("budget", [0, 1, 10**6])
