@@ -94,18 +94,23 @@ class KMeansBatch:
         return self.cent[c0:c0 + k]
 
 
+def _i32(eng, a) -> torch.Tensor:
+    # device copy of a small host index array; callers keep the tensor alive across the launch
+    return torch.as_tensor(np.asarray(a), dtype=torch.int32, device=eng.device)
+
+
 def _write_fine(eng, km: KMeansBatch, f0: np.ndarray, mbase: np.ndarray) -> None:
-    led, dev = eng.led, eng.device
-    call("mpa_km_write_level", km.struct(), ptr(eng.v), None,
-         ptr(torch.as_tensor(f0, dtype=torch.int32, device=dev)), ptr(torch.as_tensor(mbase, dtype=torch.int32, device=dev)),
+    led = eng.led
+    f0_d, mb_d = _i32(eng, f0), _i32(eng, mbase)
+    call("mpa_km_write_level", km.struct(), ptr(eng.v), None, ptr(f0_d), ptr(mb_d),
          ptr(led.kc64), ptr(led.vc64), ptr(led.kc), ptr(led.vc), dtype_code(led.dtype), ptr(led.size), ptr(led.off),
          ptr(led.mem), led.kcap, led.tcap, stream_ptr())
 
 
 def _write_coarse(eng, km: KMeansBatch, c0: np.ndarray, mbase: np.ndarray) -> None:
-    led, dev = eng.led, eng.device
-    call("mpa_km_write_level", km.struct(), None, ptr(led.vc64),
-         ptr(torch.as_tensor(c0, dtype=torch.int32, device=dev)), ptr(torch.as_tensor(mbase, dtype=torch.int32, device=dev)),
+    led = eng.led
+    c0_d, mb_d = _i32(eng, c0), _i32(eng, mbase)
+    call("mpa_km_write_level", km.struct(), None, ptr(led.vc64), ptr(c0_d), ptr(mb_d),
          ptr(led.ckc64), ptr(led.cvc64), ptr(led.ckc), ptr(led.cvc), dtype_code(led.dtype), ptr(led.csize),
          ptr(led.coff), ptr(led.child), led.ccap, led.kcap, stream_ptr())
 
@@ -255,8 +260,8 @@ def online_update(eng, seqs, cursor: int) -> dict:
     km = KMeansBatch(eng.device, eng.d, probs, torch.cat(inits), pts=eng.k_raw, tcap=eng.tcap,
                      min_iters=cfg.refine_kmeans_iters, count_init=torch.cat(counts))
     dist = torch.empty(len(probs), L, km.k_max, dtype=torch.float64, device=eng.device)
-    call("mpa_km_seq_assign", km.struct(), ptr(torch.as_tensor(tails, dtype=torch.int32, device=eng.device)), L,
-         ptr(dist), stream_ptr())
+    tails_d = _i32(eng, tails)
+    call("mpa_km_seq_assign", km.struct(), ptr(tails_d), L, ptr(dist), stream_ptr())
     rounds = km.lloyd()
     nk = km.nonempty()
     f0 = np.zeros(len(probs), np.int64)
@@ -302,9 +307,9 @@ def _split(eng, ledgers, settle: bool = True) -> int:
         dev = eng.device
         km = KMeansBatch(dev, eng.d, probs, torch.zeros(sum(p[3] for p in probs), eng.d, dtype=torch.float64,
                                                          device=dev), pts=eng.k_raw, tcap=eng.tcap)
-        call("mpa_km_assign_from_level", km.struct(), ptr(led.off), ptr(led.mem), led.kcap, led.tcap,
-             ptr(torch.as_tensor(firsts, dtype=torch.int32, device=dev)),
-             ptr(torch.as_tensor(ncl, dtype=torch.int32, device=dev)), None, stream_ptr())
+        firsts_d, ncl_d = _i32(eng, firsts), _i32(eng, ncl)
+        call("mpa_km_assign_from_level", km.struct(), ptr(led.off), ptr(led.mem), led.kcap, led.tcap, ptr(firsts_d),
+             ptr(ncl_d), None, stream_ptr())
         km.means()
         if settle:
             # (2) settle each side from its non-empty side means (clustering.py:384-394)
