@@ -1,0 +1,441 @@
+"""Benchmark of the Multipole Attention decode path on B200 (BASELINE.json metric:
+"decode attention us/step & speedup vs dense at 32K ctx; HBM GB/s vs peak").
+
+Workload (configs[1]): Qwen3-8B attention shape -- 32 q-heads, 8 kv-heads (GQA x4), head_dim 128,
+32K context, 1-level clustering (r = 16 -> ~2040 centroids / head), token budget B = 512,
+rope theta 1e6, bf16 KV cache, batch 16 sequences per GPU.  Synthetic N(0,1) Q/K/V (random-init
+model shape, torch seed 0 + rank).  The ledger is built by the GPU clustering path.
+
+A step = one decode step of one attention layer for the whole batch: q rotation, centroid
+lookup + budgeted selection, fused sparse-exact + centroid-replacement attention with the
+split-KV merge, and the KV append of the step's token.  L2 is flushed (256 MB write) before
+every timed step; each step is timed with CUDA events on the engine stream.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+N > 1 (torchrun): every rank runs its own batch (replicas, batch-sharded: no collective on
+the data path), barrier + max over ranks.  `--impl reference` times the CPU oracle (the
+reference algorithm restated in numpy; the reference package is pure Python) on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "decode attention µs/step & speedup vs dense at 32K ctx; HBM GB/s vs peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--ctx", type=int, default=32768)
+    ap.add_argument("--budget", type=int, default=512)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline leg")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no CPU leg, no clocks)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def workload_cfg(args):
+    from paper_2506_13059_b200.core import EngineConfig, HeadLayout
+
+    lay = HeadLayout(32, 8, 128)
+    cfg = EngineConfig(token_budget=args.budget, tokens_per_centroid=16, rope_theta=1e6, seed=0)
+    return lay, cfg
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.fh.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        loaded = [x for x in sm if x > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------- CPU oracle leg
+
+
+def cpu_oracle_time(lay, cfg, keys, values, queries, ledger_o, cache_len, n_steps=3):
+    """Seconds per decode step of ONE ledger (1 sequence x 1 kv-head, its G q-heads) and of one
+    dense-oracle step of the same ledger, timed with the numpy oracle on the host cores."""
+    from oracle import mpa_oracle as O
+    from paper_2506_13059_b200.core import HeadLayout
+
+    one = HeadLayout(lay.group_size, 1, lay.head_dim)
+    t0 = time.perf_counter()
+    for t in range(n_steps):
+        O.decode_step(queries[t], [ledger_o], [keys], [values], cache_len, t, cfg, one)
+    sparse = (time.perf_counter() - t0) / n_steps
+    t0 = time.perf_counter()
+    pos = np.arange(cache_len)
+    for g in range(lay.group_size):
+        O.dense_attention(queries[0][g], cache_len, keys[:cache_len], values[:cache_len], pos, lay.head_dim,
+                          cfg.rope_theta)
+    dense = time.perf_counter() - t0
+    return sparse, dense
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the reference algorithm on the CPU (oracle port) on rank 0."""
+    if rank != 0:
+        return
+    import torch
+
+    from oracle import mpa_oracle as O
+
+    lay, cfg = workload_cfg(args)
+    gen = torch.Generator().manual_seed(0)
+    ctx = args.ctx
+    keys = torch.randn(ctx, lay.head_dim, generator=gen).numpy()
+    values = torch.randn(ctx, lay.head_dim, generator=gen).numpy()
+    qs = torch.randn(args.steps + args.warmup, lay.group_size, lay.head_dim, generator=gen).numpy()
+    t0 = time.perf_counter()
+    led = O.prefill_ledger(keys, values, ctx, cfg, 0)
+    prefill_s = time.perf_counter() - t0
+    n_led = args.batch * lay.num_kv_heads
+    samples = []
+    for t in range(max(1, min(3, args.warmup))):
+        O.decode_step(qs[t], [led], [keys], [values], ctx, t, cfg, HeadLayout1(lay))
+    for t in range(args.steps):
+        t1 = time.perf_counter()
+        O.decode_step(qs[(args.warmup + t) % len(qs)], [led], [keys], [values], ctx, t, cfg, HeadLayout1(lay))
+        samples.append(time.perf_counter() - t1)
+        if sum(samples) > 60:
+            break
+    per_ledger = float(np.mean(samples))
+    us = per_ledger * n_led * 1e6
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": us, "unit": "us/step", "n_gpus": world,
+        "steps": len(samples), "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1) Q/K/V",
+        "config": {"workload": "C2 Qwen3-8B attention shape (32q/8kv/d128), 32K ctx, r=16, B=512, "
+                               f"batch {args.batch}", "batch": args.batch, "ctx": ctx},
+        "cpu_baseline": {"value": us, "unit": "us/step", "cores": cores, "kind": "port",
+                         "sample": f"{len(samples)} decode steps of 1 sequence x 1 kv-head (4 q-heads), "
+                                   f"oracle ledger built on CPU in {prefill_s:.1f}s; scaled x{n_led} ledgers "
+                                   "(the reference loops heads/sequences serially)"},
+        "e2e": {"value": us, "unit": "us/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def HeadLayout1(lay):
+    from paper_2506_13059_b200.core import HeadLayout
+
+    return HeadLayout(lay.group_size, 1, lay.head_dim)
+
+
+# ---------------------------------------------------------------------------- GPU arm
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if world > 1 and rank != 0:
+            return
+        reference_arm(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    from paper_2506_13059_b200 import clustering
+    from paper_2506_13059_b200._lib import lib as _load_lib
+    from paper_2506_13059_b200.engine import DecodeEngine
+    from paper_2506_13059_b200.roofline import decode_bytes, dense_bytes
+
+    _load_lib()
+    lay, cfg = workload_cfg(args)
+    b, ctx, d, G = args.batch, args.ctx, lay.head_dim, lay.group_size
+    W, K = max(3, args.warmup), args.steps
+    total_steps = W + K
+    dev = torch.device("cuda", local)
+    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+    tcap = ctx + 2 * total_steps + 3 * cfg.local_buffer + 8
+    eng = DecodeEngine(cfg, lay, b, tcap=tcap, dtype=torch.bfloat16, device=dev)
+    for s in range(b):  # prompt KV, one sequence at a time to bound temporaries
+        k = torch.randn(1, lay.num_kv_heads, ctx, d, generator=gen, device=dev)
+        v = torch.randn(1, lay.num_kv_heads, ctx, d, generator=gen, device=dev)
+        _write_seq(eng, s, k, v)
+        del k, v
+    eng.cache_len[:] = ctx
+    eng._sync_scalars()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    eng.prefill()
+    torch.cuda.synchronize()
+    prefill_s = time.perf_counter() - t0
+
+    Q = torch.randn(total_steps + K, b, lay.num_q_heads, d, generator=gen, device=dev)
+    KN = torch.randn(total_steps + K, b, lay.num_kv_heads, d, generator=gen, device=dev)
+    VN = torch.randn(total_steps + K, b, lay.num_kv_heads, d, generator=gen, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, n, *, start=0):
+        evs = []
+        for i in range(n):
+            flush.fill_(float(i))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn(start + i)
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        return [a.elapsed_time(c) for a, c in evs]  # ms
+
+    # ---- warmup + timed multipole steps (attend + append)
+    for i in range(W):
+        eng.step(Q[i], KN[i], VN[i])
+    torch.cuda.synchronize()
+    barrier()
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        step_ms = timed(lambda i: eng.step(Q[i], KN[i], VN[i]), K, start=W)
+        torch.cuda.synchronize()
+        barrier()
+    stats = eng.head_stats()
+    scored = eng.led.n_fine.copy()
+    ms_step = float(np.mean(step_ms))
+
+    # ---- fused kernel alone (dominant kernel) for the roofline
+    eng.rotate(Q[0])
+    eng.lookup()
+    torch.cuda.synchronize()
+    fstats = eng.head_stats()
+    fused_ms = timed(lambda i: eng.fused(), K)
+    lookup_ms = timed(lambda i: (eng.rotate(Q[0]), eng.lookup()), K)
+    nbytes = decode_bytes(fstats, eng.led.n_fine, d, G, 2)
+    fused_avg = float(np.mean(fused_ms))
+
+    # ---- dense decode comparator (same cache, same kernel family, tok == NULL)
+    for i in range(3):
+        eng.attend_dense(Q[i])
+    dense_ms = timed(lambda i: eng.attend_dense(Q[i]), K)
+    dense_avg = float(np.mean(dense_ms))
+    dbytes = dense_bytes(np.repeat(eng.cache_len, lay.num_kv_heads), d, G, 2)
+    fi_ms = flashinfer_dense(eng, Q[0], K, timed)
+
+    # ---- end to end through the public API from pinned host buffers
+    qh = Q[total_steps:total_steps + K].cpu().pin_memory()
+    kh = KN[total_steps:total_steps + K].cpu().pin_memory()
+    vh = VN[total_steps:total_steps + K].cpu().pin_memory()
+    oh = torch.empty(b, lay.num_q_heads, d, dtype=torch.float32).pin_memory()
+    e2e_ms = timed(lambda i: eng.step_host(qh[i], kh[i], vh[i], oh), K)
+    _ = oh.sum().item()
+    e2e_avg = float(np.mean(e2e_ms))
+    h2d = (qh[0].numel() + kh[0].numel() + vh[0].numel()) * 4
+    d2h = oh.numel() * 4
+
+    # ---- one online cluster update event (C4-style overhead, amortised over L steps)
+    L = cfg.local_buffer
+    need = int(2 * L - (eng.cache_len[0] - eng.buffer_start[0]))
+    if need > 0:
+        eng.write_tokens(torch.randn(b, lay.num_kv_heads, need, d, generator=gen, device=dev),
+                         torch.randn(b, lay.num_kv_heads, need, d, generator=gen, device=dev))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    upd = clustering.online_update(eng, list(range(b)), eng.cursor)
+    torch.cuda.synchronize()
+    update_ms = (time.perf_counter() - t0) * 1e3
+
+    # ---- max over ranks
+    vals = torch.tensor([ms_step, e2e_avg, fused_avg, dense_avg], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms_step, e2e_avg, fused_avg, dense_avg = (float(x) for x in vals.cpu())
+
+    if rank == 0:
+        hbm, peak_kind = peaks()
+        achieved = nbytes["fused"] / (fused_avg * 1e-3) / 1e9
+        traffic = load_traffic()
+        line = {
+            "metric": METRIC,
+            "value": ms_step * 1e3,
+            "unit": "us/step",
+            "n_gpus": world,
+            "steps": K,
+            "warmup": W,
+            "ms_per_step": ms_step,
+            "higher_is_better": False,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic N(0,1) Q/K/V (random-init Qwen3-8B attention shape), seed 1000+rank",
+            "config": {"workload": "C2: Qwen3-8B attention shape 32q/8kv/d128, 32K ctx, 1-level r=16, "
+                                   f"B={args.budget}, bf16, batch {b}/GPU", "batch": b, "ctx": ctx,
+                       "budget": args.budget, "tokens_per_centroid": 16, "l2": "flushed (256 MB write) before "
+                                                                             "every timed step",
+                       "parallelism": f"batch-sharded replicas x{world}"},
+            "speedup_vs_dense": dense_avg / ms_step,
+            "dense_us_per_step": dense_avg * 1e3,
+            "dense_gbs": dbytes / (dense_avg * 1e-3) / 1e9,
+            "flashinfer_dense_us": (fi_ms * 1e3) if fi_ms else None,
+            "sequences_per_s": world * b / (ms_step * 1e-3),
+            "roofline": {"bound": "hbm", "kernel": "mpa_sparse_decode (decode_mma_kernel)",
+                         "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "peak_kind": peak_kind, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": nbytes["fused"], "launch_us": fused_avg * 1e3},
+            "step_roofline": {"bytes": nbytes["step"], "GBs": nbytes["step"] / (ms_step * 1e-3) / 1e9,
+                              "frac": nbytes["step"] / (ms_step * 1e-3) / 1e9 / hbm,
+                              "lookup_us": float(np.mean(lookup_ms)) * 1e3},
+            "selection": {"mean_exact_tokens": float(fstats[:, 0].mean()),
+                          "mean_rejected_centroids": float(fstats[:, 1].mean()),
+                          "mean_scored_centroids": float(np.mean(scored)),
+                          "memop_ratio": nbytes["step"] / dbytes},
+            "update": {"ms_per_event": update_ms, "amortized_us_per_step": update_ms * 1e3 / L,
+                       "pct_of_step": update_ms / L / ms_step * 100.0, "lloyd_rounds": upd["rounds"],
+                       "prefill_s": prefill_s},
+            "e2e": {"value": e2e_avg * 1e3, "unit": "us/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": 6 * K,
+            "clocks": clk.summary(),
+        }
+        if not args.no_cpu and not args.profile:
+            line["cpu_baseline"] = cpu_leg(eng, lay, cfg, Q, b)
+        print(json.dumps(line), flush=True)
+    barrier()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _write_seq(eng, s, k, v):
+    """Write one sequence's prompt K/V (fp32 [1, Hkv, n, d]) into its ledger rows at position 0."""
+    import torch
+
+    from paper_2506_13059_b200._lib import MpaCache, call, dtype_code, ptr, stream_ptr
+
+    Hkv = eng.Hkv
+    n = k.shape[2]
+    sub = MpaCache(ptr(eng.k_rot[s * Hkv]), ptr(eng.k_raw[s * Hkv]), ptr(eng.v[s * Hkv]), dtype_code(eng.dtype), Hkv,
+                   eng.tcap, eng.d)
+    pos0 = torch.zeros(Hkv, dtype=torch.int32, device=eng.device)
+    kk = k.reshape(Hkv, n, eng.d).contiguous()
+    vv = v.reshape(Hkv, n, eng.d).contiguous()
+    call("mpa_kv_write", sub, ptr(kk), ptr(vv), ptr(pos0), n, ptr(eng.inv_freq), stream_ptr())
+    torch.cuda.synchronize()
+
+
+def flashinfer_dense(eng, q, K, timed):
+    """Cross-check of the dense comparator with flashinfer's decode (pre-rotated K), if usable."""
+    try:
+        import flashinfer  # noqa: F401
+        import torch
+
+        kc = eng.k_rot[:eng.Hkv, : int(eng.cache_len[0])].transpose(0, 1).contiguous()
+        vc = eng.v[:eng.Hkv, : int(eng.cache_len[0])].transpose(0, 1).contiguous()
+        qq = eng.q_rot[0].to(torch.bfloat16) * math.sqrt(eng.d)
+        flashinfer.single_decode_with_kv_cache(qq, kc, vc, kv_layout="NHD")
+        ms = timed(lambda i: flashinfer.single_decode_with_kv_cache(qq, kc, vc, kv_layout="NHD"), K)
+        return float(np.mean(ms)) * eng.n_seq  # batch = n_seq independent sequences
+    except Exception:
+        return None
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "fused_traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_leg(eng, lay, cfg, Q, b):
+    """cpu_baseline: the numpy oracle on one ledger (sequence 0, kv-head 0) with the GPU-built
+    ledger (bit-identical to the oracle's, tests/test_gpu_clustering.py), scaled to the batch."""
+    from tests.bridge import to_oracle
+
+    n = int(eng.cache_len[0])
+    h = eng.export_ledger(0)
+    led = to_oracle(h)
+    keys = eng.k_raw[0, :n].float().cpu().numpy()
+    vals = eng.v[0, :n].float().cpu().numpy()
+    qs = [Q[i, 0, :lay.group_size].cpu().numpy() for i in range(3)]
+    led.total = n
+    sparse_s, dense_s = cpu_oracle_time(lay, cfg, keys, vals, qs, led, n)
+    n_led = b * lay.num_kv_heads
+    return {"value": sparse_s * n_led * 1e6, "unit": "us/step", "cores": os.cpu_count(), "kind": "port",
+            "sample": "3 oracle decode steps of 1 sequence x 1 kv-head (4 q-heads) at the bench config, scaled "
+                      f"x{n_led} ledgers; dense oracle of the same ledger {dense_s * n_led * 1e6:.0f} us/step"}
+
+
+if __name__ == "__main__":
+    main()

@@ -260,6 +260,17 @@ class DecodeEngine:
         self.cursor += 1
         return out
 
+    def step_host(self, q_host: torch.Tensor, k_host: torch.Tensor, v_host: torch.Tensor,
+                  out_host: torch.Tensor) -> torch.Tensor:
+        """Public end-to-end step from HOST buffers (pinned for overlap): copies q / k / v in,
+        runs `step`, copies the output back into out_host; all on the current stream."""
+        q = q_host.to(self.device, non_blocking=True)
+        k = k_host.to(self.device, non_blocking=True)
+        v = v_host.to(self.device, non_blocking=True)
+        out = self.step(q, k, v)
+        out_host.copy_(out, non_blocking=True)
+        return out_host
+
     def export_ledger(self, l: int) -> HostLedger:
         s = l // self.Hkv
         return self.led.export(l, int(self.sink_end[s]), int(self.buffer_start[s]), int(self.cache_len[s]),
