@@ -76,10 +76,11 @@ int mpa_rotate_queries(const float* q, int n_seq, int n_qh, int d, const int32_t
 
 /* K9 -- centroid lookup logits, fp64: logits[l, g, i] = q_lk[seq, h*G+g] . kc[l, id_i] / sqrt(d)
  * for candidates i < n_cand[l]; id_i = cand[l, i] (cand may be NULL: id_i = i, n = lv->count)
- * (attention.py:267-276 `_scores_per_group` logits). */
+ * (attention.py:267-276 `_scores_per_group` logits).  chunk_stats (optional, d in {64,128}):
+ * [L, ceil(cap/64), G, 2] per-64-candidate (max_g, sum N e^(l - max_g)) partials of the normaliser. */
 int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group, int d,
                         const mpa_level* lv, const int32_t* cand, const int32_t* n_cand,
-                        int cand_cap, double* logits, void* stream);
+                        int cand_cap, double* logits, double* chunk_stats, void* stream);
 
 /* K10 -- Eq. 1 scores and budgeted greedy selection (attention.py:192-207, 267-290).
  * Scores: e_g,i = exp(l_g,i - max_g), Z_g = sum over candidates AND live extras of N * e,
@@ -93,7 +94,7 @@ int mpa_select(const double* logits, int group, const int32_t* cand, const int32
                const double* elogits, const int32_t* esize, const uint8_t* eflag,
                const int32_t* n_extra, int ecap,
                const int64_t* budget, int n_ledgers, uint8_t* flag, int32_t* sel_tokens,
-               void* stream);
+               const double* chunk_stats, void* stream);
 
 /* Hierarchy stage glue (attention.py:321-329): cand[l] = children of coarse clusters with
  * cflag == 1, promoted in coarse-id order, children ascending; n_cand[l]. */
@@ -117,6 +118,16 @@ int mpa_build_worklist(const mpa_level* fine, const mpa_level* coarse, int group
                        int n_kv_heads, int n_ledgers, int replacement,
                        int32_t* tok, int tok_cap, int32_t* rej, float* rej_w, int rej_cap,
                        int32_t* stats, void* stream);
+
+/* K10 + work list fused in one launch per ledger: mpa_select over the fine candidates (extras =
+ * coarse clusters with cflag == 0, hierarchy only) followed by mpa_build_worklist. */
+int mpa_select_worklist(const mpa_level* fine, const mpa_level* coarse, int group, const double* logits,
+                        const int32_t* cand, const int32_t* n_cand, int cand_cap, const double* chunk_stats,
+                        const uint8_t* cflag, const double* clogits, const int64_t* budget,
+                        const int32_t* sink_end, const int32_t* buffer_start, const int32_t* cache_len,
+                        int n_kv_heads, int n_ledgers, int replacement, uint8_t* flag,
+                        int32_t* sel_tokens, int32_t* tok, int tok_cap, int32_t* rej, float* rej_w,
+                        int rej_cap, int32_t* stats, void* stream);
 
 /* K11 + K12 -- fused sparse decode: one online softmax over the exact tokens (K_rot/V gathered
  * by index, logits q_rot . k) and the rejected-centroid pseudo-tokens (logit + ln N, value

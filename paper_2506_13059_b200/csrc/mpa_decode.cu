@@ -23,6 +23,7 @@
 //     rounding left is the KV cache itself.  Base-2 online softmax.
 //   * decode_ffma_kernel (any dtype, any even d): warp per item, FFMA, natural-log softmax,
 //     fp32 accurate expf -- the fp32 parity mode (1e-5).
+#include <climits>
 #include <cstdlib>
 
 #include "mpa_common.cuh"
@@ -212,6 +213,9 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 __device__ __forceinline__ void cp_async16(unsigned dst, const void* src, int bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
 }
+__device__ __forceinline__ void cp_async4(unsigned dst, const void* src, int bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N> __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
@@ -322,13 +326,25 @@ decode_mma_kernel(const __nv_bfloat16* __restrict__ k_rot, const __nv_bfloat16* 
 
     const size_t cache_base = (size_t)l * tcap;
     // Issue the loads of virtual tile vt (owned by this warp) into stage st.
-    auto issue = [&](int vt, int st) {
-        const unsigned kst = wbase_s + st * 2 * Geo::kMatBytes, vst = kst + Geo::kMatBytes;
-        const int row = lane >> 1;  // 2 lanes per row
+    // Row id of this lane's row (lane >> 1) in virtual tile vt: token id, or centroid code.
+    // Fetched one tile AHEAD of its cp.async issue so the dependent index load never sits
+    // on the critical path.
+    constexpr int kNoRow = INT_MIN;
+    auto fetch = [&](int vt) -> int {
+        const int row = lane >> 1;
         if (vt < ntt) {
             const int t = R.t0 + vt * 16 + row;
-            const bool ok = t < R.t1;
-            const int tokid = ok ? (tok ? __ldg(tok + (size_t)l * tok_cap + t) : t) : 0;
+            return t < R.t1 ? (tok ? __ldg(tok + (size_t)l * tok_cap + t) : t) : kNoRow;
+        }
+        const int r = R.r0 + (vt - ntt) * 16 + row;
+        return r < R.r1 ? __ldg(rej + (size_t)l * rej_cap + r) : kNoRow;
+    };
+    auto issue = [&](int vt, int st, int id) {
+        const unsigned kst = wbase_s + st * 2 * Geo::kMatBytes, vst = kst + Geo::kMatBytes;
+        const int row = lane >> 1;  // 2 lanes per row
+        const bool ok = id != kNoRow;
+        if (vt < ntt) {
+            const int tokid = ok ? id : 0;
             const __nv_bfloat16* kp = k_rot + (cache_base + tokid) * D;
             const __nv_bfloat16* vp = vcache + (cache_base + tokid) * D;
 #pragma unroll
@@ -338,9 +354,7 @@ decode_mma_kernel(const __nv_bfloat16* __restrict__ k_rot, const __nv_bfloat16* 
                 cp_async16(vst + Geo::off(row, ch), vp + ch * 8, ok ? 16 : 0);
             }
         } else {
-            const int r = R.r0 + (vt - ntt) * 16 + row;
-            const bool ok = r < R.r1;
-            const int code = ok ? __ldg(rej + (size_t)l * rej_cap + r) : 0;
+            const int code = ok ? id : 0;
             const __nv_bfloat16* vp =
                 code >= 0 ? fvc + ((size_t)l * fcap + code) * D : cvc + ((size_t)l * ccap + (-1 - code)) * D;
 #pragma unroll
@@ -348,20 +362,33 @@ decode_mma_kernel(const __nv_bfloat16* __restrict__ k_rot, const __nv_bfloat16* 
                 const int ch = (lane & 1) * (Geo::kChunks / 2) + j;
                 cp_async16(vst + Geo::off(row, ch), vp + ch * 8, ok ? 16 : 0);
             }
+            // the tile's reused lookup logits (16 x G fp32) ride along in the unused K slot
+            const int r0 = R.r0 + (vt - ntt) * 16;
+            for (int e = lane; e < 16 * G; e += 32) {
+                const int rr = e / G;
+                const bool okr = r0 + rr < R.r1;
+                cp_async4(kst + e * 4, rej_w + ((size_t)l * rej_cap + (okr ? r0 + rr : 0)) * G + (e - rr * G),
+                          okr ? 4 : 0);
+            }
         }
     };
 
     // this warp's tiles: vt = w, w + W, ...
     const int my_n = NT > w ? (NT - w + kMmaWarps - 1) / kMmaWarps : 0;
+    int pf = 0;
 #pragma unroll
     for (int i = 0; i < NST - 1; ++i) {
-        if (i < my_n) issue(w + i * kMmaWarps, i);
+        if (i < my_n) issue(w + i * kMmaWarps, i, fetch(w + i * kMmaWarps));
         cp_commit();
     }
+    if (NST - 1 < my_n) pf = fetch(w + (NST - 1) * kMmaWarps);
     for (int i = 0; i < my_n; ++i) {
         {
             const int nxt = i + NST - 1;
-            if (nxt < my_n) issue(w + nxt * kMmaWarps, nxt % NST);
+            if (nxt < my_n) {
+                issue(w + nxt * kMmaWarps, nxt % NST, pf);
+                if (nxt + 1 < my_n) pf = fetch(w + (nxt + 1) * kMmaWarps);
+            }
             cp_commit();
         }
         cp_wait<NST - 1>();
@@ -394,12 +421,12 @@ decode_mma_kernel(const __nv_bfloat16* __restrict__ k_rot, const __nv_bfloat16* 
             if (base + gr + 8 >= R.t1) x[2] = x[3] = -INFINITY;
         } else {
             const int base = R.r0 + ((vt - ntt) << 4);
+            const float* lg = reinterpret_cast<const float*>(wbase + (size_t)st * 2 * Geo::kMatBytes);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const int r = base + gr + (j >> 1) * 8;
+                const int rr = gr + (j >> 1) * 8;
                 const int h = (j & 1) ? hB : hA;
-                x[j] = r < R.r1 ? (h < G ? __ldg(rej_w + ((size_t)l * rej_cap + r) * G + h) * kLog2e : 0.f)
-                                : -INFINITY;
+                x[j] = base + rr < R.r1 ? (h < G ? lg[rr * G + h] * kLog2e : 0.f) : -INFINITY;
             }
         }
         // padded heads (>= G) must stay finite
@@ -556,7 +583,7 @@ int launch_mma(const mpa_cache* c, const float* q_rot, const int32_t* tok, const
                const int32_t* rej, const float* rej_w, const int32_t* n_rej, int rej_cap, const void* fvc, int fcap,
                const void* cvc, int ccap, int S, float* pml, float* pacc, int32_t* ticket, float* out,
                cudaStream_t st) {
-    constexpr int NST = 4;
+    constexpr int NST = 3;
     dim3 grid(S, c->n_ledgers);
     const size_t stage_bytes = (size_t)kMmaWarps * NST * 2 * TileGeom<D>::kMatBytes;
     const size_t red_bytes = sizeof(float) * kMmaWarps * 8 * (2 + D);

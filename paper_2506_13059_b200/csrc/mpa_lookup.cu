@@ -13,6 +13,8 @@
 // selected set matches the oracle except at true ties (|score gap| ~ 1e-16 relative).
 // Selection is a size-weighted radix select on the 96-bit key (~score_bits, cluster id):
 // it finds the crossing cluster without sorting, O(passes * n / threads).
+#include <cstdlib>
+
 #include "mpa_common.cuh"
 
 namespace mpa {
@@ -51,6 +53,111 @@ centroid_logits_kernel(const double* __restrict__ q_lk, int n_kv_heads, int d, c
     for (int g = 0; g < G; ++g) out[(size_t)g * cand_cap] = acc[g] / sq;
 }
 
+// Tiled variant for d in {64, 128}: a CTA stages kChunk centroid rows of the ledger with
+// coalesced 16-byte loads into padded smem, then TPC threads cooperate on one centroid (each
+// holds its slice of the G q_lookup rows in registers, fp64 FMA), reduce with shuffles, and
+// the CTA emits the chunk's per-head (max, sum N e^(l - max)) partials so the selection kernel
+// never re-reads all logits to build the Eq. 1 normaliser.
+constexpr int kChunk = 64;
+constexpr int kTiledThreads = 256;
+
+template <typename T, int G, int D>
+__global__ void __launch_bounds__(kTiledThreads)
+centroid_logits_tiled(const double* __restrict__ q_lk, const T* __restrict__ kc, int kcap,
+                      const int32_t* __restrict__ count, const int32_t* __restrict__ lv_size,
+                      const int32_t* __restrict__ cand, const int32_t* __restrict__ n_cand, int cand_cap,
+                      double* __restrict__ logits, double* __restrict__ cstats, int n_chunks) {
+    constexpr int EPC = 16 / (int)sizeof(T);              // elements per 16-byte chunk
+    constexpr int CPR = D / EPC;                          // chunks per row
+    constexpr int TPC0 = G <= 4 ? 8 : 16;
+    constexpr int TPC = TPC0 < CPR ? TPC0 : CPR;          // threads per centroid
+    constexpr int CPT = CPR / TPC;                        // chunks per thread
+    constexpr int ROWB = D * (int)sizeof(T) + 16;         // padded row bytes
+    constexpr int CPP = kTiledThreads / TPC;              // centroids per pass
+    static_assert(CPT >= 1 && CPR % TPC == 0, "tile shape");
+    extern __shared__ __align__(16) unsigned char sm[];
+    double* qs = reinterpret_cast<double*>(sm);                       // [G][D]
+    double* lgs = qs + G * D;                                          // [G][kChunk]
+    unsigned char* tile = reinterpret_cast<unsigned char*>(lgs + G * kChunk);
+    const int l = blockIdx.y, chunk = blockIdx.x;
+    const int n = cand ? n_cand[l] : count[l];
+    const int i0 = chunk * kChunk;
+    if (i0 >= n) {
+        if (cstats && threadIdx.x < G) {
+            cstats[(((size_t)l * n_chunks + chunk) * G + threadIdx.x) * 2] = -INFINITY;
+            cstats[(((size_t)l * n_chunks + chunk) * G + threadIdx.x) * 2 + 1] = 0.0;
+        }
+        return;
+    }
+    const int nv = min(kChunk, n - i0);
+    for (int j = threadIdx.x; j < G * D; j += blockDim.x) qs[j] = q_lk[(size_t)l * G * D + j];
+    for (int j = threadIdx.x; j < kChunk * CPR; j += blockDim.x) {
+        const int r = j / CPR, c = j - r * CPR;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (r < nv) {
+            const int row = cand ? __ldg(cand + (size_t)l * cand_cap + i0 + r) : i0 + r;
+            v = __ldg(reinterpret_cast<const uint4*>(kc + ((size_t)l * kcap + row) * D) + c);
+        }
+        *reinterpret_cast<uint4*>(tile + r * ROWB + c * 16) = v;
+    }
+    __syncthreads();
+    const int sub = threadIdx.x % TPC, cl = threadIdx.x / TPC;
+    double qr[G][CPT * EPC];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int c = 0; c < CPT; ++c)
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) qr[g][c * EPC + e] = qs[g * D + (sub + c * TPC) * EPC + e];
+    const double sq = sqrt((double)D);
+    for (int r = cl; r < kChunk; r += CPP) {
+        double acc[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) acc[g] = 0.0;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+            const uint4 raw = *reinterpret_cast<const uint4*>(tile + r * ROWB + (sub + c * TPC) * 16);
+            const T* x = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) {
+                const double xv = elem<T>::to_d(x[e]);
+#pragma unroll
+                for (int g = 0; g < G; ++g) acc[g] = fma(qr[g][c * EPC + e], xv, acc[g]);
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+            for (int o = 1; o < TPC; o <<= 1) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], o);
+        if (sub == 0 && r < nv) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const double v = acc[g] / sq;
+                lgs[g * kChunk + r] = v;
+                logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
+            }
+        }
+    }
+    if (!cstats) return;
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (w < G) {
+        double m = -INFINITY;
+        for (int r = lane; r < nv; r += 32) m = fmax(m, lgs[w * kChunk + r]);
+        m = warp_max(m);
+        double z = 0.0;
+        for (int r = lane; r < nv; r += 32) {
+            const int id = cand ? cand[(size_t)l * cand_cap + i0 + r] : i0 + r;
+            z += (double)lv_size[(size_t)l * kcap + id] * exp(lgs[w * kChunk + r] - m);
+        }
+        z = warp_sum(z);
+        if (lane == 0) {
+            cstats[(((size_t)l * n_chunks + chunk) * G + w) * 2] = m;
+            cstats[(((size_t)l * n_chunks + chunk) * G + w) * 2 + 1] = z;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K10 selection. One CTA per ledger.
 
@@ -60,14 +167,13 @@ __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : 
 __device__ __forceinline__ double dsum(double a, double b) { return a + b; }
 
 template <int G>
-__global__ void __launch_bounds__(kSelThreads)
-select_kernel(const double* __restrict__ logits, const int32_t* __restrict__ cand, const int32_t* __restrict__ n_cand,
-              int cand_cap, const int32_t* __restrict__ lv_size, int lv_cap, const double* __restrict__ elogits,
-              const int32_t* __restrict__ esize, const uint8_t* __restrict__ eflag, const int32_t* __restrict__ n_extra,
-              int ecap, const int64_t* __restrict__ budget, uint8_t* __restrict__ flag,
-              int32_t* __restrict__ sel_tokens) {
-    extern __shared__ unsigned char smem_raw[];
-    const int l = blockIdx.x;
+__device__ void select_core(const int l, const double* __restrict__ logits, const int32_t* __restrict__ cand,
+                            const int32_t* __restrict__ n_cand, int cand_cap, const int32_t* __restrict__ lv_size,
+                            int lv_cap, const double* __restrict__ elogits, const int32_t* __restrict__ esize,
+                            const uint8_t* __restrict__ eflag, const int32_t* __restrict__ n_extra, int ecap,
+                            const int64_t* __restrict__ budget, uint8_t* __restrict__ flag,
+                            int32_t* __restrict__ sel_tokens, const double* __restrict__ cstats, int n_chunks,
+                            unsigned char* smem_raw) {
     const int n = n_cand[l];
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem_raw);  // [cand_cap]
     int* sizes = reinterpret_cast<int*>(keys + cand_cap);                         // [cand_cap]
@@ -92,10 +198,14 @@ select_kernel(const double* __restrict__ logits, const int32_t* __restrict__ can
 
     // per-head max and size-weighted normaliser over candidates + live extras
     double mx[G], z[G];
+    const double* cs = cstats ? cstats + (size_t)l * n_chunks * G * 2 : nullptr;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         double m = -INFINITY;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) m = dmax(m, lg[(size_t)g * cand_cap + i]);
+        if (cs)
+            for (int c = threadIdx.x; c < n_chunks; c += blockDim.x) m = dmax(m, cs[(c * G + g) * 2]);
+        else
+            for (int i = threadIdx.x; i < n; i += blockDim.x) m = dmax(m, lg[(size_t)g * cand_cap + i]);
         for (int j = threadIdx.x; j < ne; j += blockDim.x)
             if (!eflag[(size_t)l * ecap + j]) m = dmax(m, elg[(size_t)g * ecap + j]);
         mx[g] = block_reduce(m, red, dmax);
@@ -103,8 +213,15 @@ select_kernel(const double* __restrict__ logits, const int32_t* __restrict__ can
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         double s = 0.0;
-        for (int i = threadIdx.x; i < n; i += blockDim.x)
-            s += (double)sizes[i] * exp(lg[(size_t)g * cand_cap + i] - mx[g]);
+        if (cs) {
+            for (int c = threadIdx.x; c < n_chunks; c += blockDim.x) {
+                const double cm = cs[(c * G + g) * 2];
+                if (cm != -INFINITY) s += cs[(c * G + g) * 2 + 1] * exp(cm - mx[g]);
+            }
+        } else {
+            for (int i = threadIdx.x; i < n; i += blockDim.x)
+                s += (double)sizes[i] * exp(lg[(size_t)g * cand_cap + i] - mx[g]);
+        }
         for (int j = threadIdx.x; j < ne; j += blockDim.x)
             if (!eflag[(size_t)l * ecap + j])
                 s += (double)esize[(size_t)l * ecap + j] * exp(elg[(size_t)g * ecap + j] - mx[g]);
@@ -225,6 +342,18 @@ select_kernel(const double* __restrict__ logits, const int32_t* __restrict__ can
     if (threadIdx.x == 0 && sel_tokens) sel_tokens[l] = (int32_t)tok;
 }
 
+template <int G>
+__global__ void __launch_bounds__(kSelThreads)
+select_kernel(const double* __restrict__ logits, const int32_t* __restrict__ cand, const int32_t* __restrict__ n_cand,
+              int cand_cap, const int32_t* __restrict__ lv_size, int lv_cap, const double* __restrict__ elogits,
+              const int32_t* __restrict__ esize, const uint8_t* __restrict__ eflag, const int32_t* __restrict__ n_extra,
+              int ecap, const int64_t* __restrict__ budget, uint8_t* __restrict__ flag,
+              int32_t* __restrict__ sel_tokens, const double* __restrict__ cstats, int n_chunks) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    select_core<G>(blockIdx.x, logits, cand, n_cand, cand_cap, lv_size, lv_cap, elogits, esize, eflag, n_extra, ecap,
+                   budget, flag, sel_tokens, cstats, n_chunks, smem_raw);
+}
+
 // ---------------------------------------------------------------------------
 
 constexpr int kListThreads = 1024;
@@ -251,8 +380,7 @@ hier_candidates_kernel(const int32_t* __restrict__ ccount, const int32_t* __rest
 }
 
 template <int G>
-__global__ void __launch_bounds__(kListThreads)
-build_worklist_kernel(const int32_t* __restrict__ fsize, const int32_t* __restrict__ fmem_off,
+__device__ void worklist_body(const int l, const int L, const int32_t* __restrict__ fsize, const int32_t* __restrict__ fmem_off,
                       const int32_t* __restrict__ fmem, int fcap, int fmem_cap, const int32_t* __restrict__ csize,
                       const int32_t* __restrict__ ccount, int ccap, const int32_t* __restrict__ cand,
                       const int32_t* __restrict__ n_cand, const int32_t* __restrict__ fcount, int cand_cap,
@@ -263,7 +391,6 @@ build_worklist_kernel(const int32_t* __restrict__ fsize, const int32_t* __restri
                       int32_t* __restrict__ tok, int tok_cap, int32_t* __restrict__ rej, float* __restrict__ rej_w,
                       int rej_cap, int32_t* __restrict__ stats) {
     __shared__ int scan[33];
-    const int l = blockIdx.x;
     const int seq = l / n_kv_heads;
     const int clen = cache_len[seq];
     const int ns = min(sink_end[seq], clen);
@@ -322,7 +449,6 @@ build_worklist_kernel(const int32_t* __restrict__ fsize, const int32_t* __restri
         }
     }
     if (threadIdx.x == 0) {
-        const int L = gridDim.x;
         stats[l] = min(tbase, tok_cap);
         stats[L + l] = min(rbase, rej_cap);
         stats[2 * L + l] = tbase - ns - nb;
@@ -330,22 +456,88 @@ build_worklist_kernel(const int32_t* __restrict__ fsize, const int32_t* __restri
     }
 }
 
+#define MPA_WORKLIST_PARAMS                                                                                      \
+    const int32_t *__restrict__ fsize, const int32_t *__restrict__ fmem_off, const int32_t *__restrict__ fmem,   \
+        int fcap, int fmem_cap, const int32_t *__restrict__ csize, const int32_t *__restrict__ ccount, int ccap, \
+        const int32_t *__restrict__ fcount, const uint8_t *__restrict__ cflag, const double *__restrict__ clogits, \
+        const int32_t *__restrict__ sink_end, const int32_t *__restrict__ buffer_start,                           \
+        const int32_t *__restrict__ cache_len, int n_kv_heads, int replacement, int32_t *__restrict__ tok,         \
+        int tok_cap, int32_t *__restrict__ rej, float *__restrict__ rej_w, int rej_cap, int32_t *__restrict__ stats
+#define MPA_WORKLIST_ARGS(cand, n_cand, cand_cap, flag, logits)                                                   \
+    fsize, fmem_off, fmem, fcap, fmem_cap, csize, ccount, ccap, cand, n_cand, fcount, cand_cap, flag, logits,     \
+        cflag, clogits, sink_end, buffer_start, cache_len, n_kv_heads, replacement, tok, tok_cap, rej, rej_w,     \
+        rej_cap, stats
+
+template <int G>
+__global__ void __launch_bounds__(kListThreads)
+build_worklist_kernel(const int32_t* __restrict__ cand, const int32_t* __restrict__ n_cand, int cand_cap,
+                      const uint8_t* __restrict__ flag, const double* __restrict__ logits, MPA_WORKLIST_PARAMS) {
+    worklist_body<G>(blockIdx.x, gridDim.x, MPA_WORKLIST_ARGS(cand, n_cand, cand_cap, flag, logits));
+}
+
+// K10 + work list in one launch per ledger (the flat path and the hierarchy's fine stage).
+template <int G>
+__global__ void __launch_bounds__(kSelThreads)
+select_worklist_kernel(const double* __restrict__ logits, const int32_t* __restrict__ cand,
+                       const int32_t* __restrict__ n_cand, int cand_cap, const int64_t* __restrict__ budget,
+                       uint8_t* __restrict__ flag, int32_t* __restrict__ sel_tokens,
+                       const double* __restrict__ cstats, int n_chunks, MPA_WORKLIST_PARAMS) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int l = blockIdx.x;
+    select_core<G>(l, logits, cand, n_cand ? n_cand : fcount, cand_cap, fsize, fcap, clogits, csize, cflag, ccount,
+                   ccap, budget, flag, sel_tokens, cstats, n_chunks, smem_raw);
+    __syncthreads();
+    worklist_body<G>(l, gridDim.x, MPA_WORKLIST_ARGS(cand, n_cand, cand_cap, flag, logits));
+}
+
 }  // namespace mpa
 
 using namespace mpa;
 
+static int g_logits_tiled = -1;
+
 extern "C" int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group, int d, const mpa_level* lv,
                                    const int32_t* cand, const int32_t* n_cand, int cand_cap, double* logits,
-                                   void* stream) {
+                                   double* chunk_stats, void* stream) {
     MPA_REQUIRE(q_lk && lv && logits && lv->kc && lv->count, MPA_ERR_ARG, "mpa_centroid_logits: null argument");
     MPA_REQUIRE(!cand || n_cand, MPA_ERR_ARG, "mpa_centroid_logits: cand without n_cand");
     MPA_REQUIRE(cand ? cand_cap >= 1 : cand_cap >= lv->cap, MPA_ERR_ARG, "mpa_centroid_logits: cand_cap %d too small",
                 cand_cap);
+    MPA_REQUIRE(!chunk_stats || lv->size, MPA_ERR_ARG, "mpa_centroid_logits: chunk stats need sizes");
+    (void)n_kv_heads;
     const int L = lv->n_ledgers;
     if (L <= 0) return 0;
     const int cap = cand ? cand_cap : lv->cap;
-    dim3 grid(ceil_div(cap, kLogitsThreads), L);
     cudaStream_t st = (cudaStream_t)stream;
+    if (g_logits_tiled < 0) {
+        const char* e = getenv("MPA_LOGITS_SIMPLE");
+        g_logits_tiled = (e && e[0] == '1') ? 0 : 1;
+    }
+    if (g_logits_tiled && (d == 64 || d == 128)) {
+        const int nch = ceil_div(cap, kChunk);
+        dim3 grid(nch, L);
+#define MPA_TILED(T, D)                                                                                              \
+    {                                                                                                                \
+        auto kern = centroid_logits_tiled<T, kG, D>;                                                                 \
+        const size_t smem = sizeof(double) * kG * (D + kChunk) + (size_t)kChunk * (D * sizeof(T) + 16);             \
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
+        kern<<<grid, kTiledThreads, smem, st>>>(q_lk, (const T*)lv->kc, lv->cap, lv->count, lv->size, cand, n_cand,  \
+                                                cand_cap, logits, chunk_stats, nch);                                 \
+    }
+        MPA_DISPATCH_G(group, {
+            if (lv->dtype == MPA_BF16) {
+                if (d == 128) MPA_TILED(__nv_bfloat16, 128) else MPA_TILED(__nv_bfloat16, 64)
+            } else if (lv->dtype == MPA_F32) {
+                if (d == 128) MPA_TILED(float, 128) else MPA_TILED(float, 64)
+            } else {
+                if (d == 128) MPA_TILED(double, 128) else MPA_TILED(double, 64)
+            }
+        });
+#undef MPA_TILED
+        return check_launch("mpa_centroid_logits(tiled)");
+    }
+    MPA_REQUIRE(!chunk_stats, MPA_ERR_UNSUPPORTED, "mpa_centroid_logits: chunk stats need d in {64,128}");
+    dim3 grid(ceil_div(cap, kLogitsThreads), L);
     MPA_DISPATCH_G(group, {
         const size_t smem = sizeof(double) * kG * d;
         if (lv->dtype == MPA_F32)
@@ -366,21 +558,54 @@ static const int kSelectMaxCap = 13312;
 extern "C" int mpa_select(const double* logits, int group, const int32_t* cand, const int32_t* n_cand, int cand_cap,
                           const int32_t* lv_size, int lv_cap, const double* elogits, const int32_t* esize,
                           const uint8_t* eflag, const int32_t* n_extra, int ecap, const int64_t* budget,
-                          int n_ledgers, uint8_t* flag, int32_t* sel_tokens, void* stream) {
+                          int n_ledgers, uint8_t* flag, int32_t* sel_tokens, const double* chunk_stats,
+                          void* stream) {
     MPA_REQUIRE(logits && n_cand && lv_size && budget && flag, MPA_ERR_ARG, "mpa_select: null argument");
     MPA_REQUIRE(!elogits || (esize && eflag && n_extra), MPA_ERR_ARG, "mpa_select: incomplete extras");
     MPA_REQUIRE(cand_cap <= kSelectMaxCap, MPA_ERR_UNSUPPORTED, "mpa_select: cand_cap %d > %d", cand_cap,
                 kSelectMaxCap);
     if (n_ledgers <= 0) return 0;
     const size_t smem = (size_t)cand_cap * 16;
+    const int nch = ceil_div(cand_cap, kChunk);
     cudaStream_t st = (cudaStream_t)stream;
     MPA_DISPATCH_G(group, {
         auto kern = select_kernel<kG>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<n_ledgers, kSelThreads, smem, st>>>(logits, cand, n_cand, cand_cap, lv_size, lv_cap, elogits, esize,
-                                                   eflag, n_extra, ecap, budget, flag, sel_tokens);
+                                                   eflag, n_extra, ecap, budget, flag, sel_tokens, chunk_stats, nch);
     });
     return check_launch("mpa_select");
+}
+
+extern "C" int mpa_select_worklist(const mpa_level* fine, const mpa_level* coarse, int group, const double* logits,
+                                   const int32_t* cand, const int32_t* n_cand, int cand_cap, const double* chunk_stats,
+                                   const uint8_t* cflag, const double* clogits, const int64_t* budget,
+                                   const int32_t* sink_end, const int32_t* buffer_start, const int32_t* cache_len,
+                                   int n_kv_heads, int n_ledgers, int replacement, uint8_t* flag,
+                                   int32_t* sel_tokens, int32_t* tok, int tok_cap, int32_t* rej, float* rej_w,
+                                   int rej_cap, int32_t* stats, void* stream) {
+    MPA_REQUIRE(fine && logits && budget && flag && sink_end && buffer_start && cache_len && tok && rej && rej_w &&
+                    stats,
+                MPA_ERR_ARG, "mpa_select_worklist: null argument");
+    MPA_REQUIRE(!cflag || (coarse && clogits), MPA_ERR_ARG, "mpa_select_worklist: coarse flags without level");
+    MPA_REQUIRE(cand ? n_cand != nullptr : cand_cap >= fine->cap, MPA_ERR_ARG,
+                "mpa_select_worklist: candidate capacity");
+    MPA_REQUIRE(cand_cap <= kSelectMaxCap, MPA_ERR_UNSUPPORTED, "mpa_select_worklist: cand_cap %d > %d", cand_cap,
+                kSelectMaxCap);
+    if (n_ledgers <= 0) return 0;
+    const size_t smem = (size_t)cand_cap * 16;
+    const int nch = ceil_div(cand_cap, kChunk);
+    cudaStream_t st = (cudaStream_t)stream;
+    MPA_DISPATCH_G(group, {
+        auto kern = select_worklist_kernel<kG>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<n_ledgers, kSelThreads, smem, st>>>(
+            logits, cand, n_cand, cand_cap, budget, flag, sel_tokens, chunk_stats, nch, fine->size, fine->off,
+            fine->idx, fine->cap, fine->idx_cap, coarse ? coarse->size : nullptr, coarse ? coarse->count : nullptr,
+            coarse ? coarse->cap : 0, fine->count, cflag, clogits, sink_end, buffer_start, cache_len, n_kv_heads,
+            replacement, tok, tok_cap, rej, rej_w, rej_cap, stats);
+    });
+    return check_launch("mpa_select_worklist");
 }
 
 extern "C" int mpa_hier_candidates(const mpa_level* coarse, const uint8_t* cflag, int n_ledgers, int32_t* cand,
@@ -409,10 +634,10 @@ extern "C" int mpa_build_worklist(const mpa_level* fine, const mpa_level* coarse
     cudaStream_t st = (cudaStream_t)stream;
     MPA_DISPATCH_G(group, {
         build_worklist_kernel<kG><<<n_ledgers, kListThreads, 0, st>>>(
-            fine->size, fine->off, fine->idx, fine->cap, fine->idx_cap, coarse ? coarse->size : nullptr,
-            coarse ? coarse->count : nullptr, coarse ? coarse->cap : 0, cand, n_cand, fine->count, cand_cap, flag,
-            logits, cflag, clogits, sink_end, buffer_start, cache_len, n_kv_heads, replacement, tok, tok_cap, rej,
-            rej_w, rej_cap, stats);
+            cand, n_cand, cand_cap, flag, logits, fine->size, fine->off, fine->idx, fine->cap, fine->idx_cap,
+            coarse ? coarse->size : nullptr, coarse ? coarse->count : nullptr, coarse ? coarse->cap : 0, fine->count,
+            cflag, clogits, sink_end, buffer_start, cache_len, n_kv_heads, replacement, tok, tok_cap, rej, rej_w,
+            rej_cap, stats);
     });
     return check_launch("mpa_build_worklist");
 }

@@ -28,8 +28,11 @@ from ._lib import MpaCache, call, dtype_code, ptr, stream_ptr
 from .core import ConfigError, EngineConfig, HeadLayout, inv_freq
 from .ledger import DeviceLedgers, HostLedger
 
+import os
+
 NUM_SMS = 148
 MAX_SPLITS = 64
+SPLIT_WAVES = float(os.environ.get("MPA_SPLIT_WAVES", "2"))
 
 
 class DecodeEngine:
@@ -71,6 +74,7 @@ class DecodeEngine:
         self.logits = torch.zeros(L, G, self.kcap, dtype=torch.float64, **z)
         self.flag = torch.zeros(L, self.kcap, dtype=torch.uint8, **z)
         self.sel_tokens = torch.zeros(L, dtype=torch.int32, **z)
+        self.cstats = torch.zeros(L, -(-self.kcap // 64), G, 2, dtype=torch.float64, **z)
         self.budget = torch.full((L,), cfg.token_budget, dtype=torch.int64, **z)
         if hier:
             self.clogits = torch.zeros(L, G, self.ccap, dtype=torch.float64, **z)
@@ -79,6 +83,7 @@ class DecodeEngine:
             self.cand = torch.zeros(L, self.kcap, dtype=torch.int32, **z)
             self.n_cand = torch.zeros(L, dtype=torch.int32, **z)
             self.csel_tokens = torch.zeros(L, dtype=torch.int32, **z)
+            self.ccstats = torch.zeros(L, -(-self.ccap // 64), G, 2, dtype=torch.float64, **z)
         self.tok_cap = tcap
         self.rej_cap = self.kcap + self.ccap
         self.tok = torch.zeros(L, self.tok_cap, dtype=torch.int32, **z)
@@ -141,9 +146,11 @@ class DecodeEngine:
 
     # ------------------------------------------------------------------ decode
     def _n_split(self, units_per_ledger: float) -> int:
-        target_ctas = 2 * NUM_SMS
+        """CTAs per ledger for the fused kernel: ~SPLIT_WAVES waves of the 2-CTA/SM residency,
+        but at least ~256 work units (tokens count 2, centroids 1) per CTA."""
+        target_ctas = SPLIT_WAVES * 2 * NUM_SMS
         s = max(1, round(target_ctas / self.L))
-        s = min(s, max(1, int(units_per_ledger // 96)), MAX_SPLITS)
+        s = min(s, max(1, int(units_per_ledger // 256)), MAX_SPLITS)
         return int(s)
 
     def _sparse_units(self) -> float:
@@ -164,36 +171,35 @@ class DecodeEngine:
         G, L = self.G, self.L
         fine = self.led.fine_level()
         replacement = 0 if self.mode == "flat-no-replacement" else 1
+        tiled = self.d in (64, 128)
+        cs = self.cstats if tiled else None
         if self.cfg.hierarchy is None:
             if int(self.led.n_fine.min()) == 0:
                 raise ConfigError("ledger has no clusters")
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, None, None, self.kcap,
-                 ptr(self.logits), st)
-            call("mpa_select", ptr(self.logits), G, None, ptr(self.led.count), self.kcap, ptr(self.led.size),
-                 self.kcap, None, None, None, None, 0, ptr(self.budget), L, ptr(self.flag), ptr(self.sel_tokens), st)
-            call("mpa_build_worklist", fine, None, G, None, None, self.kcap, ptr(self.flag), ptr(self.logits), None,
-                 None, ptr(self.sink_end_d), ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv, L,
-                 replacement, ptr(self.tok), self.tok_cap, ptr(self.rej), ptr(self.rej_w), self.rej_cap,
-                 ptr(self.stats), st)
+                 ptr(self.logits), ptr(cs), st)
+            call("mpa_select_worklist", fine, None, G, ptr(self.logits), None, None, self.kcap, ptr(cs), None, None,
+                 ptr(self.budget), ptr(self.sink_end_d), ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv,
+                 L, replacement, ptr(self.flag), ptr(self.sel_tokens), ptr(self.tok), self.tok_cap, ptr(self.rej),
+                 ptr(self.rej_w), self.rej_cap, ptr(self.stats), st)
         else:
             if int(self.led.n_coarse.min()) == 0:
                 raise ConfigError("ledger has no coarse clusters")
             coarse = self.led.coarse_level()
+            ccs = self.ccstats if tiled else None
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, coarse, None, None, self.ccap,
-                 ptr(self.clogits), st)
+                 ptr(self.clogits), ptr(ccs), st)
             call("mpa_select", ptr(self.clogits), G, None, ptr(self.led.ccount), self.ccap, ptr(self.led.csize),
                  self.ccap, None, None, None, None, 0, ptr(self.cbudget), L, ptr(self.cflag),
-                 ptr(self.csel_tokens), st)
+                 ptr(self.csel_tokens), ptr(ccs), st)
             call("mpa_hier_candidates", coarse, ptr(self.cflag), L, ptr(self.cand), ptr(self.n_cand), self.kcap, st)
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, ptr(self.cand), ptr(self.n_cand),
-                 self.kcap, ptr(self.logits), st)
-            call("mpa_select", ptr(self.logits), G, ptr(self.cand), ptr(self.n_cand), self.kcap, ptr(self.led.size),
-                 self.kcap, ptr(self.clogits), ptr(self.led.csize), ptr(self.cflag), ptr(self.led.ccount),
-                 self.ccap, ptr(self.budget), L, ptr(self.flag), ptr(self.sel_tokens), st)
-            call("mpa_build_worklist", fine, coarse, G, ptr(self.cand), ptr(self.n_cand), self.kcap, ptr(self.flag),
-                 ptr(self.logits), ptr(self.cflag), ptr(self.clogits), ptr(self.sink_end_d),
-                 ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv, L, replacement, ptr(self.tok),
-                 self.tok_cap, ptr(self.rej), ptr(self.rej_w), self.rej_cap, ptr(self.stats), st)
+                 self.kcap, ptr(self.logits), ptr(cs), st)
+            call("mpa_select_worklist", fine, coarse, G, ptr(self.logits), ptr(self.cand), ptr(self.n_cand),
+                 self.kcap, ptr(cs), ptr(self.cflag), ptr(self.clogits), ptr(self.budget), ptr(self.sink_end_d),
+                 ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv, L, replacement, ptr(self.flag),
+                 ptr(self.sel_tokens), ptr(self.tok), self.tok_cap, ptr(self.rej), ptr(self.rej_w), self.rej_cap,
+                 ptr(self.stats), st)
 
     def fused(self, n_split: int | None = None) -> torch.Tensor:
         S = n_split or self._n_split(self._sparse_units())
