@@ -88,13 +88,16 @@ int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group, int d,
  * take while the running size sum < budget[l] (the crossing cluster is included).
  * sizes: lv_size[l, id_i]; tie key: id_i.  Extras (may be NULL): logits [L, G, ecap] with sizes
  * esize[l, j] that enter only the denominators when eflag[l, j] == 0 (hierarchical union,
- * attention.py:331-334).  Writes flag[l, i] = 1 selected / 0 rejected, sel_tokens[l]. */
+ * attention.py:331-334).  Writes flag[l, i] = 1 selected / 0 rejected, sel_tokens[l].
+ * n_max (<= cand_cap, 0 = cand_cap) bounds the live candidates per ledger and sizes the shared
+ * memory: up to 8192 candidates are bitonic-sorted in smem, larger sets use a size-weighted
+ * radix select (at most 11264 candidates). */
 int mpa_select(const double* logits, int group, const int32_t* cand, const int32_t* n_cand,
                int cand_cap, const int32_t* lv_size, int lv_cap,
                const double* elogits, const int32_t* esize, const uint8_t* eflag,
                const int32_t* n_extra, int ecap,
                const int64_t* budget, int n_ledgers, uint8_t* flag, int32_t* sel_tokens,
-               const double* chunk_stats, void* stream);
+               const double* chunk_stats, int n_max, void* stream);
 
 /* Hierarchy stage glue (attention.py:321-329): cand[l] = children of coarse clusters with
  * cflag == 1, promoted in coarse-id order, children ascending; n_cand[l]. */
@@ -127,7 +130,7 @@ int mpa_select_worklist(const mpa_level* fine, const mpa_level* coarse, int grou
                         const int32_t* sink_end, const int32_t* buffer_start, const int32_t* cache_len,
                         int n_kv_heads, int n_ledgers, int replacement, uint8_t* flag,
                         int32_t* sel_tokens, int32_t* tok, int tok_cap, int32_t* rej, float* rej_w,
-                        int rej_cap, int32_t* stats, void* stream);
+                        int rej_cap, int32_t* stats, int n_max, void* stream);
 
 /* K11 + K12 -- fused sparse decode: one online softmax over the exact tokens (K_rot/V gathered
  * by index, logits q_rot . k) and the rejected-centroid pseudo-tokens (logit + ln N, value

@@ -40,6 +40,36 @@ template <> struct elem<__nv_bfloat16> {
     static __device__ __forceinline__ __nv_bfloat16 from_d(double x) { return __double2bfloat16(x); }
 };
 
+// ---- 16-byte chunk unpacking to fp64 (register-only; no address-taken locals)
+template <typename T> struct unpack16;
+template <> struct unpack16<__nv_bfloat16> {
+    static constexpr int N = 8;
+    static __device__ __forceinline__ void run(const uint4& r, double (&o)[8]) {
+        const unsigned w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            o[2 * i] = (double)__uint_as_float(w[i] << 16);
+            o[2 * i + 1] = (double)__uint_as_float(w[i] & 0xffff0000u);
+        }
+    }
+};
+template <> struct unpack16<float> {
+    static constexpr int N = 4;
+    static __device__ __forceinline__ void run(const uint4& r, double (&o)[4]) {
+        o[0] = (double)__uint_as_float(r.x);
+        o[1] = (double)__uint_as_float(r.y);
+        o[2] = (double)__uint_as_float(r.z);
+        o[3] = (double)__uint_as_float(r.w);
+    }
+};
+template <> struct unpack16<double> {
+    static constexpr int N = 2;
+    static __device__ __forceinline__ void run(const uint4& r, double (&o)[2]) {
+        o[0] = __hiloint2double((int)r.y, (int)r.x);
+        o[1] = __hiloint2double((int)r.w, (int)r.z);
+    }
+};
+
 // ---- warp / block reductions -----------------------------------------------
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

@@ -257,6 +257,7 @@ template <int D> struct TileGeom {
 };
 
 constexpr int kMmaWarps = 4;
+constexpr int kSegTiles = 64;  // tiles whose row ids are staged in smem at a time
 
 // PACKED: G <= 4, columns 0..3 carry the hi parts of q / P, columns 4..7 the lo parts.
 // Otherwise (G <= 8) hi and lo run as two separate MMAs.
@@ -325,20 +326,13 @@ decode_mma_kernel(const __nv_bfloat16* __restrict__ k_rot, const __nv_bfloat16* 
     }
 
     const size_t cache_base = (size_t)l * tcap;
-    // Issue the loads of virtual tile vt (owned by this warp) into stage st.
-    // Row id of this lane's row (lane >> 1) in virtual tile vt: token id, or centroid code.
-    // Fetched one tile AHEAD of its cp.async issue so the dependent index load never sits
-    // on the critical path.
+    // Row ids (token id, or centroid code) of a segment of kSegTiles virtual tiles are staged in
+    // smem by the whole CTA before the per-warp pipelines run over that segment, so no
+    // dependent index load ever sits between a tile and its cp.async issue.
     constexpr int kNoRow = INT_MIN;
-    auto fetch = [&](int vt) -> int {
-        const int row = lane >> 1;
-        if (vt < ntt) {
-            const int t = R.t0 + vt * 16 + row;
-            return t < R.t1 ? (tok ? __ldg(tok + (size_t)l * tok_cap + t) : t) : kNoRow;
-        }
-        const int r = R.r0 + (vt - ntt) * 16 + row;
-        return r < R.r1 ? __ldg(rej + (size_t)l * rej_cap + r) : kNoRow;
-    };
+    int* ids_s = reinterpret_cast<int*>(smem + (size_t)kMmaWarps * NST * 2 * Geo::kMatBytes);
+    int seg = 0;
+    auto fetch = [&](int vt) -> int { return ids_s[(vt - seg) * 16 + (lane >> 1)]; };
     auto issue = [&](int vt, int st, int id) {
         const unsigned kst = wbase_s + st * 2 * Geo::kMatBytes, vst = kst + Geo::kMatBytes;
         const int row = lane >> 1;  // 2 lanes per row
@@ -373,110 +367,123 @@ decode_mma_kernel(const __nv_bfloat16* __restrict__ k_rot, const __nv_bfloat16* 
         }
     };
 
-    // this warp's tiles: vt = w, w + W, ...
-    const int my_n = NT > w ? (NT - w + kMmaWarps - 1) / kMmaWarps : 0;
-    int pf = 0;
-#pragma unroll
-    for (int i = 0; i < NST - 1; ++i) {
-        if (i < my_n) issue(w + i * kMmaWarps, i, fetch(w + i * kMmaWarps));
-        cp_commit();
-    }
-    if (NST - 1 < my_n) pf = fetch(w + (NST - 1) * kMmaWarps);
-    for (int i = 0; i < my_n; ++i) {
-        {
-            const int nxt = i + NST - 1;
-            if (nxt < my_n) {
-                issue(w + nxt * kMmaWarps, nxt % NST, pf);
-                if (nxt + 1 < my_n) pf = fetch(w + (nxt + 1) * kMmaWarps);
+    for (seg = 0; seg < NT; seg += kSegTiles) {
+        const int seg_n = min(kSegTiles, NT - seg);
+        for (int k = threadIdx.x; k < seg_n * 16; k += blockDim.x) {
+            const int vt = seg + (k >> 4), row = k & 15;
+            int id;
+            if (vt < ntt) {
+                const int t = R.t0 + vt * 16 + row;
+                id = t < R.t1 ? (tok ? __ldg(tok + (size_t)l * tok_cap + t) : t) : kNoRow;
+            } else {
+                const int r = R.r0 + (vt - ntt) * 16 + row;
+                id = r < R.r1 ? __ldg(rej + (size_t)l * rej_cap + r) : kNoRow;
             }
+            ids_s[k] = id;
+        }
+        __syncthreads();
+        // this warp's tiles in the segment: vt = seg + w, seg + w + W, ...
+        const int my_n = seg_n > w ? (seg_n - w + kMmaWarps - 1) / kMmaWarps : 0;
+#pragma unroll
+        for (int i = 0; i < NST - 1; ++i) {
+            if (i < my_n) issue(seg + w + i * kMmaWarps, i, fetch(seg + w + i * kMmaWarps));
             cp_commit();
         }
-        cp_wait<NST - 1>();
-        __syncwarp();
-        const int vt = w + i * kMmaWarps, st = i % NST;
-        const unsigned kst = wbase_s + st * 2 * Geo::kMatBytes, vst = kst + Geo::kMatBytes;
+        for (int i = 0; i < my_n; ++i) {
+            {
+                const int nxt = i + NST - 1;
+                if (nxt < my_n) issue(seg + w + nxt * kMmaWarps, nxt % NST, fetch(seg + w + nxt * kMmaWarps));
+                cp_commit();
+            }
+            cp_wait<NST - 1>();
+            __syncwarp();
+            const int vt = seg + w + i * kMmaWarps, st = i % NST;
+            const unsigned kst = wbase_s + st * 2 * Geo::kMatBytes, vst = kst + Geo::kMatBytes;
 
-        // logits x[row r / r+8][head hA / hB] in log2 units
-        float x[4];
-        if (vt < ntt) {
-            float c[4] = {0.f, 0.f, 0.f, 0.f};
-            float c2[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int ks = 0; ks < KS; ++ks) {
+            // logits x[row r / r+8][head hA / hB] in log2 units
+            float x[4];
+            if (vt < ntt) {
+                float c[4] = {0.f, 0.f, 0.f, 0.f};
+                float c2[4] = {0.f, 0.f, 0.f, 0.f};
+    #pragma unroll
+                for (int ks = 0; ks < KS; ++ks) {
+                    unsigned a[4];
+                    const int row = (lane & 7) + ((lane >> 3) & 1) * 8, ch = ks * 2 + (lane >> 4);
+                    ldsm_x4(kst + Geo::off(row, ch), a);
+                    mma_bf16(c, a, qhi[ks][0], qhi[ks][1]);
+                    if (!PACKED) mma_bf16(c2, a, qlo[ks][0], qlo[ks][1]);
+                }
+                if (PACKED) {
+    #pragma unroll
+                    for (int j = 0; j < 4; ++j) x[j] = c[j] + __shfl_xor_sync(0xffffffffu, c[j], 2);
+                } else {
+    #pragma unroll
+                    for (int j = 0; j < 4; ++j) x[j] = c[j] + c2[j];
+                }
+                const int base = R.t0 + (vt << 4);
+                if (base + gr >= R.t1) x[0] = x[1] = -INFINITY;
+                if (base + gr + 8 >= R.t1) x[2] = x[3] = -INFINITY;
+            } else {
+                const int base = R.r0 + ((vt - ntt) << 4);
+                const float* lg = reinterpret_cast<const float*>(wbase + (size_t)st * 2 * Geo::kMatBytes);
+    #pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int rr = gr + (j >> 1) * 8;
+                    const int h = (j & 1) ? hB : hA;
+                    x[j] = base + rr < R.r1 ? (h < G ? lg[rr * G + h] * kLog2e : 0.f) : -INFINITY;
+                }
+            }
+            // padded heads (>= G) must stay finite
+            if (hA >= G) { x[0] = x[0] == -INFINITY ? -INFINITY : 0.f; x[2] = x[2] == -INFINITY ? -INFINITY : 0.f; }
+            if (hB >= G) { x[1] = x[1] == -INFINITY ? -INFINITY : 0.f; x[3] = x[3] == -INFINITY ? -INFINITY : 0.f; }
+
+            // online softmax (column = head) over the 16 rows of this tile
+            float tA = fmaxf(x[0], x[2]), tB = fmaxf(x[1], x[3]);
+    #pragma unroll
+            for (int off = 4; off < 32; off <<= 1) {
+                tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, off));
+                tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, off));
+            }
+            const float nA = fmaxf(mA, tA), nB = fmaxf(mB, tB);
+            const float cA = exp2f(mA - nA), cB = exp2f(mB - nB);  // mA=-inf -> 0
+            mA = nA;
+            mB = nB;
+            const float p0 = exp2f(x[0] - nA), p1 = exp2f(x[1] - nB), p2 = exp2f(x[2] - nA), p3 = exp2f(x[3] - nB);
+            sA = sA * cA + p0 + p2;
+            sB = sB * cB + p1 + p3;
+    #pragma unroll
+            for (int mt = 0; mt < KS; ++mt) {
+                o[mt][0] *= cA; o[mt][1] *= cB; o[mt][2] *= cA; o[mt][3] *= cB;
+                if (!PACKED) { o2[mt][0] *= cA; o2[mt][1] *= cB; o2[mt][2] *= cA; o2[mt][3] *= cB; }
+            }
+            // P^T fragments (B operand): hi/lo split, transposed with movmatrix
+            unsigned b0, b1, b2 = 0, b3 = 0;
+            {
+                const float h0 = bf16_round(p0), h1 = bf16_round(p1), h2 = bf16_round(p2), h3 = bf16_round(p3);
+                if (PACKED) {
+                    const bool hi = tq < 2;
+                    b0 = movm_t(hi ? pack_bf16(h0, h1) : pack_bf16(p0 - h0, p1 - h1));
+                    b1 = movm_t(hi ? pack_bf16(h2, h3) : pack_bf16(p2 - h2, p3 - h3));
+                } else {
+                    b0 = movm_t(pack_bf16(h0, h1));
+                    b1 = movm_t(pack_bf16(h2, h3));
+                    b2 = movm_t(pack_bf16(p0 - h0, p1 - h1));
+                    b3 = movm_t(pack_bf16(p2 - h2, p3 - h3));
+                }
+            }
+    #pragma unroll
+            for (int mt = 0; mt < KS; ++mt) {
                 unsigned a[4];
-                const int row = (lane & 7) + ((lane >> 3) & 1) * 8, ch = ks * 2 + (lane >> 4);
-                ldsm_x4(kst + Geo::off(row, ch), a);
-                mma_bf16(c, a, qhi[ks][0], qhi[ks][1]);
-                if (!PACKED) mma_bf16(c2, a, qlo[ks][0], qlo[ks][1]);
+                const int j = lane >> 3;
+                const int row = (lane & 7) + (j >> 1) * 8, ch = mt * 2 + (j & 1);
+                ldsm_x4_t(vst + Geo::off(row, ch), a);
+                mma_bf16(o[mt], a, b0, b1);
+                if (!PACKED) mma_bf16(o2[mt], a, b2, b3);
             }
-            if (PACKED) {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) x[j] = c[j] + __shfl_xor_sync(0xffffffffu, c[j], 2);
-            } else {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) x[j] = c[j] + c2[j];
-            }
-            const int base = R.t0 + (vt << 4);
-            if (base + gr >= R.t1) x[0] = x[1] = -INFINITY;
-            if (base + gr + 8 >= R.t1) x[2] = x[3] = -INFINITY;
-        } else {
-            const int base = R.r0 + ((vt - ntt) << 4);
-            const float* lg = reinterpret_cast<const float*>(wbase + (size_t)st * 2 * Geo::kMatBytes);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int rr = gr + (j >> 1) * 8;
-                const int h = (j & 1) ? hB : hA;
-                x[j] = base + rr < R.r1 ? (h < G ? lg[rr * G + h] * kLog2e : 0.f) : -INFINITY;
-            }
+            __syncwarp();
         }
-        // padded heads (>= G) must stay finite
-        if (hA >= G) { x[0] = x[0] == -INFINITY ? -INFINITY : 0.f; x[2] = x[2] == -INFINITY ? -INFINITY : 0.f; }
-        if (hB >= G) { x[1] = x[1] == -INFINITY ? -INFINITY : 0.f; x[3] = x[3] == -INFINITY ? -INFINITY : 0.f; }
-
-        // online softmax (column = head) over the 16 rows of this tile
-        float tA = fmaxf(x[0], x[2]), tB = fmaxf(x[1], x[3]);
-#pragma unroll
-        for (int off = 4; off < 32; off <<= 1) {
-            tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, off));
-            tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, off));
-        }
-        const float nA = fmaxf(mA, tA), nB = fmaxf(mB, tB);
-        const float cA = exp2f(mA - nA), cB = exp2f(mB - nB);  // mA=-inf -> 0
-        mA = nA;
-        mB = nB;
-        const float p0 = exp2f(x[0] - nA), p1 = exp2f(x[1] - nB), p2 = exp2f(x[2] - nA), p3 = exp2f(x[3] - nB);
-        sA = sA * cA + p0 + p2;
-        sB = sB * cB + p1 + p3;
-#pragma unroll
-        for (int mt = 0; mt < KS; ++mt) {
-            o[mt][0] *= cA; o[mt][1] *= cB; o[mt][2] *= cA; o[mt][3] *= cB;
-            if (!PACKED) { o2[mt][0] *= cA; o2[mt][1] *= cB; o2[mt][2] *= cA; o2[mt][3] *= cB; }
-        }
-        // P^T fragments (B operand): hi/lo split, transposed with movmatrix
-        unsigned b0, b1, b2 = 0, b3 = 0;
-        {
-            const float h0 = bf16_round(p0), h1 = bf16_round(p1), h2 = bf16_round(p2), h3 = bf16_round(p3);
-            if (PACKED) {
-                const bool hi = tq < 2;
-                b0 = movm_t(hi ? pack_bf16(h0, h1) : pack_bf16(p0 - h0, p1 - h1));
-                b1 = movm_t(hi ? pack_bf16(h2, h3) : pack_bf16(p2 - h2, p3 - h3));
-            } else {
-                b0 = movm_t(pack_bf16(h0, h1));
-                b1 = movm_t(pack_bf16(h2, h3));
-                b2 = movm_t(pack_bf16(p0 - h0, p1 - h1));
-                b3 = movm_t(pack_bf16(p2 - h2, p3 - h3));
-            }
-        }
-#pragma unroll
-        for (int mt = 0; mt < KS; ++mt) {
-            unsigned a[4];
-            const int j = lane >> 3;
-            const int row = (lane & 7) + (j >> 1) * 8, ch = mt * 2 + (j & 1);
-            ldsm_x4_t(vst + Geo::off(row, ch), a);
-            mma_bf16(o[mt], a, b0, b1);
-            if (!PACKED) mma_bf16(o2[mt], a, b2, b3);
-        }
-        __syncwarp();
+        cp_wait<0>();
+        __syncthreads();  // before the next segment's ids overwrite ids_s
     }
     cp_wait<0>();
 
@@ -585,11 +592,15 @@ int launch_mma(const mpa_cache* c, const float* q_rot, const int32_t* tok, const
                cudaStream_t st) {
     constexpr int NST = 3;
     dim3 grid(S, c->n_ledgers);
-    const size_t stage_bytes = (size_t)kMmaWarps * NST * 2 * TileGeom<D>::kMatBytes;
+    const size_t stage_bytes = (size_t)kMmaWarps * NST * 2 * TileGeom<D>::kMatBytes + kSegTiles * 16 * sizeof(int);
     const size_t red_bytes = sizeof(float) * kMmaWarps * 8 * (2 + D);
     const size_t smem = stage_bytes > red_bytes ? stage_bytes : red_bytes;
     auto kern = decode_mma_kernel<G, D, NST>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
     kern<<<grid, kMmaWarps * 32, smem, st>>>((const __nv_bfloat16*)c->k_rot, (const __nv_bfloat16*)c->v, c->tcap,
                                              q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej, rej_cap,
                                              (const __nv_bfloat16*)fvc, fcap, (const __nv_bfloat16*)cvc, ccap, S, pml,

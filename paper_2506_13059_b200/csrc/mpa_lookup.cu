@@ -53,13 +53,14 @@ centroid_logits_kernel(const double* __restrict__ q_lk, int n_kv_heads, int d, c
     for (int g = 0; g < G; ++g) out[(size_t)g * cand_cap] = acc[g] / sq;
 }
 
-// Tiled variant for d in {64, 128}: a CTA stages kChunk centroid rows of the ledger with
-// coalesced 16-byte loads into padded smem, then TPC threads cooperate on one centroid (each
-// holds its slice of the G q_lookup rows in registers, fp64 FMA), reduce with shuffles, and
-// the CTA emits the chunk's per-head (max, sum N e^(l - max)) partials so the selection kernel
-// never re-reads all logits to build the Eq. 1 normaliser.
-constexpr int kChunk = 64;
-constexpr int kTiledThreads = 256;
+// Tiled variant for d in {64, 128}: a CTA stages kChunk centroid rows of one ledger with
+// coalesced 16-byte loads into padded smem (all loads in flight at once), then each thread
+// computes one centroid's G dot products in fp64 reading q_lookup interleaved [d][G] from smem
+// (warp-broadcast 16-byte loads).  ~40 registers and ~40 KB smem per CTA keep several CTAs
+// resident per SM so the tile loads of one CTA overlap the fp64 math of the others.  The CTA
+// also emits the chunk's per-head (max, sum N e^(l - max)) partials of the Eq. 1 normaliser.
+constexpr int kChunk = 128;
+constexpr int kTiledThreads = 128;
 
 template <typename T, int G, int D>
 __global__ void __launch_bounds__(kTiledThreads)
@@ -69,16 +70,12 @@ centroid_logits_tiled(const double* __restrict__ q_lk, const T* __restrict__ kc,
                       double* __restrict__ logits, double* __restrict__ cstats, int n_chunks) {
     constexpr int EPC = 16 / (int)sizeof(T);              // elements per 16-byte chunk
     constexpr int CPR = D / EPC;                          // chunks per row
-    constexpr int TPC0 = G <= 4 ? 8 : 16;
-    constexpr int TPC = TPC0 < CPR ? TPC0 : CPR;          // threads per centroid
-    constexpr int CPT = CPR / TPC;                        // chunks per thread
-    constexpr int ROWB = D * (int)sizeof(T) + 16;         // padded row bytes
-    constexpr int CPP = kTiledThreads / TPC;              // centroids per pass
-    static_assert(CPT >= 1 && CPR % TPC == 0, "tile shape");
+    constexpr int ROWB = D * (int)sizeof(T) + 16;         // padded row bytes (conflict-free LDS.128)
+    constexpr int GP = (G + 1) & ~1;                      // q row padded to an even count of doubles
     extern __shared__ __align__(16) unsigned char sm[];
-    double* qs = reinterpret_cast<double*>(sm);                       // [G][D]
-    double* lgs = qs + G * D;                                          // [G][kChunk]
-    unsigned char* tile = reinterpret_cast<unsigned char*>(lgs + G * kChunk);
+    double* qs = reinterpret_cast<double*>(sm);                        // [D][GP]
+    double* red = qs + D * GP;                                         // [4 warps][G][2]
+    unsigned char* tile = reinterpret_cast<unsigned char*>(red + 4 * G * 2);
     const int l = blockIdx.y, chunk = blockIdx.x;
     const int n = cand ? n_cand[l] : count[l];
     const int i0 = chunk * kChunk;
@@ -90,71 +87,90 @@ centroid_logits_tiled(const double* __restrict__ q_lk, const T* __restrict__ kc,
         return;
     }
     const int nv = min(kChunk, n - i0);
-    for (int j = threadIdx.x; j < G * D; j += blockDim.x) qs[j] = q_lk[(size_t)l * G * D + j];
-    for (int j = threadIdx.x; j < kChunk * CPR; j += blockDim.x) {
-        const int r = j / CPR, c = j - r * CPR;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (r < nv) {
-            const int row = cand ? __ldg(cand + (size_t)l * cand_cap + i0 + r) : i0 + r;
-            v = __ldg(reinterpret_cast<const uint4*>(kc + ((size_t)l * kcap + row) * D) + c);
+    for (int j = threadIdx.x; j < G * D; j += blockDim.x) {
+        const int g = j / D, k = j - g * D;
+        qs[k * GP + g] = q_lk[(size_t)l * G * D + j];
+    }
+    {
+        constexpr int PER = 16;  // 16-byte loads in flight per thread
+        constexpr int TOTAL = kChunk * CPR;
+        for (int base = 0; base < TOTAL; base += PER * kTiledThreads) {
+            uint4 v[PER];
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                const int j = base + threadIdx.x + e * kTiledThreads;
+                const int r = j / CPR, c = j - r * CPR;
+                v[e] = make_uint4(0u, 0u, 0u, 0u);
+                if (j < TOTAL && r < nv) {
+                    const int row = cand ? __ldg(cand + (size_t)l * cand_cap + i0 + r) : i0 + r;
+                    v[e] = __ldg(reinterpret_cast<const uint4*>(kc + ((size_t)l * kcap + row) * D) + c);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                const int j = base + threadIdx.x + e * kTiledThreads;
+                const int r = j / CPR, c = j - r * CPR;
+                if (j < TOTAL) *reinterpret_cast<uint4*>(tile + r * ROWB + c * 16) = v[e];
+            }
         }
-        *reinterpret_cast<uint4*>(tile + r * ROWB + c * 16) = v;
     }
     __syncthreads();
-    const int sub = threadIdx.x % TPC, cl = threadIdx.x / TPC;
-    double qr[G][CPT * EPC];
+    const int r = threadIdx.x;
+    double acc[G];
 #pragma unroll
-    for (int g = 0; g < G; ++g)
+    for (int g = 0; g < G; ++g) acc[g] = 0.0;
+#pragma unroll 2
+    for (int c = 0; c < CPR; ++c) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(tile + r * ROWB + c * 16);
+        double xv[EPC];
+        unpack16<T>::run(raw, xv);
 #pragma unroll
-        for (int c = 0; c < CPT; ++c)
+        for (int e = 0; e < EPC; ++e) {
+            const double* qk = qs + (c * EPC + e) * GP;
+            double qv[GP];
 #pragma unroll
-            for (int e = 0; e < EPC; ++e) qr[g][c * EPC + e] = qs[g * D + (sub + c * TPC) * EPC + e];
+            for (int g = 0; g < GP; g += 2) {
+                const double2 t = *reinterpret_cast<const double2*>(qk + g);
+                qv[g] = t.x;
+                qv[g + 1] = t.y;
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) acc[g] = fma(qv[g], xv[e], acc[g]);
+        }
+    }
     const double sq = sqrt((double)D);
-    for (int r = cl; r < kChunk; r += CPP) {
-        double acc[G];
+    const bool valid = r < nv;
+    double lg[G];
 #pragma unroll
-        for (int g = 0; g < G; ++g) acc[g] = 0.0;
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) {
-            const uint4 raw = *reinterpret_cast<const uint4*>(tile + r * ROWB + (sub + c * TPC) * 16);
-            const T* x = reinterpret_cast<const T*>(&raw);
-#pragma unroll
-            for (int e = 0; e < EPC; ++e) {
-                const double xv = elem<T>::to_d(x[e]);
-#pragma unroll
-                for (int g = 0; g < G; ++g) acc[g] = fma(qr[g][c * EPC + e], xv, acc[g]);
-            }
-        }
-#pragma unroll
-        for (int g = 0; g < G; ++g)
-#pragma unroll
-            for (int o = 1; o < TPC; o <<= 1) acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], o);
-        if (sub == 0 && r < nv) {
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const double v = acc[g] / sq;
-                lgs[g * kChunk + r] = v;
-                logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
-            }
-        }
+    for (int g = 0; g < G; ++g) {
+        lg[g] = acc[g] / sq;
+        if (valid) logits[((size_t)l * G + g) * cand_cap + i0 + r] = lg[g];
     }
     if (!cstats) return;
-    __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (w < G) {
-        double m = -INFINITY;
-        for (int r = lane; r < nv; r += 32) m = fmax(m, lgs[w * kChunk + r]);
-        m = warp_max(m);
-        double z = 0.0;
-        for (int r = lane; r < nv; r += 32) {
-            const int id = cand ? cand[(size_t)l * cand_cap + i0 + r] : i0 + r;
-            z += (double)lv_size[(size_t)l * kcap + id] * exp(lgs[w * kChunk + r] - m);
-        }
-        z = warp_sum(z);
+    const int id = valid ? (cand ? cand[(size_t)l * cand_cap + i0 + r] : i0 + r) : 0;
+    const double nsz = valid ? (double)lv_size[(size_t)l * kcap + id] : 0.0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const double m = warp_max(valid ? lg[g] : -INFINITY);
+        const double z = warp_sum(valid ? nsz * exp(lg[g] - m) : 0.0);
         if (lane == 0) {
-            cstats[(((size_t)l * n_chunks + chunk) * G + w) * 2] = m;
-            cstats[(((size_t)l * n_chunks + chunk) * G + w) * 2 + 1] = z;
+            red[(w * G + g) * 2] = m;
+            red[(w * G + g) * 2 + 1] = z;
         }
+    }
+    __syncthreads();
+    if (threadIdx.x < G) {
+        const int g = threadIdx.x;
+        double M = -INFINITY;
+        for (int ww = 0; ww < kTiledThreads / 32; ++ww) M = fmax(M, red[(ww * G + g) * 2]);
+        double Z = 0.0;
+        for (int ww = 0; ww < kTiledThreads / 32; ++ww) {
+            const double m = red[(ww * G + g) * 2];
+            if (m != -INFINITY) Z += red[(ww * G + g) * 2 + 1] * exp(m - M);
+        }
+        cstats[(((size_t)l * n_chunks + chunk) * G + g) * 2] = M;
+        cstats[(((size_t)l * n_chunks + chunk) * G + g) * 2 + 1] = Z;
     }
 }
 
@@ -162,6 +178,14 @@ centroid_logits_tiled(const double* __restrict__ q_lk, const T* __restrict__ kc,
 // K10 selection. One CTA per ledger.
 
 constexpr int kSelThreads = 1024;
+constexpr int kBitonicMax = 8192;
+
+__host__ __device__ __forceinline__ int sort_width(int cap) {
+    int p = 1;
+    while (p < cap) p <<= 1;
+    if (p > kBitonicMax) p = cap;  // radix path only needs cap entries
+    return p > cap ? p : cap;
+}
 
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
 __device__ __forceinline__ double dsum(double a, double b) { return a + b; }
@@ -173,11 +197,14 @@ __device__ void select_core(const int l, const double* __restrict__ logits, cons
                             const uint8_t* __restrict__ eflag, const int32_t* __restrict__ n_extra, int ecap,
                             const int64_t* __restrict__ budget, uint8_t* __restrict__ flag,
                             int32_t* __restrict__ sel_tokens, const double* __restrict__ cstats, int n_chunks,
-                            unsigned char* smem_raw) {
+                            unsigned char* smem_raw, int smem_n) {
     const int n = n_cand[l];
-    unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem_raw);  // [cand_cap]
-    int* sizes = reinterpret_cast<int*>(keys + cand_cap);                         // [cand_cap]
-    int* ids = sizes + cand_cap;                                                  // [cand_cap]
+    // smem: keys / ids / pos sized P = max(cand_cap, bitonic width), sizes [cand_cap]
+    const int P = sort_width(smem_n);
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem_raw);  // [P]
+    int* ids = reinterpret_cast<int*>(keys + P);                                  // [P]
+    int* pos = ids + P;                                                           // [P]
+    int* sizes = pos + P;                                                         // [smem_n]
     __shared__ double red[32];
     __shared__ unsigned int hist_w[256];
     __shared__ unsigned int hist_c[256];
@@ -246,6 +273,60 @@ __device__ void select_core(const int l, const double* __restrict__ logits, cons
     long long total = 0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) total += sizes[i];
     total = block_reduce(total, reinterpret_cast<long long*>(red), [](long long a, long long b) { return a + b; });
+
+    int np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    if (np2 <= kBitonicMax) {
+        // ---- bitonic sort of (key asc, id asc) in smem, then a size prefix sum in sorted order:
+        // candidate at sorted rank k is selected iff sum of sizes of ranks < k is < B.
+        for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+            pos[i] = i;
+            if (i >= n) {
+                keys[i] = ~0ull;
+                ids[i] = 0x7fffffff;
+            }
+        }
+        __syncthreads();
+        for (int k = 2; k <= np2; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+                    const int ixj = i ^ j;
+                    if (ixj > i) {
+                        const unsigned long long ka = keys[i], kb = keys[ixj];
+                        const int ia = ids[i], ib = ids[ixj];
+                        const bool gt = ka > kb || (ka == kb && ia > ib);
+                        if (gt == ((i & k) == 0)) {
+                            keys[i] = kb;
+                            keys[ixj] = ka;
+                            ids[i] = ib;
+                            ids[ixj] = ia;
+                            const int t = pos[i];
+                            pos[i] = pos[ixj];
+                            pos[ixj] = t;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        __shared__ int scan_s[33];
+        long long base = 0, tok = 0;
+        for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+            const int i = i0 + threadIdx.x;
+            const int sz = i < n ? sizes[pos[i]] : 0;
+            int tot;
+            const long long before = base + block_exclusive_scan(sz, scan_s, &tot);
+            if (i < n) {
+                const bool sel = before < B;
+                flag[(size_t)l * cand_cap + pos[i]] = sel ? 1 : 0;
+                if (sel) tok += sz;
+            }
+            base += tot;
+        }
+        tok = block_reduce(tok, reinterpret_cast<long long*>(red), [](long long a, long long b) { return a + b; });
+        if (threadIdx.x == 0 && sel_tokens) sel_tokens[l] = (int32_t)tok;
+        return;
+    }
 
     // crossing key (key*, id*): smallest composite key with W(<=) >= B. None -> select all.
     unsigned long long kstar = ~0ull;
@@ -348,10 +429,10 @@ select_kernel(const double* __restrict__ logits, const int32_t* __restrict__ can
               int cand_cap, const int32_t* __restrict__ lv_size, int lv_cap, const double* __restrict__ elogits,
               const int32_t* __restrict__ esize, const uint8_t* __restrict__ eflag, const int32_t* __restrict__ n_extra,
               int ecap, const int64_t* __restrict__ budget, uint8_t* __restrict__ flag,
-              int32_t* __restrict__ sel_tokens, const double* __restrict__ cstats, int n_chunks) {
+              int32_t* __restrict__ sel_tokens, const double* __restrict__ cstats, int n_chunks, int smem_n) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     select_core<G>(blockIdx.x, logits, cand, n_cand, cand_cap, lv_size, lv_cap, elogits, esize, eflag, n_extra, ecap,
-                   budget, flag, sel_tokens, cstats, n_chunks, smem_raw);
+                   budget, flag, sel_tokens, cstats, n_chunks, smem_raw, smem_n);
 }
 
 // ---------------------------------------------------------------------------
@@ -481,11 +562,11 @@ __global__ void __launch_bounds__(kSelThreads)
 select_worklist_kernel(const double* __restrict__ logits, const int32_t* __restrict__ cand,
                        const int32_t* __restrict__ n_cand, int cand_cap, const int64_t* __restrict__ budget,
                        uint8_t* __restrict__ flag, int32_t* __restrict__ sel_tokens,
-                       const double* __restrict__ cstats, int n_chunks, MPA_WORKLIST_PARAMS) {
+                       const double* __restrict__ cstats, int n_chunks, int smem_n, MPA_WORKLIST_PARAMS) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int l = blockIdx.x;
     select_core<G>(l, logits, cand, n_cand ? n_cand : fcount, cand_cap, fsize, fcap, clogits, csize, cflag, ccount,
-                   ccap, budget, flag, sel_tokens, cstats, n_chunks, smem_raw);
+                   ccap, budget, flag, sel_tokens, cstats, n_chunks, smem_raw, smem_n);
     __syncthreads();
     worklist_body<G>(l, gridDim.x, MPA_WORKLIST_ARGS(cand, n_cand, cand_cap, flag, logits));
 }
@@ -519,7 +600,7 @@ extern "C" int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group
 #define MPA_TILED(T, D)                                                                                              \
     {                                                                                                                \
         auto kern = centroid_logits_tiled<T, kG, D>;                                                                 \
-        const size_t smem = sizeof(double) * kG * (D + kChunk) + (size_t)kChunk * (D * sizeof(T) + 16);             \
+        const size_t smem = sizeof(double) * (D * ((kG + 1) & ~1) + 8 * kG) + (size_t)kChunk * (D * sizeof(T) + 16); \
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
         kern<<<grid, kTiledThreads, smem, st>>>(q_lk, (const T*)lv->kc, lv->cap, lv->count, lv->size, cand, n_cand,  \
                                                 cand_cap, logits, chunk_stats, nch);                                 \
@@ -553,26 +634,28 @@ extern "C" int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group
     return check_launch("mpa_centroid_logits");
 }
 
-static const int kSelectMaxCap = 13312;
+static const int kSelectMaxCap = 11264;  // radix path: 20 B of smem per candidate
 
 extern "C" int mpa_select(const double* logits, int group, const int32_t* cand, const int32_t* n_cand, int cand_cap,
                           const int32_t* lv_size, int lv_cap, const double* elogits, const int32_t* esize,
                           const uint8_t* eflag, const int32_t* n_extra, int ecap, const int64_t* budget,
-                          int n_ledgers, uint8_t* flag, int32_t* sel_tokens, const double* chunk_stats,
+                          int n_ledgers, uint8_t* flag, int32_t* sel_tokens, const double* chunk_stats, int n_max,
                           void* stream) {
     MPA_REQUIRE(logits && n_cand && lv_size && budget && flag, MPA_ERR_ARG, "mpa_select: null argument");
     MPA_REQUIRE(!elogits || (esize && eflag && n_extra), MPA_ERR_ARG, "mpa_select: incomplete extras");
-    MPA_REQUIRE(cand_cap <= kSelectMaxCap, MPA_ERR_UNSUPPORTED, "mpa_select: cand_cap %d > %d", cand_cap,
+    if (n_max <= 0 || n_max > cand_cap) n_max = cand_cap;
+    MPA_REQUIRE(n_max <= kSelectMaxCap, MPA_ERR_UNSUPPORTED, "mpa_select: %d candidates > %d", n_max,
                 kSelectMaxCap);
     if (n_ledgers <= 0) return 0;
-    const size_t smem = (size_t)cand_cap * 16;
+    const size_t smem = (size_t)sort_width(n_max) * 16 + (size_t)n_max * 4;
     const int nch = ceil_div(cand_cap, kChunk);
     cudaStream_t st = (cudaStream_t)stream;
     MPA_DISPATCH_G(group, {
         auto kern = select_kernel<kG>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<n_ledgers, kSelThreads, smem, st>>>(logits, cand, n_cand, cand_cap, lv_size, lv_cap, elogits, esize,
-                                                   eflag, n_extra, ecap, budget, flag, sel_tokens, chunk_stats, nch);
+                                                   eflag, n_extra, ecap, budget, flag, sel_tokens, chunk_stats, nch,
+                                                   n_max);
     });
     return check_launch("mpa_select");
 }
@@ -583,24 +666,25 @@ extern "C" int mpa_select_worklist(const mpa_level* fine, const mpa_level* coars
                                    const int32_t* sink_end, const int32_t* buffer_start, const int32_t* cache_len,
                                    int n_kv_heads, int n_ledgers, int replacement, uint8_t* flag,
                                    int32_t* sel_tokens, int32_t* tok, int tok_cap, int32_t* rej, float* rej_w,
-                                   int rej_cap, int32_t* stats, void* stream) {
+                                   int rej_cap, int32_t* stats, int n_max, void* stream) {
     MPA_REQUIRE(fine && logits && budget && flag && sink_end && buffer_start && cache_len && tok && rej && rej_w &&
                     stats,
                 MPA_ERR_ARG, "mpa_select_worklist: null argument");
     MPA_REQUIRE(!cflag || (coarse && clogits), MPA_ERR_ARG, "mpa_select_worklist: coarse flags without level");
     MPA_REQUIRE(cand ? n_cand != nullptr : cand_cap >= fine->cap, MPA_ERR_ARG,
                 "mpa_select_worklist: candidate capacity");
-    MPA_REQUIRE(cand_cap <= kSelectMaxCap, MPA_ERR_UNSUPPORTED, "mpa_select_worklist: cand_cap %d > %d", cand_cap,
+    if (n_max <= 0 || n_max > cand_cap) n_max = cand_cap;
+    MPA_REQUIRE(n_max <= kSelectMaxCap, MPA_ERR_UNSUPPORTED, "mpa_select_worklist: %d candidates > %d", n_max,
                 kSelectMaxCap);
     if (n_ledgers <= 0) return 0;
-    const size_t smem = (size_t)cand_cap * 16;
+    const size_t smem = (size_t)sort_width(n_max) * 16 + (size_t)n_max * 4;
     const int nch = ceil_div(cand_cap, kChunk);
     cudaStream_t st = (cudaStream_t)stream;
     MPA_DISPATCH_G(group, {
         auto kern = select_worklist_kernel<kG>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<n_ledgers, kSelThreads, smem, st>>>(
-            logits, cand, n_cand, cand_cap, budget, flag, sel_tokens, chunk_stats, nch, fine->size, fine->off,
+            logits, cand, n_cand, cand_cap, budget, flag, sel_tokens, chunk_stats, nch, n_max, fine->size, fine->off,
             fine->idx, fine->cap, fine->idx_cap, coarse ? coarse->size : nullptr, coarse ? coarse->count : nullptr,
             coarse ? coarse->cap : 0, fine->count, cflag, clogits, sink_end, buffer_start, cache_len, n_kv_heads,
             replacement, tok, tok_cap, rej, rej_w, rej_cap, stats);

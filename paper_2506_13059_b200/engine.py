@@ -74,7 +74,7 @@ class DecodeEngine:
         self.logits = torch.zeros(L, G, self.kcap, dtype=torch.float64, **z)
         self.flag = torch.zeros(L, self.kcap, dtype=torch.uint8, **z)
         self.sel_tokens = torch.zeros(L, dtype=torch.int32, **z)
-        self.cstats = torch.zeros(L, -(-self.kcap // 64), G, 2, dtype=torch.float64, **z)
+        self.cstats = torch.zeros(L, -(-self.kcap // 128), G, 2, dtype=torch.float64, **z)
         self.budget = torch.full((L,), cfg.token_budget, dtype=torch.int64, **z)
         if hier:
             self.clogits = torch.zeros(L, G, self.ccap, dtype=torch.float64, **z)
@@ -83,7 +83,7 @@ class DecodeEngine:
             self.cand = torch.zeros(L, self.kcap, dtype=torch.int32, **z)
             self.n_cand = torch.zeros(L, dtype=torch.int32, **z)
             self.csel_tokens = torch.zeros(L, dtype=torch.int32, **z)
-            self.ccstats = torch.zeros(L, -(-self.ccap // 64), G, 2, dtype=torch.float64, **z)
+            self.ccstats = torch.zeros(L, -(-self.ccap // 128), G, 2, dtype=torch.float64, **z)
         self.tok_cap = tcap
         self.rej_cap = self.kcap + self.ccap
         self.tok = torch.zeros(L, self.tok_cap, dtype=torch.int32, **z)
@@ -181,7 +181,7 @@ class DecodeEngine:
             call("mpa_select_worklist", fine, None, G, ptr(self.logits), None, None, self.kcap, ptr(cs), None, None,
                  ptr(self.budget), ptr(self.sink_end_d), ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv,
                  L, replacement, ptr(self.flag), ptr(self.sel_tokens), ptr(self.tok), self.tok_cap, ptr(self.rej),
-                 ptr(self.rej_w), self.rej_cap, ptr(self.stats), st)
+                 ptr(self.rej_w), self.rej_cap, ptr(self.stats), int(self.led.n_fine.max()), st)
         else:
             if int(self.led.n_coarse.min()) == 0:
                 raise ConfigError("ledger has no coarse clusters")
@@ -191,7 +191,7 @@ class DecodeEngine:
                  ptr(self.clogits), ptr(ccs), st)
             call("mpa_select", ptr(self.clogits), G, None, ptr(self.led.ccount), self.ccap, ptr(self.led.csize),
                  self.ccap, None, None, None, None, 0, ptr(self.cbudget), L, ptr(self.cflag),
-                 ptr(self.csel_tokens), ptr(ccs), st)
+                 ptr(self.csel_tokens), ptr(ccs), int(self.led.n_coarse.max()), st)
             call("mpa_hier_candidates", coarse, ptr(self.cflag), L, ptr(self.cand), ptr(self.n_cand), self.kcap, st)
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, ptr(self.cand), ptr(self.n_cand),
                  self.kcap, ptr(self.logits), ptr(cs), st)
@@ -199,7 +199,7 @@ class DecodeEngine:
                  self.kcap, ptr(cs), ptr(self.cflag), ptr(self.clogits), ptr(self.budget), ptr(self.sink_end_d),
                  ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv, L, replacement, ptr(self.flag),
                  ptr(self.sel_tokens), ptr(self.tok), self.tok_cap, ptr(self.rej), ptr(self.rej_w), self.rej_cap,
-                 ptr(self.stats), st)
+                 ptr(self.stats), int(self.led.n_fine.max()), st)
 
     def fused(self, n_split: int | None = None) -> torch.Tensor:
         S = n_split or self._n_split(self._sparse_units())
