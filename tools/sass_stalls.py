@@ -10,7 +10,7 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"reg
                      capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(out)))
 h = r[1]
-rows = [x for x in r[2:] if len(x) == len(h)]
+rows = [x for x in r[2:] if len(x) == len(h) and x[0].startswith("0x")]
 si = h.index("Warp Stall Sampling (All Samples)")
 reasons = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
 agg = {c: sum(int(x[h.index(c)] or 0) for x in rows) for c in reasons}
