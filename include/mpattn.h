@@ -19,6 +19,7 @@
 #ifndef MPATTN_H
 #define MPATTN_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -108,7 +109,8 @@ int mpa_hier_candidates(const mpa_level* coarse, const uint8_t* cflag, int n_led
  *   tok[l, :]  = sinks [0, min(sink_end, cache_len)) ++ buffer [buffer_start, cache_len)
  *                ++ members of selected fine candidates;  n_tok[l]
  *   rej[l, :]  = rejected centroids as value-row codes (>= 0 fine row, < 0: coarse row -1-code)
- *                with w[l, j, g] = logit + ln(size) (fp32);  n_rej[l]
+ *                with rej_w[l, j, g] = logit + ln(size) (fp32, row stride GP = G <= 4 ? 4 : 8
+ *                floats so a 16-row tile of logits is one aligned bulk copy);  n_rej[l]
  * Fine candidates: (cand, n_cand, flag, logits); coarse rejected (hier only, may be NULL):
  * (clogits, cflag) over the coarse level.  replacement == 0 drops every centroid term
  * ("flat-no-replacement", attention.py:441).  stats is [4, L]: rows n_tok, n_rej, sel_tokens,
@@ -134,17 +136,20 @@ int mpa_select_worklist(const mpa_level* fine, const mpa_level* coarse, int grou
 
 /* K11 + K12 -- fused sparse decode: one online softmax over the exact tokens (K_rot/V gathered
  * by index, logits q_rot . k) and the rejected-centroid pseudo-tokens (logit + ln N, value
- * centroid), split over n_split CTAs per ledger, LSE-merged by the last CTA of each ledger
+ * centroid), LSE-merged in-kernel by the last finisher of each ledger
  * (attention.py:58-87, 120-137, 210-239, 473-498).  tok == NULL: dense decode over
- * [0, n_tok[l]) (the "oracle" comparator, attention.py:90-102).  part_* / ticket are
- * workspace: part_ml [L, n_split, G, 2], part_acc [L, n_split, G, d] fp32, ticket [L] int32
- * (zero-initialised once; the kernel leaves it zeroed).  out: fp32 [n_seq, Hq, d]. */
+ * [0, n_tok[l]) (the "oracle" comparator, attention.py:90-102).  rej_w rows have stride
+ * GP = G <= 4 ? 4 : 8 floats.  bf16 caches with d in {64, 128}: stream-K tensor-core kernel
+ * whose grid is one full wave (n_split <= 0) or n_split CTAs per ledger (used to test that the
+ * result does not depend on the partition); other caches: FFMA kernel with n_split (0: auto)
+ * CTAs per ledger.  workspace: >= mpa_sparse_decode_workspace(...) bytes, zero-filled once
+ * before first use (the kernel leaves its ticket area zeroed).  out: fp32 [n_seq, Hq, d]. */
+size_t mpa_sparse_decode_workspace(int n_ledgers, int group, int head_dim, int dtype, int n_split);
 int mpa_sparse_decode(const mpa_cache* cache, const float* q_rot, int n_kv_heads, int group,
                       const int32_t* tok, const int32_t* n_tok, int tok_cap,
                       const int32_t* rej, const float* rej_w, const int32_t* n_rej, int rej_cap,
                       const void* fine_vc, int fine_cap, const void* coarse_vc, int coarse_cap,
-                      int n_split, float* part_ml, float* part_acc, int32_t* ticket,
-                      float* out, void* stream);
+                      int n_split, void* workspace, size_t workspace_bytes, float* out, void* stream);
 
 /* ------------------------------------------------------------------------------------------
  * Clustering (K2-K8).  A batch of independent k-means "problems" p, each over a contiguous run

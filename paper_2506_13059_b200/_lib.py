@@ -13,7 +13,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpattn.so")
+LIB_PATH = os.environ.get("MPATTN_LIB") or os.path.join(_HERE, "libmpattn.so")  # override: experiments only
 
 MPA_F32, MPA_BF16, MPA_F64 = 0, 1, 2
 MPA_ERR_ARG, MPA_ERR_UNSUPPORTED = 1001, 1002
@@ -68,11 +68,11 @@ _SIGS = {
     "mpa_km_assign_from_level": [_KM, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp],
     "mpa_km_seq_assign": [_KM, _vp, C.c_int, _vp, _vp],
     "mpa_sparse_decode": [C.POINTER(MpaCache), _vp, C.c_int, C.c_int, _vp, _vp, C.c_int, _vp, _vp, _vp,
-                          C.c_int, _vp, C.c_int, _vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp],
+                          C.c_int, _vp, C.c_int, _vp, C.c_int, C.c_int, _vp, C.c_size_t, _vp, _vp],
 }
 
 # symbols that include/mpattn.h declares (checked by tests/test_abi.py)
-EXPORTED = ["mpa_last_error", "mpa_version", *_SIGS]
+EXPORTED = ["mpa_last_error", "mpa_version", "mpa_sparse_decode_workspace", *_SIGS]
 
 
 def _load():
@@ -84,6 +84,8 @@ def _load():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = C.c_int
+    lib.mpa_sparse_decode_workspace.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
+    lib.mpa_sparse_decode_workspace.restype = C.c_size_t
     lib.mpa_last_error.restype = C.c_char_p
     lib.mpa_version.restype = C.c_char_p
     return lib

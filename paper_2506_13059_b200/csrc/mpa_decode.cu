@@ -11,18 +11,28 @@
 //
 // One online softmax per q-head covers every item of a ledger (kv-head): exact tokens
 // (K_rot / V rows gathered by index) and rejected-centroid pseudo-tokens (logit + ln N,
-// value centroid). Items are split over n_split CTAs per ledger balanced by bytes (a token
-// costs two rows, a centroid one); the last CTA of a ledger (atomic ticket) LSE-merges the
-// split partials and writes the output, so the step needs no separate merge launch.
+// value centroid).  Partials of one ledger are LSE-merged by whoever finishes it last
+// (atomic ticket), so a step needs no separate merge launch.
 //
-// Two implementations share that structure:
-//   * decode_mma_kernel (bf16, d in {64,128}, G <= 8): per-warp 16-item tiles staged in
-//     swizzled smem by cp.async (3-4 stages in flight), S = K q^T and O^T += V^T P^T on the
-//     tensor cores with mma.sync m16n8k16 (tokens on M, q-heads on N=8).  q and P are split
-//     into bf16 hi + lo parts packed into the 8 MMA columns (G <= 4) so the only bf16
-//     rounding left is the KV cache itself.  Base-2 online softmax.
+// Two implementations:
+//   * decode_sk_kernel (bf16, d in {64,128}, G <= 8) -- the serving path.  A persistent,
+//     stream-K scheduled grid (one wave: SMs x resident CTAs) walks the concatenated 16-item
+//     tiles of ALL ledgers; CTA c owns a contiguous, byte-balanced range of that tile space
+//     (a token tile costs 2 units -- K and V rows --, a centroid tile 1), so the work per CTA
+//     is equal whatever the batch, budget or selection.  Each warp owns a ring of NST stages
+//     and streams its tiles (every NW-th tile of the CTA range) through it with one
+//     cp.async.bulk (TMA bulk engine, UBLKCP) per 256-byte row, completing on an mbarrier,
+//     so each warp keeps NST-1 tiles of gathers in flight with two instructions of issue
+//     cost.  Rows land in padded (272-byte) smem rows, conflict-free for ldmatrix.
+//     S = K q^T and O^T += V^T P^T run on the tensor cores (mma.sync m16n8k16, tokens on M,
+//     q-heads on N=8); q and P are split into bf16 hi + lo parts packed into the 8 MMA
+//     columns (G <= 4) so the only bf16 rounding left is the KV cache itself.  Base-2 online
+//     softmax with a lazy (threshold 2^8) rescale.  A warp writes one partial per ledger it
+//     touched; the last arriving warp of a ledger merges them.
 //   * decode_ffma_kernel (any dtype, any even d): warp per item, FFMA, natural-log softmax,
-//     fp32 accurate expf -- the fp32 parity mode (1e-5).
+//     fp32 accurate expf, n_split CTAs per ledger -- the fp32 parity mode (1e-5).
+#include <cuda.h>
+
 #include <climits>
 #include <cstdlib>
 
@@ -31,6 +41,12 @@
 namespace mpa {
 
 constexpr float kLog2e = 1.4426950408889634f;
+
+// padded logit stride of the rejected-centroid list (rej_w rows): 4 floats for G <= 4, else 8
+__host__ __device__ constexpr int rej_stride(int G) { return G <= 4 ? 4 : 8; }
+
+// ============================================================================
+// FFMA path (split_range over n_split CTAs per ledger)
 
 // Item range of split s of a ledger: tokens cost 2 units (K + V rows), centroids 1 unit.
 struct SplitRange {
@@ -48,8 +64,7 @@ __device__ __forceinline__ SplitRange split_range(int nt, int nr, int s, int S) 
     return r;
 }
 
-// Last-CTA merge of the n_split partials of ledger l (m in the kernel's log base).
-template <bool BASE2>
+// Last-CTA merge of the n_split partials of ledger l.
 __device__ void merge_splits(int l, int S, int G, int d, const float* part_ml, const float* part_acc, float* out) {
     for (int idx = threadIdx.x; idx < G * d; idx += blockDim.x) {
         const int g = idx / d, k = idx - g * d;
@@ -60,7 +75,7 @@ __device__ void merge_splits(int l, int S, int G, int d, const float* part_ml, c
             for (int s = 0; s < S; ++s) {
                 const float m = __ldcg(part_ml + (((size_t)l * S + s) * G + g) * 2);
                 if (m == -INFINITY) continue;
-                const float w = BASE2 ? exp2f(m - M) : expf(m - M);
+                const float w = expf(m - M);
                 sum += w * __ldcg(part_ml + (((size_t)l * S + s) * G + g) * 2 + 1);
                 acc += w * __ldcg(part_acc + (((size_t)l * S + s) * G + g) * d + k);
             }
@@ -84,9 +99,6 @@ __device__ __forceinline__ bool take_ticket(int32_t* ticket, int l, int S) {
     return s_last;
 }
 
-// ============================================================================
-// FFMA path
-
 constexpr int kFfmaWarps = 4;
 
 template <typename T, int G, int NDL>
@@ -97,6 +109,7 @@ decode_ffma_kernel(const T* __restrict__ k_rot, const T* __restrict__ vcache, in
                    const int32_t* __restrict__ n_rej, int rej_cap, const T* __restrict__ fvc, int fcap,
                    const T* __restrict__ cvc, int ccap, int S, float* __restrict__ part_ml,
                    float* __restrict__ part_acc, int32_t* __restrict__ ticket, float* __restrict__ out) {
+    constexpr int GP = rej_stride(G);
     extern __shared__ float sm[];  // [warps][G][2 + d]
     const int l = blockIdx.y, s = blockIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -163,7 +176,7 @@ decode_ffma_kernel(const T* __restrict__ k_rot, const T* __restrict__ vcache, in
             vx[j] = k < d ? elem<T>::to_f(vp[k]) : 0.f;
         }
 #pragma unroll
-        for (int g = 0; g < G; ++g) x[g] = rej_w[((size_t)l * rej_cap + r) * G + g];
+        for (int g = 0; g < G; ++g) x[g] = rej_w[((size_t)l * rej_cap + r) * GP + g];
         absorb(x, vx);
     }
 
@@ -201,23 +214,80 @@ decode_ffma_kernel(const T* __restrict__ k_rot, const T* __restrict__ vcache, in
             part_ml[(((size_t)l * S + s) * G + g) * 2 + 1] = sum;
         }
     }
-    if (take_ticket(ticket, l, S)) merge_splits<false>(l, S, G, d, part_ml, part_acc, out);
+    if (take_ticket(ticket, l, S)) merge_splits(l, S, G, d, part_ml, part_acc, out);
 }
 
 // ============================================================================
-// Tensor-core path (bf16, mma.sync m16n8k16)
+// Tensor-core stream-K path (bf16)
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async16(unsigned dst, const void* src, int bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
 }
-__device__ __forceinline__ void cp_async4(unsigned dst, const void* src, int bytes) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N> __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ bool mbar_try_wait(unsigned bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+// one TMA bulk copy global -> this CTA's shared memory, completing on an mbarrier; KV rows are
+// streamed once per step, so they are marked evict-first in L2
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+        : "memory");
+}
+// TMA tile::gather4: rows r0..r3, columns [col, col + 64) of a 2D bf16 map (box 64 x 1, 128B
+// swizzle) -> 4 x 128 B at dst (sm_100a)
+__device__ __forceinline__ void tma_gather4(unsigned dst, const CUtensorMap* map, int col, int r0, int r1, int r2,
+                                            int r3, unsigned bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar), "l"(policy)
+        : "memory");
+}
+// one box (1 row x 64 columns) of the same map
+__device__ __forceinline__ void tma_row(unsigned dst, const CUtensorMap* map, int col, int row, unsigned bar,
+                                        uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(row), "r"(bar), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+    unsigned pred = 0;
+    asm volatile("{\n .reg .b32 rx;\n .reg .pred px;\n elect.sync rx|px, %1;\n selp.b32 %0, 1, 0, px;\n}\n"
+                 : "+r"(pred)
+                 : "r"(0xffffffffu));
+    return pred != 0;
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void cp_async4(unsigned dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
 
 __device__ __forceinline__ void ldsm_x4(unsigned addr, unsigned (&r)[4]) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
@@ -247,47 +317,275 @@ __device__ __forceinline__ unsigned pack_bf16(float lo, float hi) {
 }
 __device__ __forceinline__ float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
-template <int D> struct TileGeom {
-    static constexpr int kChunks = D / 8;           // 16-byte chunks per row
-    static constexpr int kRowBytes = D * 2;
-    static constexpr int kMatBytes = 16 * kRowBytes;  // one 16-row K or V tile
-    __device__ static __forceinline__ unsigned off(int row, int chunk) {
-        return row * kRowBytes + ((chunk ^ (row & 7)) << 4);
+// Stream-K schedule over the concatenated tiles of all ledgers.  Ledger l owns tiles
+// [tp[l], tp[l+1]): ceil(nt/16) token tiles (16 tokens: K + V rows, 8 KB) then ceil(nr/32)
+// centroid tiles (32 value centroids, 8 KB, + their logits) -- equal bytes, so equal cost; an
+// empty ledger gets one empty token tile so that every ledger is finalised.  CTA c of Ce owns
+// tiles [T c / Ce, T (c+1) / Ce) of the T = tp[L] total.
+constexpr int kMinTiles = 16;  // minimum tiles per CTA (small batches use fewer CTAs)
+
+#ifdef MPA_DEBUG_TRACE
+// per-CTA phase timestamps (globaltimer ns) for timeline experiments: [cta][8]
+__device__ unsigned long long g_dbg[4096 * 8];
+__device__ __forceinline__ void dbg_stamp(int slot) {
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_dbg[blockIdx.x * 8 + slot] = t;
     }
+}
+#else
+__device__ __forceinline__ void dbg_stamp(int) {}
+#endif
+
+// byte offset of 16-byte chunk ch of row r in a TMA 128B-swizzled 16-row tile (64-column halves)
+__device__ __forceinline__ unsigned swz(int r, int ch) {
+    return (unsigned)((ch >> 3) * 2048 + r * 128 + (((ch & 7) ^ (r & 7)) << 4));
+}
+
+template <int G, int D, int NW, int NST>
+struct SkGeom {
+    static constexpr int kHalves = D / 64;           // 64-column halves per row
+    static constexpr int kMatB = 16 * D * 2;         // one 16-row K or V tile
+    static constexpr int kLgB = 32 * rej_stride(G) * 4;  // centroid-tile logits
+    static constexpr int kStageB = 2 * kMatB;        // K + V (token tile) or 2 x V (centroid tile)
+    static constexpr int kWarpB = NST * kStageB;
+    static constexpr int kStagesB = NW * kWarpB;
+    static constexpr int kLgAllB = NW * NST * kLgB;  // logits of every stage, after the tiles
+    static constexpr int kBarB = NW * NST * 8 + kLgAllB;
+    static constexpr int kRing = 8;                  // row-id ring: tiles whose ids are in smem
+    static constexpr int kIdB = NW * kRing * 32 * 4;
+    static constexpr int kPS = G * (D + 2);          // floats per partial
+    static size_t smem(int L, int C) { return 1024 + (size_t)kStagesB + kBarB + kIdB + sizeof(int) * (L + C + 2); }
 };
 
-constexpr int kMmaWarps = 4;
-constexpr int kSegTiles = 64;  // tiles whose row ids are staged in smem at a time
-
-// PACKED: G <= 4, columns 0..3 carry the hi parts of q / P, columns 4..7 the lo parts.
-// Otherwise (G <= 8) hi and lo run as two separate MMAs.
-template <int G, int D, int NST>
-__global__ void __launch_bounds__(kMmaWarps * 32)
-decode_mma_kernel(const __nv_bfloat16* __restrict__ k_rot, const __nv_bfloat16* __restrict__ vcache, int tcap,
-                  const float* __restrict__ q_rot, const int32_t* __restrict__ tok, const int32_t* __restrict__ n_tok,
-                  int tok_cap, const int32_t* __restrict__ rej, const float* __restrict__ rej_w,
-                  const int32_t* __restrict__ n_rej, int rej_cap, const __nv_bfloat16* __restrict__ fvc, int fcap,
-                  const __nv_bfloat16* __restrict__ cvc, int ccap, int S, float* __restrict__ part_ml,
-                  float* __restrict__ part_acc, int32_t* __restrict__ ticket, float* __restrict__ out) {
+template <int G, int D, int NW, int NST>
+__global__ void __launch_bounds__(NW * 32, 2)
+decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                 const __grid_constant__ CUtensorMap tm_fvc, const __grid_constant__ CUtensorMap tm_cvc, int tcap,
+                 const float* __restrict__ q_rot, const int32_t* __restrict__ tok, const int32_t* __restrict__ n_tok,
+                 int tok_cap, const int32_t* __restrict__ rej, const float* __restrict__ rej_w,
+                 const int32_t* __restrict__ n_rej, int rej_cap, int fcap, int ccap, int L, float* __restrict__ part,
+                 int32_t* __restrict__ ticket, float* __restrict__ out) {
+    dbg_stamp(0);
+    using Geo = SkGeom<G, D, NW, NST>;
     constexpr bool PACKED = G <= 4;
     constexpr int KS = D / 16;  // k-steps for QK, m-tiles for PV
-    using Geo = TileGeom<D>;
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int l = blockIdx.y, s = blockIdx.x;
+    constexpr int GP = rej_stride(G);
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int gr = lane >> 2, tq = lane & 3;
-    const int nt = n_tok[l], nr = rej ? n_rej[l] : 0;
-    const SplitRange R = split_range(nt, nr, s, S);
-    const int ntt = (R.t1 - R.t0 + 15) >> 4, nrt = (R.r1 - R.r0 + 15) >> 4, NT = ntt + nrt;
+    const int C = gridDim.x, c = blockIdx.x;
 
-    unsigned char* wbase = smem + (size_t)w * NST * 2 * Geo::kMatBytes;
-    const unsigned wbase_s = smem_u32(wbase);
-
-    // ---- q fragments (B operand, col-major 16x8 per k-step), pre-scaled by log2(e)
-    unsigned qhi[KS][2], qlo[KS][2];
+    // ---- per-ledger tile prefix sum (every CTA computes the same schedule)
+    int* tp = reinterpret_cast<int*>(smem + Geo::kStagesB + Geo::kBarB + Geo::kIdB);
+    int* idring = reinterpret_cast<int*>(smem + Geo::kStagesB + Geo::kBarB) + w * Geo::kRing * 32;
     {
+        __shared__ int scan[33];
+        int base = 0;
+        for (int l0 = 0; l0 < L; l0 += blockDim.x) {
+            const int l = l0 + threadIdx.x;
+            int n = 0;
+            if (l < L) {
+                const int nt = (__ldg(n_tok + l) + 15) >> 4, nr = rej ? (__ldg(n_rej + l) + 31) >> 5 : 0;
+                n = nt + nr > 0 ? nt + nr : 1;
+            }
+            int tot;
+            const int e = block_exclusive_scan(n, scan, &tot);
+            if (l < L) tp[l] = base + e;
+            base += tot;
+        }
+        if (threadIdx.x == 0) tp[L] = base;
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_k)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_v)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_fvc)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_cvc)) : "memory");
+    }
+    const unsigned bar0 = smem_u32(smem + Geo::kStagesB + Geo::kLgAllB) + w * NST * 8;
+    const unsigned lgbase = smem_u32(smem + Geo::kStagesB) + w * NST * Geo::kLgB;
+    if (lane == 0)
+        for (int s = 0; s < NST; ++s) mbar_init(bar0 + s * 8, 1);
+    fence_mbar_init();
+    __syncthreads();
+    const int T = tp[L];
+    const int Ce = max(1, min(C, T / kMinTiles));
+    if (c >= Ce) return;  // surplus CTA: no CTA-wide barrier follows for it
+    int* cbt = tp + (L + 1);  // [Ce + 1] first tile of each CTA
+    for (int cc = threadIdx.x; cc <= Ce; cc += blockDim.x) cbt[cc] = (int)((long long)T * cc / Ce);
+    __syncthreads();
+    dbg_stamp(1);
+    auto cta_begin = [&](int cc) -> int { return cbt[cc]; };
+    auto ledger_of_tile = [&](int g) -> int {  // largest l with tp[l] <= g
+        int lo = 0, hi = L - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (tp[mid] <= g) lo = mid;
+            else hi = mid - 1;
+        }
+        return lo;
+    };
+    const int g0 = cta_begin(c), g1 = cta_begin(c + 1);
+    const int my_n = g1 - g0 > w ? (g1 - g0 - w + NW - 1) / NW : 0;
+    const unsigned wbase = smem_u32(smem) + w * Geo::kWarpB;
+    const uint64_t policy = evict_first_policy();
+
+    // ---- tile metadata for this warp's i-th tile (global tile g0 + w + i*NW)
+    struct Meta {
+        int l, kind, i0, nv;  // ledger, 0 token / 1 centroid, first item, valid rows
+    };
+    struct Walker {  // walks this warp's tiles in order, caching the current ledger's counts
+        int l, beg, end, nt, nr, ntt;
+    };
+    auto meta_of = [&](int i, Walker& wk) -> Meta {
+        const int g = g0 + w + i * NW;
+        if (wk.l < 0 || g >= wk.end) {
+            int l = wk.l < 0 ? ledger_of_tile(g) : wk.l;
+            while (l + 1 < L && tp[l + 1] <= g) ++l;
+            wk.l = l;
+            wk.beg = tp[l];
+            wk.end = tp[l + 1];
+            wk.nt = __ldg(n_tok + l);
+            wk.nr = rej ? __ldg(n_rej + l) : 0;
+            wk.ntt = (wk.nt + 15) >> 4;
+            if (wk.ntt == 0 && wk.nr == 0) wk.ntt = 1;  // empty ledger: one empty token tile
+        }
+        const int t = g - wk.beg;
+        Meta m;
+        m.l = wk.l;
+        if (t < wk.ntt) {
+            m.kind = 0;
+            m.i0 = t * 16;
+            m.nv = max(0, min(16, wk.nt - m.i0));
+        } else {
+            m.kind = 1;
+            m.i0 = (t - wk.ntt) * 32;
+            m.nv = min(32, wk.nr - m.i0);
+        }
+        return m;
+    };
+    // row ids reach smem kRing-1 tiles before their gathers are issued (cp.async, one per lane);
+    // padding rows repeat row 0
+    constexpr int kAhead = Geo::kRing - 1;
+    auto prefetch_ids = [&](int j, const Meta& m) {
+        const int rows = m.kind == 0 ? 16 : 32;
+        if (lane < rows && m.nv > 0 && (m.kind == 1 || tok)) {
+            const int row = lane < m.nv ? lane : 0;
+            const int32_t* src = m.kind == 0 ? tok + (size_t)m.l * tok_cap + m.i0 + row
+                                             : rej + (size_t)m.l * rej_cap + m.i0 + row;
+            cp_async4(smem_u32(idring + (j % Geo::kRing) * 32 + lane), src);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    // ids of rows [r0, r0 + 16) of tile j; every lane reads the same smem words and the values
+    // are broadcast from lane 0 so the compiler keeps them in uniform registers
+    auto ids16 = [&](int j, const Meta& m, int r0, int (&id)[16]) {
+        if (m.kind == 0 && !tok) {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) id[r] = m.i0 + (r < m.nv ? r : 0);
+        } else {
+            const int4* q4 = reinterpret_cast<const int4*>(idring + (j % Geo::kRing) * 32 + r0);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int4 t = q4[v];
+                id[4 * v] = __shfl_sync(0xffffffffu, t.x, 0);
+                id[4 * v + 1] = __shfl_sync(0xffffffffu, t.y, 0);
+                id[4 * v + 2] = __shfl_sync(0xffffffffu, t.z, 0);
+                id[4 * v + 3] = __shfl_sync(0xffffffffu, t.w, 0);
+            }
+        }
+    };
+    // gathers of 16 value-centroid rows (codes >= 0 fine, < 0 coarse) into one 16-row tile; a
+    // group of 4 that straddles the fine -> coarse boundary of the list uses one 2D tile copy
+    // (box 1 row x 64 columns) per row
+    auto gather_centroids = [&](unsigned dst, const int (&id)[16], int l, unsigned bar) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int a0 = id[4 * q], a1 = id[4 * q + 1], a2 = id[4 * q + 2], a3 = id[4 * q + 3];
+            const bool fine = a0 >= 0 && a1 >= 0 && a2 >= 0 && a3 >= 0;
+            const bool coarse = a0 < 0 && a1 < 0 && a2 < 0 && a3 < 0;
+#pragma unroll
+            for (int h = 0; h < Geo::kHalves; ++h) {
+                const unsigned off = dst + h * 2048 + q * 512;
+                if (fine) {
+                    const int fb = l * fcap;
+                    tma_gather4(off, &tm_fvc, h * 64, fb + a0, fb + a1, fb + a2, fb + a3, bar, policy);
+                } else if (coarse) {
+                    const int cb = l * ccap - 1;
+                    tma_gather4(off, &tm_cvc, h * 64, cb - a0, cb - a1, cb - a2, cb - a3, bar, policy);
+                } else {
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int a = id[4 * q + r];
+                        if (a >= 0) tma_row(off + r * 128, &tm_fvc, h * 64, l * fcap + a, bar, policy);
+                        else tma_row(off + r * 128, &tm_cvc, h * 64, l * ccap - 1 - a, bar, policy);
+                    }
+                }
+            }
+        }
+    };
+    auto issue = [&](int j, int st, const Meta& m) {
+        const unsigned kst = wbase + st * Geo::kStageB, vst = kst + Geo::kMatB, lgs = lgbase + st * Geo::kLgB;
+        const unsigned bar = bar0 + st * 8;
+        int id[16], id2[16];
+        if (m.nv > 0) {
+            ids16(j, m, 0, id);
+            if (m.kind == 1) ids16(j, m, 16, id2);
+        }
+        __syncwarp();
+        if (!elect_one()) return;
+        fence_proxy_async();  // generic reads of this stage (previous tile) before the async writes
+        if (m.nv <= 0) {
+            mbar_expect_tx(bar, 0);
+            return;
+        }
+        if (m.kind == 0) {
+            mbar_expect_tx(bar, 2 * Geo::kMatB);
+            const int base = m.l * tcap;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int h = 0; h < Geo::kHalves; ++h) {
+                    const unsigned off = h * 2048 + q * 512;
+                    tma_gather4(kst + off, &tm_k, h * 64, base + id[4 * q], base + id[4 * q + 1],
+                                base + id[4 * q + 2], base + id[4 * q + 3], bar, policy);
+                    tma_gather4(vst + off, &tm_v, h * 64, base + id[4 * q], base + id[4 * q + 1],
+                                base + id[4 * q + 2], base + id[4 * q + 3], bar, policy);
+                }
+        } else {
+            const unsigned lg_bytes = m.nv * GP * 4;
+            mbar_expect_tx(bar, 2 * Geo::kMatB + lg_bytes);
+            gather_centroids(kst, id, m.l, bar);
+            gather_centroids(vst, id2, m.l, bar);
+            bulk_g2s(lgs, rej_w + ((size_t)m.l * rej_cap + m.i0) * GP, lg_bytes, bar, policy);
+        }
+    };
+
+    // ---- per-ledger softmax state
+    unsigned qhi[KS][2], qlo[PACKED ? 1 : KS][2];
+    const int hA = PACKED ? 2 * (tq & 1) : 2 * tq, hB = hA + 1;
+    float mA, mB, sA, sB;
+    float o[KS][4];
+    float o2[PACKED ? 1 : KS][4];
+    auto reset_state = [&]() {
+        mA = mB = -INFINITY;
+        sA = sB = 0.f;
+#pragma unroll
+        for (int i = 0; i < KS; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[i][j] = 0.f;
+        if (!PACKED) {
+#pragma unroll
+            for (int i = 0; i < (PACKED ? 1 : KS); ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) o2[i][j] = 0.f;
+        }
+    };
+    auto load_q = [&](int l) {
         auto qv = [&](int head, int k) -> float {
-            return head < G ? q_rot[((size_t)l * G + head) * D + k] * kLog2e : 0.f;
+            return head < G ? __ldg(q_rot + ((size_t)l * G + head) * D + k) * kLog2e : 0.f;
         };
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
@@ -303,246 +601,315 @@ decode_mma_kernel(const __nv_bfloat16* __restrict__ k_rot, const __nv_bfloat16* 
                     const float a = qv(gr, k), b = qv(gr, k + 1);
                     const float ah = bf16_round(a), bh = bf16_round(b);
                     qhi[ks][half] = pack_bf16(ah, bh);
-                    qlo[ks][half] = pack_bf16(a - ah, b - bh);
+                    qlo[PACKED ? 0 : ks][half] = pack_bf16(a - ah, b - bh);
                 }
-            }
-        }
-    }
-
-    // heads owned by this lane's two accumulator columns
-    const int hA = PACKED ? 2 * (tq & 1) : 2 * tq, hB = hA + 1;
-    float mA = -INFINITY, mB = -INFINITY, sA = 0.f, sB = 0.f;
-    float o[KS][4];
-    float o2[PACKED ? 1 : KS][4];
-#pragma unroll
-    for (int i = 0; i < KS; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) o[i][j] = 0.f;
-    if (!PACKED) {
-#pragma unroll
-        for (int i = 0; i < (PACKED ? 1 : KS); ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) o2[i][j] = 0.f;
-    }
-
-    const size_t cache_base = (size_t)l * tcap;
-    // Row ids (token id, or centroid code) of a segment of kSegTiles virtual tiles are staged in
-    // smem by the whole CTA before the per-warp pipelines run over that segment, so no
-    // dependent index load ever sits between a tile and its cp.async issue.
-    constexpr int kNoRow = INT_MIN;
-    int* ids_s = reinterpret_cast<int*>(smem + (size_t)kMmaWarps * NST * 2 * Geo::kMatBytes);
-    int seg = 0;
-    auto fetch = [&](int vt) -> int { return ids_s[(vt - seg) * 16 + (lane >> 1)]; };
-    auto issue = [&](int vt, int st, int id) {
-        const unsigned kst = wbase_s + st * 2 * Geo::kMatBytes, vst = kst + Geo::kMatBytes;
-        const int row = lane >> 1;  // 2 lanes per row
-        const bool ok = id != kNoRow;
-        if (vt < ntt) {
-            const int tokid = ok ? id : 0;
-            const __nv_bfloat16* kp = k_rot + (cache_base + tokid) * D;
-            const __nv_bfloat16* vp = vcache + (cache_base + tokid) * D;
-#pragma unroll
-            for (int j = 0; j < Geo::kChunks / 2; ++j) {
-                const int ch = (lane & 1) * (Geo::kChunks / 2) + j;
-                cp_async16(kst + Geo::off(row, ch), kp + ch * 8, ok ? 16 : 0);
-                cp_async16(vst + Geo::off(row, ch), vp + ch * 8, ok ? 16 : 0);
-            }
-        } else {
-            const int code = ok ? id : 0;
-            const __nv_bfloat16* vp =
-                code >= 0 ? fvc + ((size_t)l * fcap + code) * D : cvc + ((size_t)l * ccap + (-1 - code)) * D;
-#pragma unroll
-            for (int j = 0; j < Geo::kChunks / 2; ++j) {
-                const int ch = (lane & 1) * (Geo::kChunks / 2) + j;
-                cp_async16(vst + Geo::off(row, ch), vp + ch * 8, ok ? 16 : 0);
-            }
-            // the tile's reused lookup logits (16 x G fp32) ride along in the unused K slot
-            const int r0 = R.r0 + (vt - ntt) * 16;
-            for (int e = lane; e < 16 * G; e += 32) {
-                const int rr = e / G;
-                const bool okr = r0 + rr < R.r1;
-                cp_async4(kst + e * 4, rej_w + ((size_t)l * rej_cap + (okr ? r0 + rr : 0)) * G + (e - rr * G),
-                          okr ? 4 : 0);
             }
         }
     };
 
-    for (seg = 0; seg < NT; seg += kSegTiles) {
-        const int seg_n = min(kSegTiles, NT - seg);
-        for (int k = threadIdx.x; k < seg_n * 16; k += blockDim.x) {
-            const int vt = seg + (k >> 4), row = k & 15;
-            int id;
-            if (vt < ntt) {
-                const int t = R.t0 + vt * 16 + row;
-                id = t < R.t1 ? (tok ? __ldg(tok + (size_t)l * tok_cap + t) : t) : kNoRow;
-            } else {
-                const int r = R.r0 + (vt - ntt) * 16 + row;
-                id = r < R.r1 ? __ldg(rej + (size_t)l * rej_cap + r) : kNoRow;
-            }
-            ids_s[k] = id;
-        }
-        __syncthreads();
-        // this warp's tiles in the segment: vt = seg + w, seg + w + W, ...
-        const int my_n = seg_n > w ? (seg_n - w + kMmaWarps - 1) / kMmaWarps : 0;
+    // online softmax (column = head) + O^T += V^T P^T over 16 rows with logits x (log2 units,
+    // rows gr / gr+8, heads hA / hB); the reference max only moves when a tile exceeds it by
+    // more than 2^8, so most tiles skip the accumulator rescale
+    auto absorb16 = [&](float (&x)[4], unsigned vtile) {
+        if (hA >= G) { x[0] = x[0] == -INFINITY ? -INFINITY : 0.f; x[2] = x[2] == -INFINITY ? -INFINITY : 0.f; }
+        if (hB >= G) { x[1] = x[1] == -INFINITY ? -INFINITY : 0.f; x[3] = x[3] == -INFINITY ? -INFINITY : 0.f; }
+        float tA = fmaxf(x[0], x[2]), tB = fmaxf(x[1], x[3]);
 #pragma unroll
-        for (int i = 0; i < NST - 1; ++i) {
-            if (i < my_n) issue(seg + w + i * kMmaWarps, i, fetch(seg + w + i * kMmaWarps));
-            cp_commit();
+        for (int off = 4; off < 32; off <<= 1) {
+            tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, off));
+            tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, off));
         }
-        for (int i = 0; i < my_n; ++i) {
-            {
-                const int nxt = i + NST - 1;
-                if (nxt < my_n) issue(seg + w + nxt * kMmaWarps, nxt % NST, fetch(seg + w + nxt * kMmaWarps));
-                cp_commit();
-            }
-            cp_wait<NST - 1>();
-            __syncwarp();
-            const int vt = seg + w + i * kMmaWarps, st = i % NST;
-            const unsigned kst = wbase_s + st * 2 * Geo::kMatBytes, vst = kst + Geo::kMatBytes;
-
-            // logits x[row r / r+8][head hA / hB] in log2 units
-            float x[4];
-            if (vt < ntt) {
-                float c[4] = {0.f, 0.f, 0.f, 0.f};
-                float c2[4] = {0.f, 0.f, 0.f, 0.f};
-    #pragma unroll
-                for (int ks = 0; ks < KS; ++ks) {
-                    unsigned a[4];
-                    const int row = (lane & 7) + ((lane >> 3) & 1) * 8, ch = ks * 2 + (lane >> 4);
-                    ldsm_x4(kst + Geo::off(row, ch), a);
-                    mma_bf16(c, a, qhi[ks][0], qhi[ks][1]);
-                    if (!PACKED) mma_bf16(c2, a, qlo[ks][0], qlo[ks][1]);
-                }
-                if (PACKED) {
-    #pragma unroll
-                    for (int j = 0; j < 4; ++j) x[j] = c[j] + __shfl_xor_sync(0xffffffffu, c[j], 2);
-                } else {
-    #pragma unroll
-                    for (int j = 0; j < 4; ++j) x[j] = c[j] + c2[j];
-                }
-                const int base = R.t0 + (vt << 4);
-                if (base + gr >= R.t1) x[0] = x[1] = -INFINITY;
-                if (base + gr + 8 >= R.t1) x[2] = x[3] = -INFINITY;
-            } else {
-                const int base = R.r0 + ((vt - ntt) << 4);
-                const float* lg = reinterpret_cast<const float*>(wbase + (size_t)st * 2 * Geo::kMatBytes);
-    #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int rr = gr + (j >> 1) * 8;
-                    const int h = (j & 1) ? hB : hA;
-                    x[j] = base + rr < R.r1 ? (h < G ? lg[rr * G + h] * kLog2e : 0.f) : -INFINITY;
-                }
-            }
-            // padded heads (>= G) must stay finite
-            if (hA >= G) { x[0] = x[0] == -INFINITY ? -INFINITY : 0.f; x[2] = x[2] == -INFINITY ? -INFINITY : 0.f; }
-            if (hB >= G) { x[1] = x[1] == -INFINITY ? -INFINITY : 0.f; x[3] = x[3] == -INFINITY ? -INFINITY : 0.f; }
-
-            // online softmax (column = head) over the 16 rows of this tile
-            float tA = fmaxf(x[0], x[2]), tB = fmaxf(x[1], x[3]);
-    #pragma unroll
-            for (int off = 4; off < 32; off <<= 1) {
-                tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, off));
-                tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, off));
-            }
-            const float nA = fmaxf(mA, tA), nB = fmaxf(mB, tB);
-            const float cA = exp2f(mA - nA), cB = exp2f(mB - nB);  // mA=-inf -> 0
+        const bool upA = tA > mA + 8.f, upB = tB > mB + 8.f;
+        if (__any_sync(0xffffffffu, upA || upB)) {
+            const float nA = upA ? tA : mA, nB = upB ? tB : mB;
+            const float cA = exp2f(mA - nA), cB = exp2f(mB - nB);  // mA = -inf -> 0
             mA = nA;
             mB = nB;
-            const float p0 = exp2f(x[0] - nA), p1 = exp2f(x[1] - nB), p2 = exp2f(x[2] - nA), p3 = exp2f(x[3] - nB);
-            sA = sA * cA + p0 + p2;
-            sB = sB * cB + p1 + p3;
-    #pragma unroll
+            sA *= cA;
+            sB *= cB;
+#pragma unroll
             for (int mt = 0; mt < KS; ++mt) {
                 o[mt][0] *= cA; o[mt][1] *= cB; o[mt][2] *= cA; o[mt][3] *= cB;
-                if (!PACKED) { o2[mt][0] *= cA; o2[mt][1] *= cB; o2[mt][2] *= cA; o2[mt][3] *= cB; }
-            }
-            // P^T fragments (B operand): hi/lo split, transposed with movmatrix
-            unsigned b0, b1, b2 = 0, b3 = 0;
-            {
-                const float h0 = bf16_round(p0), h1 = bf16_round(p1), h2 = bf16_round(p2), h3 = bf16_round(p3);
-                if (PACKED) {
-                    const bool hi = tq < 2;
-                    b0 = movm_t(hi ? pack_bf16(h0, h1) : pack_bf16(p0 - h0, p1 - h1));
-                    b1 = movm_t(hi ? pack_bf16(h2, h3) : pack_bf16(p2 - h2, p3 - h3));
-                } else {
-                    b0 = movm_t(pack_bf16(h0, h1));
-                    b1 = movm_t(pack_bf16(h2, h3));
-                    b2 = movm_t(pack_bf16(p0 - h0, p1 - h1));
-                    b3 = movm_t(pack_bf16(p2 - h2, p3 - h3));
+                if (!PACKED) {
+                    o2[PACKED ? 0 : mt][0] *= cA; o2[PACKED ? 0 : mt][1] *= cB;
+                    o2[PACKED ? 0 : mt][2] *= cA; o2[PACKED ? 0 : mt][3] *= cB;
                 }
             }
-    #pragma unroll
-            for (int mt = 0; mt < KS; ++mt) {
-                unsigned a[4];
-                const int j = lane >> 3;
-                const int row = (lane & 7) + (j >> 1) * 8, ch = mt * 2 + (j & 1);
-                ldsm_x4_t(vst + Geo::off(row, ch), a);
-                mma_bf16(o[mt], a, b0, b1);
-                if (!PACKED) mma_bf16(o2[mt], a, b2, b3);
-            }
-            __syncwarp();
         }
-        cp_wait<0>();
-        __syncthreads();  // before the next segment's ids overwrite ids_s
-    }
-    cp_wait<0>();
-
-    // ---- warp -> CTA partial
-#pragma unroll
-    for (int off = 4; off < 32; off <<= 1) {
-        sA += __shfl_xor_sync(0xffffffffu, sA, off);
-        sB += __shfl_xor_sync(0xffffffffu, sB, off);
-    }
-    if (PACKED) {
-#pragma unroll
-        for (int mt = 0; mt < KS; ++mt)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) o[mt][j] += __shfl_xor_sync(0xffffffffu, o[mt][j], 2);
-    } else {
-#pragma unroll
-        for (int mt = 0; mt < KS; ++mt)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) o[mt][j] += o2[mt][j];
-    }
-    __syncthreads();  // all warps done with their stage buffers: reuse smem for the reduction
-    float* red = reinterpret_cast<float*>(smem);  // [warps][8 heads][2 + D]
-    const bool owner = PACKED ? tq < 2 : true;
-    if (owner) {
-        float* rA = red + ((size_t)w * 8 + hA) * (2 + D);
-        float* rB = red + ((size_t)w * 8 + hB) * (2 + D);
-        if (gr == 0) {
-            rA[0] = mA; rA[1] = sA;
-            rB[0] = mB; rB[1] = sB;
+        const float p0 = exp2f(x[0] - mA), p1 = exp2f(x[1] - mB), p2 = exp2f(x[2] - mA), p3 = exp2f(x[3] - mB);
+        sA += p0 + p2;
+        sB += p1 + p3;
+        // P^T fragments (B operand): hi/lo split, transposed with movmatrix
+        unsigned b0, b1, b2 = 0, b3 = 0;
+        {
+            const float h0 = bf16_round(p0), h1 = bf16_round(p1), h2 = bf16_round(p2), h3 = bf16_round(p3);
+            if (PACKED) {
+                const bool hi = tq < 2;
+                b0 = movm_t(hi ? pack_bf16(h0, h1) : pack_bf16(p0 - h0, p1 - h1));
+                b1 = movm_t(hi ? pack_bf16(h2, h3) : pack_bf16(p2 - h2, p3 - h3));
+            } else {
+                b0 = movm_t(pack_bf16(h0, h1));
+                b1 = movm_t(pack_bf16(h2, h3));
+                b2 = movm_t(pack_bf16(p0 - h0, p1 - h1));
+                b3 = movm_t(pack_bf16(p2 - h2, p3 - h3));
+            }
         }
 #pragma unroll
         for (int mt = 0; mt < KS; ++mt) {
-            rA[2 + mt * 16 + gr] = o[mt][0];
-            rB[2 + mt * 16 + gr] = o[mt][1];
-            rA[2 + mt * 16 + gr + 8] = o[mt][2];
-            rB[2 + mt * 16 + gr + 8] = o[mt][3];
+            unsigned a[4];
+            const int j = lane >> 3;
+            const int row = (lane & 7) + (j >> 1) * 8, ch = mt * 2 + (j & 1);
+            ldsm_x4_t(vtile + swz(row, ch), a);
+            mma_bf16(o[mt], a, b0, b1);
+            if (!PACKED) mma_bf16(o2[PACKED ? 0 : mt], a, b2, b3);
         }
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
-        const int g = idx / D, k = idx - g * D;
-        float M = -INFINITY;
-        for (int ww = 0; ww < kMmaWarps; ++ww) M = fmaxf(M, red[((size_t)ww * 8 + g) * (2 + D)]);
-        float sum = 0.f, a = 0.f;
-        if (M != -INFINITY)
-            for (int ww = 0; ww < kMmaWarps; ++ww) {
-                const float* p = red + ((size_t)ww * 8 + g) * (2 + D);
-                if (p[0] == -INFINITY) continue;
-                const float c = exp2f(p[0] - M);
-                sum += c * p[1];
-                a += c * p[2 + k];
+    };
+
+    // ---- end of a ledger segment of this CTA (every warp calls it for every ledger of the CTA
+    // range, in order): warp partials -> CTA partial through an L2-resident per-CTA scratch; a
+    // ledger wholly inside the CTA range is finalised here, otherwise the CTA partial goes to
+    // slot (c + l) and the last of the ledger's CTAs (atomic ticket) merges them.
+    __shared__ int s_last;
+    float* wscr = part + ((size_t)(C + L) + (size_t)c * NW + w) * Geo::kPS;
+    auto seg_end = [&](int l) {
+        float fA = sA, fB = sB;
+#pragma unroll
+        for (int off = 4; off < 32; off <<= 1) {
+            fA += __shfl_xor_sync(0xffffffffu, fA, off);
+            fB += __shfl_xor_sync(0xffffffffu, fB, off);
+        }
+        if (PACKED) {
+#pragma unroll
+            for (int mt = 0; mt < KS; ++mt)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) o[mt][j] += __shfl_xor_sync(0xffffffffu, o[mt][j], 2);
+        } else {
+#pragma unroll
+            for (int mt = 0; mt < KS; ++mt)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) o[mt][j] += o2[PACKED ? 0 : mt][j];
+        }
+        const bool owner = PACKED ? tq < 2 : true;
+        if (owner) {
+            if (gr == 0) {
+                if (hA < G) { wscr[2 * hA] = mA; wscr[2 * hA + 1] = fA; }
+                if (hB < G) { wscr[2 * hB] = mB; wscr[2 * hB + 1] = fB; }
             }
-        part_acc[(((size_t)l * S + s) * G + g) * D + k] = a;
-        if (k == 0) {
-            part_ml[(((size_t)l * S + s) * G + g) * 2] = M;
-            part_ml[(((size_t)l * S + s) * G + g) * 2 + 1] = sum;
+#pragma unroll
+            for (int mt = 0; mt < KS; ++mt) {
+                if (hA < G) {
+                    wscr[2 * G + hA * D + mt * 16 + gr] = o[mt][0];
+                    wscr[2 * G + hA * D + mt * 16 + gr + 8] = o[mt][2];
+                }
+                if (hB < G) {
+                    wscr[2 * G + hB * D + mt * 16 + gr] = o[mt][1];
+                    wscr[2 * G + hB * D + mt * 16 + gr + 8] = o[mt][3];
+                }
+            }
+        }
+        __syncthreads();
+        dbg_stamp(5);
+        const bool whole = tp[l] >= g0 && tp[l + 1] <= g1;
+        const float* wp0 = part + ((size_t)(C + L) + (size_t)c * NW) * Geo::kPS;
+        float* dst = part + (size_t)(c + l) * Geo::kPS;
+        for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+            const int g = idx / D, k = idx - g * D;
+            float mw[NW], M = -INFINITY;
+#pragma unroll
+            for (int ww = 0; ww < NW; ++ww) {
+                mw[ww] = wp0[(size_t)ww * Geo::kPS + 2 * g];
+                M = fmaxf(M, mw[ww]);
+            }
+            float S = 0.f, A = 0.f;
+            if (M != -INFINITY) {
+#pragma unroll
+                for (int ww = 0; ww < NW; ++ww) {
+                    if (mw[ww] == -INFINITY) continue;
+                    const float sc = exp2f(mw[ww] - M);
+                    S += sc * wp0[(size_t)ww * Geo::kPS + 2 * g + 1];
+                    A += sc * wp0[(size_t)ww * Geo::kPS + 2 * G + g * D + k];
+                }
+            }
+            if (whole) {
+                out[(size_t)l * G * D + idx] = A / S;
+            } else {
+                dst[2 * G + idx] = A;
+                if (k == 0) {
+                    dst[2 * g] = M;
+                    dst[2 * g + 1] = S;
+                }
+            }
+        }
+        if (!whole) {
+            __threadfence();
+            __syncthreads();
+            dbg_stamp(6);
+            // first CTA meeting ledger l: the one whose range contains tile tp[l]
+            int cf = (int)min((long long)Ce - 1, (long long)tp[l] * Ce / T);
+            while (cf + 1 < Ce && cta_begin(cf + 1) <= tp[l]) ++cf;
+            while (cf > 0 && cta_begin(cf) > tp[l]) --cf;
+            // every CTA owns >= kMinTiles tiles, so the CTAs meeting ledger l are cf .. cf + np - 1
+            // and their partials sit in consecutive slots cf + l ..
+            __shared__ int s_np;
+            if (threadIdx.x == 0) {
+                int np = 0;
+                for (int cc = cf; cc < Ce && cbt[cc] < tp[l + 1]; ++cc) ++np;
+                s_np = np;
+                const int prev = atomicAdd(ticket + l, 1);
+                s_last = prev == np - 1;
+                if (s_last) ticket[l] = 0;  // ready for the next launch / graph replay
+            }
+            __syncthreads();
+            dbg_stamp(7);
+            if (s_last) {
+                __threadfence();
+                const int np = s_np;
+                constexpr int PER = (G * D + NW * 32 - 1) / (NW * 32);
+                float M[PER], S[PER], A[PER];
+#pragma unroll
+                for (int j = 0; j < PER; ++j) {
+                    M[j] = -INFINITY;
+                    S[j] = 0.f;
+                    A[j] = 0.f;
+                }
+                for (int p0 = 0; p0 < np; p0 += 4) {
+                    // four partials' values for this thread's outputs, all loads in flight together
+                    float pm[4][PER], ps[4][PER], pa[4][PER];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int p = p0 + u;
+                        const float* P = part + (size_t)(cf + l + (p < np ? p : 0)) * Geo::kPS;
+#pragma unroll
+                        for (int j = 0; j < PER; ++j) {
+                            const int idx = threadIdx.x + j * NW * 32;
+                            const int g = min(idx, G * D - 1) / D;
+                            const bool ok = p < np && idx < G * D;
+                            pm[u][j] = ok ? __ldcg(P + 2 * g) : -INFINITY;
+                            ps[u][j] = ok ? __ldcg(P + 2 * g + 1) : 0.f;
+                            pa[u][j] = ok ? __ldcg(P + 2 * G + idx) : 0.f;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int j = 0; j < PER; ++j) {
+                            const float m = pm[u][j];
+                            if (m == -INFINITY) continue;
+                            if (m > M[j]) {
+                                const float sc = exp2f(M[j] - m);
+                                S[j] = S[j] * sc + ps[u][j];
+                                A[j] = A[j] * sc + pa[u][j];
+                                M[j] = m;
+                            } else {
+                                const float sc = exp2f(m - M[j]);
+                                S[j] += ps[u][j] * sc;
+                                A[j] += pa[u][j] * sc;
+                            }
+                        }
+                }
+#pragma unroll
+                for (int j = 0; j < PER; ++j) {
+                    const int idx = threadIdx.x + j * NW * 32;
+                    if (idx < G * D) out[(size_t)l * G * D + idx] = A[j] / S[j];
+                }
+            }
+        }
+        __syncthreads();  // the scratch is reused by the next segment
+    };
+
+    // ---- pipeline: ids run kAhead tiles ahead of the gathers, gathers NST-1 tiles ahead of the math
+    Walker wp{-1, 0, 0, 0, 0, 0}, wi = wp, wc = wp;
+    int pf = 0, issued = 0;
+    auto prefetch_next = [&]() {
+        if (pf < my_n) prefetch_ids(pf, meta_of(pf, wp));
+        else asm volatile("cp.async.commit_group;\n" ::);
+        ++pf;
+    };
+    auto issue_next = [&]() {
+        if (issued < my_n) {
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(kAhead - 1));
+            __syncwarp();
+            const Meta m = meta_of(issued, wi);
+            issue(issued, issued % NST, m);
+            ++issued;
+            prefetch_next();
+        }
+    };
+#pragma unroll 1
+    for (int i = 0; i < kAhead; ++i) prefetch_next();
+#pragma unroll 1
+    for (int i = 0; i < NST - 1; ++i) issue_next();
+
+    // ledgers met by this CTA: lf .. ll (every warp closes each of them, in order)
+    const int lf = ledger_of_tile(g0), ll = ledger_of_tile(g1 - 1);
+    int cur_l = lf;
+    bool fresh = true;  // q fragments of cur_l not loaded yet
+    reset_state();
+#pragma unroll 1
+    for (int i = 0; i < my_n; ++i) {
+        issue_next();
+        const Meta m = meta_of(i, wc);
+        while (m.l != cur_l) {
+            seg_end(cur_l);
+            ++cur_l;
+            reset_state();
+            fresh = true;
+        }
+        if (fresh) {
+            load_q(cur_l);
+            fresh = false;
+        }
+        const int st = i % NST;
+        mbar_wait(bar0 + st * 8, (i / NST) & 1);
+        if (i == 0) dbg_stamp(2);
+        if (m.nv <= 0) continue;
+        const unsigned kst = wbase + st * Geo::kStageB, vst = kst + Geo::kMatB, lgs = lgbase + st * Geo::kLgB;
+        if (m.kind == 0) {
+            // S = K q^T on the tensor cores, logits in log2 units
+            float c1[4] = {0.f, 0.f, 0.f, 0.f};
+            float c2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                unsigned a[4];
+                const int row = (lane & 7) + ((lane >> 3) & 1) * 8, ch = ks * 2 + (lane >> 4);
+                ldsm_x4(kst + swz(row, ch), a);
+                mma_bf16(c1, a, qhi[ks][0], qhi[ks][1]);
+                if (!PACKED) mma_bf16(c2, a, qlo[PACKED ? 0 : ks][0], qlo[PACKED ? 0 : ks][1]);
+            }
+            float x[4];
+            if (PACKED) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) x[j] = c1[j] + __shfl_xor_sync(0xffffffffu, c1[j], 2);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) x[j] = c1[j] + c2[j];
+            }
+            if (gr >= m.nv) x[0] = x[1] = -INFINITY;
+            if (gr + 8 >= m.nv) x[2] = x[3] = -INFINITY;
+            absorb16(x, vst);
+        } else {
+            // rejected centroids: reused lookup logits + ln N, two 16-row value tiles
+            const float* lg = reinterpret_cast<const float*>(smem + (lgs - smem_u32(smem)));
+#pragma unroll
+            for (int sub = 0; sub < 2; ++sub) {
+                if (sub * 16 >= m.nv) break;
+                float x[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int rr = sub * 16 + gr + (j >> 1) * 8;
+                    const int h = (j & 1) ? hB : hA;
+                    x[j] = rr < m.nv ? (h < G ? lg[rr * GP + h] * kLog2e : 0.f) : -INFINITY;
+                }
+                absorb16(x, sub ? vst : kst);
+            }
         }
     }
-    if (take_ticket(ticket, l, S)) merge_splits<true>(l, S, G, D, part_ml, part_acc, out);
+    dbg_stamp(3);
+    for (; cur_l <= ll; ++cur_l) {
+        seg_end(cur_l);
+        reset_state();
+    }
+    dbg_stamp(4);
 }
 
 }  // namespace mpa
@@ -550,6 +917,42 @@ decode_mma_kernel(const __nv_bfloat16* __restrict__ k_rot, const __nv_bfloat16* 
 using namespace mpa;
 
 namespace {
+
+int g_num_sms = 0;
+
+int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+// serving configuration of the stream-K kernel: 4 warps x 3 stages (~104 KB smem, 2 CTAs / SM)
+constexpr int kSkWarps = 4, kSkStages = 3;
+
+int sk_ctas_per_sm() {
+    static int occ = 0;
+    if (!occ) occ = 2;  // fixed by the smem budget (2 x 104 KB of the 228 KB per SM)
+    return occ;
+}
+
+// CTA count of the stream-K grid: n_split <= 0 -> one full wave; else n_split CTAs per ledger
+int sk_grid(int L, int n_split) {
+    const int wave = num_sms() * sk_ctas_per_sm();
+    if (n_split <= 0) return wave;
+    long long c = (long long)n_split * L;
+    if (c > 8 * wave) c = 8 * wave;
+    return (int)(c < 1 ? 1 : c);
+}
+
+bool mma_path(const mpa_cache* c, int group);
+
+size_t ws_floats_ffma(int L, int G, int d, int S) { return (size_t)L * S * G * (2 + d); }
+size_t ws_floats_sk(int L, int G, int d, int C) { return (size_t)(C + L + C * kSkWarps) * G * (d + 2); }
+size_t ws_ticket_bytes(int L) { return ((size_t)L * sizeof(int32_t) + 255) & ~(size_t)255; }
 
 template <int G>
 int launch_ffma(const mpa_cache* c, const float* q_rot, const int32_t* tok, const int32_t* n_tok, int tok_cap,
@@ -585,27 +988,56 @@ int launch_ffma(const mpa_cache* c, const float* q_rot, const int32_t* tok, cons
     return check_launch("mpa_sparse_decode(ffma)");
 }
 
+// 2D tensor map over rows of d bf16 (box: 64 columns x 1 row, 128B swizzle) for TMA gathers.
+// Encoding is pure host work; the last few maps are cached by (address, rows, d).
+int bf16_rows_map(CUtensorMap* out, const void* base, long long rows, int d) {
+    struct Entry {
+        const void* base;
+        long long rows;
+        int d;
+        CUtensorMap map;
+    };
+    static Entry cache[16];
+    static int next = 0;
+    for (auto& e : cache)
+        if (e.base == base && e.rows == rows && e.d == d) {
+            *out = e.map;
+            return 0;
+        }
+    MPA_REQUIRE(rows > 0 && rows < (1ll << 31), MPA_ERR_UNSUPPORTED, "tensor map: %lld rows", rows);
+    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+    cuuint32_t box[2] = {64, 1};
+    cuuint32_t estr[2] = {1, 1};
+    const CUresult r = cuTensorMapEncodeTiled(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    MPA_REQUIRE(r == CUDA_SUCCESS, MPA_ERR_ARG, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    cache[next] = Entry{base, rows, d, *out};
+    next = (next + 1) % 16;
+    return 0;
+}
+
 template <int G, int D>
-int launch_mma(const mpa_cache* c, const float* q_rot, const int32_t* tok, const int32_t* n_tok, int tok_cap,
-               const int32_t* rej, const float* rej_w, const int32_t* n_rej, int rej_cap, const void* fvc, int fcap,
-               const void* cvc, int ccap, int S, float* pml, float* pacc, int32_t* ticket, float* out,
-               cudaStream_t st) {
-    constexpr int NST = 3;
-    dim3 grid(S, c->n_ledgers);
-    const size_t stage_bytes = (size_t)kMmaWarps * NST * 2 * TileGeom<D>::kMatBytes + kSegTiles * 16 * sizeof(int);
-    const size_t red_bytes = sizeof(float) * kMmaWarps * 8 * (2 + D);
-    const size_t smem = stage_bytes > red_bytes ? stage_bytes : red_bytes;
-    auto kern = decode_mma_kernel<G, D, NST>;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
-    }
-    kern<<<grid, kMmaWarps * 32, smem, st>>>((const __nv_bfloat16*)c->k_rot, (const __nv_bfloat16*)c->v, c->tcap,
-                                             q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej, rej_cap,
-                                             (const __nv_bfloat16*)fvc, fcap, (const __nv_bfloat16*)cvc, ccap, S, pml,
-                                             pacc, ticket, out);
-    return check_launch("mpa_sparse_decode(mma)");
+int launch_sk(const mpa_cache* c, const float* q_rot, const int32_t* tok, const int32_t* n_tok, int tok_cap,
+              const int32_t* rej, const float* rej_w, const int32_t* n_rej, int rej_cap, const void* fvc, int fcap,
+              const void* cvc, int ccap, int C, float* part, int32_t* ticket, float* out, cudaStream_t st) {
+    using Geo = SkGeom<G, D, kSkWarps, kSkStages>;
+    const int L = c->n_ledgers;
+    const size_t smem = Geo::smem(L, C);
+    MPA_REQUIRE(smem <= 227 * 1024, MPA_ERR_UNSUPPORTED, "mpa_sparse_decode: %d ledgers exceed the smem schedule", L);
+    auto kern = decode_sk_kernel<G, D, kSkWarps, kSkStages>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    CUtensorMap tk, tv, tf, tc;
+    int rc = bf16_rows_map(&tk, c->k_rot, (long long)L * c->tcap, D);
+    if (!rc) rc = bf16_rows_map(&tv, c->v, (long long)L * c->tcap, D);
+    if (!rc) rc = fvc ? bf16_rows_map(&tf, fvc, (long long)L * fcap, D) : (tf = tk, 0);
+    if (!rc) rc = cvc ? bf16_rows_map(&tc, cvc, (long long)L * ccap, D) : (tc = tf, 0);
+    if (rc) return rc;
+    kern<<<C, kSkWarps * 32, smem, st>>>(tk, tv, tf, tc, c->tcap, q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej,
+                                         rej_cap, fcap, ccap, L, part, ticket, out);
+    return check_launch("mpa_sparse_decode(stream-K mma)");
 }
 
 int g_force_ffma = -1;
@@ -618,37 +1050,69 @@ bool force_ffma() {
     return g_force_ffma == 1;
 }
 
+bool mma_path(const mpa_cache* c, int group) {
+    return c->dtype == MPA_BF16 && (c->head_dim == 64 || c->head_dim == 128) && group <= 8 && !force_ffma();
+}
+
+int ffma_splits(int L, int n_split) {
+    if (n_split > 0) return n_split;
+    const int s = (2 * num_sms() * 2 + L - 1) / L;
+    return s < 1 ? 1 : (s > 64 ? 64 : s);
+}
+
 }  // namespace
+
+#ifdef MPA_DEBUG_TRACE
+extern "C" int mpa_debug_trace(unsigned long long* host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_dbg, sizeof(unsigned long long) * n);
+}
+#endif
+
+extern "C" size_t mpa_sparse_decode_workspace(int n_ledgers, int group, int head_dim, int dtype, int n_split) {
+    if (n_ledgers <= 0 || group <= 0 || head_dim <= 0) return 0;
+    mpa_cache probe{};
+    probe.dtype = dtype;
+    probe.head_dim = head_dim;
+    size_t fl;
+    if (mma_path(&probe, group)) fl = ws_floats_sk(n_ledgers, group, head_dim, sk_grid(n_ledgers, n_split));
+    else fl = ws_floats_ffma(n_ledgers, group, head_dim, ffma_splits(n_ledgers, n_split));
+    return ws_ticket_bytes(n_ledgers) + fl * sizeof(float);
+}
 
 extern "C" int mpa_sparse_decode(const mpa_cache* c, const float* q_rot, int n_kv_heads, int group,
                                  const int32_t* tok, const int32_t* n_tok, int tok_cap, const int32_t* rej,
                                  const float* rej_w, const int32_t* n_rej, int rej_cap, const void* fine_vc,
-                                 int fine_cap, const void* coarse_vc, int coarse_cap, int n_split, float* part_ml,
-                                 float* part_acc, int32_t* ticket, float* out, void* stream) {
-    MPA_REQUIRE(c && q_rot && n_tok && part_ml && part_acc && ticket && out, MPA_ERR_ARG,
-                "mpa_sparse_decode: null argument");
+                                 int fine_cap, const void* coarse_vc, int coarse_cap, int n_split, void* workspace,
+                                 size_t workspace_bytes, float* out, void* stream) {
+    MPA_REQUIRE(c && q_rot && n_tok && workspace && out, MPA_ERR_ARG, "mpa_sparse_decode: null argument");
     MPA_REQUIRE(!rej || (rej_w && n_rej), MPA_ERR_ARG, "mpa_sparse_decode: rej without weights/counts");
-    MPA_REQUIRE(n_split >= 1, MPA_ERR_ARG, "mpa_sparse_decode: n_split %d", n_split);
     MPA_REQUIRE(c->head_dim >= 2 && c->head_dim % 2 == 0 && c->head_dim <= 256, MPA_ERR_UNSUPPORTED,
                 "mpa_sparse_decode: head_dim %d", c->head_dim);
     (void)n_kv_heads;
-    if (c->n_ledgers <= 0) return 0;
+    const int L = c->n_ledgers;
+    if (L <= 0) return 0;
+    const size_t need = mpa_sparse_decode_workspace(L, group, c->head_dim, c->dtype, n_split);
+    MPA_REQUIRE(workspace_bytes >= need, MPA_ERR_ARG, "mpa_sparse_decode: workspace %zu bytes < %zu", workspace_bytes,
+                need);
     cudaStream_t st = (cudaStream_t)stream;
-    const bool mma_ok = c->dtype == MPA_BF16 && (c->head_dim == 64 || c->head_dim == 128) && group <= 8 &&
-                        !force_ffma();
-    if (mma_ok) {
+    int32_t* ticket = (int32_t*)workspace;
+    float* part = (float*)((char*)workspace + ws_ticket_bytes(L));
+    if (mma_path(c, group)) {
+        const int C = sk_grid(L, n_split);
         MPA_DISPATCH_G(group, {
             if (c->head_dim == 128)
-                return launch_mma<kG, 128>(c, q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej, rej_cap, fine_vc,
-                                           fine_cap, coarse_vc, coarse_cap, n_split, part_ml, part_acc, ticket, out,
-                                           st);
-            return launch_mma<kG, 64>(c, q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej, rej_cap, fine_vc, fine_cap,
-                                      coarse_vc, coarse_cap, n_split, part_ml, part_acc, ticket, out, st);
+                return launch_sk<kG, 128>(c, q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej, rej_cap, fine_vc,
+                                          fine_cap, coarse_vc, coarse_cap, C, part, ticket, out, st);
+            return launch_sk<kG, 64>(c, q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej, rej_cap, fine_vc, fine_cap,
+                                     coarse_vc, coarse_cap, C, part, ticket, out, st);
         });
     }
+    const int S = ffma_splits(L, n_split);
+    float* pml = part;
+    float* pacc = part + (size_t)L * S * group * 2;
     MPA_DISPATCH_G(group, {
         return launch_ffma<kG>(c, q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej, rej_cap, fine_vc, fine_cap,
-                               coarse_vc, coarse_cap, n_split, part_ml, part_acc, ticket, out, st);
+                               coarse_vc, coarse_cap, S, pml, pacc, ticket, out, st);
     });
     return 0;
 }

@@ -504,7 +504,7 @@ __device__ void worklist_body(const int l, const int L, const int32_t* __restric
             const double lnN = log((double)sz);
 #pragma unroll
             for (int g = 0; g < G; ++g)
-                rej_w[((size_t)l * rej_cap + rpos) * G + g] =
+                rej_w[((size_t)l * rej_cap + rpos) * (G <= 4 ? 4 : 8) + g] =
                     (float)(logits[((size_t)l * G + g) * cand_cap + i] + lnN);
         }
         tbase += ttot;
@@ -523,7 +523,7 @@ __device__ void worklist_body(const int l, const int L, const int32_t* __restric
                 const double lnN = log((double)csize[(size_t)l * ccap + c]);
 #pragma unroll
                 for (int g = 0; g < G; ++g)
-                    rej_w[((size_t)l * rej_cap + rpos) * G + g] =
+                    rej_w[((size_t)l * rej_cap + rpos) * (G <= 4 ? 4 : 8) + g] =
                         (float)(clogits[((size_t)l * G + g) * ccap + c] + lnN);
             }
             rbase += rtot;

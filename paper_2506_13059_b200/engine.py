@@ -31,8 +31,6 @@ from .ledger import DeviceLedgers, HostLedger
 import os
 
 NUM_SMS = 148
-MAX_SPLITS = 64
-SPLIT_WAVES = float(os.environ.get("MPA_SPLIT_WAVES", "2"))
 
 
 class DecodeEngine:
@@ -88,11 +86,9 @@ class DecodeEngine:
         self.rej_cap = self.kcap + self.ccap
         self.tok = torch.zeros(L, self.tok_cap, dtype=torch.int32, **z)
         self.rej = torch.zeros(L, self.rej_cap, dtype=torch.int32, **z)
-        self.rej_w = torch.zeros(L, self.rej_cap, G, dtype=torch.float32, **z)
+        self.rej_w = torch.zeros(L, self.rej_cap, 4 if G <= 4 else 8, dtype=torch.float32, **z)
         self.stats = torch.zeros(4, L, dtype=torch.int32, **z)
-        self.part_ml = torch.zeros(L, MAX_SPLITS, G, 2, dtype=torch.float32, **z)
-        self.part_acc = torch.zeros(L, MAX_SPLITS, G, d, dtype=torch.float32, **z)
-        self.ticket = torch.zeros(L, dtype=torch.int32, **z)
+        self.ws = torch.zeros(0, dtype=torch.uint8, **z)  # fused-kernel workspace (grown on demand)
         self.out = torch.zeros(n_seq, self.Hq, d, dtype=torch.float32, **z)
         self.cache_struct = MpaCache(ptr(self.k_rot), ptr(self.k_raw), ptr(self.v), dtype_code(dtype), L, tcap, d)
         self.last_split = 1
@@ -145,20 +141,12 @@ class DecodeEngine:
         self._sync_scalars()
 
     # ------------------------------------------------------------------ decode
-    def _n_split(self, units_per_ledger: float) -> int:
-        """CTAs per ledger for the fused kernel: ~SPLIT_WAVES waves of the 2-CTA/SM residency,
-        but at least ~256 work units (tokens count 2, centroids 1) per CTA."""
-        target_ctas = SPLIT_WAVES * 2 * NUM_SMS
-        s = max(1, round(target_ctas / self.L))
-        s = min(s, max(1, int(units_per_ledger // 256)), MAX_SPLITS)
-        return int(s)
-
-    def _sparse_units(self) -> float:
-        cfg = self.cfg
-        buf = float(np.max(self.cache_len - self.buffer_start))
-        sel = min(cfg.token_budget + float(self.led.max_size.max(initial=0)), float(np.max(self.cache_len)))
-        rej = float(self.led.n_fine.max(initial=0) + self.led.n_coarse.max(initial=0))
-        return 2.0 * (cfg.sink_tokens + buf + sel) + rej
+    def _workspace(self, n_split: int) -> torch.Tensor:
+        """Zero-filled workspace of mpa_sparse_decode (partials + per-ledger tickets)."""
+        need = int(_lib.lib().mpa_sparse_decode_workspace(self.L, self.G, self.d, dtype_code(self.dtype), n_split))
+        if self.ws.numel() < need:
+            self.ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
+        return self.ws
 
     def rotate(self, q: torch.Tensor) -> None:
         q = q.float().contiguous()
@@ -202,15 +190,16 @@ class DecodeEngine:
                  ptr(self.stats), int(self.led.n_fine.max()), st)
 
     def fused(self, n_split: int | None = None) -> torch.Tensor:
-        S = n_split or self._n_split(self._sparse_units())
-        self.last_split = S
+        """K11 + K12 over the current work lists.  n_split None / 0: one full wave of the
+        stream-K grid (bf16) or automatic splits (fp32); > 0: that many CTAs per ledger."""
+        S = int(n_split or 0)
+        ws = self._workspace(S)
         st = stream_ptr()
         rej = None if self.mode == "flat-no-replacement" else self.rej
         ckc = self.led.cvc if self.led.hierarchy else None
         call("mpa_sparse_decode", self.cache_struct, ptr(self.q_rot), self.Hkv, self.G, ptr(self.tok),
              ptr(self.stats[0]), self.tok_cap, ptr(rej), ptr(self.rej_w), ptr(self.stats[1]), self.rej_cap,
-             ptr(self.led.vc), self.kcap, ptr(ckc), self.ccap, S, ptr(self.part_ml), ptr(self.part_acc),
-             ptr(self.ticket), ptr(self.out), st)
+             ptr(self.led.vc), self.kcap, ptr(ckc), self.ccap, S, ptr(ws), ws.numel(), ptr(self.out), st)
         return self.out
 
     def attend(self, q: torch.Tensor, n_split: int | None = None) -> torch.Tensor:
@@ -224,10 +213,10 @@ class DecodeEngine:
     def attend_dense(self, q: torch.Tensor, n_split: int | None = None) -> torch.Tensor:
         """Dense exact attention over [0, cache_len) with the same kernel (K13 comparator)."""
         self.rotate(q)
-        S = n_split or self._n_split(2.0 * float(self.cache_len.max()))
+        S = int(n_split or 0)
+        ws = self._workspace(S)
         call("mpa_sparse_decode", self.cache_struct, ptr(self.q_rot), self.Hkv, self.G, None, ptr(self.ntok_dense_d),
-             0, None, None, None, 0, None, 0, None, 0, S, ptr(self.part_ml), ptr(self.part_acc), ptr(self.ticket),
-             ptr(self.out), stream_ptr())
+             0, None, None, None, 0, None, 0, None, 0, S, ptr(ws), ws.numel(), ptr(self.out), stream_ptr())
         return self.out
 
     # ------------------------------------------------------------------ pipeline

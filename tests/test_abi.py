@@ -51,5 +51,5 @@ def test_argument_errors_without_gpu(lib):
     assert rc == 1001
     assert b"null argument" in lib.mpa_last_error()
     rc = lib.mpa_sparse_decode(None, None, 8, 4, None, None, 0, None, None, None, 0, None, 0, None, 0, 1,
-                               None, None, None, None, None)
+                               None, ctypes.c_size_t(0), None, None)
     assert rc == 1001

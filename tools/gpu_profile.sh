@@ -4,10 +4,12 @@
 set -x
 TAG=${1:-r01}; shift
 mkdir -p gpurun_out
+if [ -z "$NOLAUNCH" ]; then
 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
     --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
     python tools/prof_step.py --steps 2 --dense "$@" > gpurun_out/prof_launch_${TAG}.log 2>&1
+fi
 ncu --profile-from-start off --set full --clock-control none --import-source on \
-    -k 'regex:decode_mma|centroid_logits|select_worklist|rotate|kv_write' -c 6 \
+    -k 'regex:decode_sk|centroid_logits|select_worklist' -c 3 \
     -o gpurun_out/step_${TAG} -f python tools/prof_step.py --steps 1 "$@" > gpurun_out/prof_full_${TAG}.log 2>&1
 tail -2 gpurun_out/prof_launch_${TAG}.log gpurun_out/prof_full_${TAG}.log
