@@ -78,10 +78,14 @@ int mpa_rotate_queries(const float* q, int n_seq, int n_qh, int d, const int32_t
 /* K9 -- centroid lookup logits, fp64: logits[l, g, i] = q_lk[seq, h*G+g] . kc[l, id_i] / sqrt(d)
  * for candidates i < n_cand[l]; id_i = cand[l, i] (cand may be NULL: id_i = i, n = lv->count)
  * (attention.py:267-276 `_scores_per_group` logits).  chunk_stats (optional, d in {64,128}):
- * [L, ceil(cap/64), G, 2] per-64-candidate (max_g, sum N e^(l - max_g)) partials of the normaliser. */
+ * [L, ceil(cap/128), G, 2] per-128-candidate (m_c = max_g l, Z_c = sum N e^(l - m_c)) partials of
+ * the normaliser.  e_local (optional, bf16 centroids only): [L, G, cand_cap] e^(l - m_c), which
+ * lets the selection form e^(l - max) = e_local e^(m_c - max) without per-candidate exps.
+ * n_max (0: cap) bounds the live candidates of every ledger (sizes the grid). */
 int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group, int d,
                         const mpa_level* lv, const int32_t* cand, const int32_t* n_cand,
-                        int cand_cap, double* logits, double* chunk_stats, void* stream);
+                        int cand_cap, double* logits, double* chunk_stats, double* e_local, int n_max,
+                        void* stream);
 
 /* K10 -- Eq. 1 scores and budgeted greedy selection (attention.py:192-207, 267-290).
  * Scores: e_g,i = exp(l_g,i - max_g), Z_g = sum over candidates AND live extras of N * e,
@@ -90,15 +94,16 @@ int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group, int d,
  * sizes: lv_size[l, id_i]; tie key: id_i.  Extras (may be NULL): logits [L, G, ecap] with sizes
  * esize[l, j] that enter only the denominators when eflag[l, j] == 0 (hierarchical union,
  * attention.py:331-334).  Writes flag[l, i] = 1 selected / 0 rejected, sel_tokens[l].
- * n_max (<= cand_cap, 0 = cand_cap) bounds the live candidates per ledger and sizes the shared
- * memory: up to 8192 candidates are bitonic-sorted in smem, larger sets use a size-weighted
- * radix select (at most 11264 candidates). */
+ * n_max (<= cand_cap, 0 = cand_cap) bounds the live candidates per ledger (at most 11264) and
+ * sizes the shared memory; the crossing candidate is found by a size-weighted radix select on
+ * the 64-bit score key then the id.  chunk_stats / e_local: the outputs of mpa_centroid_logits
+ * (both optional). */
 int mpa_select(const double* logits, int group, const int32_t* cand, const int32_t* n_cand,
                int cand_cap, const int32_t* lv_size, int lv_cap,
                const double* elogits, const int32_t* esize, const uint8_t* eflag,
                const int32_t* n_extra, int ecap,
                const int64_t* budget, int n_ledgers, uint8_t* flag, int32_t* sel_tokens,
-               const double* chunk_stats, int n_max, void* stream);
+               const double* chunk_stats, const double* e_local, int n_max, void* stream);
 
 /* Hierarchy stage glue (attention.py:321-329): cand[l] = children of coarse clusters with
  * cflag == 1, promoted in coarse-id order, children ascending; n_cand[l]. */
@@ -127,7 +132,8 @@ int mpa_build_worklist(const mpa_level* fine, const mpa_level* coarse, int group
 /* K10 + work list fused in one launch per ledger: mpa_select over the fine candidates (extras =
  * coarse clusters with cflag == 0, hierarchy only) followed by mpa_build_worklist. */
 int mpa_select_worklist(const mpa_level* fine, const mpa_level* coarse, int group, const double* logits,
-                        const int32_t* cand, const int32_t* n_cand, int cand_cap, const double* chunk_stats,
+                        const double* e_local, const int32_t* cand, const int32_t* n_cand, int cand_cap,
+                        const double* chunk_stats,
                         const uint8_t* cflag, const double* clogits, const int64_t* budget,
                         const int32_t* sink_end, const int32_t* buffer_start, const int32_t* cache_len,
                         int n_kv_heads, int n_ledgers, int replacement, uint8_t* flag,

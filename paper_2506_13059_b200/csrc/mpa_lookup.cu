@@ -575,11 +575,40 @@ select_worklist_kernel(const double* __restrict__ logits, const int32_t* __restr
 
 using namespace mpa;
 
+// serving kernels (mpa_select.cu)
+int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* lv, const int32_t* cand,
+                         const int32_t* n_cand, int cand_cap, double* logits, double* chunk_stats, double* e_local,
+                         int n_chunks, int n_max, cudaStream_t st);
+size_t mpa_select_v2_smem(int n_max);
+int mpa_launch_select_v2(const double* logits, const double* e_local, int group, const int32_t* cand,
+                         const int32_t* n_cand, int cand_cap, const int32_t* lv_size, int lv_cap,
+                         const double* elogits, const int32_t* esize, const uint8_t* eflag, const int32_t* n_extra,
+                         int ecap, const int64_t* budget, int n_ledgers, uint8_t* flag, int32_t* sel_tokens,
+                         const double* chunk_stats, int n_chunks, int n_max, cudaStream_t st);
+int mpa_launch_select_worklist_v2(const mpa_level* fine, const mpa_level* coarse, int group, const double* logits,
+                                  const double* e_local, const int32_t* cand, const int32_t* n_cand, int cand_cap,
+                                  const double* chunk_stats, int n_chunks, const uint8_t* cflag,
+                                  const double* clogits, const int64_t* budget, const int32_t* sink_end,
+                                  const int32_t* buffer_start, const int32_t* cache_len, int n_kv_heads,
+                                  int n_ledgers, int replacement, uint8_t* flag, int32_t* sel_tokens, int32_t* tok,
+                                  int tok_cap, int32_t* rej, float* rej_w, int rej_cap, int32_t* stats, int n_max,
+                                  cudaStream_t st);
+
+// MPA_LOOKUP_V1=1 selects the previous (smem-tiled logits, bitonic select) kernels for A/B runs
+static int g_v1 = -1;
+static bool lookup_v1() {
+    if (g_v1 < 0) {
+        const char* e = getenv("MPA_LOOKUP_V1");
+        g_v1 = (e && e[0] == '1') ? 1 : 0;
+    }
+    return g_v1 == 1;
+}
+
 static int g_logits_tiled = -1;
 
 extern "C" int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group, int d, const mpa_level* lv,
                                    const int32_t* cand, const int32_t* n_cand, int cand_cap, double* logits,
-                                   double* chunk_stats, void* stream) {
+                                   double* chunk_stats, double* e_local, int n_max, void* stream) {
     MPA_REQUIRE(q_lk && lv && logits && lv->kc && lv->count, MPA_ERR_ARG, "mpa_centroid_logits: null argument");
     MPA_REQUIRE(!cand || n_cand, MPA_ERR_ARG, "mpa_centroid_logits: cand without n_cand");
     MPA_REQUIRE(cand ? cand_cap >= 1 : cand_cap >= lv->cap, MPA_ERR_ARG, "mpa_centroid_logits: cand_cap %d too small",
@@ -594,6 +623,9 @@ extern "C" int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group
         const char* e = getenv("MPA_LOGITS_SIMPLE");
         g_logits_tiled = (e && e[0] == '1') ? 0 : 1;
     }
+    if (g_logits_tiled && (d == 64 || d == 128) && lv->dtype == MPA_BF16 && !lookup_v1())
+        return mpa_launch_logits_v2(q_lk, group, d, lv, cand, n_cand, cand_cap, logits, chunk_stats, e_local,
+                                    ceil_div(cap, kChunk), n_max > 0 && n_max < cap ? n_max : cap, st);
     if (g_logits_tiled && (d == 64 || d == 128)) {
         const int nch = ceil_div(cap, kChunk);
         dim3 grid(nch, L);
@@ -639,8 +671,8 @@ static const int kSelectMaxCap = 11264;  // radix path: 20 B of smem per candida
 extern "C" int mpa_select(const double* logits, int group, const int32_t* cand, const int32_t* n_cand, int cand_cap,
                           const int32_t* lv_size, int lv_cap, const double* elogits, const int32_t* esize,
                           const uint8_t* eflag, const int32_t* n_extra, int ecap, const int64_t* budget,
-                          int n_ledgers, uint8_t* flag, int32_t* sel_tokens, const double* chunk_stats, int n_max,
-                          void* stream) {
+                          int n_ledgers, uint8_t* flag, int32_t* sel_tokens, const double* chunk_stats,
+                          const double* e_local, int n_max, void* stream) {
     MPA_REQUIRE(logits && n_cand && lv_size && budget && flag, MPA_ERR_ARG, "mpa_select: null argument");
     MPA_REQUIRE(!elogits || (esize && eflag && n_extra), MPA_ERR_ARG, "mpa_select: incomplete extras");
     if (n_max <= 0 || n_max > cand_cap) n_max = cand_cap;
@@ -650,6 +682,10 @@ extern "C" int mpa_select(const double* logits, int group, const int32_t* cand, 
     const size_t smem = (size_t)sort_width(n_max) * 16 + (size_t)n_max * 4;
     const int nch = ceil_div(cand_cap, kChunk);
     cudaStream_t st = (cudaStream_t)stream;
+    if (!lookup_v1() && mpa_select_v2_smem(n_max) <= 200 * 1024)
+        return mpa_launch_select_v2(logits, e_local, group, cand, n_cand, cand_cap, lv_size, lv_cap, elogits, esize,
+                                    eflag, n_extra, ecap, budget, n_ledgers, flag, sel_tokens, chunk_stats, nch, n_max,
+                                    st);
     MPA_DISPATCH_G(group, {
         auto kern = select_kernel<kG>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -661,7 +697,8 @@ extern "C" int mpa_select(const double* logits, int group, const int32_t* cand, 
 }
 
 extern "C" int mpa_select_worklist(const mpa_level* fine, const mpa_level* coarse, int group, const double* logits,
-                                   const int32_t* cand, const int32_t* n_cand, int cand_cap, const double* chunk_stats,
+                                   const double* e_local, const int32_t* cand, const int32_t* n_cand, int cand_cap,
+                                   const double* chunk_stats,
                                    const uint8_t* cflag, const double* clogits, const int64_t* budget,
                                    const int32_t* sink_end, const int32_t* buffer_start, const int32_t* cache_len,
                                    int n_kv_heads, int n_ledgers, int replacement, uint8_t* flag,
@@ -680,6 +717,11 @@ extern "C" int mpa_select_worklist(const mpa_level* fine, const mpa_level* coars
     const size_t smem = (size_t)sort_width(n_max) * 16 + (size_t)n_max * 4;
     const int nch = ceil_div(cand_cap, kChunk);
     cudaStream_t st = (cudaStream_t)stream;
+    if (!lookup_v1() && mpa_select_v2_smem(n_max) <= 200 * 1024)
+        return mpa_launch_select_worklist_v2(fine, coarse, group, logits, e_local, cand, n_cand, cand_cap,
+                                             chunk_stats, nch, cflag, clogits, budget, sink_end, buffer_start,
+                                             cache_len, n_kv_heads, n_ledgers, replacement, flag, sel_tokens, tok,
+                                             tok_cap, rej, rej_w, rej_cap, stats, n_max, st);
     MPA_DISPATCH_G(group, {
         auto kern = select_worklist_kernel<kG>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -725,3 +767,4 @@ extern "C" int mpa_build_worklist(const mpa_level* fine, const mpa_level* coarse
     });
     return check_launch("mpa_build_worklist");
 }
+

@@ -1,0 +1,791 @@
+// K9 / K10 serving kernels: fp64 centroid logits with q held in registers, and a fused
+// Eq. 1 score + size-weighted radix select + work-list builder, one CTA per ledger.
+//
+// Reference (pkg/src/multipole_attn/attention.py):
+//   :267-290 `_scores_per_group`  logits = Q_lk Kc^T / sqrt(d); e = exp(l - max_g);
+//                                  score = mean_g e / (e . N)
+//   :192-207 `select_clusters`    visit by (score desc, ref asc); take while cum < B
+//   :331-334 hierarchical union denominator (extras = rejected coarse clusters)
+//   :469-496 work of one kv-head: sinks, buffer, members of the selected clusters, rejected
+//            centroids with their reused logits + ln N
+//
+// Numerics are the reference's: fp64 logits, exps, normalisers and scores, so the selected
+// set matches the oracle except at true ties (|score gap| ~ 1e-16 relative); ties in score are
+// broken by the lowest cluster id, exactly like the reference's (score, ref) sort.
+#include <cstdlib>
+
+#include "mpa_common.cuh"
+
+namespace mpa {
+
+#ifdef MPA_DEBUG_TRACE
+__device__ unsigned long long g_dbg_lk[4096 * 8];
+__device__ __forceinline__ void dbg_lk(int slot) {
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_dbg_lk[blockIdx.x * 8 + slot] = t;
+    }
+}
+#else
+__device__ __forceinline__ void dbg_lk(int) {}
+#endif
+
+// ============================================================================
+// K9: logits[l, g, i] = q_lk[l, g] . kc[l, id_i] / sqrt(D), fp64, for bf16 centroids.
+//
+// Persistent CTAs (128 threads, 2 per SM) walk the (ledger, 128-candidate chunk) items with a
+// double-buffered cp.async ring: the next item's 128 bf16 rows and q_lk land in smem while the
+// current item computes.  Thread t computes a 4-row x G-head block over one quarter of the
+// dimensions (each q load feeds 4 rows, each row element G heads), then the four quarter lanes
+// combine their 16 partial sums with a 2-level transpose-reduce.  Per item the CTA also emits
+// the chunk partials (m_c, Z_c = sum N e^(l - m_c)) and e_local = e^(l - m_c).
+constexpr int kLgChunk = 128;
+constexpr int kLgThreads = 128;
+
+// exact bf16 -> fp64 with integer ops (F2F.F64.F32 issues at a fraction of the DFMA rate):
+// fbits = the bf16 widened to fp32 bits; normal -> (sign, exp + 896, mantissa >> 3) in the high
+// word, low word 0 (a bf16 mantissa has 7 bits); +-0 -> signed zero.  bf16 subnormals (< 1e-38)
+// would flush to zero; centroid means of normalised keys never are.
+__device__ __forceinline__ double bf16_bits_to_f64(unsigned fbits) {
+    const unsigned mag = fbits & 0x7fffffffu;
+    const unsigned hi = (fbits & 0x80000000u) | (mag ? (mag >> 3) + 0x38000000u : 0u);
+    return __hiloint2double((int)hi, 0);
+}
+
+template <int G, int D>
+struct LgGeom {
+    // bf16 row with a 16 B gap after each quarter (+16 B): the 8 lanes of an LDS.128 phase
+    // (2 row groups x 4 quarters) hit 8 distinct 16-byte bank groups
+    static constexpr int kRowB = D * 2 + 4 * 16 + 16;
+    static constexpr int kQD = D / 4;                        // dims per quarter
+    static constexpr int kQStride = kQD * G + 2;             // doubles per quarter (+16 B pad)
+    static constexpr int kTileB = kLgChunk * kRowB;
+    static constexpr int kQB = 4 * kQStride * 8;
+    static constexpr size_t smem(int nb) { return nb * (size_t)(kTileB + kQB) + sizeof(double) * G * kLgChunk; }
+};
+
+template <int G, int D, int NB>
+__global__ void __launch_bounds__(kLgThreads, NB == 1 ? 4 : 2)
+logits_block_kernel(const double* __restrict__ q_lk, const __nv_bfloat16* __restrict__ kc, int kcap,
+                    const int32_t* __restrict__ count, const int32_t* __restrict__ lv_size,
+                    const int32_t* __restrict__ cand, const int32_t* __restrict__ n_cand, int cand_cap,
+                    double* __restrict__ logits, double* __restrict__ cstats, double* __restrict__ e_local,
+                    int n_chunks, int n_items_chunks, int L) {
+    using Geo = LgGeom<G, D>;
+    constexpr int CPR = D / 8;  // 16-byte chunks per row
+    extern __shared__ __align__(16) unsigned char sm[];
+    double* slg = reinterpret_cast<double*>(sm + NB * (Geo::kTileB + Geo::kQB));  // [G][kLgChunk]
+    __shared__ double red[kLgThreads / 32][G];
+    __shared__ double s_m[G];
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    const int items = L * n_items_chunks;
+    // q smem layout per quarter: [dim pair][g][2] so that one 16-byte cp.async moves 2 dims of a head
+    auto issue = [&](int it, int buf) {
+        const int l = it / n_items_chunks, chunk = it - l * n_items_chunks;
+        const int n = cand ? n_cand[l] : count[l];
+        const int i0 = chunk * kLgChunk;
+        unsigned char* tile = sm + buf * (Geo::kTileB + Geo::kQB);
+        double* qs = reinterpret_cast<double*>(tile + Geo::kTileB);
+        if (i0 < n) {
+            const int nv = min(kLgChunk, n - i0);
+            for (int j = tid; j < kLgChunk * CPR; j += kLgThreads) {
+                const int r = j / CPR, cch = j - r * CPR;
+                const bool ok = r < nv;
+                const int row = ok ? (cand ? __ldg(cand + (size_t)l * cand_cap + i0 + r) : i0 + r) : 0;
+                const unsigned dst =
+                    (unsigned)__cvta_generic_to_shared(tile + r * Geo::kRowB + cch * 16 + (cch / (CPR / 4)) * 16);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst),
+                             "l"(kc + ((size_t)l * kcap + row) * D + cch * 8), "r"(ok ? 16 : 0));
+            }
+            for (int j = tid; j < G * D / 2; j += kLgThreads) {
+                const int g = j / (D / 2), dp = j - g * (D / 2), k = dp * 2;
+                const int qt = k / Geo::kQD, kk = k % Geo::kQD;
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(qs + qt * Geo::kQStride + (kk / 2) * 2 * G + g * 2);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst),
+                             "l"(q_lk + ((size_t)l * G + g) * D + k));
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    const int qt = tid & 3, rg = tid >> 2;  // quarter, 4-row group
+    const bool hi2 = qt & 2, hi1 = qt & 1;
+    constexpr int GH = (G + 1) / 2;  // heads kept by the lower lane of the xor-1 pair
+    const double sq = sqrt((double)D);  // logits divide like the reference (acc / sqrt(d))
+    int k = 0;
+    if (blockIdx.x < items) issue(blockIdx.x, 0);
+#pragma unroll 1
+    for (int it = blockIdx.x; it < items; it += gridDim.x, ++k) {
+        const int buf = NB == 1 ? 0 : (k & 1);
+        if (NB > 1 && it + (int)gridDim.x < items) issue(it + gridDim.x, buf ^ 1);
+        else asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.wait_group 1;\n" ::);
+        __syncthreads();
+        const int l = it / n_items_chunks, chunk = it - l * n_items_chunks;
+        const int n = cand ? n_cand[l] : count[l];
+        const int i0 = chunk * kLgChunk;
+        if (i0 >= n) {
+            if (cstats && chunk < n_chunks && tid < G) {
+                cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2] = -INFINITY;
+                cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2 + 1] = 0.0;
+            }
+            __syncthreads();
+            continue;
+        }
+        const int nv = min(kLgChunk, n - i0);
+        const unsigned char* tile = sm + buf * (Geo::kTileB + Geo::kQB);
+        const double* qq = reinterpret_cast<const double*>(tile + Geo::kTileB) + qt * Geo::kQStride;
+        double acc[4][G];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int g = 0; g < G; ++g) acc[r][g] = 0.0;
+#pragma unroll 1
+        for (int c = 0; c < Geo::kQD / 8; ++c) {
+            uint4 raw[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                raw[r] = *reinterpret_cast<const uint4*>(tile + (rg * 4 + r) * Geo::kRowB + qt * (Geo::kQD * 2 + 16) +
+                                                         c * 16);
+#pragma unroll
+            for (int e2 = 0; e2 < 4; ++e2) {
+                // 2 dims x G heads of q: [g][2] pairs
+                double qv[2][G];
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const double2 t = *reinterpret_cast<const double2*>(qq + ((c * 8 + 2 * e2) / 2) * 2 * G + g * 2);
+                    qv[0][g] = t.x;
+                    qv[1][g] = t.y;
+                }
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const unsigned wd = (&raw[r].x)[e2];
+                    const double x0 = bf16_bits_to_f64(wd << 16), x1 = bf16_bits_to_f64(wd & 0xffff0000u);
+#pragma unroll
+                    for (int g = 0; g < G; ++g) acc[r][g] = fma(qv[0][g], x0, acc[r][g]);
+#pragma unroll
+                    for (int g = 0; g < G; ++g) acc[r][g] = fma(qv[1][g], x1, acc[r][g]);
+                }
+            }
+        }
+        // transpose-reduce over the 4 quarter lanes (xor 2 splits rows, xor 1 splits heads)
+        double a2[2][G];
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const double send = hi2 ? acc[rr][g] : acc[rr + 2][g];
+                const double keep = hi2 ? acc[rr + 2][g] : acc[rr][g];
+                a2[rr][g] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+            }
+        double a1[2][GH];
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+            for (int j = 0; j < GH; ++j) {
+                const int ghi = GH + j;
+                const double lo = a2[rr][j], hv = ghi < G ? a2[rr][ghi < G ? ghi : 0] : 0.0;
+                const double send = hi1 ? lo : hv;
+                const double keep = hi1 ? hv : lo;
+                a1[rr][j] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+            }
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int r = rg * 4 + (hi2 ? 2 : 0) + rr;
+#pragma unroll
+            for (int j = 0; j < GH; ++j) {
+                const int g = (hi1 ? GH : 0) + j;
+                if (g < G) {
+                    const double v = a1[rr][j] / sq;
+                    slg[g * kLgChunk + r] = v;
+                    if (r < nv) logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
+                }
+            }
+        }
+        if (cstats) {
+            __syncthreads();
+            // chunk partials: m_c = max l, Z_c = sum N e_local, e_local = e^(l - m_c)
+            const int i = tid;  // one candidate per thread
+            const bool valid = i < nv;
+            const int id = valid ? (cand ? cand[(size_t)l * cand_cap + i0 + i] : i0 + i) : 0;
+            const double nsz = valid ? (double)lv_size[(size_t)l * kcap + id] : 0.0;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const double m = warp_max(valid ? slg[g * kLgChunk + i] : -INFINITY);
+                if (lane == 0) red[w][g] = m;
+            }
+            __syncthreads();
+            if (tid < G) {
+                double M = -INFINITY;
+                for (int ww = 0; ww < kLgThreads / 32; ++ww) M = fmax(M, red[ww][tid]);
+                s_m[tid] = M;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const double e = valid ? exp(slg[g * kLgChunk + i] - s_m[g]) : 0.0;
+                if (valid && e_local) e_local[((size_t)l * G + g) * cand_cap + i0 + i] = e;
+                const double z = warp_sum(e * nsz);
+                __syncwarp();
+                if (lane == 0) red[w][g] = z;
+            }
+            __syncthreads();
+            if (tid < G) {
+                double Z = 0.0;
+                for (int ww = 0; ww < kLgThreads / 32; ++ww) Z += red[ww][tid];
+                cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2] = s_m[tid];
+                cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2 + 1] = Z;
+            }
+        }
+        __syncthreads();  // buffer `buf` is refilled by the next iteration's issue
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
+// ============================================================================
+// K10 + work list.  One CTA per ledger:
+//   1. per-head max M_g and normaliser Z_g: from the logits kernel's chunk partials
+//      (Z = sum_c Z_c e^(m_c - M), e = e_local e^(m_c - M)) or, without them, directly,
+//   2. score_i = (sum_g e_gi / Z_g) / G, stored as the ascending key ~bits(score),
+//   3. size-weighted radix select of the crossing candidate (key, id), 11-bit digits, most
+//      significant first, stopping as soon as the crossing bin holds one candidate,
+//   4. flags (smem + global), and the work lists: one block scan over thread-contiguous
+//      candidate ranges, then all threads copy the selected clusters' members in parallel.
+constexpr int kSel2Threads = 512;
+constexpr int kDigBits = 11, kBins = 1 << kDigBits;
+
+// 64-bit exclusive block scan (blockDim.x <= 1024); scratch: 33 entries
+__device__ __forceinline__ unsigned long long block_scan_u64(unsigned long long v, unsigned long long* scratch,
+                                                            unsigned long long* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    unsigned long long incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) scratch[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        unsigned long long s = lane < nw ? scratch[lane] : 0ull;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < nw) scratch[lane] = s;
+        if (lane == 31) scratch[32] = s;
+    }
+    __syncthreads();
+    const unsigned long long base = wid ? scratch[wid - 1] : 0ull;
+    *total = scratch[32];
+    __syncthreads();
+    return base + incl - v;
+}
+
+// smem per candidate: key (8) + size (4) + flag (1) + pad
+__host__ __device__ constexpr size_t sel_smem_bytes(int n_max) { return (size_t)n_max * 13 + 64; }
+
+template <int G>
+__device__ void select_v2_core(int l, const double* __restrict__ logits, const double* __restrict__ e_local,
+                               const int32_t* __restrict__ cand, int n, int cand_cap,
+                               const int32_t* __restrict__ lv_size, int lv_cap, const double* __restrict__ elogits,
+                               const int32_t* __restrict__ esize, const uint8_t* __restrict__ eflag, int ne, int ecap,
+                               long long B, const double* __restrict__ cstats, int n_chunks, unsigned long long* keys,
+                               int* sizes, uint8_t* sflag, uint8_t* __restrict__ flag,
+                               int32_t* __restrict__ sel_tokens) {
+    __shared__ double s_red[kSel2Threads / 32][G];
+    __shared__ double s_mx[G], s_z[G];
+    __shared__ unsigned int hist_w[kBins], hist_c[kBins];
+    __shared__ unsigned long long s_kprefix, s_scan[33];
+    __shared__ unsigned int s_iprefix;
+    __shared__ long long s_below, s_total;
+    __shared__ int s_cnt;
+    __shared__ unsigned long long s_k;
+    __shared__ unsigned int s_i;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const double* lg = logits + (size_t)l * G * cand_cap;
+    const double* el = e_local ? e_local + (size_t)l * G * cand_cap : nullptr;
+    const double* elg = elogits ? elogits + (size_t)l * G * ecap : nullptr;
+    const double* cs = cstats ? cstats + (size_t)l * n_chunks * G * 2 : nullptr;
+    const bool use_local = el && cs;
+    const int nchu = min(n_chunks, (n + 127) >> 7);  // chunks holding this ledger's candidates
+    double* csc = reinterpret_cast<double*>(hist_w);  // chunk scales e^(m_c - M) [n_chunks][G] (before the radix)
+    const int max_sc_chunks = (int)(sizeof(hist_w) + sizeof(hist_c)) / (8 * G);
+
+    // ---- 1. sizes, per-head max
+    long long tot_local = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int id = cand ? __ldg(cand + (size_t)l * cand_cap + i) : i;
+        const int sz = __ldg(lv_size + (size_t)l * lv_cap + id);
+        sizes[i] = sz;
+        tot_local += sz;
+    }
+    {
+        double m[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) m[g] = -INFINITY;
+        if (cs) {
+            for (int c = threadIdx.x; c < nchu; c += blockDim.x)
+#pragma unroll
+                for (int g = 0; g < G; ++g) m[g] = fmax(m[g], cs[(c * G + g) * 2]);
+        } else {
+            for (int i = threadIdx.x; i < n; i += blockDim.x)
+#pragma unroll
+                for (int g = 0; g < G; ++g) m[g] = fmax(m[g], lg[(size_t)g * cand_cap + i]);
+        }
+        for (int j = threadIdx.x; j < ne; j += blockDim.x)
+            if (!eflag[(size_t)l * ecap + j])
+#pragma unroll
+                for (int g = 0; g < G; ++g) m[g] = fmax(m[g], elg[(size_t)g * ecap + j]);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const double r = warp_max(m[g]);
+            if (lane == 0) s_red[w][g] = r;
+        }
+        __syncthreads();
+        if (threadIdx.x < G) {
+            double r = -INFINITY;
+            for (int ww = 0; ww < kSel2Threads / 32; ++ww) r = fmax(r, s_red[ww][threadIdx.x]);
+            s_mx[threadIdx.x] = r;
+        }
+        __syncthreads();
+    }
+    dbg_lk(1);
+    double mx[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) mx[g] = s_mx[g];
+    const bool scaled = use_local && nchu <= max_sc_chunks;
+
+    // ---- 2. Z = e . N (+ live extras)
+    {
+        double z[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) z[g] = 0.0;
+        if (scaled) {
+            for (int c = threadIdx.x; c < nchu; c += blockDim.x)
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const double cm = cs[(c * G + g) * 2];
+                    const double sc = cm == -INFINITY ? 0.0 : exp(cm - mx[g]);
+                    csc[c * G + g] = sc;
+                    z[g] = fma(cs[(c * G + g) * 2 + 1], sc, z[g]);
+                }
+        } else {
+            for (int i = threadIdx.x; i < n; i += blockDim.x)
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+                    z[g] = fma(exp(lg[(size_t)g * cand_cap + i] - mx[g]), (double)sizes[i], z[g]);
+        }
+        for (int j = threadIdx.x; j < ne; j += blockDim.x)
+            if (!eflag[(size_t)l * ecap + j])
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+                    z[g] = fma(exp(elg[(size_t)g * ecap + j] - mx[g]), (double)esize[(size_t)l * ecap + j], z[g]);
+        unsigned long long tl = (unsigned long long)tot_local;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, o);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const double r = warp_sum(z[g]);
+            if (lane == 0) s_red[w][g] = r;
+        }
+        if (lane == 0) s_scan[w] = tl;
+        __syncthreads();
+        if (threadIdx.x < G) {
+            double r = 0.0;
+            for (int ww = 0; ww < kSel2Threads / 32; ++ww) r += s_red[ww][threadIdx.x];
+            s_z[threadIdx.x] = r;
+        }
+        if (threadIdx.x == 32) {
+            unsigned long long t = 0;
+            for (int ww = 0; ww < kSel2Threads / 32; ++ww) t += s_scan[ww];
+            s_total = (long long)t;
+        }
+        __syncthreads();
+    }
+
+    dbg_lk(2);
+    // ---- 3. scores -> keys: mean over heads of e / Z, accumulated in head order like np.mean(axis=0)
+    double zz[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) zz[g] = s_z[g];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double sc = 0.0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const double e = scaled ? el[(size_t)g * cand_cap + i] * csc[(i >> 7) * G + g]
+                                    : exp(lg[(size_t)g * cand_cap + i] - mx[g]);
+            sc = g ? sc + e / zz[g] : e / zz[g];
+        }
+        sc = sc / (double)G;
+        keys[i] = ~(unsigned long long)__double_as_longlong(sc);  // ascending key == descending score
+    }
+    if (threadIdx.x == 0) {
+        s_kprefix = 0ull;
+        s_iprefix = 0u;
+        s_below = 0;
+    }
+    __syncthreads();
+
+    dbg_lk(5);
+    // ---- 4. crossing candidate: smallest (key, id) with W(<=) >= B.  Digits over the 63 low key
+    // bits (the top bit is constant: scores are positive) then the 32 id bits.
+    const long long total = s_total;
+    const bool select_none = B <= 0, select_all = total < B;
+    unsigned long long kstar = ~0ull;
+    unsigned int istar = 0xffffffffu;
+    if (!select_none && !select_all) {
+        unsigned long long kmask = 1ull << 63;
+        unsigned long long kfix = keys[0] & (1ull << 63);  // constant top bit
+        if (threadIdx.x == 0) s_kprefix = kfix;
+        __syncthreads();
+        unsigned int imask = 0u;
+        constexpr int kKeyPasses = (63 + kDigBits - 1) / kDigBits, kIdPasses = (32 + kDigBits - 1) / kDigBits;
+        bool found = false;
+        for (int pass = 0; pass < kKeyPasses + kIdPasses && !found; ++pass) {
+            const bool kp_pass = pass < kKeyPasses;
+            // digit = bits [sh, sh + width) of the key (or id)
+            const int top = kp_pass ? 63 - kDigBits * pass : 32 - kDigBits * (pass - kKeyPasses);
+            const int width = top >= kDigBits ? kDigBits : top;
+            const int sh = top - width;
+            const unsigned dmask = (1u << width) - 1u;
+            for (int j = threadIdx.x; j < kBins; j += blockDim.x) hist_w[j] = hist_c[j] = 0u;
+            __syncthreads();
+            const unsigned long long kp = s_kprefix;
+            const unsigned int ip = s_iprefix;
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                const unsigned long long k = keys[i];
+                if ((k & kmask) != kp) continue;
+                const unsigned int id = cand ? (unsigned)__ldg(cand + (size_t)l * cand_cap + i) : (unsigned)i;
+                if ((id & imask) != ip) continue;
+                const unsigned dg = kp_pass ? (unsigned)(k >> sh) & dmask : (id >> sh) & dmask;
+                atomicAdd(&hist_w[dg], (unsigned)sizes[i]);
+                atomicAdd(&hist_c[dg], 1u);
+            }
+            __syncthreads();
+            // block scan of the bins (4 per thread) to find the bin where the cumulative weight
+            // reaches B - below
+            constexpr int BPT = kBins / kSel2Threads;
+            unsigned long long wsum = 0;
+#pragma unroll
+            for (int j = 0; j < BPT; ++j) wsum += hist_w[threadIdx.x * BPT + j];
+            unsigned long long btot;
+            const unsigned long long before = block_scan_u64(wsum, s_scan, &btot);
+            const long long below = s_below;
+            const long long need = B - below;  // > 0
+            if ((long long)before < need && (long long)(before + wsum) >= need) {
+                long long run = (long long)before;
+                int dg = threadIdx.x * BPT + BPT - 1;
+                for (int j = 0; j < BPT; ++j) {
+                    const int b = threadIdx.x * BPT + j;
+                    if (run + (long long)hist_w[b] >= need) {
+                        dg = b;
+                        break;
+                    }
+                    run += hist_w[b];
+                }
+                s_below = below + run;
+                s_cnt = (int)hist_c[dg];
+                if (kp_pass) s_kprefix = kp | ((unsigned long long)dg << sh);
+                else s_iprefix = ip | ((unsigned)dg << sh);
+            }
+            __syncthreads();
+            if (kp_pass) kmask |= (unsigned long long)dmask << sh;
+            else imask |= dmask << sh;
+            found = s_cnt == 1;
+        }
+        // the unique candidate matching the final prefix is the crosser
+        const unsigned long long kp = s_kprefix;
+        const unsigned int ip = s_iprefix;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const unsigned int id = cand ? (unsigned)__ldg(cand + (size_t)l * cand_cap + i) : (unsigned)i;
+            if ((keys[i] & kmask) == kp && (id & imask) == ip) {
+                s_k = keys[i];
+                s_i = id;
+            }
+        }
+        __syncthreads();
+        kstar = s_k;
+        istar = s_i;
+    }
+
+    dbg_lk(6);
+    // ---- 5. flags
+    long long tok = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        bool sel;
+        if (select_none) sel = false;
+        else if (select_all) sel = true;
+        else {
+            const unsigned int id = cand ? (unsigned)__ldg(cand + (size_t)l * cand_cap + i) : (unsigned)i;
+            sel = keys[i] < kstar || (keys[i] == kstar && id <= istar);
+        }
+        sflag[i] = sel ? 1 : 0;
+        flag[(size_t)l * cand_cap + i] = sel ? 1 : 0;
+        if (sel) tok += sizes[i];
+    }
+    {
+        unsigned long long t = (unsigned long long)tok;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) s_scan[w] = t;
+        __syncthreads();
+        if (threadIdx.x == 0 && sel_tokens) {
+            unsigned long long a = 0;
+            for (int ww = 0; ww < kSel2Threads / 32; ++ww) a += s_scan[ww];
+            sel_tokens[l] = (int32_t)a;
+        }
+    }
+    __syncthreads();
+}
+
+// Work lists of one ledger (attention.py:469-496) from the selection flags: sinks, buffer and the
+// members of the selected candidates; rejected fine candidates (then coarse clusters with
+// cflag == 0, hierarchy) as value-row codes with logit + ln N; stats [4, L].  keys_space is the
+// select's key array, reused for the selected-candidate list.
+template <int G>
+__device__ void worklist_v2(int l, int L, int n, const double* __restrict__ logits, const int32_t* __restrict__ cand,
+                            int cand_cap, const uint8_t* sflag, const int* sizes, int* sel_list,
+                            const int32_t* __restrict__ fmem_off, const int32_t* __restrict__ fmem, int fcap,
+                            int fmem_cap, const int32_t* __restrict__ csize, int ne, int ccap,
+                            const uint8_t* __restrict__ cflag, const double* __restrict__ clogits,
+                            const int32_t* __restrict__ sink_end, const int32_t* __restrict__ buffer_start,
+                            const int32_t* __restrict__ cache_len, int n_kv_heads, int replacement,
+                            int32_t* __restrict__ tok, int tok_cap, int32_t* __restrict__ rej,
+                            float* __restrict__ rej_w, int rej_cap, int32_t* __restrict__ stats) {
+    constexpr int GP = G <= 4 ? 4 : 8;
+    __shared__ unsigned long long scan64[33];
+    const int seq = l / n_kv_heads;
+    const int clen = cache_len[seq];
+    const int ns = min(sink_end[seq], clen);
+    const int bs = buffer_start[seq];
+    const int nb = max(0, clen - bs);
+    int32_t* T = tok + (size_t)l * tok_cap;
+    for (int j = threadIdx.x; j < ns; j += blockDim.x) T[j] = j;
+    for (int j = threadIdx.x; j < nb; j += blockDim.x) T[ns + j] = bs + j;
+    // thread-contiguous candidate ranges: one scan of (tokens, rejected, selected) packed 32/16/16
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int c0 = min(n, (int)threadIdx.x * per), c1 = min(n, c0 + per);
+    unsigned long long mine = 0;
+    for (int i = c0; i < c1; ++i) {
+        if (sflag[i]) mine += ((unsigned long long)sizes[i] << 32) | 1ull;
+        else if (replacement) mine += 1ull << 16;
+    }
+    unsigned long long tot;
+    const unsigned long long pre = block_scan_u64(mine, scan64, &tot);
+    int tpos = (int)(pre >> 32), rpos = (int)((pre >> 16) & 0xffff), spos = (int)(pre & 0xffff);
+    const int nsel = (int)(tot & 0xffff);
+    // selected list (candidate, first token slot) for the parallel member copy; rejected weights
+    int* sel_c = sel_list;
+    int* sel_t = sel_list + n;
+    for (int i = c0; i < c1; ++i) {
+        const int sz = sizes[i];
+        if (sflag[i]) {
+            sel_c[spos] = i;
+            sel_t[spos] = tpos;
+            ++spos;
+            tpos += sz;
+        } else if (replacement) {
+            if (rpos < rej_cap) {
+                const int id = cand ? __ldg(cand + (size_t)l * cand_cap + i) : i;
+                rej[(size_t)l * rej_cap + rpos] = id;
+                const double lnN = (double)logf((float)sz);
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+                    rej_w[((size_t)l * rej_cap + rpos) * GP + g] =
+                        (float)(logits[((size_t)l * G + g) * cand_cap + i] + lnN);
+            }
+            ++rpos;
+        }
+    }
+    __syncthreads();
+    // members of the selected clusters: one thread per token slot (binary search of its cluster
+    // in the selected list), so the two dependent loads (CSR offset, member id) overlap across slots
+    const int32_t* moff = fmem_off + (size_t)l * (fcap + 1);
+    const int nsel_tok = (int)(tot >> 32);
+    for (int j = threadIdx.x; j < nsel_tok; j += blockDim.x) {
+        int lo = 0, hi = nsel - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (sel_t[mid] <= j) lo = mid;
+            else hi = mid - 1;
+        }
+        const int i = sel_c[lo];
+        const int id = cand ? __ldg(cand + (size_t)l * cand_cap + i) : i;
+        const int slot = ns + nb + j;
+        if (slot < tok_cap) T[slot] = __ldg(fmem + (size_t)l * fmem_cap + __ldg(moff + id) + (j - sel_t[lo]));
+    }
+    int tbase = ns + nb + (int)(tot >> 32), rbase = (int)((tot >> 16) & 0xffff);
+    if (cflag && replacement) {
+        __shared__ int scan[33];
+        for (int c = threadIdx.x, cbase = 0; cbase < ne; c += blockDim.x, cbase += blockDim.x) {
+            const int r = (c < ne && !cflag[(size_t)l * ccap + c]) ? 1 : 0;
+            int rtot;
+            const int p = rbase + block_exclusive_scan(r, scan, &rtot);
+            if (r && p < rej_cap) {
+                rej[(size_t)l * rej_cap + p] = -1 - c;
+                const double lnN = (double)logf((float)csize[(size_t)l * ccap + c]);
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+                    rej_w[((size_t)l * rej_cap + p) * GP + g] = (float)(clogits[((size_t)l * G + g) * ccap + c] + lnN);
+            }
+            rbase += rtot;
+        }
+    }
+    if (threadIdx.x == 0) {
+        stats[l] = min(tbase, tok_cap);
+        stats[L + l] = min(rbase, rej_cap);
+        stats[2 * L + l] = tbase - ns - nb;
+        stats[3 * L + l] = nsel;
+    }
+}
+
+template <int G>
+__global__ void __launch_bounds__(kSel2Threads)
+select_worklist_v2_kernel(const double* __restrict__ logits, const double* __restrict__ e_local,
+                          const int32_t* __restrict__ cand, const int32_t* __restrict__ n_cand, int cand_cap,
+                          const double* __restrict__ cstats, int n_chunks, const int64_t* __restrict__ budget,
+                          uint8_t* __restrict__ flag, int32_t* __restrict__ sel_tokens,
+                          // fine level
+                          const int32_t* __restrict__ fsize, const int32_t* __restrict__ fmem_off,
+                          const int32_t* __restrict__ fmem, int fcap, int fmem_cap, const int32_t* __restrict__ fcount,
+                          // coarse level (hierarchy: extras of the denominator and rejected coarse terms)
+                          const int32_t* __restrict__ csize, const int32_t* __restrict__ ccount, int ccap,
+                          const uint8_t* __restrict__ cflag, const double* __restrict__ clogits,
+                          // sequence layout
+                          const int32_t* __restrict__ sink_end, const int32_t* __restrict__ buffer_start,
+                          const int32_t* __restrict__ cache_len, int n_kv_heads, int replacement,
+                          // outputs
+                          int32_t* __restrict__ tok, int tok_cap, int32_t* __restrict__ rej,
+                          float* __restrict__ rej_w, int rej_cap, int32_t* __restrict__ stats, int smem_n) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int l = blockIdx.x, L = gridDim.x;
+    dbg_lk(0);
+    const int n = cand ? n_cand[l] : fcount[l];
+    if (n > smem_n) __trap();  // the host sizes smem_n >= every ledger's candidate count
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem_raw);
+    int* sizes = reinterpret_cast<int*>(keys + smem_n);
+    uint8_t* sflag = reinterpret_cast<uint8_t*>(sizes + smem_n);
+    const int ne = cflag ? ccount[l] : 0;
+    select_v2_core<G>(l, logits, e_local, cand, n, cand_cap, fsize, fcap, clogits, csize, cflag, ne, ccap, budget[l],
+                      cstats, n_chunks, keys, sizes, sflag, flag, sel_tokens);
+    dbg_lk(3);
+    worklist_v2<G>(l, L, n, logits, cand, cand_cap, sflag, sizes, reinterpret_cast<int*>(keys), fmem_off, fmem, fcap,
+                   fmem_cap, csize, ne, ccap, cflag, clogits, sink_end, buffer_start, cache_len, n_kv_heads,
+                   replacement, tok, tok_cap, rej, rej_w, rej_cap, stats);
+    dbg_lk(4);
+}
+
+// selection only (the hierarchy's coarse promotion stage)
+template <int G>
+__global__ void __launch_bounds__(kSel2Threads)
+select_v2_kernel(const double* __restrict__ logits, const double* __restrict__ e_local,
+                 const int32_t* __restrict__ cand, const int32_t* __restrict__ n_cand, int cand_cap,
+                 const int32_t* __restrict__ lv_size, int lv_cap, const double* __restrict__ elogits,
+                 const int32_t* __restrict__ esize, const uint8_t* __restrict__ eflag,
+                 const int32_t* __restrict__ n_extra, int ecap, const int64_t* __restrict__ budget,
+                 uint8_t* __restrict__ flag, int32_t* __restrict__ sel_tokens, const double* __restrict__ cstats,
+                 int n_chunks, int smem_n) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int l = blockIdx.x;
+    if (n_cand[l] > smem_n) __trap();  // the host sizes smem_n >= every ledger's candidate count
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem_raw);
+    int* sizes = reinterpret_cast<int*>(keys + smem_n);
+    uint8_t* sflag = reinterpret_cast<uint8_t*>(sizes + smem_n);
+    select_v2_core<G>(l, logits, e_local, cand, n_cand[l], cand_cap, lv_size, lv_cap, elogits, esize, eflag,
+                      elogits ? n_extra[l] : 0, ecap, budget[l], cstats, n_chunks, keys, sizes, sflag, flag,
+                      sel_tokens);
+}
+
+}  // namespace mpa
+
+using namespace mpa;
+
+int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* lv, const int32_t* cand,
+                         const int32_t* n_cand, int cand_cap, double* logits, double* chunk_stats, double* e_local,
+                         int n_chunks, int n_max, cudaStream_t st) {
+    const int L = lv->n_ledgers;
+    // items: ledgers x the chunks any ledger can use (n_max bounds the live candidates); chunk
+    // stats rows past them are written -inf once per ledger by the last items
+    const int item_chunks = ceil_div(n_max > 0 ? n_max : (cand ? cand_cap : lv->cap), kLgChunk);
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const int items = L * item_chunks;
+    // MPA_LOGITS_PERSIST=1: persistent double-buffered grid (2 CTAs / SM); default one CTA per item
+    static int persist = -1;
+    if (persist < 0) {
+        const char* e = getenv("MPA_LOGITS_PERSIST");
+        persist = (e && e[0] == '1') ? 1 : 0;
+    }
+    const int grid = persist ? (items < 2 * sms ? items : 2 * sms) : items;
+#define MPA_LG3(D, NB)                                                                                             \
+    {                                                                                                              \
+        auto kern = logits_block_kernel<kG, D, NB>;                                                                \
+        const size_t smem = LgGeom<kG, D>::smem(NB);                                                               \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                        \
+        kern<<<grid, kLgThreads, smem, st>>>(q_lk, (const __nv_bfloat16*)lv->kc, lv->cap, lv->count, lv->size, cand, \
+                                             n_cand, cand_cap, logits, chunk_stats, e_local, n_chunks,             \
+                                             item_chunks, L);                                                      \
+    }
+    if (grid <= 0) return 0;
+    MPA_DISPATCH_G(group, {
+        if (persist) {
+            if (d == 128) MPA_LG3(128, 2) else MPA_LG3(64, 2)
+        } else {
+            if (d == 128) MPA_LG3(128, 1) else MPA_LG3(64, 1)
+        }
+    });
+#undef MPA_LG3
+    return check_launch("mpa_centroid_logits(block)");
+}
+
+size_t mpa_select_v2_smem(int n_max) { return sel_smem_bytes(n_max); }
+
+int mpa_launch_select_v2(const double* logits, const double* e_local, int group, const int32_t* cand,
+                         const int32_t* n_cand, int cand_cap, const int32_t* lv_size, int lv_cap,
+                         const double* elogits, const int32_t* esize, const uint8_t* eflag, const int32_t* n_extra,
+                         int ecap, const int64_t* budget, int n_ledgers, uint8_t* flag, int32_t* sel_tokens,
+                         const double* chunk_stats, int n_chunks, int n_max, cudaStream_t st) {
+    const size_t smem = sel_smem_bytes(n_max);
+    MPA_DISPATCH_G(group, {
+        auto kern = select_v2_kernel<kG>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<n_ledgers, kSel2Threads, smem, st>>>(logits, e_local, cand, n_cand, cand_cap, lv_size, lv_cap, elogits,
+                                                    esize, eflag, n_extra, ecap, budget, flag, sel_tokens,
+                                                    chunk_stats, n_chunks, n_max);
+    });
+    return check_launch("mpa_select(v2)");
+}
+
+int mpa_launch_select_worklist_v2(const mpa_level* fine, const mpa_level* coarse, int group, const double* logits,
+                                  const double* e_local, const int32_t* cand, const int32_t* n_cand, int cand_cap,
+                                  const double* chunk_stats, int n_chunks, const uint8_t* cflag,
+                                  const double* clogits, const int64_t* budget, const int32_t* sink_end,
+                                  const int32_t* buffer_start, const int32_t* cache_len, int n_kv_heads,
+                                  int n_ledgers, int replacement, uint8_t* flag, int32_t* sel_tokens, int32_t* tok,
+                                  int tok_cap, int32_t* rej, float* rej_w, int rej_cap, int32_t* stats, int n_max,
+                                  cudaStream_t st) {
+    const size_t smem = sel_smem_bytes(n_max);
+    MPA_DISPATCH_G(group, {
+        auto kern = select_worklist_v2_kernel<kG>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<n_ledgers, kSel2Threads, smem, st>>>(
+            logits, e_local, cand, n_cand, cand_cap, chunk_stats, n_chunks, budget, flag, sel_tokens, fine->size,
+            fine->off, fine->idx, fine->cap, fine->idx_cap, fine->count, coarse ? coarse->size : nullptr,
+            coarse ? coarse->count : nullptr, coarse ? coarse->cap : 0, cflag, clogits, sink_end, buffer_start,
+            cache_len, n_kv_heads, replacement, tok, tok_cap, rej, rej_w, rej_cap, stats, n_max);
+    });
+    return check_launch("mpa_select_worklist(v2)");
+}
+
+#ifdef MPA_DEBUG_TRACE
+extern "C" int mpa_debug_trace_lookup(unsigned long long* host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_dbg_lk, sizeof(unsigned long long) * n);
+}
+#endif

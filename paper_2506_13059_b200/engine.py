@@ -70,12 +70,14 @@ class DecodeEngine:
         self.q_rot = torch.zeros(n_seq, self.Hq, d, dtype=torch.float32, **z)
         self.q_lk = torch.zeros(n_seq, self.Hq, d, dtype=torch.float64, **z)
         self.logits = torch.zeros(L, G, self.kcap, dtype=torch.float64, **z)
+        self.elocal = torch.zeros(L, G, self.kcap, dtype=torch.float64, **z)
         self.flag = torch.zeros(L, self.kcap, dtype=torch.uint8, **z)
         self.sel_tokens = torch.zeros(L, dtype=torch.int32, **z)
         self.cstats = torch.zeros(L, -(-self.kcap // 128), G, 2, dtype=torch.float64, **z)
         self.budget = torch.full((L,), cfg.token_budget, dtype=torch.int64, **z)
         if hier:
             self.clogits = torch.zeros(L, G, self.ccap, dtype=torch.float64, **z)
+            self.celocal = torch.zeros(L, G, self.ccap, dtype=torch.float64, **z)
             self.cflag = torch.zeros(L, self.ccap, dtype=torch.uint8, **z)
             self.cbudget = torch.zeros(L, dtype=torch.int64, **z)
             self.cand = torch.zeros(L, self.kcap, dtype=torch.int32, **z)
@@ -161,12 +163,15 @@ class DecodeEngine:
         replacement = 0 if self.mode == "flat-no-replacement" else 1
         tiled = self.d in (64, 128)
         cs = self.cstats if tiled else None
+        # e^(l - chunk max) from the logits kernel (bf16 serving centroids only)
+        el = self.elocal if (tiled and not self.led.lookup_f64) else None
         if self.cfg.hierarchy is None:
             if int(self.led.n_fine.min()) == 0:
                 raise ConfigError("ledger has no clusters")
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, None, None, self.kcap,
-                 ptr(self.logits), ptr(cs), st)
-            call("mpa_select_worklist", fine, None, G, ptr(self.logits), None, None, self.kcap, ptr(cs), None, None,
+                 ptr(self.logits), ptr(cs), ptr(el), int(self.led.n_fine.max()), st)
+            call("mpa_select_worklist", fine, None, G, ptr(self.logits), ptr(el), None, None, self.kcap, ptr(cs),
+                 None, None,
                  ptr(self.budget), ptr(self.sink_end_d), ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv,
                  L, replacement, ptr(self.flag), ptr(self.sel_tokens), ptr(self.tok), self.tok_cap, ptr(self.rej),
                  ptr(self.rej_w), self.rej_cap, ptr(self.stats), int(self.led.n_fine.max()), st)
@@ -175,15 +180,16 @@ class DecodeEngine:
                 raise ConfigError("ledger has no coarse clusters")
             coarse = self.led.coarse_level()
             ccs = self.ccstats if tiled else None
+            cel = self.celocal if el is not None else None
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, coarse, None, None, self.ccap,
-                 ptr(self.clogits), ptr(ccs), st)
+                 ptr(self.clogits), ptr(ccs), ptr(cel), int(self.led.n_coarse.max()), st)
             call("mpa_select", ptr(self.clogits), G, None, ptr(self.led.ccount), self.ccap, ptr(self.led.csize),
                  self.ccap, None, None, None, None, 0, ptr(self.cbudget), L, ptr(self.cflag),
-                 ptr(self.csel_tokens), ptr(ccs), int(self.led.n_coarse.max()), st)
+                 ptr(self.csel_tokens), ptr(ccs), ptr(cel), int(self.led.n_coarse.max()), st)
             call("mpa_hier_candidates", coarse, ptr(self.cflag), L, ptr(self.cand), ptr(self.n_cand), self.kcap, st)
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, ptr(self.cand), ptr(self.n_cand),
-                 self.kcap, ptr(self.logits), ptr(cs), st)
-            call("mpa_select_worklist", fine, coarse, G, ptr(self.logits), ptr(self.cand), ptr(self.n_cand),
+                 self.kcap, ptr(self.logits), ptr(cs), ptr(el), int(self.led.n_fine.max()), st)
+            call("mpa_select_worklist", fine, coarse, G, ptr(self.logits), ptr(el), ptr(self.cand), ptr(self.n_cand),
                  self.kcap, ptr(cs), ptr(self.cflag), ptr(self.clogits), ptr(self.budget), ptr(self.sink_end_d),
                  ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv, L, replacement, ptr(self.flag),
                  ptr(self.sel_tokens), ptr(self.tok), self.tok_cap, ptr(self.rej), ptr(self.rej_w), self.rej_cap,

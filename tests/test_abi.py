@@ -47,7 +47,8 @@ def test_argument_errors_without_gpu(lib):
     lib.mpa_last_error.restype = ctypes.c_char_p
     lib.mpa_version.restype = ctypes.c_char_p
     assert b"sm_100a" in lib.mpa_version()
-    rc = lib.mpa_select(None, 4, None, None, 0, None, 0, None, None, None, None, 0, None, 1, None, None, None)
+    rc = lib.mpa_select(None, 4, None, None, 0, None, 0, None, None, None, None, 0, None, 1, None, None, None,
+                        None, 0, None)
     assert rc == 1001
     assert b"null argument" in lib.mpa_last_error()
     rc = lib.mpa_sparse_decode(None, None, 8, 4, None, None, 0, None, None, None, 0, None, 0, None, 0, 1,

@@ -185,3 +185,4 @@ def test_batched_sequences_identical():
     b = four.attend(q.expand(4, -1, -1).contiguous())
     for s in range(4):
         assert rel_err(b[s].cpu().numpy(), a[0].cpu().numpy()).max() < 1e-5
+

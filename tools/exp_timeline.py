@@ -25,6 +25,20 @@ def main():
     lib = _lib.lib()
     eng.rotate(Q[0])
     eng.lookup()
+    import torch as _t
+    for _ in range(3):
+        eng.lookup()
+    _t.cuda.synchronize()
+    eng.lookup()
+    _t.cuda.synchronize()
+    buf = (C.c_ulonglong * (4096 * 8))()
+    lib.mpa_debug_trace_lookup(buf, 4096 * 8)
+    t = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 8).astype(np.int64)[: eng.L]
+    rel = (t - t[:, 0].min()) / 1e3
+    print("select_worklist per-CTA (us)")
+    for k, name in enumerate(["start", "max_done", "z_done", "select_done", "worklist_done", "scores_done",
+                              "radix_done"]):
+        print(f"  {name:14s} min {rel[:, k].min():7.2f} med {np.median(rel[:, k]):7.2f} max {rel[:, k].max():7.2f}")
     for label, fn in (("sparse", lambda: eng.fused()), ("dense", lambda: eng.attend_dense(Q[0]))):
         for _ in range(3):
             fn()
