@@ -69,6 +69,14 @@ typedef struct mpa_level {
 int mpa_kv_write(const mpa_cache* cache, const float* k_src, const float* v_src,
                  const int32_t* pos0, int n_tok, const double* inv_freq, void* stream);
 
+/* K14 -- append n_tok tokens per ledger at the end of each sequence: positions
+ * cache_len[l / n_kv_heads] + t (same writes as mpa_kv_write); then cache_len[s] += n_tok and, if
+ * given, ntok_dense[l] += n_tok, done on the device by the last block (ticket: one int32
+ * workspace, zero-initialised once, left zeroed) -- pipeline.py:156-159 without a host round trip. */
+int mpa_kv_append(const mpa_cache* cache, const float* k_src, const float* v_src, int n_kv_heads, int n_tok,
+                  int32_t* cache_len, int32_t* ntok_dense, const double* inv_freq, int32_t* ticket,
+                  void* stream);
+
 /* K1 -- rotate queries: q_rot = rotate(q, qpos[seq]) * scale (fp32, exact view) and
  * q_lk = rotate(q, delta) (fp64, lookup view; rope.py:66-68).  q: fp32 [n_seq, n_qh, d]. */
 int mpa_rotate_queries(const float* q, int n_seq, int n_qh, int d, const int32_t* qpos,

@@ -59,6 +59,46 @@ __global__ void kv_write_kernel(T* __restrict__ k_rot, T* __restrict__ k_raw, T*
     }
 }
 
+// Append at the current end of each sequence: token t of ledger l goes to position
+// cache_len[l / n_kv_heads] + t; the last block to finish (atomic ticket) advances cache_len (and
+// the dense-comparator lengths) by n_tok, so a decode step needs no host round trip or extra launch.
+template <typename T>
+__global__ void kv_append_kernel(T* __restrict__ k_rot, T* __restrict__ k_raw, T* __restrict__ v,
+                                 const float* __restrict__ k_src, const float* __restrict__ v_src, int n_kv_heads,
+                                 int n_seq, int32_t* __restrict__ cache_len, int32_t* __restrict__ ntok_dense,
+                                 int n_tok, int tcap, int d, const double* __restrict__ inv_freq,
+                                 int32_t* __restrict__ ticket) {
+    const int l = blockIdx.y, t = blockIdx.x;
+    const int pos = cache_len[l / n_kv_heads] + t;
+    const size_t src = ((size_t)l * n_tok + t) * d;
+    const size_t dst = ((size_t)l * tcap + pos) * d;
+    for (int i = threadIdx.x; i < d / 2; i += blockDim.x) {
+        const double x = (double)k_src[src + 2 * i];
+        const double y = (double)k_src[src + 2 * i + 1];
+        double sn, cs;
+        sincos((double)pos * inv_freq[i], &sn, &cs);
+        k_rot[dst + 2 * i] = elem<T>::from_d(__dsub_rn(__dmul_rn(x, cs), __dmul_rn(y, sn)));
+        k_rot[dst + 2 * i + 1] = elem<T>::from_d(__dadd_rn(__dmul_rn(x, sn), __dmul_rn(y, cs)));
+        k_raw[dst + 2 * i] = elem<T>::from_d(x);
+        k_raw[dst + 2 * i + 1] = elem<T>::from_d(y);
+        v[dst + 2 * i] = elem<T>::from_d((double)v_src[src + 2 * i]);
+        v[dst + 2 * i + 1] = elem<T>::from_d((double)v_src[src + 2 * i + 1]);
+    }
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const int prev = atomicAdd(ticket, 1);
+        s_last = prev == (int)(gridDim.x * gridDim.y) - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    for (int s = threadIdx.x; s < n_seq; s += blockDim.x) cache_len[s] += n_tok;
+    if (ntok_dense)
+        for (int j = threadIdx.x; j < n_seq * n_kv_heads; j += blockDim.x) ntok_dense[j] += n_tok;
+    if (threadIdx.x == 0) *ticket = 0;
+}
+
 __global__ void rotate_queries_kernel(const float* __restrict__ q, int n_qh, int d,
                                       const int32_t* __restrict__ qpos, int delta,
                                       const double* __restrict__ inv_freq, float scale,
@@ -108,6 +148,32 @@ extern "C" int mpa_kv_write(const mpa_cache* c, const float* k_src, const float*
     else
         MPA_REQUIRE(false, MPA_ERR_ARG, "mpa_kv_write: bad dtype %d", c->dtype);
     return check_launch("mpa_kv_write");
+}
+
+extern "C" int mpa_kv_append(const mpa_cache* c, const float* k_src, const float* v_src, int n_kv_heads, int n_tok,
+                             int32_t* cache_len, int32_t* ntok_dense, const double* inv_freq, int32_t* ticket,
+                             void* stream) {
+    MPA_REQUIRE(c && k_src && v_src && cache_len && inv_freq && ticket, MPA_ERR_ARG, "mpa_kv_append: null argument");
+    MPA_REQUIRE(c->head_dim >= 2 && c->head_dim % 2 == 0, MPA_ERR_ARG, "mpa_kv_append: bad head_dim %d",
+                c->head_dim);
+    MPA_REQUIRE(n_kv_heads >= 1 && c->n_ledgers % n_kv_heads == 0, MPA_ERR_ARG, "mpa_kv_append: n_kv_heads %d",
+                n_kv_heads);
+    if (n_tok <= 0 || c->n_ledgers <= 0) return 0;
+    dim3 grid(n_tok, c->n_ledgers);
+    const int threads = c->head_dim / 2 < 64 ? 32 : 64;
+    const int n_seq = c->n_ledgers / n_kv_heads;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (c->dtype == MPA_F32)
+        kv_append_kernel<float><<<grid, threads, 0, st>>>((float*)c->k_rot, (float*)c->k_raw, (float*)c->v, k_src,
+                                                          v_src, n_kv_heads, n_seq, cache_len, ntok_dense, n_tok,
+                                                          c->tcap, c->head_dim, inv_freq, ticket);
+    else if (c->dtype == MPA_BF16)
+        kv_append_kernel<__nv_bfloat16><<<grid, threads, 0, st>>>(
+            (__nv_bfloat16*)c->k_rot, (__nv_bfloat16*)c->k_raw, (__nv_bfloat16*)c->v, k_src, v_src, n_kv_heads, n_seq,
+            cache_len, ntok_dense, n_tok, c->tcap, c->head_dim, inv_freq, ticket);
+    else
+        MPA_REQUIRE(false, MPA_ERR_ARG, "mpa_kv_append: bad dtype %d", c->dtype);
+    return check_launch("mpa_kv_append");
 }
 
 extern "C" int mpa_rotate_queries(const float* q, int n_seq, int n_qh, int d, const int32_t* qpos, int delta,

@@ -36,7 +36,7 @@ NUM_SMS = 148
 class DecodeEngine:
     def __init__(self, cfg: EngineConfig, layout: HeadLayout, n_seq: int, tcap: int,
                  dtype: torch.dtype = torch.bfloat16, device="cuda", kcap: int | None = None,
-                 ccap: int | None = None, mode: str = "multipole"):
+                 ccap: int | None = None, mode: str = "multipole", use_graphs: bool | None = None):
         if not torch.cuda.is_available():
             raise RuntimeError("DecodeEngine needs a CUDA device (B200); there is no CPU fallback")
         _lib.lib()  # fail loudly if libmpattn.so is missing
@@ -66,6 +66,7 @@ class DecodeEngine:
         self.sink_end_d = torch.zeros(n_seq, dtype=torch.int32, **z)
         self.buffer_start_d = torch.zeros(n_seq, dtype=torch.int32, **z)
         self.ntok_dense_d = torch.zeros(L, dtype=torch.int32, **z)
+        self.append_ticket = torch.zeros(1, dtype=torch.int32, **z)
         # workspace
         self.q_rot = torch.zeros(n_seq, self.Hq, d, dtype=torch.float32, **z)
         self.q_lk = torch.zeros(n_seq, self.Hq, d, dtype=torch.float64, **z)
@@ -95,6 +96,8 @@ class DecodeEngine:
         self.cache_struct = MpaCache(ptr(self.k_rot), ptr(self.k_raw), ptr(self.v), dtype_code(dtype), L, tcap, d)
         self.last_split = 1
         self.cursor = 0
+        self.use_graphs = (os.environ.get("MPA_NO_GRAPH") != "1") if use_graphs is None else use_graphs
+        self._graph = None
         self.last_lloyd_rounds = 0
         self.last_update: dict | None = None
 
@@ -102,16 +105,19 @@ class DecodeEngine:
     def write_tokens(self, k: torch.Tensor, v: torch.Tensor, pos0: torch.Tensor | None = None) -> None:
         """Write n new tokens per ledger: k, v fp32 [n_seq, Hkv, n, d] (device) at cache_len."""
         n = k.shape[2]
+        k = k.reshape(self.L, n, self.d).float().contiguous()
+        v = v.reshape(self.L, n, self.d).float().contiguous()
         if pos0 is None:
             if int(self.cache_len.max()) + n > self.tcap:
                 raise RuntimeError(f"KV cache capacity {self.tcap} exceeded")
-            pos0 = self.cache_len_d.repeat_interleave(self.Hkv)
-        k = k.reshape(self.L, n, self.d).float().contiguous()
-        v = v.reshape(self.L, n, self.d).float().contiguous()
-        call("mpa_kv_write", self.cache_struct, ptr(k), ptr(v), ptr(pos0), n, ptr(self.inv_freq), stream_ptr())
+            # positions and the length counters advance on the device (one launch)
+            call("mpa_kv_append", self.cache_struct, ptr(k), ptr(v), self.Hkv, n, ptr(self.cache_len_d),
+                 ptr(self.ntok_dense_d), ptr(self.inv_freq), ptr(self.append_ticket), stream_ptr())
+        else:
+            call("mpa_kv_write", self.cache_struct, ptr(k), ptr(v), ptr(pos0), n, ptr(self.inv_freq), stream_ptr())
+            self.cache_len_d += n
+            self.ntok_dense_d += n
         self.cache_len += n
-        self.cache_len_d += n
-        self.ntok_dense_d += n
 
     def set_prompt_layout(self) -> None:
         """Sinks / buffer split of the prompt (clustering.py:295-299)."""
@@ -125,6 +131,7 @@ class DecodeEngine:
         self._sync_scalars()
 
     def _sync_scalars(self) -> None:
+        self.invalidate_graph()
         self.sink_end_d.copy_(torch.as_tensor(self.sink_end, dtype=torch.int32))
         self.buffer_start_d.copy_(torch.as_tensor(self.buffer_start, dtype=torch.int32))
         self.cache_len_d.copy_(torch.as_tensor(self.cache_len, dtype=torch.int32))
@@ -244,13 +251,53 @@ class DecodeEngine:
         L = self.cfg.local_buffer
         return [s for s in range(self.n_seq) if self.cache_len[s] - self.buffer_start[s] >= 2 * L]
 
+    # ------------------------------------------------------------------ CUDA graph of a step
+    def _graphable(self) -> bool:
+        return self.use_graphs and self.mode in ("multipole", "flat-no-replacement")
+
+    def invalidate_graph(self) -> None:
+        """The captured step bakes in ledger-dependent launch arguments (cluster counts, split
+        sizes): any change to the ledgers or the layout drops it."""
+        self._graph = None
+
+    def _capture_step(self) -> None:
+        n, Hq, Hkv, d, dev = self.n_seq, self.Hq, self.Hkv, self.d, self.device
+        self._gq = torch.zeros(n, Hq, d, dtype=torch.float32, device=dev)
+        self._gk = torch.zeros(n, Hkv, 1, d, dtype=torch.float32, device=dev)
+        self._gv = torch.zeros(n, Hkv, 1, d, dtype=torch.float32, device=dev)
+        self._workspace(0)
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.attend(self._gq)  # warm-up outside the capture (function attributes, tensor maps)
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.attend(self._gq)
+            call("mpa_kv_append", self.cache_struct, ptr(self._gk), ptr(self._gv), self.Hkv, 1, ptr(self.cache_len_d),
+                 ptr(self.ntok_dense_d), ptr(self.inv_freq), ptr(self.append_ticket), stream_ptr())
+        self._graph = g
+
     def step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor) -> torch.Tensor:
         """Attend, append the step's token, then run the online update when a buffer holds 2L
-        tokens (pipeline.py:124-191).  q [n_seq, Hq, d], k_new / v_new [n_seq, Hkv, d] (fp32)."""
+        tokens (pipeline.py:124-191).  q [n_seq, Hq, d], k_new / v_new [n_seq, Hkv, d] (fp32).
+        Between ledger changes the attend + append chain replays as one CUDA graph."""
         from . import clustering
 
-        out = self.attend(q)
-        self.write_tokens(k_new[:, :, None], v_new[:, :, None])
+        if self._graphable():
+            if int(self.cache_len.max()) + 1 > self.tcap:
+                raise RuntimeError(f"KV cache capacity {self.tcap} exceeded")
+            if self._graph is None:
+                self._capture_step()
+            self._gq.copy_(q)
+            self._gk.copy_(k_new[:, :, None])
+            self._gv.copy_(v_new[:, :, None])
+            self._graph.replay()
+            self.cache_len += 1
+            out = self.out
+        else:
+            out = self.attend(q)
+            self.write_tokens(k_new[:, :, None], v_new[:, :, None])
         todo = self.needs_update()
         self.last_update = None
         if todo:
@@ -258,6 +305,7 @@ class DecodeEngine:
                 self.last_update = clustering.positional_update(self, todo)
             else:
                 self.last_update = clustering.online_update(self, todo, self.cursor)
+            self.invalidate_graph()
         self.cursor += 1
         return out
 

@@ -170,3 +170,35 @@ def test_update_cadence_and_attend_before_append():
     oa, _ = G.step(a, q, tr.keys[:, pos], tr.values[:, pos])
     ob, _ = G.step(b, q, -tr.keys[:, pos], -tr.values[:, pos])
     assert np.array_equal(oa, ob)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_engine_step_graph_matches_eager(dtype):
+    """DecodeEngine.step replayed as a CUDA graph (attend + device-side append) gives the same
+    outputs, selections and ledgers as the eager launch sequence, across online updates."""
+    from paper_2506_13059_b200.engine import DecodeEngine
+
+    tr = gen_synthetic(8, 1000, HeadLayout(8, 2, 64), 0.1, seed=5, decode_steps=60)
+    cfg = EngineConfig(block_size=256, alpha=128, local_buffer=16, sink_tokens=5, token_budget=64, seed=5)
+    P = tr.prompt_len
+    engs = []
+    for graphs in (True, False):
+        e = DecodeEngine(cfg, tr.layout, 2, tcap=tr.total_len + 8, dtype=dtype, use_graphs=graphs)
+        k = torch.as_tensor(tr.keys[:, :P]).cuda()[None].repeat(2, 1, 1, 1)
+        v = torch.as_tensor(tr.values[:, :P]).cuda()[None].repeat(2, 1, 1, 1)
+        e.write_tokens(k, v)
+        e.prefill()
+        engs.append(e)
+    n_upd = 0
+    for t in range(60):
+        q = torch.as_tensor(tr.queries[:, t]).cuda()[None].repeat(2, 1, 1)
+        kn = torch.as_tensor(tr.keys[:, P + t]).cuda()[None].repeat(2, 1, 1)
+        vn = torch.as_tensor(tr.values[:, P + t]).cuda()[None].repeat(2, 1, 1)
+        outs = [e.step(q, kn, vn).clone() for e in engs]
+        assert torch.equal(outs[0], outs[1]), t
+        assert np.array_equal(engs[0].cache_len, engs[1].cache_len)
+        assert torch.equal(engs[0].cache_len_d, engs[1].cache_len_d)
+        n_upd += engs[0].last_update is not None
+    assert n_upd >= 3
+    for h in range(engs[0].L):
+        _assert_same_ledger(to_oracle(engs[0].export_ledger(h)), to_oracle(engs[1].export_ledger(h)), f"h={h}")
