@@ -454,7 +454,7 @@ def main():
             "dense_gbs": dbytes / (dense_avg * 1e-3) / 1e9,
             "flashinfer_dense_us": (fi_ms * 1e3) if fi_ms else None,
             "sequences_per_s": world * b / (ms_step * 1e-3),
-            "roofline": {"bound": "hbm", "kernel": "mpa_sparse_decode (decode_mma_kernel)",
+            "roofline": {"bound": "hbm", "kernel": "mpa_sparse_decode (decode_sk_kernel)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "peak_kind": peak_kind, "traffic": traffic,
                          "algorithmic_bytes_per_launch": nbytes["fused"], "launch_us": fused_avg * 1e3},
@@ -469,7 +469,7 @@ def main():
                        "pct_of_step": update_ms / L / ms_step * 100.0, "lloyd_rounds": upd["rounds"],
                        "prefill_s": prefill_s},
             "e2e": {"value": e2e_avg * 1e3, "unit": "us/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": 6 * K,
+            "gpu_launches": 5 * K,  # per step: rotate, logits, select+lists, fused decode, append (one graph)
             "clocks": clk.summary(),
         }
         if not args.no_cpu and not args.profile:
