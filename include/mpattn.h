@@ -200,11 +200,21 @@ typedef struct mpa_km {
     int32_t* cstart;         /* [sum k] first position of each cluster in order */
     int32_t* state;          /* [n_prob, 4] active, rounds, changed, has_empty */
     int32_t* flag;           /* [2] device scratch for the Lloyd driver loop (any active, max rounds) */
+    /* tensor-core assignment (bf16 points, d = 128): optional; NULL -> fp64 CUDA-core kernel */
+    int64_t pts_rows;        /* rows of the pts source ([L, tcap] flattened)            */
+    int32_t sum_n, sum_k;    /* total points / centroids of the batch                    */
+    void* tc_ws;             /* >= mpa_km_tc_workspace(n_prob, sum_k, sum_n, d) bytes    */
+    int64_t tc_ws_bytes;
 } mpa_km;
+
+/* Workspace of the tcgen05 assignment path (bf16 centroid terms, norms, recheck list). */
+size_t mpa_km_tc_workspace(int n_prob, int sum_k, int sum_n, int d);
 
 /* Lloyd to a fixed point for every problem (assign -> repair empties -> converged? -> means),
  * at least min_iters update rounds and at most min_iters + 100 (clustering.py:30, 123-143).
- * The assignment is the fp64 argmin of ||p||^2 + ||c||^2 - 2 p.c (first minimum); means are
+ * The assignment is the fp64 argmin of ||p||^2 + ||c||^2 - 2 p.c (first minimum) -- with
+ * tc_ws given (bf16 points, d = 128) the contraction runs on tcgen05 with fp64 certification of
+ * every point's best-vs-second margin and an exact fp64 re-score of the rest; means are
  * sequential fp64 member sums in ascending point order (bit-equal to np.add.at / np.mean).
  * Weighted mode (wts != NULL) keeps the centroid of an empty cluster (clustering.py:236-242).
  * Host-driven loop: one 8-byte readback per round.  *rounds_out = max rounds over problems. */

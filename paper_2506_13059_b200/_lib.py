@@ -42,7 +42,8 @@ class MpaKm(C.Structure):
                 ("wts", _vp), ("rows64_cap", _i32), ("n_max", _i32), ("k_max", _i32), ("min_iters", _i32),
                 ("prob_l", _vp), ("prob_start", _vp), ("prob_n", _vp), ("prob_k", _vp), ("pt_off", _vp),
                 ("c_off", _vp), ("assign", _vp), ("prev", _vp), ("p2", _vp), ("cent", _vp), ("c2", _vp),
-                ("count", _vp), ("order", _vp), ("cstart", _vp), ("state", _vp), ("flag", _vp)]
+                ("count", _vp), ("order", _vp), ("cstart", _vp), ("state", _vp), ("flag", _vp),
+                ("pts_rows", _i64), ("sum_n", _i32), ("sum_k", _i32), ("tc_ws", _vp), ("tc_ws_bytes", _i64)]
 
 
 _KM = C.POINTER(MpaKm)
@@ -73,7 +74,7 @@ _SIGS = {
 }
 
 # symbols that include/mpattn.h declares (checked by tests/test_abi.py)
-EXPORTED = ["mpa_last_error", "mpa_version", "mpa_sparse_decode_workspace", *_SIGS]
+EXPORTED = ["mpa_last_error", "mpa_version", "mpa_sparse_decode_workspace", "mpa_km_tc_workspace", *_SIGS]
 
 
 def _load():
@@ -85,6 +86,8 @@ def _load():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = C.c_int
+    lib.mpa_km_tc_workspace.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+    lib.mpa_km_tc_workspace.restype = C.c_size_t
     lib.mpa_sparse_decode_workspace.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
     lib.mpa_sparse_decode_workspace.restype = C.c_size_t
     lib.mpa_last_error.restype = C.c_char_p

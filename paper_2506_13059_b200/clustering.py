@@ -60,6 +60,15 @@ class KMeansBatch:
         self.min_iters = min_iters
         self.n_max = int(n.max()) if self.P else 0
         self.k_max = int(k.max()) if self.P else 0
+        self.sum_n, self.sum_k = N, K
+        # tcgen05 assignment (csrc/mpa_km_tc.cu) for bf16 key sources with d = 128
+        self.pts_rows = int(pts.shape[0] * pts.shape[1]) if pts is not None else 0
+        self.tc_ws = None
+        if pts is not None and pts.dtype == torch.bfloat16 and d == 128 and self.P:
+            from ._lib import lib
+
+            nb = int(lib().mpa_km_tc_workspace(self.P, K, N, d))
+            self.tc_ws = torch.empty(nb, dtype=torch.uint8, device=device)
 
     def struct(self) -> MpaKm:
         pts, tcap, pts64, wts, rcap = self.src
@@ -68,7 +77,8 @@ class KMeansBatch:
                      ptr(wts), rcap, self.n_max, self.k_max, self.min_iters, ptr(t["l"]), ptr(t["start"]),
                      ptr(t["n"]), ptr(t["k"]), ptr(t["pt_off"]), ptr(t["c_off"]), ptr(self.assign), ptr(self.prev),
                      ptr(self.p2), ptr(self.cent), ptr(self.c2), ptr(self.count), ptr(self.order), ptr(self.cstart),
-                     ptr(self.state), ptr(self.flag))
+                     ptr(self.state), ptr(self.flag), self.pts_rows, self.sum_n, self.sum_k, ptr(self.tc_ws),
+                     self.tc_ws.numel() if self.tc_ws is not None else 0)
 
     def lloyd(self) -> int:
         import ctypes

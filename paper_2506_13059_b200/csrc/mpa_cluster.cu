@@ -18,7 +18,11 @@
 // fp64 and matches numpy's except at true ties (|margin| ~ 1e-16 relative).
 #include <cub/block/block_radix_sort.cuh>
 
+#include <cstdlib>
+
 #include "mpa_common.cuh"
+
+int mpa_km_assign_tc(const mpa_km& k, cudaStream_t st);  // mpa_km_tc.cu
 
 namespace mpa {
 
@@ -637,6 +641,17 @@ void launch_round(const mpa_km& k, int grouping_only, cudaStream_t st) {
     km_round_kernel<<<k.n_prob, kRoundThreads, kRoundSmem, st>>>(k, grouping_only);
 }
 
+// tcgen05 assignment for bf16 point sources with d = 128 when a workspace is supplied
+// (MPA_KM_FP64=1 forces the fp64 CUDA-core kernel for A/B runs)
+bool use_tc(const mpa_km& k) {
+    static int force_fp64 = -1;
+    if (force_fp64 < 0) {
+        const char* e = getenv("MPA_KM_FP64");
+        force_fp64 = (e && e[0] == '1') ? 1 : 0;
+    }
+    return !force_fp64 && k.tc_ws && k.pts && !k.pts64 && k.pts_dtype == MPA_BF16 && k.d == 128 && k.pts_rows > 0;
+}
+
 int validate(const mpa_km* km) {
     MPA_REQUIRE(km && km->prob_l && km->prob_start && km->prob_n && km->prob_k && km->pt_off && km->c_off &&
                     km->assign && km->prev && km->cent && km->count && km->order && km->cstart && km->state,
@@ -666,8 +681,13 @@ extern "C" int mpa_km_lloyd(const mpa_km* km, int32_t* rounds_out, void* stream)
     cudaError_t e;
     int32_t hflag[2] = {0, 0};
     int rounds = 0;
+    const bool tc = use_tc(k);
     for (int r = 0; r < k.min_iters + kMaxExtraRounds + 2; ++r) {
-        km_assign_kernel<<<dim3(ceil_div(k.n_max, kAsgBM), P), kAsgThreads, 0, st>>>(k);
+        if (tc) {
+            if (int rc = mpa_km_assign_tc(k, st)) return rc;
+        } else {
+            km_assign_kernel<<<dim3(ceil_div(k.n_max, kAsgBM), P), kAsgThreads, 0, st>>>(k);
+        }
         launch_round(k, 0, st);
         km_means_kernel<<<dim3(ceil_div(k.k_max, kMeansWarps), P), kMeansWarps * 32, 0, st>>>(k, 0);
         km_c2_kernel<<<dim3(ceil_div(k.k_max, 128), P), 128, 0, st>>>(k, 1);

@@ -1,0 +1,331 @@
+// K2 on the 5th-generation tensor cores: the k-means assignment contraction P . C^T of every
+// Lloyd problem, tcgen05.mma (kind::f16, bf16 x bf16 -> fp32 in TMEM) fed by TMA, with an
+// fp64 certification that keeps the assignment identical to the exact fp64 argmin.
+//
+// Reference: clustering.py:84-88 (`_sq_dists` = ||p||^2 + ||c||^2 - 2 p.c) and :134 (argmin,
+// first minimum).
+//
+// Exactness.  Points are the bf16 K_raw cache rows (exact in bf16).  Each fp64 centroid is
+// split into three bf16 terms c = c1 + c2 + c3 + r (|r| <= 2^-24 |c| per element); the three
+// partial products accumulate into one fp32 TMEM accumulator, so acc = p.c + e with
+// |e| <= ~2^-16 (||p||^2 + ||c||^2) (fp32 accumulation over d = 128 exact products + the split
+// residual; the bound used below is 8x looser).  The epilogue computes d_j = c2_j - 2 acc_j in
+// fp32 and keeps, per point, the best (lowest index on ties) and the second-best candidate.
+// If second - best > 2 tau with tau = 2^-13 (||p||^2 + max_j ||c_j||^2), the exact fp64
+// argmin is provably the same unique index; otherwise the point is re-scored by
+// km_recheck_kernel with the exact fp64 formula of km_assign_kernel (sequential fp64 dot,
+// (p2 + c2) - 2 dot, first minimum).  Certified and re-checked points therefore assign exactly
+// like the fp64 kernel.  In practice only a handful of points per 8K-point problem fall
+// inside the band (SURVEY 7.3-2 measured best/second margins < 1e-3 for 2-11 of 8192).
+//
+// CTA = one (problem, 128-point tile); warp 4 issues TMA + MMA (one elected thread), warps 0-3
+// drain TMEM (one point per lane).  N tiles of 256 centroids, 6 K-major sub-tiles each
+// (3 terms x 2 x 64 columns), a 4-deep TMA ring, double-buffered 256-column accumulators.
+#include "mpa_common.cuh"
+#include "mpa_tc.cuh"
+
+namespace mpa {
+
+constexpr int kTcM = 128, kTcN = 256, kTcStages = 4, kTcSub = 6;
+constexpr int kTcThreads = 160;
+constexpr int kTcABytes = 2 * kTcM * 128;   // 2 x 64-column chunks of the point tile
+constexpr int kTcBBytes = kTcN * 128;       // one 256-row x 64-column centroid sub-tile
+constexpr int kTcSmem = 1024 + kTcABytes + kTcStages * kTcBBytes;
+
+struct TcWs {
+    __nv_bfloat16* terms;  // [3][kpad][d]
+    float* c2f;            // [kpad]
+    double* c2max;         // [n_prob]
+    int32_t* recheck;      // [sum n][2] (problem, point)
+    int32_t* n_recheck;    // [1]
+    int kpad;
+};
+
+__host__ __device__ inline size_t tc_ws_layout(int n_prob, int sum_k, int sum_n, int d, int* kpad_out,
+                                              size_t* off) {
+    const int kpad = (sum_k + 255) / 256 * 256 + 256;
+    size_t o = 0;
+    off[0] = o;
+    o += (size_t)3 * kpad * d * 2;
+    o = (o + 255) & ~(size_t)255;
+    off[1] = o;
+    o += (size_t)kpad * 4;
+    o = (o + 255) & ~(size_t)255;
+    off[2] = o;
+    o += (size_t)n_prob * 8;
+    o = (o + 255) & ~(size_t)255;
+    off[3] = o;
+    o += (size_t)sum_n * 8;
+    off[4] = o;
+    o += 256;
+    if (kpad_out) *kpad_out = kpad;
+    return o;
+}
+
+// fp64 centroids -> three bf16 terms, fp32 norms; per-problem max norm; recheck counter reset
+__global__ void km_tc_prep_kernel(mpa_km km, TcWs ws) {
+    const int p = blockIdx.y;
+    if (!km.state[p * 4 + 0]) return;
+    const int K = km.prob_k[p], d = km.d, c0 = km.c_off[p];
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < K * d; e += gridDim.x * blockDim.x) {
+        const int j = e / d, k = e - j * d;
+        const double c = km.cent[(size_t)(c0 + j) * d + k];
+        const __nv_bfloat16 t1 = __double2bfloat16(c);
+        const double r1 = c - (double)__bfloat162float(t1);
+        const __nv_bfloat16 t2 = __double2bfloat16(r1);
+        const double r2 = r1 - (double)__bfloat162float(t2);
+        const __nv_bfloat16 t3 = __double2bfloat16(r2);
+        ws.terms[((size_t)0 * ws.kpad + c0 + j) * d + k] = t1;
+        ws.terms[((size_t)1 * ws.kpad + c0 + j) * d + k] = t2;
+        ws.terms[((size_t)2 * ws.kpad + c0 + j) * d + k] = t3;
+        if (k == 0) ws.c2f[c0 + j] = (float)km.c2[c0 + j];
+    }
+}
+
+__global__ void km_tc_norms_kernel(mpa_km km, TcWs ws) {
+    const int p = blockIdx.x;
+    if (p == 0 && threadIdx.x == 0) *ws.n_recheck = 0;
+    double m = 0.0;
+    for (int j = threadIdx.x; j < km.prob_k[p]; j += blockDim.x) m = fmax(m, km.c2[km.c_off[p] + j]);
+    __shared__ double red[32];
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double r = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, red[w]);
+        ws.c2max[p] = r;
+    }
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+km_assign_tc_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_constant__ CUtensorMap tm_terms, mpa_km km,
+                    TcWs ws) {
+    const int p = blockIdx.y, tile = blockIdx.x;
+    if (!km.state[p * 4 + 0]) return;
+    const int n = km.prob_n[p], K = km.prob_k[p];
+    if (tile * kTcM >= n) return;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    unsigned char* sa = smem;
+    unsigned char* sb = smem + kTcABytes;
+    __shared__ __align__(8) uint64_t bar_a, bar_full[kTcStages], bar_empty[kTcStages], bar_acc_full[2],
+        bar_acc_empty[2];
+    __shared__ uint32_t tmem_base;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) tmem_alloc(&tmem_base, 512);
+    if (threadIdx.x == 0) {
+        mbar_init(smem_u32(&bar_a), 1);
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(smem_u32(&bar_full[s]), 1);
+            mbar_init(smem_u32(&bar_empty[s]), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&bar_acc_full[b]), 1);
+            mbar_init(smem_u32(&bar_acc_empty[b]), 4);
+        }
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    const int n_nt = (K + kTcN - 1) / kTcN, S = n_nt * kTcSub;
+    const int c_off = km.c_off[p];
+
+    if (warp == 4) {
+        if (lane == 0) {
+            prefetch_tmap(&tm_pts);
+            prefetch_tmap(&tm_terms);
+            const int row0 = km.prob_l[p] * km.tcap + km.prob_start[p] + tile * kTcM;
+            mbar_expect_tx(smem_u32(&bar_a), kTcABytes);
+            tma_load_2d(smem_u32(sa), &tm_pts, 0, row0, smem_u32(&bar_a));
+            tma_load_2d(smem_u32(sa + kTcM * 128), &tm_pts, 64, row0, smem_u32(&bar_a));
+            auto issue_b = [&](int s) {
+                const int nt = s / kTcSub, u = s - nt * kTcSub, t = u >> 1, c = u & 1;
+                const unsigned slot = smem_u32(sb + (s % kTcStages) * kTcBBytes);
+                mbar_expect_tx(smem_u32(&bar_full[s % kTcStages]), kTcBBytes);
+                tma_load_2d(slot, &tm_terms, c * 64, t * ws.kpad + c_off + nt * kTcN,
+                            smem_u32(&bar_full[s % kTcStages]));
+            };
+            for (int s = 0; s < kTcStages && s < S; ++s) issue_b(s);
+            mbar_wait(smem_u32(&bar_a), 0);
+            tc_fence_after();
+            const uint32_t idesc = umma_idesc_bf16_f32(kTcM, kTcN);
+            for (int nt = 0; nt < n_nt; ++nt) {
+                const int buf = nt & 1;
+                if (nt >= 2) mbar_wait(smem_u32(&bar_acc_empty[buf]), ((nt - 2) >> 1) & 1);
+                tc_fence_after();
+                for (int u = 0; u < kTcSub; ++u) {
+                    const int s = nt * kTcSub + u, c = u & 1;
+                    mbar_wait(smem_u32(&bar_full[s % kTcStages]), (s / kTcStages) & 1);
+                    tc_fence_after();
+                    const unsigned bslot = smem_u32(sb + (s % kTcStages) * kTcBBytes);
+                    const unsigned aslot = smem_u32(sa + c * kTcM * 128);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        umma_bf16(tmem + buf * kTcN, umma_desc_sw128(aslot + k * 32), umma_desc_sw128(bslot + k * 32),
+                                  idesc, (u | k) ? 1u : 0u);
+                    umma_commit(smem_u32(&bar_empty[s % kTcStages]));
+                    // refill the slot used one step earlier (its MMAs are queued ahead of this step's)
+                    if (s >= 1 && s - 1 + kTcStages < S) {
+                        mbar_wait(smem_u32(&bar_empty[(s - 1) % kTcStages]), ((s - 1) / kTcStages) & 1);
+                        issue_b(s - 1 + kTcStages);
+                    }
+                }
+                umma_commit(smem_u32(&bar_acc_full[buf]));
+            }
+        }
+        __syncwarp();
+    } else {
+        // epilogue: this lane's point = TMEM lane warp*32 + lane
+        const int i = tile * kTcM + warp * 32 + lane;
+        float best = INFINITY, second = INFINITY;
+        int jbest = 0x7fffffff;
+        for (int nt = 0; nt < n_nt; ++nt) {
+            const int buf = nt & 1;
+            mbar_wait(smem_u32(&bar_acc_full[buf]), (nt >> 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c0 = 0; c0 < kTcN; c0 += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + buf * kTcN + c0, v);
+                tmem_ld_wait();
+                const int jb = nt * kTcN + c0;
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    const int j = jb + q;
+                    if (j < K) {
+                        const float dj = __ldg(ws.c2f + c_off + j) - 2.f * __uint_as_float(v[q]);
+                        if (dj < best) {
+                            second = best;
+                            best = dj;
+                            jbest = j;
+                        } else if (dj < second) {
+                            second = dj;
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bar_acc_empty[buf]));
+        }
+        if (i < n) {
+            const int g = km.pt_off[p] + i;
+            const double tau = ldexp(km.p2[g] + ws.c2max[p], -13);
+            if ((double)second - (double)best > 2.0 * tau) {
+                km.assign[g] = jbest;
+            } else {
+                const int r = atomicAdd(ws.n_recheck, 1);
+                ws.recheck[2 * r] = p;
+                ws.recheck[2 * r + 1] = i;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+// exact fp64 re-scoring of the uncertified points: one warp per point, same arithmetic as
+// km_assign_kernel (sequential fp64 dot, (p2 + c2) - 2 dot, first minimum)
+__global__ void km_recheck_kernel(mpa_km km, TcWs ws) {
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    const int lane = threadIdx.x & 31;
+    const int nr = *ws.n_recheck;
+    for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < nr; r += warps) {
+        const int p = ws.recheck[2 * r], i = ws.recheck[2 * r + 1];
+        const int K = km.prob_k[p], d = km.d, l = km.prob_l[p], row = km.prob_start[p] + i;
+        const int g = km.pt_off[p] + i;
+        const double p2 = km.p2[g];
+        const __nv_bfloat16* pt = reinterpret_cast<const __nv_bfloat16*>(km.pts) + ((size_t)l * km.tcap + row) * d;
+        double best = INFINITY;
+        int jb = 0x7fffffff;
+        for (int j = lane; j < K; j += 32) {
+            const double* c = km.cent + (size_t)(km.c_off[p] + j) * d;
+            double dot = 0.0;
+            for (int k = 0; k < d; ++k) dot = fma((double)__bfloat162float(pt[k]), c[k], dot);
+            const double dist = __dsub_rn(__dadd_rn(p2, km.c2[km.c_off[p] + j]), __dmul_rn(2.0, dot));
+            if (dist < best || (dist == best && j < jb)) {
+                best = dist;
+                jb = j;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, jb, o);
+            if (ob < best || (ob == best && oj < jb)) {
+                best = ob;
+                jb = oj;
+            }
+        }
+        if (lane == 0) km.assign[g] = jb;
+    }
+}
+
+}  // namespace mpa
+
+using namespace mpa;
+
+namespace {
+
+int encode_rows_map(CUtensorMap* out, const void* base, long long rows, int d, int box_rows) {
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        const cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        MPA_REQUIRE(e == cudaSuccess && q == cudaDriverEntryPointSuccess && fn, MPA_ERR_UNSUPPORTED,
+                    "cuTensorMapEncodeTiled unavailable (%d)", (int)e);
+        encode = reinterpret_cast<EncodeFn>(fn);
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    MPA_REQUIRE(r == CUDA_SUCCESS, MPA_ERR_ARG, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return 0;
+}
+
+}  // namespace
+
+// workspace of the tensor-core assignment for a batch (n_prob problems, sum_k centroids,
+// sum_n points, dimension d)
+extern "C" size_t mpa_km_tc_workspace(int n_prob, int sum_k, int sum_n, int d) {
+    if (n_prob <= 0 || sum_k <= 0 || sum_n <= 0 || d <= 0) return 0;
+    size_t off[5];
+    return tc_ws_layout(n_prob, sum_k, sum_n, d, nullptr, off);
+}
+
+// one assignment pass on the tensor cores (used by mpa_km_lloyd when km->tc_ws is given)
+int mpa_km_assign_tc(const mpa_km& k, cudaStream_t st) {
+    size_t off[5];
+    int kpad = 0;
+    const size_t need = tc_ws_layout(k.n_prob, k.sum_k, k.sum_n, k.d, &kpad, off);
+    MPA_REQUIRE(k.tc_ws && (size_t)k.tc_ws_bytes >= need, MPA_ERR_ARG, "mpa_km: tensor-core workspace %lld < %zu",
+                (long long)k.tc_ws_bytes, need);
+    char* base = (char*)k.tc_ws;
+    TcWs ws{(__nv_bfloat16*)(base + off[0]), (float*)(base + off[1]), (double*)(base + off[2]),
+            (int32_t*)(base + off[3]), (int32_t*)(base + off[4]), kpad};
+    CUtensorMap tp, tt;
+    if (int rc = encode_rows_map(&tp, k.pts, (long long)k.pts_rows, k.d, kTcM)) return rc;
+    if (int rc = encode_rows_map(&tt, ws.terms, 3ll * kpad, k.d, kTcN)) return rc;
+    km_tc_norms_kernel<<<k.n_prob, 256, 0, st>>>(k, ws);
+    km_tc_prep_kernel<<<dim3(ceil_div(k.k_max * k.d, 256 * 8), k.n_prob), 256, 0, st>>>(k, ws);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(km_assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
+        attr = true;
+    }
+    km_assign_tc_kernel<<<dim3(ceil_div(k.n_max, kTcM), k.n_prob), kTcThreads, kTcSmem, st>>>(tp, tt, k, ws);
+    km_recheck_kernel<<<148, 256, 0, st>>>(k, ws);
+    return check_launch("mpa_km_assign(tcgen05)");
+}

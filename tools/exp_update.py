@@ -1,0 +1,67 @@
+"""Time one online-update event at the bench workload, phase by phase (host wall clock with
+device syncs), plus the GPU kernel time of each phase via CUDA events."""
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    import torch
+
+    import bench
+    from paper_2506_13059_b200 import clustering
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--ctx", type=int, default=32768)
+    a = ap.parse_args()
+    args = argparse.Namespace(batch=a.batch, ctx=a.ctx, budget=512, steps=2, warmup=3)
+    eng, Q, KN, VN, _ = bench.build_engine(args, 0, torch.device("cuda", 0))
+    L = eng.cfg.local_buffer
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    need = int(2 * L - (eng.cache_len[0] - eng.buffer_start[0]))
+    eng.write_tokens(torch.randn(eng.n_seq, eng.Hkv, need, 128, generator=gen, device="cuda"),
+                     torch.randn(eng.n_seq, eng.Hkv, need, 128, generator=gen, device="cuda"))
+    torch.cuda.synchronize()
+    orig = {name: getattr(clustering, name) for name in ("_write_fine", "_refresh_counts", "_split", "_hierarchy")}
+    times = {}
+
+    def wrap(name, fn):
+        def w(*x, **k):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = fn(*x, **k)
+            torch.cuda.synchronize()
+            times[name] = times.get(name, 0.0) + time.perf_counter() - t0
+            return r
+        return w
+
+    for name, fn in orig.items():
+        setattr(clustering, name, wrap(name, fn))
+    KM = clustering.KMeansBatch
+    orig_lloyd = KM.lloyd
+
+    def lloyd(self):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = orig_lloyd(self)
+        torch.cuda.synchronize()
+        times["lloyd"] = times.get("lloyd", 0.0) + time.perf_counter() - t0
+        times["lloyd_rounds"] = r
+        return r
+
+    KM.lloyd = lloyd
+    t0 = time.perf_counter()
+    upd = clustering.online_update(eng, list(range(eng.n_seq)), 0)
+    torch.cuda.synchronize()
+    total = time.perf_counter() - t0
+    print("update total ms", round(total * 1e3, 2), upd)
+    for k, v in times.items():
+        print(f"  {k:16s} {v * 1e3 if k != 'lloyd_rounds' else v:9.2f}")
+
+
+if __name__ == "__main__":
+    main()

@@ -46,6 +46,14 @@ def main():
     if args.dense:
         eng.attend_dense(Q[0])
     if args.update:
+        L = eng.cfg.local_buffer
+        need = int(2 * L - (eng.cache_len[0] - eng.buffer_start[0]))
+        if need > 0:
+            torch.cuda.cudart().cudaProfilerStop()
+            eng.write_tokens(torch.randn(eng.n_seq, eng.Hkv, need, eng.d, device=eng.device),
+                             torch.randn(eng.n_seq, eng.Hkv, need, eng.d, device=eng.device))
+            torch.cuda.synchronize()
+            torch.cuda.cudart().cudaProfilerStart()
         clustering.online_update(eng, list(range(eng.n_seq)), eng.cursor)
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStop()
