@@ -240,12 +240,21 @@ __global__ void km_recheck_kernel(mpa_km km, TcWs ws) {
         const int g = km.pt_off[p] + i;
         const double p2 = km.p2[g];
         const __nv_bfloat16* pt = reinterpret_cast<const __nv_bfloat16*>(km.pts) + ((size_t)l * km.tcap + row) * d;
+        __shared__ double xs[8][128];  // the point, fp64, per warp
+        double* x = xs[threadIdx.x >> 5];
+        for (int k = lane; k < 128; k += 32) x[k] = (double)__bfloat162float(pt[k]);
+        __syncwarp();
         double best = INFINITY;
         int jb = 0x7fffffff;
         for (int j = lane; j < K; j += 32) {
-            const double* c = km.cent + (size_t)(km.c_off[p] + j) * d;
-            double dot = 0.0;
-            for (int k = 0; k < d; ++k) dot = fma((double)__bfloat162float(pt[k]), c[k], dot);
+            const double2* c = reinterpret_cast<const double2*>(km.cent + (size_t)(km.c_off[p] + j) * d);
+            double dot = 0.0;  // sequential over k, like km_assign_kernel
+#pragma unroll 8
+            for (int k2 = 0; k2 < 64; ++k2) {
+                const double2 cv = __ldg(c + k2);
+                dot = fma(x[2 * k2], cv.x, dot);
+                dot = fma(x[2 * k2 + 1], cv.y, dot);
+            }
             const double dist = __dsub_rn(__dadd_rn(p2, km.c2[km.c_off[p] + j]), __dmul_rn(2.0, dot));
             if (dist < best || (dist == best && j < jb)) {
                 best = dist;
@@ -262,6 +271,7 @@ __global__ void km_recheck_kernel(mpa_km km, TcWs ws) {
             }
         }
         if (lane == 0) km.assign[g] = jb;
+        __syncwarp();
     }
 }
 
@@ -326,6 +336,6 @@ int mpa_km_assign_tc(const mpa_km& k, cudaStream_t st) {
         attr = true;
     }
     km_assign_tc_kernel<<<dim3(ceil_div(k.n_max, kTcM), k.n_prob), kTcThreads, kTcSmem, st>>>(tp, tt, k, ws);
-    km_recheck_kernel<<<148, 256, 0, st>>>(k, ws);
+    km_recheck_kernel<<<64, 256, 0, st>>>(k, ws);
     return check_launch("mpa_km_assign(tcgen05)");
 }

@@ -63,5 +63,33 @@ def main():
         print(f"  {k:16s} {v * 1e3 if k != 'lloyd_rounds' else v:9.2f}")
 
 
+def recheck_stats():
+    """Rows re-scored in fp64 by the last tcgen05 assignment pass of a Lloyd call."""
+    import torch
+
+    from paper_2506_13059_b200 import clustering
+
+    orig = clustering.KMeansBatch.lloyd
+
+    def lloyd(self):
+        r = orig(self)
+        if self.tc_ws is not None:
+            kpad = (self.sum_k + 255) // 256 * 256 + 256
+            o = 3 * kpad * self.d * 2
+            o = (o + 255) & ~255
+            o += kpad * 4
+            o = (o + 255) & ~255
+            o += self.P * 8
+            o = (o + 255) & ~255
+            o += self.sum_n * 8
+            cnt = int(self.tc_ws[o:o + 4].view(torch.int32).item())
+            print(f"  recheck rows (last pass): {cnt} of {self.sum_n}")
+        return r
+
+    clustering.KMeansBatch.lloyd = lloyd
+
+
 if __name__ == "__main__":
+    if os.environ.get("RECHECK"):
+        recheck_stats()
     main()
