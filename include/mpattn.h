@@ -166,6 +166,61 @@ int mpa_sparse_decode(const mpa_cache* cache, const float* q_rot, int n_kv_heads
                       int n_split, void* workspace, size_t workspace_bytes, float* out, void* stream);
 
 /* ------------------------------------------------------------------------------------------
+ * Sequence-sharded decode (one long context over P ranks): rank r holds a
+ * contiguous range of every ledger's W-blocks (the last rank also the final block, sinks and
+ * buffer); fine ids are global = gid_off[l] + local id, so the reference's (block, cluster)
+ * tie-break order is preserved.  Per step:
+ *   1. mpa_centroid_logits (local) -> mpa_head_norms -> all-gather -> mpa_merge_norms: the
+ *      global (M, Z) of Eq. 1 (attention.py:276-278 normalise over ALL clusters of the head);
+ *   2. mpa_select_worklist_sharded(prefix): each rank's candidates that can be globally selected
+ *      (its local take-while-cum<B prefix) -> all-gather -> mpa_global_cut: the global crossing
+ *      candidate, identical on every rank (attention.py:192-207);
+ *   3. mpa_select_worklist_sharded(cross): flags + work lists of the local candidates;
+ *   4. mpa_sparse_decode_partials -> all-gather -> mpa_merge_rank_partials (attention.py:230-239).
+ * Heads / batch shard without any exchange. */
+typedef struct mpa_prefix_entry {
+    uint64_t key;     /* ~bits(score): ascending key == descending score */
+    uint32_t gid;     /* global cluster id */
+    int32_t size;
+} mpa_prefix_entry;
+typedef struct mpa_cross {
+    uint64_t key;     /* 0: select none; ~0: select all */
+    uint32_t gid;
+    uint32_t pad;
+} mpa_cross;
+
+/* out[l, g] = (M, Z) of this rank's candidates from mpa_centroid_logits' chunk partials. */
+int mpa_head_norms(const double* chunk_stats, int n_chunks, const int32_t* count, int n_ledgers, int group,
+                   double* out, void* stream);
+/* parts [P, L, G, 2] (every rank's (M, Z)) -> out [L, G, 2] global (M, Z). */
+int mpa_merge_norms(const double* parts, int n_ranks, int n_ledgers, int group, double* out, void* stream);
+/* Flat selection of a sharded ledger with the global normalisers mz [L, G, 2] and global ids
+ * gid_off[l] + i.  Local pass (prefix != NULL, cross == NULL): writes the rank's candidate prefix
+ * prefix[l, 0 .. prefix_n[l]) (prefix_n zeroed by the caller, capacity prefix_cap >= budget + 1).
+ * Final pass (cross != NULL): flags, sel_tokens, work lists and stats as mpa_select_worklist. */
+int mpa_select_worklist_sharded(const mpa_level* fine, int group, const double* logits, const double* e_local,
+                                const double* chunk_stats, const int64_t* budget, const int32_t* sink_end,
+                                const int32_t* buffer_start, const int32_t* cache_len, int n_kv_heads,
+                                int replacement, uint8_t* flag, int32_t* sel_tokens, int32_t* tok, int tok_cap,
+                                int32_t* rej, float* rej_w, int rej_cap, int32_t* stats, int n_max,
+                                const double* mz, const void* cross, void* prefix, int32_t* prefix_n,
+                                int prefix_cap, const int32_t* gid_off, void* stream);
+/* prefix [P, L, cap] + prefix_n [P, L] of every rank -> cross [L] (mpa_cross). */
+int mpa_global_cut(const void* prefix, const int32_t* prefix_n, int n_ranks, int n_ledgers, int prefix_cap,
+                   const int64_t* budget, void* cross, void* stream);
+/* mpa_sparse_decode writing per (ledger, q-head) partials [L, G, 2 + d] = (m natural-log, s,
+ * a[d]) instead of a / s. */
+int mpa_sparse_decode_partials(const mpa_cache* cache, const float* q_rot, int n_kv_heads, int group,
+                               const int32_t* tok, const int32_t* n_tok, int tok_cap,
+                               const int32_t* rej, const float* rej_w, const int32_t* n_rej, int rej_cap,
+                               const void* fine_vc, int fine_cap, const void* coarse_vc, int coarse_cap,
+                               int n_split, void* workspace, size_t workspace_bytes, float* part_out,
+                               void* stream);
+/* parts [P, L, G, 2 + d] -> out [L, G, d] (LSE merge + finalize). */
+int mpa_merge_rank_partials(const float* parts, int n_ranks, int n_ledgers, int group, int head_dim, float* out,
+                            void* stream);
+
+/* ------------------------------------------------------------------------------------------
  * Clustering (K2-K8).  A batch of independent k-means "problems" p, each over a contiguous run
  * of points: rows prob_start[p] .. +prob_n[p] of ledger prob_l[p] -- either pre-rotation keys
  * (pts: [L, tcap, d] in pts_dtype) or fp64 rows (pts64: [L, rows64_cap, d], the fine centroids,

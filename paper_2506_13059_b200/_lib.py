@@ -63,6 +63,15 @@ _SIGS = {
     "mpa_build_worklist": [C.POINTER(MpaLevel), C.POINTER(MpaLevel), C.c_int, _vp, _vp, C.c_int, _vp, _vp,
                            _vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int, _vp, _vp,
                            C.c_int, _vp, _vp],
+    "mpa_head_norms": [_vp, C.c_int, _vp, C.c_int, C.c_int, _vp, _vp],
+    "mpa_merge_norms": [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp],
+    "mpa_select_worklist_sharded": [C.POINTER(MpaLevel), C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int,
+                                    C.c_int, _vp, _vp, _vp, C.c_int, _vp, _vp, C.c_int, _vp, C.c_int, _vp, _vp,
+                                    _vp, _vp, C.c_int, _vp, _vp],
+    "mpa_global_cut": [_vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp],
+    "mpa_sparse_decode_partials": [C.POINTER(MpaCache), _vp, C.c_int, C.c_int, _vp, _vp, C.c_int, _vp, _vp, _vp,
+                                   C.c_int, _vp, C.c_int, _vp, C.c_int, C.c_int, _vp, C.c_size_t, _vp, _vp],
+    "mpa_merge_rank_partials": [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp],
     "mpa_km_lloyd": [_KM, C.POINTER(_i32), _vp],
     "mpa_km_means": [_KM, _vp],
     "mpa_km_count_nonempty": [_KM, _vp, _vp],

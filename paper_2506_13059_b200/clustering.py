@@ -150,9 +150,11 @@ def _head(eng, l: int) -> int:
 # ---------------------------------------------------------------------------- prefill
 
 
-def prefill_ledgers(eng) -> None:
+def prefill_ledgers(eng, owned=None) -> None:
     """Blockwise k-means of every ledger's prompt (clustering.py:288-326); k = ceil(n / r),
-    init = default_rng(block_seed(seed, head, b)).choice(n, k, replace=False)."""
+    init = default_rng(block_seed(seed, head, b)).choice(n, k, replace=False).
+    owned(b, n_blocks) -> bool restricts the ledger to some of its blocks (sequence sharding:
+    block seeds keep their global index b, fine ids are local to the owned blocks)."""
     cfg, led = eng.cfg, eng.led
     W = cfg.block_size
     eng.set_prompt_layout()
@@ -163,8 +165,13 @@ def prefill_ledgers(eng) -> None:
         s0, b0 = int(eng.sink_end[s]), int(eng.buffer_start[s])
         nsealed = (b0 - s0) // W
         spans = [(s0 + b * W, s0 + b * W + W) for b in range(nsealed)] + [(s0 + nsealed * W, b0)]
+        if owned is not None:
+            spans = [sp if owned(b, len(spans)) else None for b, sp in enumerate(spans)]
         tables.append(spans)
-        for b, (lo, hi) in enumerate(spans):
+        for b, sp in enumerate(spans):
+            if sp is None:
+                continue
+            lo, hi = sp
             n = hi - lo
             if n <= 0:
                 continue
@@ -183,7 +190,10 @@ def prefill_ledgers(eng) -> None:
     for l in range(eng.L):
         s0 = int(eng.sink_end[l // eng.Hkv])
         rows, acc = [], 0
-        for b, (lo, hi) in enumerate(tables[l]):
+        for b, sp in enumerate(tables[l]):
+            if sp is None:
+                continue
+            lo, hi = sp
             i = per.get((l, b))
             fk = int(nk[i]) if i is not None else 0
             if i is not None:

@@ -41,6 +41,7 @@
 namespace mpa {
 
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
 
 // padded logit stride of the rejected-centroid list (rej_w rows): 4 floats for G <= 4, else 8
 __host__ __device__ constexpr int rej_stride(int G) { return G <= 4 ? 4 : 8; }
@@ -64,8 +65,25 @@ __device__ __forceinline__ SplitRange split_range(int nt, int nr, int s, int S) 
     return r;
 }
 
+// A ledger's result: out = a / s, or (part_out != NULL, sequence-sharded decode) its unnormalised
+// partial [m (natural-log units), s, a[d]] per q-head for the cross-rank merge.
+__device__ __forceinline__ void emit_result(float* out, float* part_out, int l, int G, int d, int g, int k, float m_nat,
+                                            float s, float a) {
+    if (part_out) {
+        float* P = part_out + ((size_t)l * G + g) * (d + 2);
+        if (k == 0) {
+            P[0] = m_nat;
+            P[1] = s;
+        }
+        P[2 + k] = a;
+    } else {
+        out[((size_t)l * G + g) * d + k] = a / s;
+    }
+}
+
 // Last-CTA merge of the n_split partials of ledger l.
-__device__ void merge_splits(int l, int S, int G, int d, const float* part_ml, const float* part_acc, float* out) {
+__device__ void merge_splits(int l, int S, int G, int d, const float* part_ml, const float* part_acc, float* out,
+                             float* part_out) {
     for (int idx = threadIdx.x; idx < G * d; idx += blockDim.x) {
         const int g = idx / d, k = idx - g * d;
         float M = -INFINITY;
@@ -80,7 +98,7 @@ __device__ void merge_splits(int l, int S, int G, int d, const float* part_ml, c
                 acc += w * __ldcg(part_acc + (((size_t)l * S + s) * G + g) * d + k);
             }
         }
-        out[((size_t)l * G + g) * d + k] = acc / sum;
+        emit_result(out, part_out, l, G, d, g, k, M, sum, acc);
     }
 }
 
@@ -108,7 +126,8 @@ decode_ffma_kernel(const T* __restrict__ k_rot, const T* __restrict__ vcache, in
                    int tok_cap, const int32_t* __restrict__ rej, const float* __restrict__ rej_w,
                    const int32_t* __restrict__ n_rej, int rej_cap, const T* __restrict__ fvc, int fcap,
                    const T* __restrict__ cvc, int ccap, int S, float* __restrict__ part_ml,
-                   float* __restrict__ part_acc, int32_t* __restrict__ ticket, float* __restrict__ out) {
+                   float* __restrict__ part_acc, int32_t* __restrict__ ticket, float* __restrict__ out,
+                   float* __restrict__ part_out) {
     constexpr int GP = rej_stride(G);
     extern __shared__ float sm[];  // [warps][G][2 + d]
     const int l = blockIdx.y, s = blockIdx.x;
@@ -214,7 +233,7 @@ decode_ffma_kernel(const T* __restrict__ k_rot, const T* __restrict__ vcache, in
             part_ml[(((size_t)l * S + s) * G + g) * 2 + 1] = sum;
         }
     }
-    if (take_ticket(ticket, l, S)) merge_splits(l, S, G, d, part_ml, part_acc, out);
+    if (take_ticket(ticket, l, S)) merge_splits(l, S, G, d, part_ml, part_acc, out, part_out);
 }
 
 // ============================================================================
@@ -366,7 +385,7 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
                  const float* __restrict__ q_rot, const int32_t* __restrict__ tok, const int32_t* __restrict__ n_tok,
                  int tok_cap, const int32_t* __restrict__ rej, const float* __restrict__ rej_w,
                  const int32_t* __restrict__ n_rej, int rej_cap, int fcap, int ccap, int L, float* __restrict__ part,
-                 int32_t* __restrict__ ticket, float* __restrict__ out) {
+                 int32_t* __restrict__ ticket, float* __restrict__ out, float* __restrict__ part_out) {
     dbg_stamp(0);
     using Geo = SkGeom<G, D, NW, NST>;
     constexpr bool PACKED = G <= 4;
@@ -731,7 +750,7 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
                 }
             }
             if (whole) {
-                out[(size_t)l * G * D + idx] = A / S;
+                emit_result(out, part_out, l, G, D, g, k, M * kLn2, S, A);
             } else {
                 dst[2 * G + idx] = A;
                 if (k == 0) {
@@ -810,7 +829,8 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
 #pragma unroll
                 for (int j = 0; j < PER; ++j) {
                     const int idx = threadIdx.x + j * NW * 32;
-                    if (idx < G * D) out[(size_t)l * G * D + idx] = A[j] / S[j];
+                    if (idx < G * D)
+                        emit_result(out, part_out, l, G, D, idx / D, idx % D, M[j] * kLn2, S[j], A[j]);
                 }
             }
         }
@@ -958,7 +978,7 @@ template <int G>
 int launch_ffma(const mpa_cache* c, const float* q_rot, const int32_t* tok, const int32_t* n_tok, int tok_cap,
                 const int32_t* rej, const float* rej_w, const int32_t* n_rej, int rej_cap, const void* fvc, int fcap,
                 const void* cvc, int ccap, int S, float* pml, float* pacc, int32_t* ticket, float* out,
-                cudaStream_t st) {
+                float* part_out, cudaStream_t st) {
     const int d = c->head_dim;
     const int ndl = ceil_div(d, 32);
     dim3 grid(S, c->n_ledgers);
@@ -969,7 +989,8 @@ int launch_ffma(const mpa_cache* c, const float* q_rot, const int32_t* tok, cons
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         kern<<<grid, kFfmaWarps * 32, smem, st>>>((const T*)c->k_rot, (const T*)c->v, c->tcap, d, q_rot, tok,   \
                                                   n_tok, tok_cap, rej, rej_w, n_rej, rej_cap, (const T*)fvc,    \
-                                                  fcap, (const T*)cvc, ccap, S, pml, pacc, ticket, out);        \
+                                                  fcap, (const T*)cvc, ccap, S, pml, pacc, ticket, out,         \
+                                                  part_out);                                                    \
     }
 #define MPA_FFMA_NDL(T)                                    \
     switch (ndl) {                                         \
@@ -1034,7 +1055,8 @@ int bf16_rows_map(CUtensorMap* out, const void* base, long long rows, int d) {
 template <int G, int D>
 int launch_sk(const mpa_cache* c, const float* q_rot, const int32_t* tok, const int32_t* n_tok, int tok_cap,
               const int32_t* rej, const float* rej_w, const int32_t* n_rej, int rej_cap, const void* fvc, int fcap,
-              const void* cvc, int ccap, int C, float* part, int32_t* ticket, float* out, cudaStream_t st) {
+              const void* cvc, int ccap, int C, float* part, int32_t* ticket, float* out, float* part_out,
+              cudaStream_t st) {
     using Geo = SkGeom<G, D, kSkWarps, kSkStages>;
     const int L = c->n_ledgers;
     const size_t smem = Geo::smem(L, C);
@@ -1048,7 +1070,7 @@ int launch_sk(const mpa_cache* c, const float* q_rot, const int32_t* tok, const 
     if (!rc) rc = cvc ? bf16_rows_map(&tc, cvc, (long long)L * ccap, D) : (tc = tf, 0);
     if (rc) return rc;
     kern<<<C, kSkWarps * 32, smem, st>>>(tk, tv, tf, tc, c->tcap, q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej,
-                                         rej_cap, fcap, ccap, L, part, ticket, out);
+                                         rej_cap, fcap, ccap, L, part, ticket, out, part_out);
     return check_launch("mpa_sparse_decode(stream-K mma)");
 }
 
@@ -1091,12 +1113,12 @@ extern "C" size_t mpa_sparse_decode_workspace(int n_ledgers, int group, int head
     return ws_ticket_bytes(n_ledgers) + fl * sizeof(float);
 }
 
-extern "C" int mpa_sparse_decode(const mpa_cache* c, const float* q_rot, int n_kv_heads, int group,
+static int sparse_decode_impl(const mpa_cache* c, const float* q_rot, int n_kv_heads, int group,
                                  const int32_t* tok, const int32_t* n_tok, int tok_cap, const int32_t* rej,
                                  const float* rej_w, const int32_t* n_rej, int rej_cap, const void* fine_vc,
                                  int fine_cap, const void* coarse_vc, int coarse_cap, int n_split, void* workspace,
-                                 size_t workspace_bytes, float* out, void* stream) {
-    MPA_REQUIRE(c && q_rot && n_tok && workspace && out, MPA_ERR_ARG, "mpa_sparse_decode: null argument");
+                                 size_t workspace_bytes, float* out, float* part_out, void* stream) {
+    MPA_REQUIRE(c && q_rot && n_tok && workspace && (out || part_out), MPA_ERR_ARG, "mpa_sparse_decode: null argument");
     MPA_REQUIRE(!rej || (rej_w && n_rej), MPA_ERR_ARG, "mpa_sparse_decode: rej without weights/counts");
     MPA_REQUIRE(c->head_dim >= 2 && c->head_dim % 2 == 0 && c->head_dim <= 256, MPA_ERR_UNSUPPORTED,
                 "mpa_sparse_decode: head_dim %d", c->head_dim);
@@ -1114,9 +1136,9 @@ extern "C" int mpa_sparse_decode(const mpa_cache* c, const float* q_rot, int n_k
         MPA_DISPATCH_G(group, {
             if (c->head_dim == 128)
                 return launch_sk<kG, 128>(c, q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej, rej_cap, fine_vc,
-                                          fine_cap, coarse_vc, coarse_cap, C, part, ticket, out, st);
+                                          fine_cap, coarse_vc, coarse_cap, C, part, ticket, out, part_out, st);
             return launch_sk<kG, 64>(c, q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej, rej_cap, fine_vc, fine_cap,
-                                     coarse_vc, coarse_cap, C, part, ticket, out, st);
+                                     coarse_vc, coarse_cap, C, part, ticket, out, part_out, st);
         });
     }
     const int S = ffma_splits(L, n_split);
@@ -1124,7 +1146,61 @@ extern "C" int mpa_sparse_decode(const mpa_cache* c, const float* q_rot, int n_k
     float* pacc = part + (size_t)L * S * group * 2;
     MPA_DISPATCH_G(group, {
         return launch_ffma<kG>(c, q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej, rej_cap, fine_vc, fine_cap,
-                               coarse_vc, coarse_cap, S, pml, pacc, ticket, out, st);
+                               coarse_vc, coarse_cap, S, pml, pacc, ticket, out, part_out, st);
     });
     return 0;
+}
+
+extern "C" int mpa_sparse_decode(const mpa_cache* c, const float* q_rot, int n_kv_heads, int group,
+                                 const int32_t* tok, const int32_t* n_tok, int tok_cap, const int32_t* rej,
+                                 const float* rej_w, const int32_t* n_rej, int rej_cap, const void* fine_vc,
+                                 int fine_cap, const void* coarse_vc, int coarse_cap, int n_split, void* workspace,
+                                 size_t workspace_bytes, float* out, void* stream) {
+    MPA_REQUIRE(out, MPA_ERR_ARG, "mpa_sparse_decode: null argument");
+    return sparse_decode_impl(c, q_rot, n_kv_heads, group, tok, n_tok, tok_cap, rej, rej_w, n_rej, rej_cap, fine_vc,
+                              fine_cap, coarse_vc, coarse_cap, n_split, workspace, workspace_bytes, out, nullptr,
+                              stream);
+}
+
+extern "C" int mpa_sparse_decode_partials(const mpa_cache* c, const float* q_rot, int n_kv_heads, int group,
+                                          const int32_t* tok, const int32_t* n_tok, int tok_cap, const int32_t* rej,
+                                          const float* rej_w, const int32_t* n_rej, int rej_cap,
+                                          const void* fine_vc, int fine_cap, const void* coarse_vc, int coarse_cap,
+                                          int n_split, void* workspace, size_t workspace_bytes, float* part_out,
+                                          void* stream) {
+    MPA_REQUIRE(part_out, MPA_ERR_ARG, "mpa_sparse_decode_partials: null argument");
+    return sparse_decode_impl(c, q_rot, n_kv_heads, group, tok, n_tok, tok_cap, rej, rej_w, n_rej, rej_cap, fine_vc,
+                              fine_cap, coarse_vc, coarse_cap, n_split, workspace, workspace_bytes, nullptr, part_out,
+                              stream);
+}
+
+// LSE merge of per-rank partials [P][L][G][2 + d] (m natural-log, s, a) -> out [L][G][d]
+// (attention.py:230-239 merge_partials + :44-47 finalize, across sequence shards)
+__global__ void merge_rank_partials_kernel(const float* __restrict__ parts, int P, int LG, int d,
+                                           float* __restrict__ out) {
+    const int lg = blockIdx.x;
+    for (int k = threadIdx.x; k < d; k += blockDim.x) {
+        float M = -INFINITY;
+        for (int r = 0; r < P; ++r) M = fmaxf(M, parts[((size_t)r * LG + lg) * (d + 2)]);
+        float S = 0.f, A = 0.f;
+        if (M != -INFINITY)
+            for (int r = 0; r < P; ++r) {
+                const float* Pp = parts + ((size_t)r * LG + lg) * (d + 2);
+                if (Pp[0] == -INFINITY) continue;
+                const float w = expf(Pp[0] - M);
+                S += w * Pp[1];
+                A += w * Pp[2 + k];
+            }
+        out[(size_t)lg * d + k] = A / S;
+    }
+}
+
+extern "C" int mpa_merge_rank_partials(const float* parts, int n_ranks, int n_ledgers, int group, int head_dim,
+                                       float* out, void* stream) {
+    MPA_REQUIRE(parts && out, MPA_ERR_ARG, "mpa_merge_rank_partials: null argument");
+    MPA_REQUIRE(n_ranks >= 1 && group >= 1 && head_dim >= 1, MPA_ERR_ARG, "mpa_merge_rank_partials: sizes");
+    if (n_ledgers <= 0) return 0;
+    merge_rank_partials_kernel<<<n_ledgers * group, 128, 0, (cudaStream_t)stream>>>(parts, n_ranks, n_ledgers * group,
+                                                                                   head_dim, out);
+    return check_launch("mpa_merge_rank_partials");
 }

@@ -283,6 +283,115 @@ __device__ __forceinline__ unsigned long long block_scan_u64(unsigned long long 
     return base + incl - v;
 }
 
+// ---- sequence sharding (a ledger's blocks spread over ranks): global normalisers, the
+// cross-rank crossing candidate, and each rank's candidates that can be globally selected
+struct Cross {
+    unsigned long long k;  // ~bits(score) of the crossing candidate; 0 = select none, ~0 = select all
+    unsigned int i;        // its global cluster id (tie-break)
+    unsigned int pad;
+};
+struct PrefixEntry {
+    unsigned long long key;
+    unsigned int gid;
+    int size;
+};
+struct ShardCtl {
+    const double* mz = nullptr;        // [L, G, 2] global (M, Z)
+    const Cross* cross = nullptr;      // [L] global crossing candidate (final pass)
+    PrefixEntry* prefix = nullptr;     // [L, prefix_cap] local pass output
+    int32_t* prefix_n = nullptr;       // [L] (zeroed by the caller)
+    int prefix_cap = 0;
+    const int32_t* gid_off = nullptr;  // [L] global id of this rank's first candidate
+};
+
+// Crossing candidate of a size-weighted "take while cum < B" over n entries visited by
+// (key asc, id asc): the smallest (key, id) whose cumulative weight reaches B.  11-bit digits
+// over the 63 low key bits (the top bit is constant for non-negative scores) then the id; stops
+// as soon as the crossing bin holds one entry.  Requires 0 < B <= total weight.  Block-wide.
+template <typename IdFn>
+__device__ void radix_cross(const unsigned long long* keys, const int* sizes, IdFn id_of, int n, long long B,
+                            unsigned long long& kstar, unsigned int& istar) {
+    __shared__ unsigned int hist_w[kBins], hist_c[kBins];
+    __shared__ unsigned long long s_kprefix, s_scan[33];
+    __shared__ unsigned int s_iprefix;
+    __shared__ long long s_below;
+    __shared__ int s_cnt;
+    __shared__ unsigned long long s_k;
+    __shared__ unsigned int s_i;
+    unsigned long long kmask = 1ull << 63;
+    if (threadIdx.x == 0) {
+        s_kprefix = keys[0] & (1ull << 63);
+        s_iprefix = 0u;
+        s_below = 0;
+        s_cnt = 0;
+    }
+    __syncthreads();
+    unsigned int imask = 0u;
+    constexpr int kKeyPasses = (63 + kDigBits - 1) / kDigBits, kIdPasses = (32 + kDigBits - 1) / kDigBits;
+    bool found = false;
+    for (int pass = 0; pass < kKeyPasses + kIdPasses && !found; ++pass) {
+        const bool kp_pass = pass < kKeyPasses;
+        const int top = kp_pass ? 63 - kDigBits * pass : 32 - kDigBits * (pass - kKeyPasses);
+        const int width = top >= kDigBits ? kDigBits : top;
+        const int sh = top - width;
+        const unsigned dmask = (1u << width) - 1u;
+        for (int j = threadIdx.x; j < kBins; j += blockDim.x) hist_w[j] = hist_c[j] = 0u;
+        __syncthreads();
+        const unsigned long long kp = s_kprefix;
+        const unsigned int ip = s_iprefix;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const unsigned long long k = keys[i];
+            if ((k & kmask) != kp) continue;
+            const unsigned int id = id_of(i);
+            if ((id & imask) != ip) continue;
+            const unsigned dg = kp_pass ? (unsigned)(k >> sh) & dmask : (id >> sh) & dmask;
+            atomicAdd(&hist_w[dg], (unsigned)sizes[i]);
+            atomicAdd(&hist_c[dg], 1u);
+        }
+        __syncthreads();
+        const int bpt = kBins / blockDim.x;
+        unsigned long long wsum = 0;
+        for (int j = 0; j < bpt; ++j) wsum += hist_w[threadIdx.x * bpt + j];
+        unsigned long long btot;
+        const unsigned long long before = block_scan_u64(wsum, s_scan, &btot);
+        const long long below = s_below;
+        const long long need = B - below;  // > 0
+        if ((long long)before < need && (long long)(before + wsum) >= need) {
+            long long run = (long long)before;
+            int dg = threadIdx.x * bpt + bpt - 1;
+            for (int j = 0; j < bpt; ++j) {
+                const int b = threadIdx.x * bpt + j;
+                if (run + (long long)hist_w[b] >= need) {
+                    dg = b;
+                    break;
+                }
+                run += hist_w[b];
+            }
+            s_below = below + run;
+            s_cnt = (int)hist_c[dg];
+            if (kp_pass) s_kprefix = kp | ((unsigned long long)dg << sh);
+            else s_iprefix = ip | ((unsigned)dg << sh);
+        }
+        __syncthreads();
+        if (kp_pass) kmask |= (unsigned long long)dmask << sh;
+        else imask |= dmask << sh;
+        found = s_cnt == 1;
+    }
+    const unsigned long long kp = s_kprefix;
+    const unsigned int ip = s_iprefix;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const unsigned int id = id_of(i);
+        if ((keys[i] & kmask) == kp && (id & imask) == ip) {
+            s_k = keys[i];
+            s_i = id;
+        }
+    }
+    __syncthreads();
+    kstar = s_k;
+    istar = s_i;
+    __syncthreads();
+}
+
 // smem per candidate: key (8) + size (4) + flag (1) + pad
 __host__ __device__ constexpr size_t sel_smem_bytes(int n_max) { return (size_t)n_max * 13 + 64; }
 
@@ -293,16 +402,18 @@ __device__ void select_v2_core(int l, const double* __restrict__ logits, const d
                                const int32_t* __restrict__ esize, const uint8_t* __restrict__ eflag, int ne, int ecap,
                                long long B, const double* __restrict__ cstats, int n_chunks, unsigned long long* keys,
                                int* sizes, uint8_t* sflag, uint8_t* __restrict__ flag,
-                               int32_t* __restrict__ sel_tokens) {
+                               int32_t* __restrict__ sel_tokens, const ShardCtl& sh = ShardCtl{}) {
+    const double* mz_ext = sh.mz;
+    const Cross* ext_cross = sh.cross;
+    PrefixEntry* prefix = sh.prefix;
+    int32_t* prefix_n = sh.prefix_n;
+    const int prefix_cap = sh.prefix_cap;
+    const int gid_off = sh.gid_off ? sh.gid_off[l] : 0;
     __shared__ double s_red[kSel2Threads / 32][G];
     __shared__ double s_mx[G], s_z[G];
-    __shared__ unsigned int hist_w[kBins], hist_c[kBins];
-    __shared__ unsigned long long s_kprefix, s_scan[33];
-    __shared__ unsigned int s_iprefix;
-    __shared__ long long s_below, s_total;
-    __shared__ int s_cnt;
-    __shared__ unsigned long long s_k;
-    __shared__ unsigned int s_i;
+    __shared__ double csc[2048];  // chunk scales e^(m_c - M) [n_chunks][G]
+    __shared__ unsigned long long s_scan[33];
+    __shared__ long long s_total;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const double* lg = logits + (size_t)l * G * cand_cap;
     const double* el = e_local ? e_local + (size_t)l * G * cand_cap : nullptr;
@@ -310,8 +421,7 @@ __device__ void select_v2_core(int l, const double* __restrict__ logits, const d
     const double* cs = cstats ? cstats + (size_t)l * n_chunks * G * 2 : nullptr;
     const bool use_local = el && cs;
     const int nchu = min(n_chunks, (n + 127) >> 7);  // chunks holding this ledger's candidates
-    double* csc = reinterpret_cast<double*>(hist_w);  // chunk scales e^(m_c - M) [n_chunks][G] (before the radix)
-    const int max_sc_chunks = (int)(sizeof(hist_w) + sizeof(hist_c)) / (8 * G);
+    const int max_sc_chunks = 2048 / G;
 
     // ---- 1. sizes, per-head max
     long long tot_local = 0;
@@ -352,6 +462,11 @@ __device__ void select_v2_core(int l, const double* __restrict__ logits, const d
         __syncthreads();
     }
     dbg_lk(1);
+    if (mz_ext) {  // global (M, Z) of a sequence-sharded ledger
+        __syncthreads();
+        if (threadIdx.x < G) s_mx[threadIdx.x] = mz_ext[((size_t)l * G + threadIdx.x) * 2];
+        __syncthreads();
+    }
     double mx[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) mx[g] = s_mx[g];
@@ -395,7 +510,7 @@ __device__ void select_v2_core(int l, const double* __restrict__ logits, const d
         if (threadIdx.x < G) {
             double r = 0.0;
             for (int ww = 0; ww < kSel2Threads / 32; ++ww) r += s_red[ww][threadIdx.x];
-            s_z[threadIdx.x] = r;
+            s_z[threadIdx.x] = mz_ext ? mz_ext[((size_t)l * G + threadIdx.x) * 2 + 1] : r;
         }
         if (threadIdx.x == 32) {
             unsigned long long t = 0;
@@ -421,93 +536,23 @@ __device__ void select_v2_core(int l, const double* __restrict__ logits, const d
         sc = sc / (double)G;
         keys[i] = ~(unsigned long long)__double_as_longlong(sc);  // ascending key == descending score
     }
-    if (threadIdx.x == 0) {
-        s_kprefix = 0ull;
-        s_iprefix = 0u;
-        s_below = 0;
-    }
     __syncthreads();
 
     dbg_lk(5);
-    // ---- 4. crossing candidate: smallest (key, id) with W(<=) >= B.  Digits over the 63 low key
-    // bits (the top bit is constant: scores are positive) then the 32 id bits.
+    // ---- 4. crossing candidate: smallest (key, id) with W(<=) >= B (or given by the caller:
+    // the cross-rank cut of a sequence-sharded ledger)
     const long long total = s_total;
-    const bool select_none = B <= 0, select_all = total < B;
+    const bool select_none = ext_cross ? ext_cross[l].k == 0ull : B <= 0;
+    const bool select_all = ext_cross ? ext_cross[l].k == ~0ull : total < B;
     unsigned long long kstar = ~0ull;
     unsigned int istar = 0xffffffffu;
-    if (!select_none && !select_all) {
-        unsigned long long kmask = 1ull << 63;
-        unsigned long long kfix = keys[0] & (1ull << 63);  // constant top bit
-        if (threadIdx.x == 0) s_kprefix = kfix;
-        __syncthreads();
-        unsigned int imask = 0u;
-        constexpr int kKeyPasses = (63 + kDigBits - 1) / kDigBits, kIdPasses = (32 + kDigBits - 1) / kDigBits;
-        bool found = false;
-        for (int pass = 0; pass < kKeyPasses + kIdPasses && !found; ++pass) {
-            const bool kp_pass = pass < kKeyPasses;
-            // digit = bits [sh, sh + width) of the key (or id)
-            const int top = kp_pass ? 63 - kDigBits * pass : 32 - kDigBits * (pass - kKeyPasses);
-            const int width = top >= kDigBits ? kDigBits : top;
-            const int sh = top - width;
-            const unsigned dmask = (1u << width) - 1u;
-            for (int j = threadIdx.x; j < kBins; j += blockDim.x) hist_w[j] = hist_c[j] = 0u;
-            __syncthreads();
-            const unsigned long long kp = s_kprefix;
-            const unsigned int ip = s_iprefix;
-            for (int i = threadIdx.x; i < n; i += blockDim.x) {
-                const unsigned long long k = keys[i];
-                if ((k & kmask) != kp) continue;
-                const unsigned int id = cand ? (unsigned)__ldg(cand + (size_t)l * cand_cap + i) : (unsigned)i;
-                if ((id & imask) != ip) continue;
-                const unsigned dg = kp_pass ? (unsigned)(k >> sh) & dmask : (id >> sh) & dmask;
-                atomicAdd(&hist_w[dg], (unsigned)sizes[i]);
-                atomicAdd(&hist_c[dg], 1u);
-            }
-            __syncthreads();
-            // block scan of the bins (4 per thread) to find the bin where the cumulative weight
-            // reaches B - below
-            constexpr int BPT = kBins / kSel2Threads;
-            unsigned long long wsum = 0;
-#pragma unroll
-            for (int j = 0; j < BPT; ++j) wsum += hist_w[threadIdx.x * BPT + j];
-            unsigned long long btot;
-            const unsigned long long before = block_scan_u64(wsum, s_scan, &btot);
-            const long long below = s_below;
-            const long long need = B - below;  // > 0
-            if ((long long)before < need && (long long)(before + wsum) >= need) {
-                long long run = (long long)before;
-                int dg = threadIdx.x * BPT + BPT - 1;
-                for (int j = 0; j < BPT; ++j) {
-                    const int b = threadIdx.x * BPT + j;
-                    if (run + (long long)hist_w[b] >= need) {
-                        dg = b;
-                        break;
-                    }
-                    run += hist_w[b];
-                }
-                s_below = below + run;
-                s_cnt = (int)hist_c[dg];
-                if (kp_pass) s_kprefix = kp | ((unsigned long long)dg << sh);
-                else s_iprefix = ip | ((unsigned)dg << sh);
-            }
-            __syncthreads();
-            if (kp_pass) kmask |= (unsigned long long)dmask << sh;
-            else imask |= dmask << sh;
-            found = s_cnt == 1;
-        }
-        // the unique candidate matching the final prefix is the crosser
-        const unsigned long long kp = s_kprefix;
-        const unsigned int ip = s_iprefix;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const unsigned int id = cand ? (unsigned)__ldg(cand + (size_t)l * cand_cap + i) : (unsigned)i;
-            if ((keys[i] & kmask) == kp && (id & imask) == ip) {
-                s_k = keys[i];
-                s_i = id;
-            }
-        }
-        __syncthreads();
-        kstar = s_k;
-        istar = s_i;
+    if (ext_cross) {
+        kstar = ext_cross[l].k;
+        istar = ext_cross[l].i;
+    } else if (!select_none && !select_all) {
+        radix_cross(keys, sizes, [&](int i) -> unsigned {
+            return (unsigned)gid_off + (cand ? (unsigned)__ldg(cand + (size_t)l * cand_cap + i) : (unsigned)i);
+        }, n, B, kstar, istar);
     }
 
     dbg_lk(6);
@@ -518,10 +563,19 @@ __device__ void select_v2_core(int l, const double* __restrict__ logits, const d
         if (select_none) sel = false;
         else if (select_all) sel = true;
         else {
-            const unsigned int id = cand ? (unsigned)__ldg(cand + (size_t)l * cand_cap + i) : (unsigned)i;
+            const unsigned int id =
+                (unsigned)gid_off + (cand ? (unsigned)__ldg(cand + (size_t)l * cand_cap + i) : (unsigned)i);
             sel = keys[i] < kstar || (keys[i] == kstar && id <= istar);
         }
         sflag[i] = sel ? 1 : 0;
+        if (sel && prefix) {  // sharded local pass: this rank's candidates that can be globally selected
+            const int q = atomicAdd(prefix_n + l, 1);
+            if (q < prefix_cap) {
+                prefix[(size_t)l * prefix_cap + q] = PrefixEntry{
+                    keys[i], (unsigned)gid_off + (cand ? (unsigned)__ldg(cand + (size_t)l * cand_cap + i) : (unsigned)i),
+                    sizes[i]};
+            }
+        }
         flag[(size_t)l * cand_cap + i] = sel ? 1 : 0;
         if (sel) tok += sizes[i];
     }
@@ -658,7 +712,8 @@ select_worklist_v2_kernel(const double* __restrict__ logits, const double* __res
                           const int32_t* __restrict__ cache_len, int n_kv_heads, int replacement,
                           // outputs
                           int32_t* __restrict__ tok, int tok_cap, int32_t* __restrict__ rej,
-                          float* __restrict__ rej_w, int rej_cap, int32_t* __restrict__ stats, int smem_n) {
+                          float* __restrict__ rej_w, int rej_cap, int32_t* __restrict__ stats, int smem_n,
+                          ShardCtl sh) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int l = blockIdx.x, L = gridDim.x;
     dbg_lk(0);
@@ -669,8 +724,9 @@ select_worklist_v2_kernel(const double* __restrict__ logits, const double* __res
     uint8_t* sflag = reinterpret_cast<uint8_t*>(sizes + smem_n);
     const int ne = cflag ? ccount[l] : 0;
     select_v2_core<G>(l, logits, e_local, cand, n, cand_cap, fsize, fcap, clogits, csize, cflag, ne, ccap, budget[l],
-                      cstats, n_chunks, keys, sizes, sflag, flag, sel_tokens);
+                      cstats, n_chunks, keys, sizes, sflag, flag, sel_tokens, sh);
     dbg_lk(3);
+    if (sh.prefix && !sh.cross) return;  // sharded local pass: only the candidate prefix is needed
     worklist_v2<G>(l, L, n, logits, cand, cand_cap, sflag, sizes, reinterpret_cast<int*>(keys), fmem_off, fmem, fcap,
                    fmem_cap, csize, ne, ccap, cflag, clogits, sink_end, buffer_start, cache_len, n_kv_heads,
                    replacement, tok, tok_cap, rej, rej_w, rej_cap, stats);
@@ -695,7 +751,86 @@ select_v2_kernel(const double* __restrict__ logits, const double* __restrict__ e
     uint8_t* sflag = reinterpret_cast<uint8_t*>(sizes + smem_n);
     select_v2_core<G>(l, logits, e_local, cand, n_cand[l], cand_cap, lv_size, lv_cap, elogits, esize, eflag,
                       elogits ? n_extra[l] : 0, ecap, budget[l], cstats, n_chunks, keys, sizes, sflag, flag,
-                      sel_tokens);
+                      sel_tokens, ShardCtl{});
+}
+
+// per (ledger, head): (M, Z) of this rank's candidates from the chunk partials
+__global__ void head_norms_kernel(const double* __restrict__ cstats, int n_chunks, const int32_t* __restrict__ count,
+                                  int G, double* __restrict__ out) {
+    const int l = blockIdx.x, g = threadIdx.x;
+    if (g >= G) return;
+    const int nchu = min(n_chunks, (count[l] + 127) >> 7);
+    const double* cs = cstats + (size_t)l * n_chunks * G * 2;
+    double M = -INFINITY;
+    for (int c = 0; c < nchu; ++c) M = fmax(M, cs[(c * G + g) * 2]);
+    double Z = 0.0;
+    for (int c = 0; c < nchu; ++c) {
+        const double cm = cs[(c * G + g) * 2];
+        if (cm != -INFINITY) Z += cs[(c * G + g) * 2 + 1] * exp(cm - M);
+    }
+    out[((size_t)l * G + g) * 2] = M;
+    out[((size_t)l * G + g) * 2 + 1] = Z;
+}
+
+// global (M, Z) from every rank's [P][L][G][2]
+__global__ void merge_norms_kernel(const double* __restrict__ parts, int P, int LG, double* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= LG) return;
+    double M = -INFINITY;
+    for (int r = 0; r < P; ++r) M = fmax(M, parts[((size_t)r * LG + i) * 2]);
+    double Z = 0.0;
+    for (int r = 0; r < P; ++r) {
+        const double m = parts[((size_t)r * LG + i) * 2];
+        if (m != -INFINITY) Z += parts[((size_t)r * LG + i) * 2 + 1] * exp(m - M);
+    }
+    out[(size_t)i * 2] = M;
+    out[(size_t)i * 2 + 1] = Z;
+}
+
+// the global crossing candidate of each ledger from every rank's prefix [P][L][cap]
+__global__ void __launch_bounds__(kSel2Threads)
+global_cut_kernel(const PrefixEntry* __restrict__ prefix, const int32_t* __restrict__ prefix_n, int P, int L,
+                  int cap, const int64_t* __restrict__ budget, Cross* __restrict__ cross) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int l = blockIdx.x;
+    const int nmax = P * cap;
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem_raw);
+    int* sizes = reinterpret_cast<int*>(keys + nmax);
+    unsigned int* ids = reinterpret_cast<unsigned int*>(sizes + nmax);
+    __shared__ int s_base[65];
+    __shared__ unsigned long long s_tot[kSel2Threads / 32];
+    if (threadIdx.x == 0) {
+        int b = 0;
+        for (int r = 0; r < P; ++r) {
+            s_base[r] = b;
+            b += min(prefix_n[(size_t)r * L + l], cap);
+        }
+        s_base[P] = b;
+    }
+    __syncthreads();
+    const int n = s_base[P];
+    unsigned long long tot = 0;
+    for (int r = 0; r < P; ++r) {
+        const int cnt = s_base[r + 1] - s_base[r];
+        for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+            const PrefixEntry e = prefix[((size_t)r * L + l) * cap + j];
+            keys[s_base[r] + j] = e.key;
+            sizes[s_base[r] + j] = e.size;
+            ids[s_base[r] + j] = e.gid;
+            tot += (unsigned long long)e.size;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if ((threadIdx.x & 31) == 0) s_tot[threadIdx.x >> 5] = tot;
+    __syncthreads();
+    unsigned long long total = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) total += s_tot[w];
+    const long long B = budget[l];
+    Cross c{~0ull, 0xffffffffu, 0u};
+    if (B <= 0) c = Cross{0ull, 0u, 0u};
+    else if ((long long)total >= B && n > 0) radix_cross(keys, sizes, [&](int i) { return ids[i]; }, n, B, c.k, c.i);
+    if (threadIdx.x == 0) cross[l] = c;
 }
 
 }  // namespace mpa
@@ -770,7 +905,7 @@ int mpa_launch_select_worklist_v2(const mpa_level* fine, const mpa_level* coarse
                                   const int32_t* buffer_start, const int32_t* cache_len, int n_kv_heads,
                                   int n_ledgers, int replacement, uint8_t* flag, int32_t* sel_tokens, int32_t* tok,
                                   int tok_cap, int32_t* rej, float* rej_w, int rej_cap, int32_t* stats, int n_max,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, const ShardCtl& sh) {
     const size_t smem = sel_smem_bytes(n_max);
     MPA_DISPATCH_G(group, {
         auto kern = select_worklist_v2_kernel<kG>;
@@ -779,7 +914,7 @@ int mpa_launch_select_worklist_v2(const mpa_level* fine, const mpa_level* coarse
             logits, e_local, cand, n_cand, cand_cap, chunk_stats, n_chunks, budget, flag, sel_tokens, fine->size,
             fine->off, fine->idx, fine->cap, fine->idx_cap, fine->count, coarse ? coarse->size : nullptr,
             coarse ? coarse->count : nullptr, coarse ? coarse->cap : 0, cflag, clogits, sink_end, buffer_start,
-            cache_len, n_kv_heads, replacement, tok, tok_cap, rej, rej_w, rej_cap, stats, n_max);
+            cache_len, n_kv_heads, replacement, tok, tok_cap, rej, rej_w, rej_cap, stats, n_max, sh);
     });
     return check_launch("mpa_select_worklist(v2)");
 }
@@ -789,3 +924,81 @@ extern "C" int mpa_debug_trace_lookup(unsigned long long* host, int n) {
     return (int)cudaMemcpyFromSymbol(host, g_dbg_lk, sizeof(unsigned long long) * n);
 }
 #endif
+
+// unsharded entry (mpa_lookup.cu)
+int mpa_launch_select_worklist_v2(const mpa_level* fine, const mpa_level* coarse, int group, const double* logits,
+                                  const double* e_local, const int32_t* cand, const int32_t* n_cand, int cand_cap,
+                                  const double* chunk_stats, int n_chunks, const uint8_t* cflag,
+                                  const double* clogits, const int64_t* budget, const int32_t* sink_end,
+                                  const int32_t* buffer_start, const int32_t* cache_len, int n_kv_heads,
+                                  int n_ledgers, int replacement, uint8_t* flag, int32_t* sel_tokens, int32_t* tok,
+                                  int tok_cap, int32_t* rej, float* rej_w, int rej_cap, int32_t* stats, int n_max,
+                                  cudaStream_t st) {
+    return mpa_launch_select_worklist_v2(fine, coarse, group, logits, e_local, cand, n_cand, cand_cap, chunk_stats,
+                                         n_chunks, cflag, clogits, budget, sink_end, buffer_start, cache_len,
+                                         n_kv_heads, n_ledgers, replacement, flag, sel_tokens, tok, tok_cap, rej,
+                                         rej_w, rej_cap, stats, n_max, st, ShardCtl{});
+}
+
+extern "C" int mpa_head_norms(const double* chunk_stats, int n_chunks, const int32_t* count, int n_ledgers, int group,
+                              double* out, void* stream) {
+    MPA_REQUIRE(chunk_stats && count && out, MPA_ERR_ARG, "mpa_head_norms: null argument");
+    if (n_ledgers <= 0) return 0;
+    head_norms_kernel<<<n_ledgers, 32, 0, (cudaStream_t)stream>>>(chunk_stats, n_chunks, count, group, out);
+    return check_launch("mpa_head_norms");
+}
+
+extern "C" int mpa_merge_norms(const double* parts, int n_ranks, int n_ledgers, int group, double* out,
+                               void* stream) {
+    MPA_REQUIRE(parts && out, MPA_ERR_ARG, "mpa_merge_norms: null argument");
+    const int LG = n_ledgers * group;
+    if (LG <= 0) return 0;
+    merge_norms_kernel<<<ceil_div(LG, 128), 128, 0, (cudaStream_t)stream>>>(parts, n_ranks, LG, out);
+    return check_launch("mpa_merge_norms");
+}
+
+extern "C" int mpa_global_cut(const void* prefix, const int32_t* prefix_n, int n_ranks, int n_ledgers, int prefix_cap,
+                              const int64_t* budget, void* cross, void* stream) {
+    MPA_REQUIRE(prefix && prefix_n && budget && cross, MPA_ERR_ARG, "mpa_global_cut: null argument");
+    MPA_REQUIRE(n_ranks >= 1 && n_ranks <= 64, MPA_ERR_UNSUPPORTED, "mpa_global_cut: %d ranks", n_ranks);
+    const size_t smem = (size_t)n_ranks * prefix_cap * 16;
+    MPA_REQUIRE(smem <= 200 * 1024, MPA_ERR_UNSUPPORTED, "mpa_global_cut: %d x %d prefix entries", n_ranks,
+                prefix_cap);
+    if (n_ledgers <= 0) return 0;
+    cudaFuncSetAttribute(global_cut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    global_cut_kernel<<<n_ledgers, kSel2Threads, smem, (cudaStream_t)stream>>>(
+        (const PrefixEntry*)prefix, prefix_n, n_ranks, n_ledgers, prefix_cap, budget, (Cross*)cross);
+    return check_launch("mpa_global_cut");
+}
+
+extern "C" int mpa_select_worklist_sharded(const mpa_level* fine, int group, const double* logits,
+                                           const double* e_local, const double* chunk_stats, const int64_t* budget,
+                                           const int32_t* sink_end, const int32_t* buffer_start,
+                                           const int32_t* cache_len, int n_kv_heads, int replacement, uint8_t* flag,
+                                           int32_t* sel_tokens, int32_t* tok, int tok_cap, int32_t* rej,
+                                           float* rej_w, int rej_cap, int32_t* stats, int n_max, const double* mz,
+                                           const void* cross, void* prefix, int32_t* prefix_n, int prefix_cap,
+                                           const int32_t* gid_off, void* stream) {
+    MPA_REQUIRE(fine && logits && chunk_stats && budget && flag && sink_end && buffer_start && cache_len && tok &&
+                    rej && rej_w && stats && mz && gid_off,
+                MPA_ERR_ARG, "mpa_select_worklist_sharded: null argument");
+    MPA_REQUIRE((cross != nullptr) != (prefix != nullptr), MPA_ERR_ARG,
+                "mpa_select_worklist_sharded: exactly one of cross (final pass) / prefix (local pass)");
+    MPA_REQUIRE(!prefix || prefix_n, MPA_ERR_ARG, "mpa_select_worklist_sharded: prefix without counts");
+    if (n_max <= 0 || n_max > fine->cap) n_max = fine->cap;
+    MPA_REQUIRE(mpa_select_v2_smem(n_max) <= 200 * 1024, MPA_ERR_UNSUPPORTED,
+                "mpa_select_worklist_sharded: %d candidates", n_max);
+    if (fine->n_ledgers <= 0) return 0;
+    ShardCtl sh;
+    sh.mz = mz;
+    sh.cross = (const Cross*)cross;
+    sh.prefix = (PrefixEntry*)prefix;
+    sh.prefix_n = prefix_n;
+    sh.prefix_cap = prefix_cap;
+    sh.gid_off = gid_off;
+    return mpa_launch_select_worklist_v2(fine, nullptr, group, logits, e_local, nullptr, nullptr, fine->cap,
+                                         chunk_stats, ceil_div(fine->cap, 128), nullptr, nullptr, budget, sink_end,
+                                         buffer_start, cache_len, n_kv_heads, fine->n_ledgers, replacement, flag,
+                                         sel_tokens, tok, tok_cap, rej, rej_w, rej_cap, stats, n_max,
+                                         (cudaStream_t)stream, sh);
+}
