@@ -46,13 +46,22 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--batch", type=int, default=16)
-    ap.add_argument("--ctx", type=int, default=32768)
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"],
+                    help="BASELINE configs: c2 (default, the metric's config), c3 (R1-14B 64K 2-level), "
+                         "c4 (online updates while generating), c5 (128K sequence-sharded over the ranks)")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--ctx", type=int, default=None)
     ap.add_argument("--budget", type=int, default=512)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline leg")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no CPU leg, no clocks)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    dflt = {"c2": (16, 32768), "c3": (16, 65536), "c4": (8, 16384), "c5": (16, 131072)}[a.workload]
+    a.batch = a.batch or dflt[0]
+    a.ctx = a.ctx or dflt[1]
+    if a.workload == "c4" and a.steps == 20:
+        a.steps = 512  # spans four online-update events (L = 128)
+    return a
 
 
 def peaks():
@@ -65,11 +74,31 @@ def peaks():
 
 
 def workload_cfg(args):
-    from paper_2506_13059_b200.core import EngineConfig, HeadLayout
+    from paper_2506_13059_b200.core import EngineConfig, HeadLayout, HierarchyConfig
 
+    if getattr(args, "workload", "c2") == "c3":  # DeepSeek-R1-Distill-Qwen-14B attention: 40 q / 8 kv
+        lay = HeadLayout(40, 8, 128)
+        cfg = EngineConfig(token_budget=args.budget, rope_theta=1e6, seed=0,
+                           hierarchy=HierarchyConfig(64, 8, 0.25))
+        return lay, cfg
     lay = HeadLayout(32, 8, 128)
     cfg = EngineConfig(token_budget=args.budget, tokens_per_centroid=16, rope_theta=1e6, seed=0)
     return lay, cfg
+
+
+def workload_label(args, world=1):
+    b, ctx, B = args.batch, args.ctx, args.budget
+    w = getattr(args, "workload", "c2")
+    if w == "c3":
+        return (f"C3: DeepSeek-R1-Distill-Qwen-14B attention shape 40q/8kv/d128, {ctx // 1024}K ctx, 2-level "
+                f"r1=64/r2=8/p=0.25, B={B}, bf16, batch {b}/GPU")
+    if w == "c4":
+        return (f"C4: Qwen3-8B attention shape 32q/8kv/d128, {ctx // 1024}K prompt + generated tokens with online "
+                f"cluster updates every L=128 steps, r=16, B={B}, bf16, batch {b}/GPU")
+    if w == "c5":
+        return (f"C5: Qwen3-8B attention shape 32q/8kv/d128, {ctx // 1024}K ctx KV-sequence-sharded over {world} "
+                f"GPU(s) (NCCL all-gather merge), r=16, B={B}, bf16, batch {b}")
+    return f"C2: Qwen3-8B attention shape 32q/8kv/d128, {ctx // 1024}K ctx, 1-level r=16, B={B}, bf16, batch {b}/GPU"
 
 
 class Clocks:
@@ -321,6 +350,10 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.workload != "c2":
+        args.no_cpu = True  # the CPU side-by-side is quoted on the metric's config (c2)
+    if args.workload == "c5" and world > 1:
+        return main_sharded(args, rank, world, local)
 
     def barrier():
         if world > 1:
@@ -377,7 +410,8 @@ def main():
                 eng.attend(Q[0])
             torch.cuda.synchronize()
     stats = eng.head_stats()
-    scored = eng.led.n_fine.copy()
+    scored = (eng.led.n_fine.copy() if cfg.hierarchy is None
+              else eng.led.n_coarse + eng.n_cand.cpu().numpy().astype(np.int64))
     ms_step = float(np.mean(step_ms))
 
     # ---- fused kernel alone (dominant kernel) for the roofline
@@ -387,7 +421,7 @@ def main():
     fstats = eng.head_stats()
     fused_ms = timed(lambda i: eng.fused(), K)
     lookup_ms = timed(lambda i: (eng.rotate(Q[0]), eng.lookup()), K)
-    nbytes = decode_bytes(fstats, eng.led.n_fine, d, G, 2)
+    nbytes = decode_bytes(fstats, scored, d, G, 2)
     fused_avg = float(np.mean(fused_ms))
 
     # ---- dense decode comparator (same cache, same kernel family, tok == NULL)
@@ -444,9 +478,9 @@ def main():
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic N(0,1) Q/K/V (random-init Qwen3-8B attention shape), seed 1000+rank",
-            "config": {"workload": "C2: Qwen3-8B attention shape 32q/8kv/d128, 32K ctx, 1-level r=16, "
-                                   f"B={args.budget}, bf16, batch {b}/GPU", "batch": b, "ctx": ctx,
-                       "budget": args.budget, "tokens_per_centroid": 16, "l2": "flushed (256 MB write) before "
+            "config": {"workload": workload_label(args, world), "batch": b, "ctx": ctx,
+                       "budget": args.budget, "tokens_per_centroid": cfg.fine_ratio,
+                       "l2": "flushed (256 MB write) before "
                                                                              "every timed step",
                        "parallelism": f"batch-sharded replicas x{world}"},
             "speedup_vs_dense": dense_avg / ms_step,
@@ -478,6 +512,114 @@ def main():
     barrier()
     if world > 1:
         dist.destroy_process_group()
+
+
+def main_sharded(args, rank, world, local):
+    """C5 at N > 1: one 128K context per sequence, KV blocks sharded over the ranks
+    (paper_2506_13059_b200/sharded.py); three NCCL all-gathers per step; strong scaling."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_13059_b200._lib import lib as _load_lib
+    from paper_2506_13059_b200.sharded import ShardedDecodeEngine, TorchComm
+
+    _load_lib()
+    lay, cfg = workload_cfg(args)
+    b, ctx, d = args.batch, args.ctx, lay.head_dim
+    W, K = max(3, args.warmup), args.steps
+    dev = torch.device("cuda", local)
+    comm = TorchComm()
+    gen = torch.Generator(device=dev).manual_seed(1000)  # identical prompt / queries on every rank
+    tcap = ctx + 2 * (W + 2 * K) + 3 * cfg.local_buffer + 8
+    se = ShardedDecodeEngine(cfg, lay, b, tcap, rank, world, dtype=torch.bfloat16, device=dev)
+    eng = se.eng
+    for s_ in range(b):
+        k = torch.randn(1, lay.num_kv_heads, ctx, d, generator=gen, device=dev)
+        v = torch.randn(1, lay.num_kv_heads, ctx, d, generator=gen, device=dev)
+        _write_seq(eng, s_, k, v)
+        del k, v
+    eng.cache_len[:] = ctx
+    eng._sync_scalars()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    se.prefill_local()
+    n_all = comm.all_gather(torch.as_tensor(eng.led.n_fine, dtype=torch.int64, device=dev)).cpu().numpy()
+    se.set_gid_offsets(n_all)
+    torch.cuda.synchronize()
+    prefill_s = time.perf_counter() - t0
+    n = W + 2 * K
+    Q = torch.randn(n, b, lay.num_q_heads, d, generator=gen, device=dev)
+    KN = torch.randn(n, b, lay.num_kv_heads, d, generator=gen, device=dev)
+    VN = torch.randn(n, b, lay.num_kv_heads, d, generator=gen, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        out = se.attend(Q[i], comm)
+        eng.write_tokens(KN[i][:, :, None], VN[i][:, :, None])
+        return out
+
+    def timed(fn, count, start=0):
+        evs = []
+        for i in range(count):
+            flush.fill_(float(i))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn(start + i)
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        return [a.elapsed_time(c) for a, c in evs]
+
+    for i in range(W):
+        step(i)
+    torch.cuda.synchronize()
+    dist.barrier()
+    with Clocks(local) as clk:
+        dist.barrier()
+        step_ms = timed(step, K, W)
+        dist.barrier()
+    # dense comparator over this rank's token range, merged across ranks the same way
+    s0 = int(eng.sink_end[0])
+    Wb = cfg.block_size
+    n_sealed = (int(eng.buffer_start[0]) - s0) // Wb
+    lo_b, hi_b = n_sealed * rank // world, n_sealed * (rank + 1) // world
+    lo = 0 if rank == 0 else s0 + lo_b * Wb
+    hi_fn = (lambda: int(eng.cache_len[0])) if rank == world - 1 else (lambda: s0 + hi_b * Wb)
+    ids = torch.arange(lo, hi_fn(), dtype=torch.int32, device=dev)
+    tokd = torch.zeros(eng.L, max(1, ids.numel()), dtype=torch.int32, device=dev)
+    tokd[:, : ids.numel()] = ids
+    ntokd = torch.full((eng.L,), ids.numel(), dtype=torch.int32, device=dev)
+    from paper_2506_13059_b200._lib import call, ptr, stream_ptr
+
+    def dense(i):
+        eng.rotate(Q[i])
+        ws = eng._workspace(0)
+        call("mpa_sparse_decode_partials", eng.cache_struct, ptr(eng.q_rot), eng.Hkv, eng.G, ptr(tokd), ptr(ntokd),
+             tokd.shape[1], None, None, None, 0, None, 0, None, 0, 0, ptr(ws), ws.numel(), ptr(se.part), stream_ptr())
+        return se.phase_merge(comm.all_gather(se.part))
+
+    for i in range(3):
+        dense(i)
+    dense_ms = timed(dense, K)
+    vals = torch.tensor([float(np.mean(step_ms)), float(np.mean(dense_ms))], device=dev, dtype=torch.float64)
+    dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms_step, dense_avg = (float(x) for x in vals.cpu())
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": ms_step * 1e3, "unit": "us/step", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic N(0,1) Q/K/V (random-init Qwen3-8B attention shape)",
+            "config": {"workload": workload_label(args, world), "batch": b, "ctx": ctx, "budget": args.budget,
+                       "parallelism": f"KV-sequence-sharded x{world} (NCCL all-gather of (M,Z), candidate "
+                                      "prefixes and (m,s,a) partials)",
+                       "l2": "flushed (256 MB write) before every timed step"},
+            "speedup_vs_dense": dense_avg / ms_step, "dense_us_per_step": dense_avg * 1e3,
+            "sequences_per_s": b / (ms_step * 1e-3), "prefill_s": prefill_s,
+            "gpu_launches": 12 * K, "clocks": clk.summary(),
+        }), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def _write_seq(eng, s, k, v):

@@ -15,6 +15,7 @@
 #include <cstdlib>
 
 #include "mpa_common.cuh"
+#include "mpa_tc.cuh"
 
 namespace mpa {
 
@@ -240,6 +241,185 @@ logits_block_kernel(const double* __restrict__ q_lk, const __nv_bfloat16* __rest
         __syncthreads();  // buffer `buf` is refilled by the next iteration's issue
     }
     asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
+// ---- TMA-fed variant (bf16, D = 128): the 128-row chunk lands in smem through 2 TMA tile
+// copies (flat candidates, contiguous rows) or 64 tile::gather4 copies (candidate lists), 128B
+// swizzled; no per-thread copy instructions.  Rows of thread (rg, qt) are rg + 32 r, and quarter
+// qt visits its 4 chunks starting at 2 (qt >> 1) so the 8 lanes of an LDS.128 phase hit 8
+// distinct bank groups.  bf16 -> fp64 by integer ops (exact for every nonzero bf16; a zero
+// element becomes 2^-127, below the fp64 resolution of any logit sum).
+__device__ __forceinline__ double bf16hi_to_f64(unsigned fbits) {  // fbits: bf16 in the high half
+    return __hiloint2double((int)((((int)fbits >> 3) & 0x8FFFE000) + 0x38000000), 0);
+}
+
+template <int G>
+__global__ void __launch_bounds__(kLgThreads)
+logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_constant__ CUtensorMap tm_row,
+                  const double* __restrict__ q_lk, int kcap, const int32_t* __restrict__ count,
+                  const int32_t* __restrict__ lv_size, const int32_t* __restrict__ cand,
+                  const int32_t* __restrict__ n_cand, int cand_cap, double* __restrict__ logits,
+                  double* __restrict__ cstats, double* __restrict__ e_local, int n_chunks) {
+    constexpr int D = 128, QD = 32, QS = QD * G + 2;
+    extern __shared__ __align__(1024) unsigned char sm_raw[];
+    unsigned char* tile = sm_raw + ((1024 - (smem_u32(sm_raw) & 1023)) & 1023);  // [2 halves][128][128 B]
+    double* qs = reinterpret_cast<double*>(tile + 2 * kLgChunk * 128);          // [4][QD][G] (+pad)
+    double* slg = qs + 4 * QS;                                                  // [G][128]
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ double red[kLgThreads / 32][G];
+    __shared__ double s_m[G];
+    const int l = blockIdx.y, chunk = blockIdx.x, tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    const int n = cand ? n_cand[l] : count[l];
+    const int i0 = chunk * kLgChunk;
+    if (i0 >= n) {
+        if (cstats && chunk < n_chunks && tid < G) {
+            cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2] = -INFINITY;
+            cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2 + 1] = 0.0;
+        }
+        return;
+    }
+    const int nv = min(kLgChunk, n - i0);
+    if (tid == 0) {
+        mbar_init(smem_u32(&bar), 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid < 32) {
+        if (!cand) {
+            if (tid == 0) {
+                mbar_expect_tx(smem_u32(&bar), 2 * kLgChunk * 128);
+                const int row0 = l * kcap + i0;
+                tma_load_2d(smem_u32(tile), &tm_tile, 0, row0, smem_u32(&bar));
+                tma_load_2d(smem_u32(tile + kLgChunk * 128), &tm_tile, 64, row0, smem_u32(&bar));
+            }
+        } else {
+            // lane j gathers rows 4j .. 4j+3 (rows past nv repeat the chunk's first candidate)
+            int id[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int rr = 4 * tid + r;
+                id[r] = l * kcap + __ldg(cand + (size_t)l * cand_cap + i0 + (rr < nv ? rr : 0));
+            }
+            if (tid == 0) mbar_expect_tx(smem_u32(&bar), 2 * kLgChunk * 128);
+            __syncwarp();
+            for (int h = 0; h < 2; ++h)
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_u32(tile + h * kLgChunk * 128 + tid * 512)),
+                    "l"(reinterpret_cast<uint64_t>(&tm_row)), "r"(h * 64), "r"(id[0]), "r"(id[1]), "r"(id[2]),
+                    "r"(id[3]), "r"(smem_u32(&bar))
+                    : "memory");
+        }
+    }
+    for (int j = tid; j < G * D; j += kLgThreads) {
+        const int g = j / D, k = j - g * D;
+        qs[(k / QD) * QS + (k % QD) * G + g] = q_lk[(size_t)l * G * D + j];
+    }
+    __syncthreads();
+    mbar_wait(smem_u32(&bar), 0);
+
+    const int qt = tid & 3, rg = tid >> 2;
+    const double* qq = qs + qt * QS;
+    double acc[4][G];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int g = 0; g < G; ++g) acc[r][g] = 0.0;
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+        const int c = (cc + 2 * (qt >> 1)) & 3;  // this quarter's 16-byte chunk (8 dims)
+        const int ch = (qt & 1) * 4 + c;         // chunk within the 64-column half
+        uint4 raw[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int row = rg + 32 * r;
+            raw[r] = *reinterpret_cast<const uint4*>(tile + (qt >> 1) * kLgChunk * 128 + row * 128 +
+                                                     ((ch ^ (row & 7)) << 4));
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            double qv[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) qv[g] = qq[(c * 8 + e) * G + g];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const unsigned wd = (&raw[r].x)[e >> 1];
+                const double x = bf16hi_to_f64((e & 1) ? (wd & 0xffff0000u) : (wd << 16));
+#pragma unroll
+                for (int g = 0; g < G; ++g) acc[r][g] = fma(qv[g], x, acc[r][g]);
+            }
+        }
+    }
+    // transpose-reduce over the 4 quarter lanes (xor 2 splits rows, xor 1 splits heads)
+    const bool hi2 = qt & 2, hi1 = qt & 1;
+    constexpr int GH = (G + 1) / 2;
+    double a2[2][G];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const double send = hi2 ? acc[rr][g] : acc[rr + 2][g];
+            const double keep = hi2 ? acc[rr + 2][g] : acc[rr][g];
+            a2[rr][g] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+    double a1[2][GH];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+        for (int j = 0; j < GH; ++j) {
+            const int ghi = GH + j;
+            const double lo = a2[rr][j], hv = ghi < G ? a2[rr][ghi < G ? ghi : 0] : 0.0;
+            const double send = hi1 ? lo : hv;
+            const double keep = hi1 ? hv : lo;
+            a1[rr][j] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+        }
+    const double sq = sqrt((double)D);
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+        const int r = rg + 32 * ((hi2 ? 2 : 0) + rr);
+#pragma unroll
+        for (int j = 0; j < GH; ++j) {
+            const int g = (hi1 ? GH : 0) + j;
+            if (g < G) {
+                const double v = a1[rr][j] / sq;
+                slg[g * kLgChunk + r] = v;
+                if (r < nv) logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
+            }
+        }
+    }
+    if (!cstats) return;
+    __syncthreads();
+    const int i = tid;
+    const bool valid = i < nv;
+    const int id = valid ? (cand ? cand[(size_t)l * cand_cap + i0 + i] : i0 + i) : 0;
+    const double nsz = valid ? (double)lv_size[(size_t)l * kcap + id] : 0.0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const double m = warp_max(valid ? slg[g * kLgChunk + i] : -INFINITY);
+        if (lane == 0) red[w][g] = m;
+    }
+    __syncthreads();
+    if (tid < G) {
+        double M = -INFINITY;
+        for (int ww = 0; ww < kLgThreads / 32; ++ww) M = fmax(M, red[ww][tid]);
+        s_m[tid] = M;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const double e = valid ? exp(slg[g * kLgChunk + i] - s_m[g]) : 0.0;
+        if (valid && e_local) e_local[((size_t)l * G + g) * cand_cap + i0 + i] = e;
+        const double z = warp_sum(e * nsz);
+        __syncwarp();
+        if (lane == 0) red[w][g] = z;
+    }
+    __syncthreads();
+    if (tid < G) {
+        double Z = 0.0;
+        for (int ww = 0; ww < kLgThreads / 32; ++ww) Z += red[ww][tid];
+        cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2] = s_m[tid];
+        cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2 + 1] = Z;
+    }
 }
 
 // ============================================================================
@@ -837,6 +1017,30 @@ global_cut_kernel(const PrefixEntry* __restrict__ prefix, const int32_t* __restr
 
 using namespace mpa;
 
+static int encode_bf16_rows(CUtensorMap* out, const void* base, long long rows, int d, int box_rows) {
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        const cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        MPA_REQUIRE(e == cudaSuccess && q == cudaDriverEntryPointSuccess && fn, MPA_ERR_UNSUPPORTED,
+                    "cuTensorMapEncodeTiled unavailable (%d)", (int)e);
+        encode = reinterpret_cast<EncodeFn>(fn);
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    MPA_REQUIRE(r == CUDA_SUCCESS, MPA_ERR_ARG, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return 0;
+}
+
 int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* lv, const int32_t* cand,
                          const int32_t* n_cand, int cand_cap, double* logits, double* chunk_stats, double* e_local,
                          int n_chunks, int n_max, cudaStream_t st) {
@@ -869,6 +1073,20 @@ int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* 
                                              item_chunks, L);                                                      \
     }
     if (grid <= 0) return 0;
+    if (d == 128 && !persist) {
+        CUtensorMap tt, tr;
+        if (int rc = encode_bf16_rows(&tt, lv->kc, (long long)L * lv->cap, 128, kLgChunk)) return rc;
+        if (int rc = encode_bf16_rows(&tr, lv->kc, (long long)L * lv->cap, 128, 1)) return rc;
+        dim3 g2(item_chunks, L);
+        MPA_DISPATCH_G(group, {
+            auto kern = logits_tma_kernel<kG>;
+            const size_t smem = 1024 + 2 * kLgChunk * 128 + sizeof(double) * (4 * (32 * kG + 2) + kG * kLgChunk);
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            kern<<<g2, kLgThreads, smem, st>>>(tt, tr, q_lk, lv->cap, lv->count, lv->size, cand, n_cand, cand_cap,
+                                               logits, chunk_stats, e_local, n_chunks);
+        });
+        return check_launch("mpa_centroid_logits(tma)");
+    }
     MPA_DISPATCH_G(group, {
         if (persist) {
             if (d == 128) MPA_LG3(128, 2) else MPA_LG3(64, 2)
