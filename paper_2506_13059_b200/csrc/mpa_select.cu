@@ -260,11 +260,11 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
                   const int32_t* __restrict__ lv_size, const int32_t* __restrict__ cand,
                   const int32_t* __restrict__ n_cand, int cand_cap, double* __restrict__ logits,
                   double* __restrict__ cstats, double* __restrict__ e_local, int n_chunks) {
-    constexpr int D = 128, QD = 32, QS = QD * G + 2;
+    constexpr int D = 128, QD = 32, QRow = QD + 2;  // q slot: 32 dims (+16 B pad) per (head, quarter)
     extern __shared__ __align__(1024) unsigned char sm_raw[];
     unsigned char* tile = sm_raw + ((1024 - (smem_u32(sm_raw) & 1023)) & 1023);  // [2 halves][128][128 B]
-    double* qs = reinterpret_cast<double*>(tile + 2 * kLgChunk * 128);          // [4][QD][G] (+pad)
-    double* slg = qs + 4 * QS;                                                  // [G][128]
+    double* qs = reinterpret_cast<double*>(tile + 2 * kLgChunk * 128);          // [G][4][QRow]
+    double* slg = qs + G * 4 * QRow;                                            // [G][128]
     __shared__ __align__(8) uint64_t bar;
     __shared__ double red[kLgThreads / 32][G];
     __shared__ double s_m[G];
@@ -285,9 +285,19 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
     }
     __syncthreads();
     if (tid < 32) {
+        if (tid == 0) {
+            // one expect_tx (a single arrive) for everything this barrier phase receives
+            mbar_expect_tx(smem_u32(&bar), G * 4 * QD * 8 + 2 * kLgChunk * 128);
+            // q_lk rows of the GQA group: one 256 B bulk copy per (head, quarter) into padded slots
+            for (int j = 0; j < G * 4; ++j)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                        smem_u32(qs + j * QRow)),
+                    "l"(q_lk + ((size_t)l * G + j / 4) * D + (j % 4) * QD), "r"(QD * 8), "r"(smem_u32(&bar))
+                    : "memory");
+        }
         if (!cand) {
             if (tid == 0) {
-                mbar_expect_tx(smem_u32(&bar), 2 * kLgChunk * 128);
                 const int row0 = l * kcap + i0;
                 tma_load_2d(smem_u32(tile), &tm_tile, 0, row0, smem_u32(&bar));
                 tma_load_2d(smem_u32(tile + kLgChunk * 128), &tm_tile, 64, row0, smem_u32(&bar));
@@ -300,7 +310,6 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
                 const int rr = 4 * tid + r;
                 id[r] = l * kcap + __ldg(cand + (size_t)l * cand_cap + i0 + (rr < nv ? rr : 0));
             }
-            if (tid == 0) mbar_expect_tx(smem_u32(&bar), 2 * kLgChunk * 128);
             __syncwarp();
             for (int h = 0; h < 2; ++h)
                 asm volatile(
@@ -311,15 +320,10 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
                     : "memory");
         }
     }
-    for (int j = tid; j < G * D; j += kLgThreads) {
-        const int g = j / D, k = j - g * D;
-        qs[(k / QD) * QS + (k % QD) * G + g] = q_lk[(size_t)l * G * D + j];
-    }
-    __syncthreads();
     mbar_wait(smem_u32(&bar), 0);
 
     const int qt = tid & 3, rg = tid >> 2;
-    const double* qq = qs + qt * QS;
+    const double* qq = qs + qt * QRow;
     double acc[4][G];
 #pragma unroll
     for (int r = 0; r < 4; ++r)
@@ -340,7 +344,7 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
         for (int e = 0; e < 8; ++e) {
             double qv[G];
 #pragma unroll
-            for (int g = 0; g < G; ++g) qv[g] = qq[(c * 8 + e) * G + g];
+            for (int g = 0; g < G; ++g) qv[g] = qq[g * 4 * QRow + c * 8 + e];
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 const unsigned wd = (&raw[r].x)[e >> 1];
@@ -1080,7 +1084,7 @@ int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* 
         dim3 g2(item_chunks, L);
         MPA_DISPATCH_G(group, {
             auto kern = logits_tma_kernel<kG>;
-            const size_t smem = 1024 + 2 * kLgChunk * 128 + sizeof(double) * (4 * (32 * kG + 2) + kG * kLgChunk);
+            const size_t smem = 1024 + 2 * kLgChunk * 128 + sizeof(double) * (kG * 4 * 34 + kG * kLgChunk);
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             kern<<<g2, kLgThreads, smem, st>>>(tt, tr, q_lk, lv->cap, lv->count, lv->size, cand, n_cand, cand_cap,
                                                logits, chunk_stats, e_local, n_chunks);
