@@ -264,21 +264,36 @@ def online_update(eng, seqs, cursor: int) -> dict:
     for s in seqs:
         if eng.cache_len[s] - eng.buffer_start[s] < 2 * L:
             raise RuntimeError(f"buffer underflow: have {eng.cache_len[s] - eng.buffer_start[s]} tokens, need {2 * L}")
-    probs, inits, counts, tails = [], [], [], []
+    probs, tails = [], []
+    old_src, old_dst, new_src, new_dst = [], [], [], []
+    c_at = 0
+    samples = {}  # the draw depends on (seed, cursor, kv-head) only (pipeline.py:170-172): once per head
     for l in ledgers:
         s = l // eng.Hkv
         F = led.blocks[l][-1]
         bs = int(eng.buffer_start[s])
-        rng = update_rng(cfg.seed, cursor, _head(eng, l))
-        samp = rng.choice(L, size=n_new, replace=False)
-        old = led.kc64[l, F.f0:F.f0 + F.fk]
-        inits.append(torch.cat([old, eng.k_raw[l, bs + torch.as_tensor(samp, device=eng.device)].double()]))
-        counts.append(torch.cat([led.size[l, F.f0:F.f0 + F.fk],
-                                 torch.zeros(n_new, dtype=torch.int32, device=eng.device)]))
+        h = _head(eng, l)
+        if h not in samples:
+            samples[h] = update_rng(cfg.seed, cursor, h).choice(L, size=n_new, replace=False)
+        samp = samples[h]
+        # problem centroids: the final block's clusters, then the sampled tokens (clustering.py:430-434)
+        old_src.append(l * led.kcap + F.f0 + np.arange(F.fk))
+        old_dst.append(c_at + np.arange(F.fk))
+        new_src.append(l * eng.tcap + bs + samp)
+        new_dst.append(c_at + F.fk + np.arange(n_new))
+        c_at += F.fk + n_new
         probs.append((l, F.start, bs + L - F.start, F.fk + n_new))
         tails.append(bs - F.start)
-    km = KMeansBatch(eng.device, eng.d, probs, torch.cat(inits), pts=eng.k_raw, tcap=eng.tcap,
-                     min_iters=cfg.refine_kmeans_iters, count_init=torch.cat(counts))
+    dev = eng.device
+    idx = lambda parts: torch.as_tensor(np.concatenate(parts), dtype=torch.int64, device=dev)
+    osrc, odst, nsrc, ndst = idx(old_src), idx(old_dst), idx(new_src), idx(new_dst)
+    init = torch.empty(c_at, eng.d, dtype=torch.float64, device=dev)
+    init[odst] = led.kc64.view(-1, eng.d)[osrc]
+    init[ndst] = eng.k_raw.view(-1, eng.d)[nsrc].double()
+    counts = torch.zeros(c_at, dtype=torch.int32, device=dev)
+    counts[odst] = led.size.view(-1)[osrc]
+    km = KMeansBatch(dev, eng.d, probs, init, pts=eng.k_raw, tcap=eng.tcap,
+                     min_iters=cfg.refine_kmeans_iters, count_init=counts)
     dist = torch.empty(len(probs), L, km.k_max, dtype=torch.float64, device=eng.device)
     tails_d = _i32(eng, tails)
     call("mpa_km_seq_assign", km.struct(), ptr(tails_d), L, ptr(dist), stream_ptr())

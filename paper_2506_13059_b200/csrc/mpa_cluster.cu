@@ -538,20 +538,38 @@ __global__ void km_assign_from_level_kernel(mpa_km km, const int32_t* __restrict
 
 // ---------------------------------------------------------------------------- K6 sequential
 
-__global__ void km_seq_dist_kernel(mpa_km km, const int32_t* __restrict__ tail, int n_new, double* dist) {
+// distances of the n_new appended tokens to every starting centroid (direct form, fp64):
+// the tokens are staged once per CTA in smem (exact as fp32: bf16 / fp32 key sources), each
+// thread owns one centroid and eight independent token accumulators
+__global__ void __launch_bounds__(128) km_seq_dist_kernel(mpa_km km, const int32_t* __restrict__ tail, int n_new,
+                                                          double* dist) {
+    extern __shared__ float xs[];  // [n_new][d]
     const int p = blockIdx.y;
     const int K = km.prob_k[p], d = km.d;
+    const int l = km.prob_l[p], row0 = km.prob_start[p] + tail[p];
+    for (int e = threadIdx.x; e < n_new * d; e += blockDim.x) {
+        const int t = e / d, k = e - t * d;
+        xs[e] = (float)point_elem(km, l, row0 + t, k);
+    }
+    __syncthreads();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= K) return;
-    const int l = km.prob_l[p], row0 = km.prob_start[p] + tail[p];
     const double* c = km.cent + (size_t)(km.c_off[p] + j) * d;
-    for (int t = 0; t < n_new; ++t) {
-        double s = 0.0;
+    for (int t0 = 0; t0 < n_new; t0 += 8) {
+        double s[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s[u] = 0.0;
         for (int k = 0; k < d; ++k) {
-            const double df = __dsub_rn(c[k], point_elem(km, l, row0 + t, k));
-            s = __dadd_rn(s, __dmul_rn(df, df));
+            const double ck = __ldg(c + k);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const double df = __dsub_rn(ck, (double)xs[(t0 + u < n_new ? t0 + u : 0) * d + k]);
+                s[u] = __dadd_rn(s[u], __dmul_rn(df, df));
+            }
         }
-        dist[((size_t)p * n_new + t) * km.k_max + j] = s;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (t0 + u < n_new) dist[((size_t)p * n_new + t0 + u) * km.k_max + j] = s[u];
     }
 }
 
@@ -762,7 +780,11 @@ extern "C" int mpa_km_seq_assign(const mpa_km* km, const int32_t* tail_start, in
     MPA_REQUIRE(tail_start && dist, MPA_ERR_ARG, "mpa_km_seq_assign: null argument");
     if (km->n_prob <= 0 || n_new <= 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
-    km_seq_dist_kernel<<<dim3(ceil_div(km->k_max, 128), km->n_prob), 128, 0, st>>>(*km, tail_start, n_new, dist);
+    const size_t smem = sizeof(float) * n_new * km->d;
+    MPA_REQUIRE(smem <= 200 * 1024 && !km->pts64, MPA_ERR_UNSUPPORTED, "mpa_km_seq_assign: %d tokens x d %d", n_new,
+                km->d);
+    cudaFuncSetAttribute(km_seq_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    km_seq_dist_kernel<<<dim3(ceil_div(km->k_max, 128), km->n_prob), 128, smem, st>>>(*km, tail_start, n_new, dist);
     km_seq_assign_kernel<<<km->n_prob, 1024, 0, st>>>(*km, tail_start, n_new, dist);
     return check_launch("mpa_km_seq_assign");
 }

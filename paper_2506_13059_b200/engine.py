@@ -131,7 +131,6 @@ class DecodeEngine:
         self._sync_scalars()
 
     def _sync_scalars(self) -> None:
-        self.invalidate_graph()
         self.sink_end_d.copy_(torch.as_tensor(self.sink_end, dtype=torch.int32))
         self.buffer_start_d.copy_(torch.as_tensor(self.buffer_start, dtype=torch.int32))
         self.cache_len_d.copy_(torch.as_tensor(self.cache_len, dtype=torch.int32))
@@ -162,9 +161,21 @@ class DecodeEngine:
         call("mpa_rotate_queries", ptr(q), self.n_seq, self.Hq, self.d, ptr(self.cache_len_d), self.cfg.window_offset,
              ptr(self.inv_freq), 1.0 / math.sqrt(self.d), ptr(self.q_rot), ptr(self.q_lk), stream_ptr())
 
+    def _cluster_bounds(self):
+        """Per-ledger cluster-count bounds passed to the lookup kernels (grid / smem sizing).
+        They carry headroom, so a captured step graph stays valid while the online updates
+        grow the final block (+ceil(L/r) clusters each) until a bound is crossed."""
+        need_f, need_c = int(self.led.n_fine.max(initial=0)), int(self.led.n_coarse.max(initial=0))
+        if getattr(self, "_bf", None) is None or need_f > self._bf or need_c > self._bc:
+            self._bf = min(self.kcap, (need_f + 255) // 128 * 128)
+            self._bc = min(self.ccap, (need_c + 255) // 128 * 128) if self.ccap else 0
+            self.invalidate_graph()
+        return self._bf, self._bc
+
     def lookup(self) -> None:
         """K9 + K10 + work lists for the current q_lk (flat or hierarchical)."""
         st = stream_ptr()
+        self._bound_fine, self._bound_coarse = self._cluster_bounds()
         G, L = self.G, self.L
         fine = self.led.fine_level()
         replacement = 0 if self.mode == "flat-no-replacement" else 1
@@ -176,12 +187,12 @@ class DecodeEngine:
             if int(self.led.n_fine.min()) == 0:
                 raise ConfigError("ledger has no clusters")
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, None, None, self.kcap,
-                 ptr(self.logits), ptr(cs), ptr(el), int(self.led.n_fine.max()), st)
+                 ptr(self.logits), ptr(cs), ptr(el), self._bound_fine, st)
             call("mpa_select_worklist", fine, None, G, ptr(self.logits), ptr(el), None, None, self.kcap, ptr(cs),
                  None, None,
                  ptr(self.budget), ptr(self.sink_end_d), ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv,
                  L, replacement, ptr(self.flag), ptr(self.sel_tokens), ptr(self.tok), self.tok_cap, ptr(self.rej),
-                 ptr(self.rej_w), self.rej_cap, ptr(self.stats), int(self.led.n_fine.max()), st)
+                 ptr(self.rej_w), self.rej_cap, ptr(self.stats), self._bound_fine, st)
         else:
             if int(self.led.n_coarse.min()) == 0:
                 raise ConfigError("ledger has no coarse clusters")
@@ -189,18 +200,18 @@ class DecodeEngine:
             ccs = self.ccstats if tiled else None
             cel = self.celocal if el is not None else None
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, coarse, None, None, self.ccap,
-                 ptr(self.clogits), ptr(ccs), ptr(cel), int(self.led.n_coarse.max()), st)
+                 ptr(self.clogits), ptr(ccs), ptr(cel), self._bound_coarse, st)
             call("mpa_select", ptr(self.clogits), G, None, ptr(self.led.ccount), self.ccap, ptr(self.led.csize),
                  self.ccap, None, None, None, None, 0, ptr(self.cbudget), L, ptr(self.cflag),
-                 ptr(self.csel_tokens), ptr(ccs), ptr(cel), int(self.led.n_coarse.max()), st)
+                 ptr(self.csel_tokens), ptr(ccs), ptr(cel), self._bound_coarse, st)
             call("mpa_hier_candidates", coarse, ptr(self.cflag), L, ptr(self.cand), ptr(self.n_cand), self.kcap, st)
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, ptr(self.cand), ptr(self.n_cand),
-                 self.kcap, ptr(self.logits), ptr(cs), ptr(el), int(self.led.n_fine.max()), st)
+                 self.kcap, ptr(self.logits), ptr(cs), ptr(el), self._bound_fine, st)
             call("mpa_select_worklist", fine, coarse, G, ptr(self.logits), ptr(el), ptr(self.cand), ptr(self.n_cand),
                  self.kcap, ptr(cs), ptr(self.cflag), ptr(self.clogits), ptr(self.budget), ptr(self.sink_end_d),
                  ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv, L, replacement, ptr(self.flag),
                  ptr(self.sel_tokens), ptr(self.tok), self.tok_cap, ptr(self.rej), ptr(self.rej_w), self.rej_cap,
-                 ptr(self.stats), int(self.led.n_fine.max()), st)
+                 ptr(self.stats), self._bound_fine, st)
 
     def fused(self, n_split: int | None = None) -> torch.Tensor:
         """K11 + K12 over the current work lists.  n_split None / 0: one full wave of the
@@ -287,6 +298,7 @@ class DecodeEngine:
         if self._graphable():
             if int(self.cache_len.max()) + 1 > self.tcap:
                 raise RuntimeError(f"KV cache capacity {self.tcap} exceeded")
+            self._cluster_bounds()  # recaptures only if the cluster counts outgrew the captured bounds
             if self._graph is None:
                 self._capture_step()
             self._gq.copy_(q)
@@ -305,7 +317,8 @@ class DecodeEngine:
                 self.last_update = clustering.positional_update(self, todo)
             else:
                 self.last_update = clustering.online_update(self, todo, self.cursor)
-            self.invalidate_graph()
+            # the captured graph's launch arguments stay valid while the cluster bounds hold
+            self._cluster_bounds()
         self.cursor += 1
         return out
 

@@ -5,6 +5,8 @@ import os
 import sys
 import time
 
+import numpy as np
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
@@ -89,7 +91,73 @@ def recheck_stats():
     clustering.KMeansBatch.lloyd = lloyd
 
 
+def call_stats():
+    """Per C-ABI call wall time (device-synchronised) inside one update."""
+    import collections
+
+    import torch
+
+    from paper_2506_13059_b200 import clustering
+
+    orig = clustering.call
+    tot = collections.defaultdict(float)
+
+    def call(name, *a):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = orig(name, *a)
+        torch.cuda.synchronize()
+        tot[name] += time.perf_counter() - t0
+        return r
+
+    clustering.call = call
+    orig_init = clustering.KMeansBatch.__init__
+
+    def init(self, *a, **k):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        orig_init(self, *a, **k)
+        torch.cuda.synchronize()
+        tot["KMeansBatch.__init__"] += time.perf_counter() - t0
+
+    clustering.KMeansBatch.__init__ = init
+    import atexit
+
+    atexit.register(lambda: [print(f"  call {k:28s} {v * 1e3:8.2f} ms") for k, v in sorted(tot.items(), key=lambda x: -x[1])])
+
+
+def steady_state():
+    """Wall time of eng.step around an update in steady state (after a first update), and of
+    the graph recapture that follows it."""
+    import torch
+
+    import bench
+
+    args = argparse.Namespace(batch=8, ctx=16384, budget=512, steps=300, warmup=3)
+    eng, Q, KN, VN, _ = bench.build_engine(args, 0, torch.device("cuda", 0))
+    L = eng.cfg.local_buffer
+    t_up, t_other = [], []
+    for i in range(3 * L + 10):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng.step(Q[i % Q.shape[0]], KN[i % KN.shape[0]], VN[i % VN.shape[0]])
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        (t_up if eng.last_update is not None else t_other).append(dt)
+    g0 = time.perf_counter()
+    eng.invalidate_graph()
+    eng._capture_step()
+    torch.cuda.synchronize()
+    print(f"steps {len(t_other)} median {np.median(t_other) * 1e6:.1f} us; update steps {[round(x * 1e3, 2) for x in t_up]} ms;"
+          f" recapture {(time.perf_counter() - g0) * 1e3:.2f} ms")
+
+
 if __name__ == "__main__":
     if os.environ.get("RECHECK"):
         recheck_stats()
-    main()
+    if os.environ.get("CALLS"):
+        call_stats()
+    if os.environ.get("STEADY"):
+        steady_state()
+    else:
+        main()
