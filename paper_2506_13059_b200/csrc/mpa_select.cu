@@ -536,10 +536,11 @@ __device__ void radix_cross(const unsigned long long* keys, const int* sizes, Id
         const int bpt = kBins / blockDim.x;
         unsigned long long wsum = 0;
         for (int j = 0; j < bpt; ++j) wsum += hist_w[threadIdx.x * bpt + j];
-        unsigned long long btot;
-        const unsigned long long before = block_scan_u64(wsum, s_scan, &btot);
+        // every thread reads s_below before the scan's barriers; the owner rewrites it after them
         const long long below = s_below;
         const long long need = B - below;  // > 0
+        unsigned long long btot;
+        const unsigned long long before = block_scan_u64(wsum, s_scan, &btot);
         if ((long long)before < need && (long long)(before + wsum) >= need) {
             long long run = (long long)before;
             int dg = threadIdx.x * bpt + bpt - 1;
