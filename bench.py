@@ -14,8 +14,10 @@ every timed step; each step is timed with CUDA events on the engine stream.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
 
 N > 1 (torchrun): every rank runs its own batch (replicas, batch-sharded: no collective on
-the data path), barrier + max over ranks.  `--impl reference` times the CPU oracle (the
-reference algorithm restated in numpy; the reference package is pure Python) on rank 0.
+the data path), barrier + max over ranks; `--workload c5` at N > 1 shards one long context
+over the ranks instead.  `--impl reference` times the reference package itself (pure Python,
+installed into baseline/_ref by __graft_entry__.build()) on rank 0's host cores, falling back to
+the oracle port when it is not importable.
 """
 
 from __future__ import annotations
@@ -464,7 +466,7 @@ def main():
     if rank == 0:
         hbm, peak_kind = peaks()
         achieved = nbytes["fused"] / (fused_avg * 1e-3) / 1e9
-        traffic = load_traffic()
+        traffic = load_traffic(args.workload, b)
         line = {
             "metric": METRIC,
             "value": ms_step * 1e3,
@@ -655,13 +657,18 @@ def flashinfer_dense(eng, q, K, timed):
         return None
 
 
-def load_traffic():
+def load_traffic(workload, batch):
+    """dram read+write bytes per decode_sk_kernel launch from the committed ncu --set full capture,
+    only when that capture was taken on this workload (else null)."""
     p = os.path.join(ROOT, "profiles", "fused_traffic.json")
     try:
         with open(p) as fh:
-            return json.load(fh).get("dram_bytes_per_launch")
+            rec = json.load(fh)
+        if rec.get("workload") == workload and int(rec.get("batch", -1)) == batch:
+            return rec.get("dram_bytes_per_launch")
     except Exception:
-        return None
+        pass
+    return None
 
 
 def reference_cpu_time(keys, values, qs, ctx, budget, group, d, n_steps=3):

@@ -78,7 +78,8 @@ int mpa_kv_append(const mpa_cache* cache, const float* k_src, const float* v_src
                   void* stream);
 
 /* K1 -- rotate queries: q_rot = rotate(q, qpos[seq]) * scale (fp32, exact view) and
- * q_lk = rotate(q, delta) (fp64, lookup view; rope.py:66-68).  q: fp32 [n_seq, n_qh, d]. */
+ * q_lk = rotate(q, delta) (fp64, lookup view; rope.py:66-68).  q: fp32 [n_seq, n_qh, d].
+ * Either output may be NULL (not both): the views are independent. */
 int mpa_rotate_queries(const float* q, int n_seq, int n_qh, int d, const int32_t* qpos,
                        int delta, const double* inv_freq, float scale,
                        float* q_rot, double* q_lk, void* stream);
@@ -89,11 +90,14 @@ int mpa_rotate_queries(const float* q, int n_seq, int n_qh, int d, const int32_t
  * [L, ceil(cap/128), G, 2] per-128-candidate (m_c = max_g l, Z_c = sum N e^(l - m_c)) partials of
  * the normaliser.  e_local (optional, bf16 centroids only): [L, G, cand_cap] e^(l - m_c), which
  * lets the selection form e^(l - max) = e_local e^(m_c - max) without per-candidate exps.
- * n_max (0: cap) bounds the live candidates of every ledger (sizes the grid). */
+ * n_max (0: cap) bounds the live candidates of every ledger (sizes the grid).
+ * rej_w (optional; flat level, bf16, d = 128, with chunk_stats): [L, rej_cap, GP] fp32 replacement
+ * weights of EVERY candidate, rej_w[l, i, g] = logit + ln(size) -- the contiguous-centroid work
+ * list of mpa_select_worklist (rej == NULL) then masks the selected ones. */
 int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group, int d,
                         const mpa_level* lv, const int32_t* cand, const int32_t* n_cand,
                         int cand_cap, double* logits, double* chunk_stats, double* e_local, int n_max,
-                        void* stream);
+                        float* rej_w, int rej_cap, void* stream);
 
 /* K10 -- Eq. 1 scores and budgeted greedy selection (attention.py:192-207, 267-290).
  * Scores: e_g,i = exp(l_g,i - max_g), Z_g = sum over candidates AND live extras of N * e,
@@ -138,7 +142,11 @@ int mpa_build_worklist(const mpa_level* fine, const mpa_level* coarse, int group
                        int32_t* stats, void* stream);
 
 /* K10 + work list fused in one launch per ledger: mpa_select over the fine candidates (extras =
- * coarse clusters with cflag == 0, hierarchy only) followed by mpa_build_worklist. */
+ * coarse clusters with cflag == 0, hierarchy only) followed by mpa_build_worklist.
+ * rej == NULL with replacement (flat level only): contiguous-centroid work list -- no rejected
+ * list is written; rej_w already holds every candidate's weight (mpa_centroid_logits rej_w) and
+ * the selected candidates' rows are set to -inf, so mpa_sparse_decode can stream the fine value
+ * centroids [0, count[l]) in order (see there).  stats row 1 still counts the rejected. */
 int mpa_select_worklist(const mpa_level* fine, const mpa_level* coarse, int group, const double* logits,
                         const double* e_local, const int32_t* cand, const int32_t* n_cand, int cand_cap,
                         const double* chunk_stats,
@@ -152,7 +160,10 @@ int mpa_select_worklist(const mpa_level* fine, const mpa_level* coarse, int grou
  * by index, logits q_rot . k) and the rejected-centroid pseudo-tokens (logit + ln N, value
  * centroid), LSE-merged in-kernel by the last finisher of each ledger
  * (attention.py:58-87, 120-137, 210-239, 473-498).  tok == NULL: dense decode over
- * [0, n_tok[l]) (the "oracle" comparator, attention.py:90-102).  rej_w rows have stride
+ * [0, n_tok[l]) (the "oracle" comparator, attention.py:90-102).  Centroid terms: rej != NULL:
+ * the listed value rows; rej == NULL and rej_w != NULL (stream-K path only): every fine value
+ * centroid [0, n_rej[l]) in order with rej_w indexed by centroid (-inf = selected, no term);
+ * rej_w == NULL: none.  rej_w rows have stride
  * GP = G <= 4 ? 4 : 8 floats.  bf16 caches with d in {64, 128}: stream-K tensor-core kernel
  * whose grid is one full wave (n_split <= 0) or n_split CTAs per ledger (used to test that the
  * result does not depend on the partition); other caches: FFMA kernel with n_split (0: auto)

@@ -381,11 +381,13 @@ struct SkGeom {
 template <int G, int D, int NW, int NST>
 __global__ void __launch_bounds__(NW * 32, 2)
 decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                 const __grid_constant__ CUtensorMap tm_fvc, const __grid_constant__ CUtensorMap tm_cvc, int tcap,
+                 const __grid_constant__ CUtensorMap tm_fvc, const __grid_constant__ CUtensorMap tm_cvc,
+                 const __grid_constant__ CUtensorMap tm_k16, const __grid_constant__ CUtensorMap tm_v16,
+                 const __grid_constant__ CUtensorMap tm_fvc16, int tcap,
                  const float* __restrict__ q_rot, const int32_t* __restrict__ tok, const int32_t* __restrict__ n_tok,
                  int tok_cap, const int32_t* __restrict__ rej, const float* __restrict__ rej_w,
                  const int32_t* __restrict__ n_rej, int rej_cap, int fcap, int ccap, int L, float* __restrict__ part,
-                 int32_t* __restrict__ ticket, float* __restrict__ out, float* __restrict__ part_out) {
+                 int32_t* __restrict__ ticket, float* __restrict__ out, float* __restrict__ part_out, int tok_runs) {
     dbg_stamp(0);
     using Geo = SkGeom<G, D, NW, NST>;
     constexpr bool PACKED = G <= 4;
@@ -396,6 +398,9 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int gr = lane >> 2, tq = lane & 3;
     const int C = gridDim.x, c = blockIdx.x;
+    // centroid terms: listed rows (rej), every fine centroid in order (rej == NULL, rej_w: the
+    // contiguous-centroid list, selected ones weighted -inf), or none
+    const bool has_rej = rej || rej_w;
 
     // ---- per-ledger tile prefix sum (every CTA computes the same schedule)
     int* tp = reinterpret_cast<int*>(smem + Geo::kStagesB + Geo::kBarB + Geo::kIdB);
@@ -407,7 +412,7 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             const int l = l0 + threadIdx.x;
             int n = 0;
             if (l < L) {
-                const int nt = (__ldg(n_tok + l) + 15) >> 4, nr = rej ? (__ldg(n_rej + l) + 31) >> 5 : 0;
+                const int nt = (__ldg(n_tok + l) + 15) >> 4, nr = has_rej ? (__ldg(n_rej + l) + 31) >> 5 : 0;
                 n = nt + nr > 0 ? nt + nr : 1;
             }
             int tot;
@@ -422,6 +427,9 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_v)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_fvc)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_cvc)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_k16)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_v16)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_fvc16)) : "memory");
     }
     const unsigned bar0 = smem_u32(smem + Geo::kStagesB + Geo::kLgAllB) + w * NST * 8;
     const unsigned lgbase = smem_u32(smem + Geo::kStagesB) + w * NST * Geo::kLgB;
@@ -467,7 +475,7 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             wk.beg = tp[l];
             wk.end = tp[l + 1];
             wk.nt = __ldg(n_tok + l);
-            wk.nr = rej ? __ldg(n_rej + l) : 0;
+            wk.nr = has_rej ? __ldg(n_rej + l) : 0;
             wk.ntt = (wk.nt + 15) >> 4;
             if (wk.ntt == 0 && wk.nr == 0) wk.ntt = 1;  // empty ledger: one empty token tile
         }
@@ -490,7 +498,7 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     constexpr int kAhead = Geo::kRing - 1;
     auto prefetch_ids = [&](int j, const Meta& m) {
         const int rows = m.kind == 0 ? 16 : 32;
-        if (lane < rows && m.nv > 0 && (m.kind == 1 || tok)) {
+        if (lane < rows && m.nv > 0 && (m.kind == 1 ? rej != nullptr : tok != nullptr)) {
             const int row = lane < m.nv ? lane : 0;
             const int32_t* src = m.kind == 0 ? tok + (size_t)m.l * tok_cap + m.i0 + row
                                              : rej + (size_t)m.l * rej_cap + m.i0 + row;
@@ -549,7 +557,8 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         const unsigned kst = wbase + st * Geo::kStageB, vst = kst + Geo::kMatB, lgs = lgbase + st * Geo::kLgB;
         const unsigned bar = bar0 + st * 8;
         int id[16], id2[16];
-        if (m.nv > 0) {
+        const bool rows_in_order = m.kind == 1 && !rej;  // contiguous-centroid list
+        if (m.nv > 0 && !rows_in_order) {
             ids16(j, m, 0, id);
             if (m.kind == 1) ids16(j, m, 16, id2);
         }
@@ -563,6 +572,18 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         if (m.kind == 0) {
             mbar_expect_tx(bar, 2 * Geo::kMatB);
             const int base = m.l * tcap;
+            // a run of consecutive tokens (sinks, buffer, dense decode) is one 16-row box per half
+            bool run = tok_runs != 0;
+#pragma unroll
+            for (int r = 1; r < 16; ++r) run = run && (r >= m.nv || id[r] == id[0] + r);
+            if (run) {
+#pragma unroll
+                for (int h = 0; h < Geo::kHalves; ++h) {
+                    tma_row(kst + h * 2048, &tm_k16, h * 64, base + id[0], bar, policy);
+                    tma_row(vst + h * 2048, &tm_v16, h * 64, base + id[0], bar, policy);
+                }
+                return;
+            }
 #pragma unroll
             for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -576,8 +597,17 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         } else {
             const unsigned lg_bytes = m.nv * GP * 4;
             mbar_expect_tx(bar, 2 * Geo::kMatB + lg_bytes);
-            gather_centroids(kst, id, m.l, bar);
-            gather_centroids(vst, id2, m.l, bar);
+            if (rows_in_order) {
+                const int row0 = m.l * fcap + m.i0;
+#pragma unroll
+                for (int h = 0; h < Geo::kHalves; ++h) {
+                    tma_row(kst + h * 2048, &tm_fvc16, h * 64, row0, bar, policy);
+                    tma_row(vst + h * 2048, &tm_fvc16, h * 64, row0 + 16, bar, policy);
+                }
+            } else {
+                gather_centroids(kst, id, m.l, bar);
+                gather_centroids(vst, id2, m.l, bar);
+            }
             bulk_g2s(lgs, rej_w + ((size_t)m.l * rej_cap + m.i0) * GP, lg_bytes, bar, policy);
         }
     };
@@ -655,7 +685,9 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
                 }
             }
         }
-        const float p0 = exp2f(x[0] - mA), p1 = exp2f(x[1] - mB), p2 = exp2f(x[2] - mA), p3 = exp2f(x[3] - mB);
+        // masked rows (-inf) weigh exactly 0, also while the running max is still -inf
+        const float p0 = x[0] == -INFINITY ? 0.f : exp2f(x[0] - mA), p1 = x[1] == -INFINITY ? 0.f : exp2f(x[1] - mB);
+        const float p2 = x[2] == -INFINITY ? 0.f : exp2f(x[2] - mA), p3 = x[3] == -INFINITY ? 0.f : exp2f(x[3] - mB);
         sA += p0 + p2;
         sB += p1 + p3;
         // P^T fragments (B operand): hi/lo split, transposed with movmatrix
@@ -1011,24 +1043,24 @@ int launch_ffma(const mpa_cache* c, const float* q_rot, const int32_t* tok, cons
 
 // 2D tensor map over rows of d bf16 (box: 64 columns x 1 row, 128B swizzle) for TMA gathers.
 // Encoding is pure host work; the last few maps are cached by (address, rows, d).
-int bf16_rows_map(CUtensorMap* out, const void* base, long long rows, int d) {
+int bf16_rows_map(CUtensorMap* out, const void* base, long long rows, int d, int box_rows = 1) {
     struct Entry {
         const void* base;
         long long rows;
-        int d;
+        int d, box_rows;
         CUtensorMap map;
     };
-    static Entry cache[16];
+    static Entry cache[32];
     static int next = 0;
     for (auto& e : cache)
-        if (e.base == base && e.rows == rows && e.d == d) {
+        if (e.base == base && e.rows == rows && e.d == d && e.box_rows == box_rows) {
             *out = e.map;
             return 0;
         }
     MPA_REQUIRE(rows > 0 && rows < (1ll << 31), MPA_ERR_UNSUPPORTED, "tensor map: %lld rows", rows);
     cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)d * 2};
-    cuuint32_t box[2] = {64, 1};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     // resolved through the runtime so the library has no link-time libcuda dependency
     using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1047,9 +1079,20 @@ int bf16_rows_map(CUtensorMap* out, const void* base, long long rows, int d) {
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     MPA_REQUIRE(r == CUDA_SUCCESS, MPA_ERR_ARG, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-    cache[next] = Entry{base, rows, d, *out};
-    next = (next + 1) % 16;
+    cache[next] = Entry{base, rows, d, box_rows, *out};
+    next = (next + 1) % 32;
     return 0;
+}
+
+// token tiles that are runs of consecutive rows use 16-row boxes: MPA_SK_TOKRUN=0 never,
+// (default: measured no faster than the gathers), 1 sparse lists only, 2 also the dense decode
+int tok_runs(bool sparse) {
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = getenv("MPA_SK_TOKRUN");
+        mode = e ? atoi(e) : 0;
+    }
+    return mode == 2 || (mode == 1 && sparse) ? 1 : 0;
 }
 
 template <int G, int D>
@@ -1063,14 +1106,19 @@ int launch_sk(const mpa_cache* c, const float* q_rot, const int32_t* tok, const 
     MPA_REQUIRE(smem <= 227 * 1024, MPA_ERR_UNSUPPORTED, "mpa_sparse_decode: %d ledgers exceed the smem schedule", L);
     auto kern = decode_sk_kernel<G, D, kSkWarps, kSkStages>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    CUtensorMap tk, tv, tf, tc;
+    CUtensorMap tk, tv, tf, tc, tk16, tv16, tf16;
     int rc = bf16_rows_map(&tk, c->k_rot, (long long)L * c->tcap, D);
     if (!rc) rc = bf16_rows_map(&tv, c->v, (long long)L * c->tcap, D);
+    if (!rc) rc = bf16_rows_map(&tk16, c->k_rot, (long long)L * c->tcap, D, 16);
+    if (!rc) rc = bf16_rows_map(&tv16, c->v, (long long)L * c->tcap, D, 16);
     if (!rc) rc = fvc ? bf16_rows_map(&tf, fvc, (long long)L * fcap, D) : (tf = tk, 0);
+    if (!rc) rc = fvc ? bf16_rows_map(&tf16, fvc, (long long)L * fcap, D, 16) : (tf16 = tk16, 0);
     if (!rc) rc = cvc ? bf16_rows_map(&tc, cvc, (long long)L * ccap, D) : (tc = tf, 0);
     if (rc) return rc;
-    kern<<<C, kSkWarps * 32, smem, st>>>(tk, tv, tf, tc, c->tcap, q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej,
-                                         rej_cap, fcap, ccap, L, part, ticket, out, part_out);
+    MPA_REQUIRE(rej || !rej_w || fvc, MPA_ERR_ARG, "mpa_sparse_decode: contiguous-centroid list without fine_vc");
+    kern<<<C, kSkWarps * 32, smem, st>>>(tk, tv, tf, tc, tk16, tv16, tf16, c->tcap, q_rot, tok, n_tok, tok_cap, rej,
+                                         rej_w, n_rej, rej_cap, fcap, ccap, L, part, ticket, out, part_out,
+                                         tok_runs(tok != nullptr));
     return check_launch("mpa_sparse_decode(stream-K mma)");
 }
 
@@ -1120,6 +1168,7 @@ static int sparse_decode_impl(const mpa_cache* c, const float* q_rot, int n_kv_h
                                  size_t workspace_bytes, float* out, float* part_out, void* stream) {
     MPA_REQUIRE(c && q_rot && n_tok && workspace && (out || part_out), MPA_ERR_ARG, "mpa_sparse_decode: null argument");
     MPA_REQUIRE(!rej || (rej_w && n_rej), MPA_ERR_ARG, "mpa_sparse_decode: rej without weights/counts");
+    MPA_REQUIRE(!rej_w || n_rej, MPA_ERR_ARG, "mpa_sparse_decode: rej_w without counts");
     MPA_REQUIRE(c->head_dim >= 2 && c->head_dim % 2 == 0 && c->head_dim <= 256, MPA_ERR_UNSUPPORTED,
                 "mpa_sparse_decode: head_dim %d", c->head_dim);
     (void)n_kv_heads;
@@ -1141,6 +1190,8 @@ static int sparse_decode_impl(const mpa_cache* c, const float* q_rot, int n_kv_h
                                      coarse_vc, coarse_cap, C, part, ticket, out, part_out, st);
         });
     }
+    MPA_REQUIRE(rej || !rej_w, MPA_ERR_UNSUPPORTED,
+                "mpa_sparse_decode: the contiguous-centroid list needs the bf16 tensor-core path");
     const int S = ffma_splits(L, n_split);
     float* pml = part;
     float* pacc = part + (size_t)L * S * group * 2;

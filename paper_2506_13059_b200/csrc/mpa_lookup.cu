@@ -578,7 +578,7 @@ using namespace mpa;
 // serving kernels (mpa_select.cu)
 int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* lv, const int32_t* cand,
                          const int32_t* n_cand, int cand_cap, double* logits, double* chunk_stats, double* e_local,
-                         int n_chunks, int n_max, cudaStream_t st);
+                         int n_chunks, int n_max, float* rej_w, int rej_cap, cudaStream_t st);
 size_t mpa_select_v2_smem(int n_max);
 int mpa_launch_select_v2(const double* logits, const double* e_local, int group, const int32_t* cand,
                          const int32_t* n_cand, int cand_cap, const int32_t* lv_size, int lv_cap,
@@ -608,7 +608,8 @@ static int g_logits_tiled = -1;
 
 extern "C" int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group, int d, const mpa_level* lv,
                                    const int32_t* cand, const int32_t* n_cand, int cand_cap, double* logits,
-                                   double* chunk_stats, double* e_local, int n_max, void* stream) {
+                                   double* chunk_stats, double* e_local, int n_max, float* rej_w, int rej_cap,
+                                   void* stream) {
     MPA_REQUIRE(q_lk && lv && logits && lv->kc && lv->count, MPA_ERR_ARG, "mpa_centroid_logits: null argument");
     MPA_REQUIRE(!cand || n_cand, MPA_ERR_ARG, "mpa_centroid_logits: cand without n_cand");
     MPA_REQUIRE(cand ? cand_cap >= 1 : cand_cap >= lv->cap, MPA_ERR_ARG, "mpa_centroid_logits: cand_cap %d too small",
@@ -625,7 +626,8 @@ extern "C" int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group
     }
     if (g_logits_tiled && (d == 64 || d == 128) && lv->dtype == MPA_BF16 && !lookup_v1())
         return mpa_launch_logits_v2(q_lk, group, d, lv, cand, n_cand, cand_cap, logits, chunk_stats, e_local,
-                                    ceil_div(cap, kChunk), n_max > 0 && n_max < cap ? n_max : cap, st);
+                                    ceil_div(cap, kChunk), n_max > 0 && n_max < cap ? n_max : cap, rej_w, rej_cap, st);
+    MPA_REQUIRE(!rej_w, MPA_ERR_UNSUPPORTED, "mpa_centroid_logits: rej_w needs the bf16 TMA path");
     if (g_logits_tiled && (d == 64 || d == 128)) {
         const int nch = ceil_div(cap, kChunk);
         dim3 grid(nch, L);
@@ -704,9 +706,10 @@ extern "C" int mpa_select_worklist(const mpa_level* fine, const mpa_level* coars
                                    int n_kv_heads, int n_ledgers, int replacement, uint8_t* flag,
                                    int32_t* sel_tokens, int32_t* tok, int tok_cap, int32_t* rej, float* rej_w,
                                    int rej_cap, int32_t* stats, int n_max, void* stream) {
-    MPA_REQUIRE(fine && logits && budget && flag && sink_end && buffer_start && cache_len && tok && rej && rej_w &&
-                    stats,
+    MPA_REQUIRE(fine && logits && budget && flag && sink_end && buffer_start && cache_len && tok && rej_w && stats,
                 MPA_ERR_ARG, "mpa_select_worklist: null argument");
+    MPA_REQUIRE(rej || (!cand && !cflag), MPA_ERR_UNSUPPORTED,
+                "mpa_select_worklist: the contiguous-centroid list (rej == NULL) needs the flat level");
     MPA_REQUIRE(!cflag || (coarse && clogits), MPA_ERR_ARG, "mpa_select_worklist: coarse flags without level");
     MPA_REQUIRE(cand ? n_cand != nullptr : cand_cap >= fine->cap, MPA_ERR_ARG,
                 "mpa_select_worklist: candidate capacity");
@@ -717,6 +720,8 @@ extern "C" int mpa_select_worklist(const mpa_level* fine, const mpa_level* coars
     const size_t smem = (size_t)sort_width(n_max) * 16 + (size_t)n_max * 4;
     const int nch = ceil_div(cand_cap, kChunk);
     cudaStream_t st = (cudaStream_t)stream;
+    MPA_REQUIRE(rej || (!lookup_v1() && mpa_select_v2_smem(n_max) <= 200 * 1024), MPA_ERR_UNSUPPORTED,
+                "mpa_select_worklist: contiguous-centroid list needs the v2 kernel");
     if (!lookup_v1() && mpa_select_v2_smem(n_max) <= 200 * 1024)
         return mpa_launch_select_worklist_v2(fine, coarse, group, logits, e_local, cand, n_cand, cand_cap,
                                              chunk_stats, nch, cflag, clogits, budget, sink_end, buffer_start,

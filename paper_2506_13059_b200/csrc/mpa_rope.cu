@@ -109,13 +109,13 @@ __global__ void rotate_queries_kernel(const float* __restrict__ q, int n_qh, int
     for (int i = threadIdx.x; i < d / 2; i += blockDim.x) {
         const double x = (double)q[base + 2 * i], y = (double)q[base + 2 * i + 1];
         double sn, cs;
-        sincos(p * inv_freq[i], &sn, &cs);
-        if (q_rot) {
+        if (q_rot) {  // either view may be skipped (the step graph computes them on two branches)
+            sincos(p * inv_freq[i], &sn, &cs);
             q_rot[base + 2 * i] = (float)(__dsub_rn(__dmul_rn(x, cs), __dmul_rn(y, sn)) * (double)scale);
             q_rot[base + 2 * i + 1] = (float)(__dadd_rn(__dmul_rn(x, sn), __dmul_rn(y, cs)) * (double)scale);
         }
-        sincos((double)delta * inv_freq[i], &sn, &cs);
         if (q_lk) {
+            sincos((double)delta * inv_freq[i], &sn, &cs);
             q_lk[base + 2 * i] = __dsub_rn(__dmul_rn(x, cs), __dmul_rn(y, sn));
             q_lk[base + 2 * i + 1] = __dadd_rn(__dmul_rn(x, sn), __dmul_rn(y, cs));
         }
@@ -178,7 +178,7 @@ extern "C" int mpa_kv_append(const mpa_cache* c, const float* k_src, const float
 
 extern "C" int mpa_rotate_queries(const float* q, int n_seq, int n_qh, int d, const int32_t* qpos, int delta,
                                   const double* inv_freq, float scale, float* q_rot, double* q_lk, void* stream) {
-    MPA_REQUIRE(q && qpos && inv_freq, MPA_ERR_ARG, "mpa_rotate_queries: null argument");
+    MPA_REQUIRE(q && qpos && inv_freq && (q_rot || q_lk), MPA_ERR_ARG, "mpa_rotate_queries: null argument");
     MPA_REQUIRE(d >= 2 && d % 2 == 0, MPA_ERR_ARG, "mpa_rotate_queries: bad head_dim %d", d);
     if (n_seq <= 0 || n_qh <= 0) return 0;
     rotate_queries_kernel<<<dim3(n_qh, n_seq), 64, 0, (cudaStream_t)stream>>>(q, n_qh, d, qpos, delta, inv_freq,

@@ -252,6 +252,13 @@ logits_block_kernel(const double* __restrict__ q_lk, const __nv_bfloat16* __rest
 __device__ __forceinline__ double bf16hi_to_f64(unsigned fbits) {  // fbits: bf16 in the high half
     return __hiloint2double((int)((((int)fbits >> 3) & 0x8FFFE000) + 0x38000000), 0);
 }
+// the same without the exponent re-bias: exactly x * 2^-896 (a normal fp64 for every bf16, zero
+// included), so q . x accumulates the exact bits of q . x scaled by 2^-896 and one exact
+// multiply by 2^896 at the end restores them -- one integer op less per element
+__device__ __forceinline__ double bf16hi_to_f64_s896(unsigned fbits) {
+    return __hiloint2double((int)(((int)fbits >> 3) & 0x8FFFE000), 0);
+}
+constexpr double kUnscale896 = 0x1p896;
 
 template <int G>
 __global__ void __launch_bounds__(kLgThreads)
@@ -259,7 +266,8 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
                   const double* __restrict__ q_lk, int kcap, const int32_t* __restrict__ count,
                   const int32_t* __restrict__ lv_size, const int32_t* __restrict__ cand,
                   const int32_t* __restrict__ n_cand, int cand_cap, double* __restrict__ logits,
-                  double* __restrict__ cstats, double* __restrict__ e_local, int n_chunks) {
+                  double* __restrict__ cstats, double* __restrict__ e_local, int n_chunks,
+                  float* __restrict__ rej_w, int rej_cap) {
     constexpr int D = 128, QD = 32, QRow = QD + 2;  // q slot: 32 dims (+16 B pad) per (head, quarter)
     extern __shared__ __align__(1024) unsigned char sm_raw[];
     unsigned char* tile = sm_raw + ((1024 - (smem_u32(sm_raw) & 1023)) & 1023);  // [2 halves][128][128 B]
@@ -348,7 +356,7 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 const unsigned wd = (&raw[r].x)[e >> 1];
-                const double x = bf16hi_to_f64((e & 1) ? (wd & 0xffff0000u) : (wd << 16));
+                const double x = bf16hi_to_f64_s896((e & 1) ? (wd & 0xffff0000u) : (wd << 16));
 #pragma unroll
                 for (int g = 0; g < G; ++g) acc[r][g] = fma(qv[g], x, acc[r][g]);
             }
@@ -385,7 +393,7 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
         for (int j = 0; j < GH; ++j) {
             const int g = (hi1 ? GH : 0) + j;
             if (g < G) {
-                const double v = a1[rr][j] / sq;
+                const double v = (a1[rr][j] * kUnscale896) / sq;
                 slg[g * kLgChunk + r] = v;
                 if (r < nv) logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
             }
@@ -396,7 +404,20 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
     const int i = tid;
     const bool valid = i < nv;
     const int id = valid ? (cand ? cand[(size_t)l * cand_cap + i0 + i] : i0 + i) : 0;
-    const double nsz = valid ? (double)lv_size[(size_t)l * kcap + id] : 0.0;
+    const int isz = valid ? lv_size[(size_t)l * kcap + id] : 0;
+    const double nsz = (double)isz;
+    if (rej_w && valid) {
+        // replacement weights of every candidate, indexed by candidate (logit + ln N, the value
+        // worklist_v2 would write for a rejected one); the selection masks the selected to -inf
+        constexpr int GP = G <= 4 ? 4 : 8;
+        const double lnN = (double)logf((float)isz);
+        float wv[GP];
+#pragma unroll
+        for (int g = 0; g < GP; ++g) wv[g] = g < G ? (float)(slg[(g < G ? g : 0) * kLgChunk + i] + lnN) : 0.f;
+        float4* dst = reinterpret_cast<float4*>(rej_w + ((size_t)l * rej_cap + i0 + i) * GP);
+#pragma unroll
+        for (int v = 0; v < GP / 4; ++v) dst[v] = make_float4(wv[4 * v], wv[4 * v + 1], wv[4 * v + 2], wv[4 * v + 3]);
+    }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         const double m = warp_max(valid ? slg[g * kLgChunk + i] : -INFINITY);
@@ -423,6 +444,240 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
         for (int ww = 0; ww < kLgThreads / 32; ++ww) Z += red[ww][tid];
         cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2] = s_m[tid];
         cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2 + 1] = Z;
+    }
+}
+
+// ---- persistent TMA variant (bf16, D = 128, the serving default): 3 CTAs / SM walk the
+// (ledger, chunk) items with a 2-stage ring, so the next item's rows and q slots are in flight
+// (TMA, one mbarrier per stage) while the current item computes; per-item math and outputs are
+// those of logits_tma_kernel.  The chunk's logits for the epilogue reuse the consumed tile.
+template <int G>
+struct LgPGeom {  // [tile 0][tile 1][q slots 0][q slots 1]; 3 CTAs fit in an SM
+    static constexpr int kTileB = 2 * kLgChunk * 128;  // two 64-column halves, 1024-aligned
+    static constexpr int kQB = G * 4 * 34 * 8;         // padded q slots
+    static constexpr size_t smem() { return 1024 + 2 * (size_t)(kTileB + kQB); }
+};
+
+template <int G>
+__global__ void __launch_bounds__(kLgThreads, 3)
+logits_persist_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_constant__ CUtensorMap tm_row,
+                      const double* __restrict__ q_lk, int kcap, const int32_t* __restrict__ count,
+                      const int32_t* __restrict__ lv_size, const int32_t* __restrict__ cand,
+                      const int32_t* __restrict__ n_cand, int cand_cap, double* __restrict__ logits,
+                      double* __restrict__ cstats, double* __restrict__ e_local, int n_chunks,
+                      float* __restrict__ rej_w, int rej_cap, int item_chunks, int L) {
+    using Geo = LgPGeom<G>;
+    constexpr int D = 128, QD = 32, QRow = QD + 2;
+    extern __shared__ __align__(1024) unsigned char sm_raw[];
+    unsigned char* base = sm_raw + ((1024 - (smem_u32(sm_raw) & 1023)) & 1023);
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ double red[kLgThreads / 32][G];
+    __shared__ double s_m[G];
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    const int n_items = L * item_chunks;
+    if (tid == 0) {
+        mbar_init(smem_u32(&bar[0]), 1);
+        mbar_init(smem_u32(&bar[1]), 1);
+        fence_mbar_init();
+        prefetch_tmap(&tm_tile);
+        prefetch_tmap(&tm_row);
+    }
+    __syncthreads();
+    auto live = [&](int l) { return cand ? __ldg(n_cand + l) : __ldg(count + l); };
+    // warp 0: loads of item `it` into stage s (nothing for a chunk past the ledger's candidates)
+    auto issue = [&](int it, int s) {
+        const int l = it / item_chunks, i0 = (it - l * item_chunks) * kLgChunk;
+        const int n = live(l);
+        if (i0 >= n) return;
+        const int nv = min(kLgChunk, n - i0);
+        unsigned char* tile = base + s * Geo::kTileB;
+        double* qs = reinterpret_cast<double*>(base + 2 * Geo::kTileB + s * Geo::kQB);
+        const unsigned b = smem_u32(&bar[s]);
+        fence_proxy_async_smem();  // the stage's previous generic reads before the async writes
+        if (lane == 0) {
+            mbar_expect_tx(b, G * 4 * QD * 8 + Geo::kTileB);
+            for (int j = 0; j < G * 4; ++j)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                        smem_u32(qs + j * QRow)),
+                    "l"(q_lk + ((size_t)l * G + j / 4) * D + (j % 4) * QD), "r"(QD * 8), "r"(b)
+                    : "memory");
+        }
+        if (!cand) {
+            if (lane == 0) {
+                tma_load_2d(smem_u32(tile), &tm_tile, 0, l * kcap + i0, b);
+                tma_load_2d(smem_u32(tile + kLgChunk * 128), &tm_tile, 64, l * kcap + i0, b);
+            }
+        } else {
+            int id[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int rr = 4 * lane + r;
+                id[r] = l * kcap + __ldg(cand + (size_t)l * cand_cap + i0 + (rr < nv ? rr : 0));
+            }
+            __syncwarp();
+            for (int h = 0; h < 2; ++h)
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_u32(tile + h * kLgChunk * 128 + lane * 512)),
+                    "l"(reinterpret_cast<uint64_t>(&tm_row)), "r"(h * 64), "r"(id[0]), "r"(id[1]), "r"(id[2]),
+                    "r"(id[3]), "r"(b)
+                    : "memory");
+        }
+    };
+
+    unsigned phase = 0u;  // bit s: parity of stage s's next completion
+    int it = blockIdx.x;
+    if (it < n_items && w == 0) issue(it, 0);
+#pragma unroll 1
+    for (int k = 0; it < n_items; ++k, it += gridDim.x) {
+        const int s = k & 1;
+        if (it + (int)gridDim.x < n_items && w == 0) issue(it + gridDim.x, s ^ 1);
+        const int l = it / item_chunks, chunk = it - l * item_chunks;
+        const int n = live(l), i0 = chunk * kLgChunk;
+        if (i0 >= n) {
+            if (cstats && chunk < n_chunks && tid < G) {
+                cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2] = -INFINITY;
+                cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2 + 1] = 0.0;
+            }
+            continue;
+        }
+        const int nv = min(kLgChunk, n - i0);
+        // epilogue inputs, loaded before the wait
+        const bool valid = tid < nv;
+        const int id = valid ? (cand ? __ldg(cand + (size_t)l * cand_cap + i0 + tid) : i0 + tid) : 0;
+        const int isz = valid && cstats ? __ldg(lv_size + (size_t)l * kcap + id) : 0;
+        unsigned char* tile = base + s * Geo::kTileB;
+        const double* qs = reinterpret_cast<const double*>(base + 2 * Geo::kTileB + s * Geo::kQB);
+        mbar_wait(smem_u32(&bar[s]), (phase >> s) & 1u);
+        phase ^= 1u << s;
+
+        const int qt = tid & 3, rg = tid >> 2;
+        const double* qq = qs + qt * QRow;
+        double acc[4][G];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int g = 0; g < G; ++g) acc[r][g] = 0.0;
+        uint4 raw[4];
+        auto load_raw = [&](int cc, uint4 (&dst)[4]) {
+            const int c = (cc + 2 * (qt >> 1)) & 3;
+            const int ch = (qt & 1) * 4 + c;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int row = rg + 32 * r;
+                dst[r] = *reinterpret_cast<const uint4*>(tile + (qt >> 1) * kLgChunk * 128 + row * 128 +
+                                                         ((ch ^ (row & 7)) << 4));
+            }
+        };
+        load_raw(0, raw);
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+            const int c = (cc + 2 * (qt >> 1)) & 3;
+            uint4 nxt[4];
+            if (cc < 3) load_raw(cc + 1, nxt);  // next chunk's rows in flight during this one's math
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                double qv[G];
+#pragma unroll
+                for (int g = 0; g < G; ++g) qv[g] = qq[g * 4 * QRow + c * 8 + e];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const unsigned wd = (&raw[r].x)[e >> 1];
+                    const double x = bf16hi_to_f64_s896((e & 1) ? (wd & 0xffff0000u) : (wd << 16));
+#pragma unroll
+                    for (int g = 0; g < G; ++g) acc[r][g] = fma(qv[g], x, acc[r][g]);
+                }
+            }
+            if (cc < 3)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) raw[r] = nxt[r];
+        }
+        // transpose-reduce over the 4 quarter lanes (xor 2 splits rows, xor 1 splits heads)
+        const bool hi2 = qt & 2, hi1 = qt & 1;
+        constexpr int GH = (G + 1) / 2;
+        double a2[2][G];
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const double send = hi2 ? acc[rr][g] : acc[rr + 2][g];
+                const double keep = hi2 ? acc[rr + 2][g] : acc[rr][g];
+                a2[rr][g] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+            }
+        double a1[2][GH];
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+            for (int j = 0; j < GH; ++j) {
+                const int ghi = GH + j;
+                const double lo = a2[rr][j], hv = ghi < G ? a2[rr][ghi < G ? ghi : 0] : 0.0;
+                const double send = hi1 ? lo : hv;
+                const double keep = hi1 ? hv : lo;
+                a1[rr][j] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+            }
+        __syncthreads();  // every read of the tile is done: the chunk's logits reuse its space
+        double* slg = reinterpret_cast<double*>(tile);  // [G][128]
+        const double sq = sqrt((double)D);
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int r = rg + 32 * ((hi2 ? 2 : 0) + rr);
+#pragma unroll
+            for (int j = 0; j < GH; ++j) {
+                const int g = (hi1 ? GH : 0) + j;
+                if (g < G) {
+                    const double v = (a1[rr][j] * kUnscale896) / sq;
+                    slg[g * kLgChunk + r] = v;
+                    if (r < nv) logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
+                }
+            }
+        }
+        if (cstats) {
+            __syncthreads();
+            const int i = tid;
+            const double nsz = (double)isz;
+            if (rej_w && valid) {
+                constexpr int GP = G <= 4 ? 4 : 8;
+                const double lnN = (double)logf((float)isz);
+                float wv[GP];
+#pragma unroll
+                for (int g = 0; g < GP; ++g) wv[g] = g < G ? (float)(slg[(g < G ? g : 0) * kLgChunk + i] + lnN) : 0.f;
+                float4* dst = reinterpret_cast<float4*>(rej_w + ((size_t)l * rej_cap + i0 + i) * GP);
+#pragma unroll
+                for (int v = 0; v < GP / 4; ++v)
+                    dst[v] = make_float4(wv[4 * v], wv[4 * v + 1], wv[4 * v + 2], wv[4 * v + 3]);
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const double m = warp_max(valid ? slg[g * kLgChunk + i] : -INFINITY);
+                if (lane == 0) red[w][g] = m;
+            }
+            __syncthreads();
+            if (tid < G) {
+                double M = -INFINITY;
+                for (int ww = 0; ww < kLgThreads / 32; ++ww) M = fmax(M, red[ww][tid]);
+                s_m[tid] = M;
+            }
+            __syncthreads();
+            double z[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const double e = valid ? exp(slg[g * kLgChunk + i] - s_m[g]) : 0.0;
+                if (valid && e_local) e_local[((size_t)l * G + g) * cand_cap + i0 + i] = e;
+                z[g] = warp_sum(e * nsz);
+            }
+            if (lane == 0)
+#pragma unroll
+                for (int g = 0; g < G; ++g) red[w][g] = z[g];
+            __syncthreads();
+            if (tid < G) {
+                double Z = 0.0;
+                for (int ww = 0; ww < kLgThreads / 32; ++ww) Z += red[ww][tid];
+                cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2] = s_m[tid];
+                cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2 + 1] = Z;
+            }
+        }
+        __syncthreads();  // end of item: the stage (tile + slg) may be refilled
     }
 }
 
@@ -825,8 +1080,12 @@ __device__ void worklist_v2(int l, int L, int n, const double* __restrict__ logi
             sel_t[spos] = tpos;
             ++spos;
             tpos += sz;
+            if (replacement && !rej) {  // contiguous-centroid list: mask the selected candidate
+#pragma unroll
+                for (int g = 0; g < G; ++g) rej_w[((size_t)l * rej_cap + i) * GP + g] = -INFINITY;
+            }
         } else if (replacement) {
-            if (rpos < rej_cap) {
+            if (rej && rpos < rej_cap) {
                 const int id = cand ? __ldg(cand + (size_t)l * cand_cap + i) : i;
                 rej[(size_t)l * rej_cap + rpos] = id;
                 const double lnN = (double)logf((float)sz);
@@ -1048,7 +1307,7 @@ static int encode_bf16_rows(CUtensorMap* out, const void* base, long long rows, 
 
 int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* lv, const int32_t* cand,
                          const int32_t* n_cand, int cand_cap, double* logits, double* chunk_stats, double* e_local,
-                         int n_chunks, int n_max, cudaStream_t st) {
+                         int n_chunks, int n_max, float* rej_w, int rej_cap, cudaStream_t st) {
     const int L = lv->n_ledgers;
     // items: ledgers x the chunks any ledger can use (n_max bounds the live candidates); chunk
     // stats rows past them are written -inf once per ledger by the last items
@@ -1078,6 +1337,28 @@ int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* 
                                              item_chunks, L);                                                      \
     }
     if (grid <= 0) return 0;
+    MPA_REQUIRE(!rej_w || (d == 128 && !persist && !cand && chunk_stats && rej_cap >= lv->cap), MPA_ERR_UNSUPPORTED,
+                "mpa_centroid_logits: per-candidate replacement weights need the flat d = 128 TMA path");
+    static int oneshot = -1;  // MPA_LOGITS_TMA_PERSIST=1: the persistent TMA ring (measured slower)
+    if (oneshot < 0) {
+        const char* e = getenv("MPA_LOGITS_TMA_PERSIST");
+        oneshot = (e && e[0] == '1') ? 0 : 1;
+    }
+    if (d == 128 && !persist && !oneshot) {
+        CUtensorMap tt, tr;
+        if (int rc = encode_bf16_rows(&tt, lv->kc, (long long)L * lv->cap, 128, kLgChunk)) return rc;
+        if (int rc = encode_bf16_rows(&tr, lv->kc, (long long)L * lv->cap, 128, 1)) return rc;
+        MPA_DISPATCH_G(group, {
+            auto kern = logits_persist_kernel<kG>;
+            const size_t smem = LgPGeom<kG>::smem();
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            const int pgrid = items < 3 * sms ? items : 3 * sms;
+            kern<<<pgrid, kLgThreads, smem, st>>>(tt, tr, q_lk, lv->cap, lv->count, lv->size, cand, n_cand, cand_cap,
+                                                  logits, chunk_stats, e_local, n_chunks, rej_w, rej_cap,
+                                                  item_chunks, L);
+        });
+        return check_launch("mpa_centroid_logits(tma persistent)");
+    }
     if (d == 128 && !persist) {
         CUtensorMap tt, tr;
         if (int rc = encode_bf16_rows(&tt, lv->kc, (long long)L * lv->cap, 128, kLgChunk)) return rc;
@@ -1088,7 +1369,7 @@ int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* 
             const size_t smem = 1024 + 2 * kLgChunk * 128 + sizeof(double) * (kG * 4 * 34 + kG * kLgChunk);
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             kern<<<g2, kLgThreads, smem, st>>>(tt, tr, q_lk, lv->cap, lv->count, lv->size, cand, n_cand, cand_cap,
-                                               logits, chunk_stats, e_local, n_chunks);
+                                               logits, chunk_stats, e_local, n_chunks, rej_w, rej_cap);
         });
         return check_launch("mpa_centroid_logits(tma)");
     }
@@ -1203,7 +1484,7 @@ extern "C" int mpa_select_worklist_sharded(const mpa_level* fine, int group, con
                                            const void* cross, void* prefix, int32_t* prefix_n, int prefix_cap,
                                            const int32_t* gid_off, void* stream) {
     MPA_REQUIRE(fine && logits && chunk_stats && budget && flag && sink_end && buffer_start && cache_len && tok &&
-                    rej && rej_w && stats && mz && gid_off,
+                    rej_w && stats && mz && gid_off,
                 MPA_ERR_ARG, "mpa_select_worklist_sharded: null argument");
     MPA_REQUIRE((cross != nullptr) != (prefix != nullptr), MPA_ERR_ARG,
                 "mpa_select_worklist_sharded: exactly one of cross (final pass) / prefix (local pass)");

@@ -96,6 +96,11 @@ class DecodeEngine:
         self.cache_struct = MpaCache(ptr(self.k_rot), ptr(self.k_raw), ptr(self.v), dtype_code(dtype), L, tcap, d)
         self.last_split = 1
         self.cursor = 0
+        # contiguous-centroid work list (flat bf16 serving path): the logits kernel writes every
+        # centroid's replacement weight, the selection masks the selected ones, and the fused kernel
+        # streams the value centroids in order with 16-row TMA boxes (include/mpattn.h)
+        self.rej_dense = (not hier and mode == "multipole" and dtype == torch.bfloat16 and d == 128 and G <= 8
+                          and os.environ.get("MPA_REJ_LIST") != "1")
         self.use_graphs = (os.environ.get("MPA_NO_GRAPH") != "1") if use_graphs is None else use_graphs
         self._graph = None
         self.last_lloyd_rounds = 0
@@ -156,10 +161,12 @@ class DecodeEngine:
             self.ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
         return self.ws
 
-    def rotate(self, q: torch.Tensor) -> None:
+    def rotate(self, q: torch.Tensor, exact: bool = True, lookup: bool = True) -> None:
+        """Exact view q_rot (at cache_len) and / or lookup view q_lk (at the window offset)."""
         q = q.float().contiguous()
         call("mpa_rotate_queries", ptr(q), self.n_seq, self.Hq, self.d, ptr(self.cache_len_d), self.cfg.window_offset,
-             ptr(self.inv_freq), 1.0 / math.sqrt(self.d), ptr(self.q_rot), ptr(self.q_lk), stream_ptr())
+             ptr(self.inv_freq), 1.0 / math.sqrt(self.d), ptr(self.q_rot) if exact else None,
+             ptr(self.q_lk) if lookup else None, stream_ptr())
 
     def _cluster_bounds(self):
         """Per-ledger cluster-count bounds passed to the lookup kernels (grid / smem sizing).
@@ -186,13 +193,16 @@ class DecodeEngine:
         if self.cfg.hierarchy is None:
             if int(self.led.n_fine.min()) == 0:
                 raise ConfigError("ledger has no clusters")
+            dense = self.rej_dense and el is not None
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, None, None, self.kcap,
-                 ptr(self.logits), ptr(cs), ptr(el), self._bound_fine, st)
+                 ptr(self.logits), ptr(cs), ptr(el), self._bound_fine, ptr(self.rej_w) if dense else None,
+                 self.rej_cap, st)
             call("mpa_select_worklist", fine, None, G, ptr(self.logits), ptr(el), None, None, self.kcap, ptr(cs),
                  None, None,
                  ptr(self.budget), ptr(self.sink_end_d), ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv,
-                 L, replacement, ptr(self.flag), ptr(self.sel_tokens), ptr(self.tok), self.tok_cap, ptr(self.rej),
-                 ptr(self.rej_w), self.rej_cap, ptr(self.stats), self._bound_fine, st)
+                 L, replacement, ptr(self.flag), ptr(self.sel_tokens), ptr(self.tok), self.tok_cap,
+                 None if dense else ptr(self.rej), ptr(self.rej_w), self.rej_cap, ptr(self.stats), self._bound_fine,
+                 st)
         else:
             if int(self.led.n_coarse.min()) == 0:
                 raise ConfigError("ledger has no coarse clusters")
@@ -200,13 +210,13 @@ class DecodeEngine:
             ccs = self.ccstats if tiled else None
             cel = self.celocal if el is not None else None
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, coarse, None, None, self.ccap,
-                 ptr(self.clogits), ptr(ccs), ptr(cel), self._bound_coarse, st)
+                 ptr(self.clogits), ptr(ccs), ptr(cel), self._bound_coarse, None, 0, st)
             call("mpa_select", ptr(self.clogits), G, None, ptr(self.led.ccount), self.ccap, ptr(self.led.csize),
                  self.ccap, None, None, None, None, 0, ptr(self.cbudget), L, ptr(self.cflag),
                  ptr(self.csel_tokens), ptr(ccs), ptr(cel), self._bound_coarse, st)
             call("mpa_hier_candidates", coarse, ptr(self.cflag), L, ptr(self.cand), ptr(self.n_cand), self.kcap, st)
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, ptr(self.cand), ptr(self.n_cand),
-                 self.kcap, ptr(self.logits), ptr(cs), ptr(el), self._bound_fine, st)
+                 self.kcap, ptr(self.logits), ptr(cs), ptr(el), self._bound_fine, None, 0, st)
             call("mpa_select_worklist", fine, coarse, G, ptr(self.logits), ptr(el), ptr(self.cand), ptr(self.n_cand),
                  self.kcap, ptr(cs), ptr(self.cflag), ptr(self.clogits), ptr(self.budget), ptr(self.sink_end_d),
                  ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv, L, replacement, ptr(self.flag),
@@ -219,12 +229,21 @@ class DecodeEngine:
         S = int(n_split or 0)
         ws = self._workspace(S)
         st = stream_ptr()
-        rej = None if self.mode == "flat-no-replacement" else self.rej
+        rej, rej_w, n_rej = self._centroid_terms()
         ckc = self.led.cvc if self.led.hierarchy else None
         call("mpa_sparse_decode", self.cache_struct, ptr(self.q_rot), self.Hkv, self.G, ptr(self.tok),
-             ptr(self.stats[0]), self.tok_cap, ptr(rej), ptr(self.rej_w), ptr(self.stats[1]), self.rej_cap,
+             ptr(self.stats[0]), self.tok_cap, ptr(rej), ptr(rej_w), ptr(n_rej), self.rej_cap,
              ptr(self.led.vc), self.kcap, ptr(ckc), self.ccap, S, ptr(ws), ws.numel(), ptr(self.out), st)
         return self.out
+
+    def _centroid_terms(self):
+        """(rej, rej_w, n_rej) of mpa_sparse_decode: none, the rejected list, or every fine centroid
+        in order (contiguous-centroid list, selected ones weighted -inf)."""
+        if self.mode == "flat-no-replacement":
+            return None, None, None
+        if self.rej_dense and not self.led.lookup_f64:
+            return None, self.rej_w, self.led.count
+        return self.rej, self.rej_w, self.stats[1]
 
     def attend(self, q: torch.Tensor, n_split: int | None = None) -> torch.Tensor:
         """One multipole decode step over the current cache; q fp32 [n_seq, Hq, d] (device)."""
@@ -283,10 +302,26 @@ class DecodeEngine:
             self.attend(self._gq)  # warm-up outside the capture (function attributes, tensor maps)
         torch.cuda.current_stream().wait_stream(side)
         g = torch.cuda.CUDAGraph()
+        exact_br, append_br = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         with torch.cuda.graph(g):
-            self.attend(self._gq)
-            call("mpa_kv_append", self.cache_struct, ptr(self._gk), ptr(self._gv), self.Hkv, 1, ptr(self.cache_len_d),
-                 ptr(self.ntok_dense_d), ptr(self.inv_freq), ptr(self.append_ticket), stream_ptr())
+            # critical path: q_lk -> logits -> select + work lists -> fused decode.  Off it, on
+            # graph branches: the exact-view rotation (needed only by the fused kernel) and the KV
+            # append (writes row cache_len, which this step's lists never read; it advances the
+            # length counters after the selection has read them)
+            main = torch.cuda.current_stream()
+            exact_br.wait_stream(main)
+            with torch.cuda.stream(exact_br):
+                self.rotate(self._gq, exact=True, lookup=False)
+            self.rotate(self._gq, exact=False, lookup=True)
+            self.lookup()
+            append_br.wait_stream(main)
+            with torch.cuda.stream(append_br):
+                call("mpa_kv_append", self.cache_struct, ptr(self._gk), ptr(self._gv), self.Hkv, 1,
+                     ptr(self.cache_len_d), ptr(self.ntok_dense_d), ptr(self.inv_freq), ptr(self.append_ticket),
+                     stream_ptr())
+            main.wait_stream(exact_br)
+            self.fused()
+            main.wait_stream(append_br)
         self._graph = g
 
     def step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor) -> torch.Tensor:

@@ -120,8 +120,9 @@ class ShardedDecodeEngine:
         st = stream_ptr()
         fine = e.led.fine_level()
         el = e.elocal if not e.led.lookup_f64 else None
+        dense = e.rej_dense and el is not None
         call("mpa_centroid_logits", ptr(e.q_lk), e.Hkv, e.G, e.d, fine, None, None, e.kcap, ptr(e.logits),
-             ptr(e.cstats), ptr(el), int(e.led.n_fine.max()), st)
+             ptr(e.cstats), ptr(el), int(e.led.n_fine.max()), ptr(e.rej_w) if dense else None, e.rej_cap, st)
         call("mpa_head_norms", ptr(e.cstats), e.cstats.shape[1], ptr(e.led.count), e.L, e.G, ptr(self.mz_loc), st)
         return self.mz_loc
 
@@ -145,15 +146,17 @@ class ShardedDecodeEngine:
         st = stream_ptr()
         call("mpa_global_cut", ptr(prefix_all), ptr(prefix_n_all), self.world, e.L, self.prefix_cap, ptr(e.budget),
              ptr(self.cross), st)
+        rej = e._centroid_terms()[0] if e.mode != "flat-no-replacement" else e.rej
         sink, buf = self._layout()
         el = e.elocal if not e.led.lookup_f64 else None
         call("mpa_select_worklist_sharded", e.led.fine_level(), e.G, ptr(e.logits), ptr(el), ptr(e.cstats),
              ptr(e.budget), ptr(sink), ptr(buf), ptr(e.cache_len_d), e.Hkv, 1, ptr(e.flag), ptr(e.sel_tokens),
-             ptr(e.tok), e.tok_cap, ptr(e.rej), ptr(e.rej_w), e.rej_cap, ptr(e.stats), int(e.led.n_fine.max()),
+             ptr(e.tok), e.tok_cap, ptr(rej), ptr(e.rej_w), e.rej_cap, ptr(e.stats), int(e.led.n_fine.max()),
              ptr(self.mz), ptr(self.cross), None, None, self.prefix_cap, ptr(self.gid_off), st)
         ws = e._workspace(0)
+        rej, rej_w, n_rej = e._centroid_terms()
         call("mpa_sparse_decode_partials", e.cache_struct, ptr(e.q_rot), e.Hkv, e.G, ptr(e.tok), ptr(e.stats[0]),
-             e.tok_cap, ptr(e.rej), ptr(e.rej_w), ptr(e.stats[1]), e.rej_cap, ptr(e.led.vc), e.kcap, None, 0, 0,
+             e.tok_cap, ptr(rej), ptr(rej_w), ptr(n_rej), e.rej_cap, ptr(e.led.vc), e.kcap, None, 0, 0,
              ptr(ws), ws.numel(), ptr(self.part), st)
         return self.part
 
