@@ -93,7 +93,8 @@ int mpa_rotate_queries(const float* q, int n_seq, int n_qh, int d, const int32_t
  * n_max (0: cap) bounds the live candidates of every ledger (sizes the grid).
  * rej_w (optional; flat level, bf16, d = 128, with chunk_stats): [L, rej_cap, GP] fp32 replacement
  * weights of EVERY candidate, rej_w[l, i, g] = logit + ln(size) -- the contiguous-centroid work
- * list of mpa_select_worklist (rej == NULL) then masks the selected ones. */
+ * list of mpa_select_worklist (rej == NULL) then masks the selected ones; with rej_w the fp64
+ * logits output is optional (NULL: not written -- the selection reads e_local and chunk_stats). */
 int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group, int d,
                         const mpa_level* lv, const int32_t* cand, const int32_t* n_cand,
                         int cand_cap, double* logits, double* chunk_stats, double* e_local, int n_max,

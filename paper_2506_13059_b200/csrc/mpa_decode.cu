@@ -717,12 +717,14 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     };
 
     // ---- end of a ledger segment of this CTA (every warp calls it for every ledger of the CTA
-    // range, in order): warp partials -> CTA partial through an L2-resident per-CTA scratch; a
-    // ledger wholly inside the CTA range is finalised here, otherwise the CTA partial goes to
-    // slot (c + l) and the last of the ledger's CTAs (atomic ticket) merges them.
+    // range, in order): warp partials -> CTA partial through shared memory (each warp writes
+    // into the ring stage it is not using: `fs`, the one consumed last); a ledger wholly inside
+    // the CTA range is finalised here, otherwise the CTA partial goes to slot (c + l) and the
+    // last of the ledger's CTAs (atomic ticket) merges them.
     __shared__ int s_last;
-    float* wscr = part + ((size_t)(C + L) + (size_t)c * NW + w) * Geo::kPS;
-    auto seg_end = [&](int l) {
+    __shared__ unsigned s_poff[NW];
+    auto seg_end = [&](int l, int fs) {
+        float* wscr = reinterpret_cast<float*>(smem + w * Geo::kWarpB + fs * Geo::kStageB);
         float fA = sA, fB = sB;
 #pragma unroll
         for (int off = 4; off < 32; off <<= 1) {
@@ -758,17 +760,17 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
                 }
             }
         }
+        if (lane == 0) s_poff[w] = (unsigned)(w * Geo::kWarpB + fs * Geo::kStageB);
         __syncthreads();
         dbg_stamp(5);
         const bool whole = tp[l] >= g0 && tp[l + 1] <= g1;
-        const float* wp0 = part + ((size_t)(C + L) + (size_t)c * NW) * Geo::kPS;
         float* dst = part + (size_t)(c + l) * Geo::kPS;
         for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
             const int g = idx / D, k = idx - g * D;
             float mw[NW], M = -INFINITY;
 #pragma unroll
             for (int ww = 0; ww < NW; ++ww) {
-                mw[ww] = wp0[(size_t)ww * Geo::kPS + 2 * g];
+                mw[ww] = reinterpret_cast<const float*>(smem + s_poff[ww])[2 * g];
                 M = fmaxf(M, mw[ww]);
             }
             float S = 0.f, A = 0.f;
@@ -776,9 +778,10 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
 #pragma unroll
                 for (int ww = 0; ww < NW; ++ww) {
                     if (mw[ww] == -INFINITY) continue;
+                    const float* wp = reinterpret_cast<const float*>(smem + s_poff[ww]);
                     const float sc = exp2f(mw[ww] - M);
-                    S += sc * wp0[(size_t)ww * Geo::kPS + 2 * g + 1];
-                    A += sc * wp0[(size_t)ww * Geo::kPS + 2 * G + g * D + k];
+                    S += sc * wp[2 * g + 1];
+                    A += sc * wp[2 * G + g * D + k];
                 }
             }
             if (whole) {
@@ -899,14 +902,16 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     reset_state();
 #pragma unroll 1
     for (int i = 0; i < my_n; ++i) {
-        issue_next();
         const Meta m = meta_of(i, wc);
+        // stages (i, i+1) % NST are in flight; (i + NST - 1) % NST was consumed last and is free
+        // until issue_next() below refills it -- seg_end stages this warp's partial there
         while (m.l != cur_l) {
-            seg_end(cur_l);
+            seg_end(cur_l, (i + NST - 1) % NST);
             ++cur_l;
             reset_state();
             fresh = true;
         }
+        issue_next();
         if (fresh) {
             load_q(cur_l);
             fresh = false;
@@ -957,8 +962,8 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         }
     }
     dbg_stamp(3);
-    for (; cur_l <= ll; ++cur_l) {
-        seg_end(cur_l);
+    for (; cur_l <= ll; ++cur_l) {  // the ring is drained: any stage is free
+        seg_end(cur_l, 0);
         reset_state();
     }
     dbg_stamp(4);

@@ -610,7 +610,8 @@ extern "C" int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group
                                    const int32_t* cand, const int32_t* n_cand, int cand_cap, double* logits,
                                    double* chunk_stats, double* e_local, int n_max, float* rej_w, int rej_cap,
                                    void* stream) {
-    MPA_REQUIRE(q_lk && lv && logits && lv->kc && lv->count, MPA_ERR_ARG, "mpa_centroid_logits: null argument");
+    MPA_REQUIRE(q_lk && lv && lv->kc && lv->count, MPA_ERR_ARG, "mpa_centroid_logits: null argument");
+    MPA_REQUIRE(logits || rej_w, MPA_ERR_ARG, "mpa_centroid_logits: logits may be NULL only with rej_w");
     MPA_REQUIRE(!cand || n_cand, MPA_ERR_ARG, "mpa_centroid_logits: cand without n_cand");
     MPA_REQUIRE(cand ? cand_cap >= 1 : cand_cap >= lv->cap, MPA_ERR_ARG, "mpa_centroid_logits: cand_cap %d too small",
                 cand_cap);
@@ -706,7 +707,9 @@ extern "C" int mpa_select_worklist(const mpa_level* fine, const mpa_level* coars
                                    int n_kv_heads, int n_ledgers, int replacement, uint8_t* flag,
                                    int32_t* sel_tokens, int32_t* tok, int tok_cap, int32_t* rej, float* rej_w,
                                    int rej_cap, int32_t* stats, int n_max, void* stream) {
-    MPA_REQUIRE(fine && logits && budget && flag && sink_end && buffer_start && cache_len && tok && rej_w && stats,
+    MPA_REQUIRE(logits || (!rej && e_local && chunk_stats), MPA_ERR_ARG,
+                "mpa_select_worklist: logits may be NULL only for the contiguous-centroid list");
+    MPA_REQUIRE(fine && budget && flag && sink_end && buffer_start && cache_len && tok && rej_w && stats,
                 MPA_ERR_ARG, "mpa_select_worklist: null argument");
     MPA_REQUIRE(rej || (!cand && !cflag), MPA_ERR_UNSUPPORTED,
                 "mpa_select_worklist: the contiguous-centroid list (rej == NULL) needs the flat level");

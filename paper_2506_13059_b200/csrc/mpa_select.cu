@@ -395,7 +395,7 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
             if (g < G) {
                 const double v = (a1[rr][j] * kUnscale896) / sq;
                 slg[g * kLgChunk + r] = v;
-                if (r < nv) logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
+                if (logits && r < nv) logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
             }
         }
     }
@@ -628,7 +628,7 @@ logits_persist_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_
                 if (g < G) {
                     const double v = (a1[rr][j] * kUnscale896) / sq;
                     slg[g * kLgChunk + r] = v;
-                    if (r < nv) logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
+                    if (logits && r < nv) logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
                 }
             }
         }
@@ -832,8 +832,8 @@ __device__ void radix_cross(const unsigned long long* keys, const int* sizes, Id
     __syncthreads();
 }
 
-// smem per candidate: key (8) + size (4) + flag (1) + pad
-__host__ __device__ constexpr size_t sel_smem_bytes(int n_max) { return (size_t)n_max * 13 + 64; }
+// smem per candidate: key (8) + size (4) + member offset (4) + flag (1) + pad
+__host__ __device__ constexpr size_t sel_smem_bytes(int n_max) { return (size_t)n_max * 17 + 64; }
 
 template <int G>
 __device__ void select_v2_core(int l, const double* __restrict__ logits, const double* __restrict__ e_local,
@@ -842,7 +842,10 @@ __device__ void select_v2_core(int l, const double* __restrict__ logits, const d
                                const int32_t* __restrict__ esize, const uint8_t* __restrict__ eflag, int ne, int ecap,
                                long long B, const double* __restrict__ cstats, int n_chunks, unsigned long long* keys,
                                int* sizes, uint8_t* sflag, uint8_t* __restrict__ flag,
-                               int32_t* __restrict__ sel_tokens, const ShardCtl& sh = ShardCtl{}) {
+                               int32_t* __restrict__ sel_tokens, const ShardCtl& sh = ShardCtl{},
+                               const int32_t* __restrict__ moff = nullptr, int* offs = nullptr) {
+    // moff / offs (work-list builds): the candidates' member-CSR offsets, staged into smem here
+    // with the other per-candidate loads so the member copy makes one dependent load, not two
     const double* mz_ext = sh.mz;
     const Cross* ext_cross = sh.cross;
     PrefixEntry* prefix = sh.prefix;
@@ -863,12 +866,42 @@ __device__ void select_v2_core(int l, const double* __restrict__ logits, const d
     const int nchu = min(n_chunks, (n + 127) >> 7);  // chunks holding this ledger's candidates
     const int max_sc_chunks = 2048 / G;
 
+    // ---- 0. this thread's first kPF candidates: sizes and e_local loads issued together up
+    // front, so their latency overlaps the normaliser phases (thread-strided like every loop here)
+    constexpr int kPF = 5;
+    int szr[kPF], ofr[kPF];
+    double elr[kPF][G];
+#pragma unroll
+    for (int u = 0; u < kPF; ++u) {
+        const int i = threadIdx.x + u * blockDim.x;
+        szr[u] = ofr[u] = 0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) elr[u][g] = 0.0;
+        if (i < n) {
+            const int id = cand ? __ldg(cand + (size_t)l * cand_cap + i) : i;
+            szr[u] = __ldg(lv_size + (size_t)l * lv_cap + id);
+            if (offs) ofr[u] = __ldg(moff + (size_t)l * (lv_cap + 1) + id);
+            if (use_local)
+#pragma unroll
+                for (int g = 0; g < G; ++g) elr[u][g] = __ldcg(el + (size_t)g * cand_cap + i);
+        }
+    }
     // ---- 1. sizes, per-head max
     long long tot_local = 0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+#pragma unroll
+    for (int u = 0; u < kPF; ++u) {
+        const int i = threadIdx.x + u * blockDim.x;
+        if (i < n) {
+            sizes[i] = szr[u];
+            if (offs) offs[i] = ofr[u];
+            tot_local += szr[u];
+        }
+    }
+    for (int i = threadIdx.x + kPF * blockDim.x; i < n; i += blockDim.x) {
         const int id = cand ? __ldg(cand + (size_t)l * cand_cap + i) : i;
         const int sz = __ldg(lv_size + (size_t)l * lv_cap + id);
         sizes[i] = sz;
+        if (offs) offs[i] = __ldg(moff + (size_t)l * (lv_cap + 1) + id);
         tot_local += sz;
     }
     {
@@ -965,17 +998,23 @@ __device__ void select_v2_core(int l, const double* __restrict__ logits, const d
     double zz[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) zz[g] = s_z[g];
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    auto score_key = [&](int i, const double* elv) {
         double sc = 0.0;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            const double e = scaled ? el[(size_t)g * cand_cap + i] * csc[(i >> 7) * G + g]
+            const double e = scaled ? (elv ? elv[g] : el[(size_t)g * cand_cap + i]) * csc[(i >> 7) * G + g]
                                     : exp(lg[(size_t)g * cand_cap + i] - mx[g]);
             sc = g ? sc + e / zz[g] : e / zz[g];
         }
         sc = sc / (double)G;
         keys[i] = ~(unsigned long long)__double_as_longlong(sc);  // ascending key == descending score
+    };
+#pragma unroll
+    for (int u = 0; u < kPF; ++u) {
+        const int i = threadIdx.x + u * blockDim.x;
+        if (i < n) score_key(i, elr[u]);
     }
+    for (int i = threadIdx.x + kPF * blockDim.x; i < n; i += blockDim.x) score_key(i, nullptr);
     __syncthreads();
 
     dbg_lk(5);
@@ -1042,7 +1081,7 @@ template <int G>
 __device__ void worklist_v2(int l, int L, int n, const double* __restrict__ logits, const int32_t* __restrict__ cand,
                             int cand_cap, const uint8_t* sflag, const int* sizes, int* sel_list,
                             const int32_t* __restrict__ fmem_off, const int32_t* __restrict__ fmem, int fcap,
-                            int fmem_cap, const int32_t* __restrict__ csize, int ne, int ccap,
+                            int fmem_cap, const int* offs, const int32_t* __restrict__ csize, int ne, int ccap,
                             const uint8_t* __restrict__ cflag, const double* __restrict__ clogits,
                             const int32_t* __restrict__ sink_end, const int32_t* __restrict__ buffer_start,
                             const int32_t* __restrict__ cache_len, int n_kv_heads, int replacement,
@@ -1110,9 +1149,8 @@ __device__ void worklist_v2(int l, int L, int n, const double* __restrict__ logi
             else hi = mid - 1;
         }
         const int i = sel_c[lo];
-        const int id = cand ? __ldg(cand + (size_t)l * cand_cap + i) : i;
         const int slot = ns + nb + j;
-        if (slot < tok_cap) T[slot] = __ldg(fmem + (size_t)l * fmem_cap + __ldg(moff + id) + (j - sel_t[lo]));
+        if (slot < tok_cap) T[slot] = __ldg(fmem + (size_t)l * fmem_cap + offs[i] + (j - sel_t[lo]));
     }
     int tbase = ns + nb + (int)(tot >> 32), rbase = (int)((tot >> 16) & 0xffff);
     if (cflag && replacement) {
@@ -1165,14 +1203,16 @@ select_worklist_v2_kernel(const double* __restrict__ logits, const double* __res
     if (n > smem_n) __trap();  // the host sizes smem_n >= every ledger's candidate count
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem_raw);
     int* sizes = reinterpret_cast<int*>(keys + smem_n);
-    uint8_t* sflag = reinterpret_cast<uint8_t*>(sizes + smem_n);
+    int* offs = sizes + smem_n;
+    uint8_t* sflag = reinterpret_cast<uint8_t*>(offs + smem_n);
     const int ne = cflag ? ccount[l] : 0;
+    const bool lists = !(sh.prefix && !sh.cross);
     select_v2_core<G>(l, logits, e_local, cand, n, cand_cap, fsize, fcap, clogits, csize, cflag, ne, ccap, budget[l],
-                      cstats, n_chunks, keys, sizes, sflag, flag, sel_tokens, sh);
+                      cstats, n_chunks, keys, sizes, sflag, flag, sel_tokens, sh, fmem_off, lists ? offs : nullptr);
     dbg_lk(3);
     if (sh.prefix && !sh.cross) return;  // sharded local pass: only the candidate prefix is needed
     worklist_v2<G>(l, L, n, logits, cand, cand_cap, sflag, sizes, reinterpret_cast<int*>(keys), fmem_off, fmem, fcap,
-                   fmem_cap, csize, ne, ccap, cflag, clogits, sink_end, buffer_start, cache_len, n_kv_heads,
+                   fmem_cap, offs, csize, ne, ccap, cflag, clogits, sink_end, buffer_start, cache_len, n_kv_heads,
                    replacement, tok, tok_cap, rej, rej_w, rej_cap, stats);
     dbg_lk(4);
 }

@@ -103,6 +103,8 @@ class DecodeEngine:
                           and os.environ.get("MPA_REJ_LIST") != "1")
         self.use_graphs = (os.environ.get("MPA_NO_GRAPH") != "1") if use_graphs is None else use_graphs
         self._graph = None
+        self.time_fused = False  # bench: CUDA events around the fused kernel inside the step graph
+        self._fev = None
         self.last_lloyd_rounds = 0
         self.last_update: dict | None = None
 
@@ -194,10 +196,10 @@ class DecodeEngine:
             if int(self.led.n_fine.min()) == 0:
                 raise ConfigError("ledger has no clusters")
             dense = self.rej_dense and el is not None
+            lg = None if dense else ptr(self.logits)  # the contiguous-centroid list never reads them
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, None, None, self.kcap,
-                 ptr(self.logits), ptr(cs), ptr(el), self._bound_fine, ptr(self.rej_w) if dense else None,
-                 self.rej_cap, st)
-            call("mpa_select_worklist", fine, None, G, ptr(self.logits), ptr(el), None, None, self.kcap, ptr(cs),
+                 lg, ptr(cs), ptr(el), self._bound_fine, ptr(self.rej_w) if dense else None, self.rej_cap, st)
+            call("mpa_select_worklist", fine, None, G, lg, ptr(el), None, None, self.kcap, ptr(cs),
                  None, None,
                  ptr(self.budget), ptr(self.sink_end_d), ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv,
                  L, replacement, ptr(self.flag), ptr(self.sel_tokens), ptr(self.tok), self.tok_cap,
@@ -301,6 +303,8 @@ class DecodeEngine:
         with torch.cuda.stream(side):
             self.attend(self._gq)  # warm-up outside the capture (function attributes, tensor maps)
         torch.cuda.current_stream().wait_stream(side)
+        self._fev = ((torch.cuda.Event(enable_timing=True, external=True),
+                      torch.cuda.Event(enable_timing=True, external=True)) if self.time_fused else None)
         g = torch.cuda.CUDAGraph()
         exact_br, append_br = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         with torch.cuda.graph(g):
@@ -320,7 +324,11 @@ class DecodeEngine:
                      ptr(self.cache_len_d), ptr(self.ntok_dense_d), ptr(self.inv_freq), ptr(self.append_ticket),
                      stream_ptr())
             main.wait_stream(exact_br)
+            if self._fev:
+                self._fev[0].record()
             self.fused()
+            if self._fev:
+                self._fev[1].record()
             main.wait_stream(append_br)
         self._graph = g
 
@@ -328,6 +336,9 @@ class DecodeEngine:
         """Attend, append the step's token, then run the online update when a buffer holds 2L
         tokens (pipeline.py:124-191).  q [n_seq, Hq, d], k_new / v_new [n_seq, Hkv, d] (fp32).
         Between ledger changes the attend + append chain replays as one CUDA graph."""
+        return self._step(q, k_new, v_new, host=False)
+
+    def _step(self, q, k_new, v_new, host: bool) -> torch.Tensor:
         from . import clustering
 
         if self._graphable():
@@ -336,13 +347,20 @@ class DecodeEngine:
             self._cluster_bounds()  # recaptures only if the cluster counts outgrew the captured bounds
             if self._graph is None:
                 self._capture_step()
-            self._gq.copy_(q)
-            self._gk.copy_(k_new[:, :, None])
-            self._gv.copy_(v_new[:, :, None])
+            if host:  # host -> device straight into the graph's input buffers
+                self._gq.copy_(q, non_blocking=True)
+                self._gk.copy_(k_new[:, :, None], non_blocking=True)
+                self._gv.copy_(v_new[:, :, None], non_blocking=True)
+            else:  # (torch._foreach_copy_ measured 6 us slower than the three copies)
+                self._gq.copy_(q)
+                self._gk.copy_(k_new[:, :, None])
+                self._gv.copy_(v_new[:, :, None])
             self._graph.replay()
             self.cache_len += 1
             out = self.out
         else:
+            if host:
+                q, k_new, v_new = (x.to(self.device, non_blocking=True) for x in (q, k_new, v_new))
             out = self.attend(q)
             self.write_tokens(k_new[:, :, None], v_new[:, :, None])
         todo = self.needs_update()
@@ -361,12 +379,14 @@ class DecodeEngine:
                   out_host: torch.Tensor) -> torch.Tensor:
         """Public end-to-end step from HOST buffers (pinned for overlap): copies q / k / v in,
         runs `step`, copies the output back into out_host; all on the current stream."""
-        q = q_host.to(self.device, non_blocking=True)
-        k = k_host.to(self.device, non_blocking=True)
-        v = v_host.to(self.device, non_blocking=True)
-        out = self.step(q, k, v)
+        out = self._step(q_host, k_host, v_host, host=True)
         out_host.copy_(out, non_blocking=True)
         return out_host
+
+    def last_fused_ms(self) -> float | None:
+        """Device time of the fused kernel inside the last graph replay (time_fused = True;
+        call after synchronising)."""
+        return self._fev[0].elapsed_time(self._fev[1]) if self._fev else None
 
     def export_ledger(self, l: int) -> HostLedger:
         s = l // self.Hkv
