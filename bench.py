@@ -8,8 +8,9 @@ model shape, torch seed 0 + rank).  The ledger is built by the GPU clustering pa
 
 A step = one decode step of one attention layer for the whole batch: q rotation, centroid
 lookup + budgeted selection, fused sparse-exact + centroid-replacement attention with the
-split-KV merge, and the KV append of the step's token.  L2 is flushed (256 MB write) before
-every timed step; each step is timed with CUDA events on the engine stream.
+split-KV merge, and the KV append of the step's token.  L2 is flushed (256 MB write, then a
+256 MB read so no dirty flush lines are left to write back) before every timed step; each
+step is timed with CUDA events on the engine stream.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
 
@@ -374,13 +375,13 @@ def main():
     eng, Q, KN, VN, prefill_s = build_engine(args, rank, dev)
     gen = torch.Generator(device=dev).manual_seed(2000 + rank)
     total_steps = W + K
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flush = L2Flush(dev)
     stream = torch.cuda.current_stream()
 
     def timed(fn, n, *, start=0):
         evs = []
         for i in range(n):
-            flush.fill_(float(i))
+            flush(i)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             fn(start + i)
@@ -427,7 +428,7 @@ def main():
     # come warm from the selection kernel as inside the step graph
     fev = []
     for i in range(K):
-        flush.fill_(float(i))
+        flush(i)
         eng.rotate(Q[i])
         eng.lookup()
         a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -498,8 +499,7 @@ def main():
             "data": "synthetic N(0,1) Q/K/V (random-init Qwen3-8B attention shape), seed 1000+rank",
             "config": {"workload": workload_label(args, world), "batch": b, "ctx": ctx,
                        "budget": args.budget, "tokens_per_centroid": cfg.fine_ratio,
-                       "l2": "flushed (256 MB write) before "
-                                                                             "every timed step",
+                       "l2": L2Flush.DESC,
                        "parallelism": f"batch-sharded replicas x{world}"},
             "speedup_vs_dense": dense_avg / ms_step,
             "dense_us_per_step": dense_avg * 1e3,
@@ -572,7 +572,7 @@ def main_sharded(args, rank, world, local):
     Q = torch.randn(n, b, lay.num_q_heads, d, generator=gen, device=dev)
     KN = torch.randn(n, b, lay.num_kv_heads, d, generator=gen, device=dev)
     VN = torch.randn(n, b, lay.num_kv_heads, d, generator=gen, device=dev)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flush = L2Flush(dev)
     stream = torch.cuda.current_stream()
 
     def step(i):
@@ -583,7 +583,7 @@ def main_sharded(args, rank, world, local):
     def timed(fn, count, start=0):
         evs = []
         for i in range(count):
-            flush.fill_(float(i))
+            flush(i)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             fn(start + i)
@@ -634,13 +634,32 @@ def main_sharded(args, rank, world, local):
             "config": {"workload": workload_label(args, world), "batch": b, "ctx": ctx, "budget": args.budget,
                        "parallelism": f"KV-sequence-sharded x{world} (NCCL all-gather of (M,Z), candidate "
                                       "prefixes and (m,s,a) partials)",
-                       "l2": "flushed (256 MB write) before every timed step"},
+                       "l2": L2Flush.DESC},
             "speedup_vs_dense": dense_avg / ms_step, "dense_us_per_step": dense_avg * 1e3,
             "sequences_per_s": b / (ms_step * 1e-3), "prefill_s": prefill_s,
             "gpu_launches": 12 * K, "clocks": clk.summary(),
         }), flush=True)
     dist.barrier()
     dist.destroy_process_group()
+
+
+class L2Flush:
+    """Between timed steps: write a 256 MB buffer (evicts everything; L2 > 126 MB), then read
+    another 256 MB one, so the step starts with a cold L2 that holds no dirty lines -- the write
+    flush alone would charge the step for writing back 126 MB of the flush buffer."""
+
+    DESC = "flushed before every timed step (256 MB write, then 256 MB read: cold and clean)"
+
+    def __init__(self, dev):
+        import torch
+
+        self.w = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+        self.r = torch.zeros(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+        self.acc = torch.zeros((), dtype=torch.float32, device=dev)
+
+    def __call__(self, i):
+        self.w.fill_(float(i))
+        self.acc += self.r.sum()
 
 
 def _write_seq(eng, s, k, v):

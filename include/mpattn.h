@@ -147,7 +147,8 @@ int mpa_build_worklist(const mpa_level* fine, const mpa_level* coarse, int group
  * rej == NULL with replacement (flat level only): contiguous-centroid work list -- no rejected
  * list is written; rej_w already holds every candidate's weight (mpa_centroid_logits rej_w) and
  * the selected candidates' rows are set to -inf, so mpa_sparse_decode can stream the fine value
- * centroids [0, count[l]) in order (see there).  stats row 1 still counts the rejected. */
+ * centroids [0, count[l]) in order (see there).  stats row 1 still counts the rejected; e_local
+ * is consumed (its L2 lines are discarded without write-back: undefined afterwards). */
 int mpa_select_worklist(const mpa_level* fine, const mpa_level* coarse, int group, const double* logits,
                         const double* e_local, const int32_t* cand, const int32_t* n_cand, int cand_cap,
                         const double* chunk_stats,

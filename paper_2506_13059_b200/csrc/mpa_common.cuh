@@ -71,6 +71,16 @@ template <> struct unpack16<double> {
 };
 
 // ---- warp / block reductions -----------------------------------------------
+// drop dead scratch from L2 without writing it back (discard.global.L2): every 128-byte line
+// lying wholly inside [p, p + bytes) -- lines shared with live neighbours are left alone.
+// Block-cooperative over threads [t0, t0 + nt).
+__device__ __forceinline__ void discard_l2_range(const void* p, size_t bytes, int t, int nt) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uintptr_t lo = (a + 127) & ~(uintptr_t)127, hi = (a + bytes) & ~(uintptr_t)127;
+    for (uintptr_t x = lo + (uintptr_t)t * 128; x < hi; x += (uintptr_t)nt * 128)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(x) : "memory");
+}
+
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -1211,6 +1211,13 @@ select_worklist_v2_kernel(const double* __restrict__ logits, const double* __res
                       cstats, n_chunks, keys, sizes, sflag, flag, sel_tokens, sh, fmem_off, lists ? offs : nullptr);
     dbg_lk(3);
     if (sh.prefix && !sh.cross) return;  // sharded local pass: only the candidate prefix is needed
+    if (!rej && replacement && e_local) {
+        // serving path: this was the last read of the ledger's e_local (the next step's logits
+        // kernel rewrites it) -- drop it from L2 instead of letting the decode evict it to HBM
+        for (int g = 0; g < G; ++g)
+            discard_l2_range(e_local + ((size_t)l * G + g) * cand_cap, (size_t)n * sizeof(double), threadIdx.x,
+                             blockDim.x);
+    }
     worklist_v2<G>(l, L, n, logits, cand, cand_cap, sflag, sizes, reinterpret_cast<int*>(keys), fmem_off, fmem, fcap,
                    fmem_cap, offs, csize, ne, ccap, cflag, clogits, sink_end, buffer_start, cache_len, n_kv_heads,
                    replacement, tok, tok_cap, rej, rej_w, rej_cap, stats);
