@@ -306,6 +306,17 @@ __device__ __forceinline__ void cp_async4(unsigned dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async16_hint(unsigned dst, const void* src, uint64_t policy) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "l"(policy)
+                 : "memory");
+}
+// arrive on the mbarrier once this thread's cp.async copies so far have landed (pending count +1 now)
+__device__ __forceinline__ void cp_async_mbar_arrive(unsigned bar) {
+    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive1(unsigned bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
 
 __device__ __forceinline__ void ldsm_x4(unsigned addr, unsigned (&r)[4]) {
@@ -356,6 +367,13 @@ __device__ __forceinline__ void dbg_stamp(int slot) {
 #else
 __device__ __forceinline__ void dbg_stamp(int) {}
 #endif
+#ifdef MPA_DEBUG_RAMP  // slots 5-7 time the pipeline ramp instead of the segment merge
+#define DBG_SEG(k)
+#define DBG_RAMP(k) dbg_stamp(k)
+#else
+#define DBG_SEG(k) dbg_stamp(k)
+#define DBG_RAMP(k)
+#endif
 
 // byte offset of 16-byte chunk ch of row r in a TMA 128B-swizzled 16-row tile (64-column halves)
 __device__ __forceinline__ unsigned swz(int r, int ch) {
@@ -375,7 +393,7 @@ struct SkGeom {
     static constexpr int kRing = 8;                  // row-id ring: tiles whose ids are in smem
     static constexpr int kIdB = NW * kRing * 32 * 4;
     static constexpr int kPS = G * (D + 2);          // floats per partial
-    static size_t smem(int L, int C) { return 1024 + (size_t)kStagesB + kBarB + kIdB + sizeof(int) * (L + C + 2); }
+    static size_t smem(int L, int C) { return 1024 + (size_t)kStagesB + kBarB + kIdB + sizeof(int) * (3 * L + C + 2); }
 };
 
 template <int G, int D, int NW, int NST>
@@ -383,11 +401,13 @@ __global__ void __launch_bounds__(NW * 32, 2)
 decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                  const __grid_constant__ CUtensorMap tm_fvc, const __grid_constant__ CUtensorMap tm_cvc,
                  const __grid_constant__ CUtensorMap tm_k16, const __grid_constant__ CUtensorMap tm_v16,
-                 const __grid_constant__ CUtensorMap tm_fvc16, int tcap,
+                 const __grid_constant__ CUtensorMap tm_fvc16, int tcap, const __nv_bfloat16* __restrict__ k_rows,
+                 const __nv_bfloat16* __restrict__ v_rows,
                  const float* __restrict__ q_rot, const int32_t* __restrict__ tok, const int32_t* __restrict__ n_tok,
                  int tok_cap, const int32_t* __restrict__ rej, const float* __restrict__ rej_w,
                  const int32_t* __restrict__ n_rej, int rej_cap, int fcap, int ccap, int L, float* __restrict__ part,
-                 int32_t* __restrict__ ticket, float* __restrict__ out, float* __restrict__ part_out, int tok_runs) {
+                 int32_t* __restrict__ ticket, float* __restrict__ out, float* __restrict__ part_out, int tok_runs,
+                 int tok_lsu) {
     dbg_stamp(0);
     using Geo = SkGeom<G, D, NW, NST>;
     constexpr bool PACKED = G <= 4;
@@ -405,6 +425,7 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     // ---- per-ledger tile prefix sum (every CTA computes the same schedule)
     int* tp = reinterpret_cast<int*>(smem + Geo::kStagesB + Geo::kBarB + Geo::kIdB);
     int* idring = reinterpret_cast<int*>(smem + Geo::kStagesB + Geo::kBarB) + w * Geo::kRing * 32;
+    int* cnt_s = tp + (L + 1) + (C + 1);  // [L][2] token / centroid counts
     {
         __shared__ int scan[33];
         int base = 0;
@@ -412,7 +433,10 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             const int l = l0 + threadIdx.x;
             int n = 0;
             if (l < L) {
-                const int nt = (__ldg(n_tok + l) + 15) >> 4, nr = has_rej ? (__ldg(n_rej + l) + 31) >> 5 : 0;
+                const int ct = __ldg(n_tok + l), cr = has_rej ? __ldg(n_rej + l) : 0;
+                cnt_s[2 * l] = ct;  // the walkers read the counts from here, not from global
+                cnt_s[2 * l + 1] = cr;
+                const int nt = (ct + 15) >> 4, nr = (cr + 31) >> 5;
                 n = nt + nr > 0 ? nt + nr : 1;
             }
             int tot;
@@ -474,8 +498,8 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             wk.l = l;
             wk.beg = tp[l];
             wk.end = tp[l + 1];
-            wk.nt = __ldg(n_tok + l);
-            wk.nr = has_rej ? __ldg(n_rej + l) : 0;
+            wk.nt = cnt_s[2 * l];
+            wk.nr = cnt_s[2 * l + 1];
             wk.ntt = (wk.nt + 15) >> 4;
             if (wk.ntt == 0 && wk.nr == 0) wk.ntt = 1;  // empty ledger: one empty token tile
         }
@@ -556,11 +580,36 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     auto issue = [&](int j, int st, const Meta& m) {
         const unsigned kst = wbase + st * Geo::kStageB, vst = kst + Geo::kMatB, lgs = lgbase + st * Geo::kLgB;
         const unsigned bar = bar0 + st * 8;
+        (void)lgs;
         int id[16], id2[16];
         const bool rows_in_order = m.kind == 1 && !rej;  // contiguous-centroid list
         if (m.nv > 0 && !rows_in_order) {
             ids16(j, m, 0, id);
             if (m.kind == 1) ids16(j, m, 16, id2);
+        }
+        if (m.kind == 0 && m.nv > 0 && tok_lsu) {
+            // token tile through the LSU: every lane copies 16-byte chunks (row r, K or V, chunk
+            // ch) straight into the swizzled stage -- 2 x 256 B rows per warp instruction, which
+            // the TMA unit would need 4 gather4 instructions for; completion on the stage mbarrier
+            constexpr int CPR = D / 8;  // 16-byte chunks per row
+            const size_t lbase = (size_t)m.l * tcap;
+#pragma unroll
+            for (int it = 0; it < CPR; ++it) {
+                const int jj = lane + 32 * it, ch = jj % CPR, kv = (jj / CPR) & 1, r = jj / (2 * CPR);
+                // row index with compile-time register indices (r0 constant, +1 for the upper lanes at d = 64)
+                constexpr int kRowsPerIt = 32 / (2 * CPR);
+                const int r0 = it * kRowsPerIt;
+                int rid = id[r0];
+                if constexpr (kRowsPerIt > 1) {
+                    if (lane >= 2 * CPR) rid = id[r0 + 1];
+                }
+                const __nv_bfloat16* src = (kv ? v_rows : k_rows) + (lbase + rid) * D + ch * 8;
+                cp_async16_hint((kv ? vst : kst) + swz(r, ch), src, policy);
+            }
+            cp_async_mbar_arrive(bar);
+            __syncwarp();
+            if (elect_one()) mbar_arrive1(bar);  // the phase's one expected arrival
+            return;
         }
         __syncwarp();
         if (!elect_one()) return;
@@ -762,7 +811,7 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         }
         if (lane == 0) s_poff[w] = (unsigned)(w * Geo::kWarpB + fs * Geo::kStageB);
         __syncthreads();
-        dbg_stamp(5);
+        DBG_SEG(5);
         const bool whole = tp[l] >= g0 && tp[l + 1] <= g1;
         float* dst = part + (size_t)(c + l) * Geo::kPS;
         for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
@@ -797,7 +846,7 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         if (!whole) {
             __threadfence();
             __syncthreads();
-            dbg_stamp(6);
+            DBG_SEG(6);
             // first CTA meeting ledger l: the one whose range contains tile tp[l]
             int cf = (int)min((long long)Ce - 1, (long long)tp[l] * Ce / T);
             while (cf + 1 < Ce && cta_begin(cf + 1) <= tp[l]) ++cf;
@@ -814,7 +863,7 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
                 if (s_last) ticket[l] = 0;  // ready for the next launch / graph replay
             }
             __syncthreads();
-            dbg_stamp(7);
+            DBG_SEG(7);
             if (s_last) {
                 __threadfence();
                 const int np = s_np;
@@ -892,8 +941,13 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     };
 #pragma unroll 1
     for (int i = 0; i < kAhead; ++i) prefetch_next();
+    DBG_RAMP(5);
 #pragma unroll 1
-    for (int i = 0; i < NST - 1; ++i) issue_next();
+    for (int i = 0; i < NST - 1; ++i) {
+        issue_next();
+        if (i == 0) DBG_RAMP(6);
+    }
+    DBG_RAMP(7);
 
     // ledgers met by this CTA: lf .. ll (every warp closes each of them, in order)
     const int lf = ledger_of_tile(g0), ll = ledger_of_tile(g1 - 1);
@@ -1100,6 +1154,17 @@ int tok_runs(bool sparse) {
     return mode == 2 || (mode == 1 && sparse) ? 1 : 0;
 }
 
+// token tiles through the LSU (cp.async) instead of TMA gathers: MPA_SK_TOKLSU=0 never,
+// 1 sparse lists (default), 2 also the dense decode
+int tok_lsu(bool sparse) {
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = getenv("MPA_SK_TOKLSU");
+        mode = e ? atoi(e) : 1;
+    }
+    return mode == 2 || (mode == 1 && sparse) ? 1 : 0;
+}
+
 template <int G, int D>
 int launch_sk(const mpa_cache* c, const float* q_rot, const int32_t* tok, const int32_t* n_tok, int tok_cap,
               const int32_t* rej, const float* rej_w, const int32_t* n_rej, int rej_cap, const void* fvc, int fcap,
@@ -1121,9 +1186,10 @@ int launch_sk(const mpa_cache* c, const float* q_rot, const int32_t* tok, const 
     if (!rc) rc = cvc ? bf16_rows_map(&tc, cvc, (long long)L * ccap, D) : (tc = tf, 0);
     if (rc) return rc;
     MPA_REQUIRE(rej || !rej_w || fvc, MPA_ERR_ARG, "mpa_sparse_decode: contiguous-centroid list without fine_vc");
-    kern<<<C, kSkWarps * 32, smem, st>>>(tk, tv, tf, tc, tk16, tv16, tf16, c->tcap, q_rot, tok, n_tok, tok_cap, rej,
-                                         rej_w, n_rej, rej_cap, fcap, ccap, L, part, ticket, out, part_out,
-                                         tok_runs(tok != nullptr));
+    kern<<<C, kSkWarps * 32, smem, st>>>(tk, tv, tf, tc, tk16, tv16, tf16, c->tcap, (const __nv_bfloat16*)c->k_rot,
+                                         (const __nv_bfloat16*)c->v, q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej,
+                                         rej_cap, fcap, ccap, L, part, ticket, out, part_out, tok_runs(tok != nullptr),
+                                         tok_lsu(tok != nullptr));
     return check_launch("mpa_sparse_decode(stream-K mma)");
 }
 

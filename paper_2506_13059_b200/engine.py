@@ -31,6 +31,7 @@ from .ledger import DeviceLedgers, HostLedger
 import os
 
 NUM_SMS = 148
+_SK_SPLIT = int(os.environ.get("MPA_SK_SPLIT", "0"))  # experiments: CTAs per ledger of the fused grid
 
 
 class DecodeEngine:
@@ -228,7 +229,7 @@ class DecodeEngine:
     def fused(self, n_split: int | None = None) -> torch.Tensor:
         """K11 + K12 over the current work lists.  n_split None / 0: one full wave of the
         stream-K grid (bf16) or automatic splits (fp32); > 0: that many CTAs per ledger."""
-        S = int(n_split or 0)
+        S = int(n_split or 0) or _SK_SPLIT
         ws = self._workspace(S)
         st = stream_ptr()
         rej, rej_w, n_rej = self._centroid_terms()

@@ -57,7 +57,10 @@ def main():
         slow = np.argsort(-np.nan_to_num(rel[:, 4]))[:3]
         for cidx in slow:
             print("   slow cta", cidx, np.round(rel[cidx], 2))
-        for k, name in enumerate(["start", "sched", "first", "loopend", "end", "seg_sync", "seg_fence", "seg_ticket"]):
+        names = ["start", "sched", "first", "loopend", "end", "seg_sync", "seg_fence", "seg_ticket"]
+        if os.environ.get("RAMP"):
+            names[5:] = ["ids_issued", "issue0_done", "issue1_done"]
+        for k, name in enumerate(names):
             col = rel[:, k]
             print(f"  {name:8s} min {np.nanmin(col):7.2f} med {np.nanmedian(col):7.2f} max {np.nanmax(col):7.2f} us")
 
