@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <cstdlib>
+#include <utility>
 
 #include "mpattn.h"
 
@@ -141,6 +143,34 @@ __host__ __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b -
 }  // namespace mpa
 
 // Runtime GQA group size -> compile-time kG (1..8).
+// ---- programmatic dependent launch (PDL): a kernel launched with launch_pdl may start while
+// its stream predecessor finishes; it must pdl_wait() before touching that predecessor's outputs
+// (and every PDL kernel waits at some point, so completion stays transitive along the chain)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+inline bool pdl_enabled() {  // MPA_PDL=0 turns the attribute off (the waits are then no-ops)
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("MPA_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 #define MPA_DISPATCH_G(G, ...)                                                                      \
     switch (G) {                                                                                    \
         case 1: { constexpr int kG = 1; __VA_ARGS__; } break;                                      \

@@ -426,6 +426,17 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     int* tp = reinterpret_cast<int*>(smem + Geo::kStagesB + Geo::kBarB + Geo::kIdB);
     int* idring = reinterpret_cast<int*>(smem + Geo::kStagesB + Geo::kBarB) + w * Geo::kRing * 32;
     int* cnt_s = tp + (L + 1) + (C + 1);  // [L][2] token / centroid counts
+    if (threadIdx.x == 0) {  // before the PDL wait: nothing here depends on the selection
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_k)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_v)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_fvc)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_cvc)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_k16)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_v16)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_fvc16)) : "memory");
+    }
+    pdl_wait();  // work lists, counts and weights come from the selection kernel
+    pdl_trigger();
     {
         __shared__ int scan[33];
         int base = 0;
@@ -445,15 +456,6 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             base += tot;
         }
         if (threadIdx.x == 0) tp[L] = base;
-    }
-    if (threadIdx.x == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_k)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_v)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_fvc)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_cvc)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_k16)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_v16)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_fvc16)) : "memory");
     }
     const unsigned bar0 = smem_u32(smem + Geo::kStagesB + Geo::kLgAllB) + w * NST * 8;
     const unsigned lgbase = smem_u32(smem + Geo::kStagesB) + w * NST * Geo::kLgB;
@@ -1186,10 +1188,10 @@ int launch_sk(const mpa_cache* c, const float* q_rot, const int32_t* tok, const 
     if (!rc) rc = cvc ? bf16_rows_map(&tc, cvc, (long long)L * ccap, D) : (tc = tf, 0);
     if (rc) return rc;
     MPA_REQUIRE(rej || !rej_w || fvc, MPA_ERR_ARG, "mpa_sparse_decode: contiguous-centroid list without fine_vc");
-    kern<<<C, kSkWarps * 32, smem, st>>>(tk, tv, tf, tc, tk16, tv16, tf16, c->tcap, (const __nv_bfloat16*)c->k_rot,
-                                         (const __nv_bfloat16*)c->v, q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej,
-                                         rej_cap, fcap, ccap, L, part, ticket, out, part_out, tok_runs(tok != nullptr),
-                                         tok_lsu(tok != nullptr));
+    launch_pdl(kern, dim3(C), dim3(kSkWarps * 32), smem, st, tk, tv, tf, tc, tk16, tv16, tf16, c->tcap,
+               (const __nv_bfloat16*)c->k_rot, (const __nv_bfloat16*)c->v, q_rot, tok, n_tok, tok_cap, rej, rej_w,
+               n_rej, rej_cap, fcap, ccap, L, part, ticket, out, part_out, tok_runs(tok != nullptr),
+               tok_lsu(tok != nullptr));
     return check_launch("mpa_sparse_decode(stream-K mma)");
 }
 

@@ -11,6 +11,7 @@
 // the reference), sincos in fp64, result rounded once to the cache dtype.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 
 #include "mpa_common.cuh"
 
@@ -103,6 +104,8 @@ __global__ void rotate_queries_kernel(const float* __restrict__ q, int n_qh, int
                                       const int32_t* __restrict__ qpos, int delta,
                                       const double* __restrict__ inv_freq, float scale,
                                       float* __restrict__ q_rot, double* __restrict__ q_lk) {
+    pdl_wait();     // (PDL kernels trigger only after their own wait: a dependent's early phase may
+    pdl_trigger();  // then read anything older than this kernel -- the lookup starts its centroid loads)
     const int s = blockIdx.y, h = blockIdx.x;
     const size_t base = ((size_t)s * n_qh + h) * d;
     const double p = (double)qpos[s];
@@ -181,7 +184,7 @@ extern "C" int mpa_rotate_queries(const float* q, int n_seq, int n_qh, int d, co
     MPA_REQUIRE(q && qpos && inv_freq && (q_rot || q_lk), MPA_ERR_ARG, "mpa_rotate_queries: null argument");
     MPA_REQUIRE(d >= 2 && d % 2 == 0, MPA_ERR_ARG, "mpa_rotate_queries: bad head_dim %d", d);
     if (n_seq <= 0 || n_qh <= 0) return 0;
-    rotate_queries_kernel<<<dim3(n_qh, n_seq), 64, 0, (cudaStream_t)stream>>>(q, n_qh, d, qpos, delta, inv_freq,
-                                                                             scale, q_rot, q_lk);
+    launch_pdl(rotate_queries_kernel, dim3(n_qh, n_seq), dim3(64), 0, (cudaStream_t)stream, q, n_qh, d, qpos, delta,
+               inv_freq, scale, q_rot, q_lk);
     return check_launch("mpa_rotate_queries");
 }

@@ -277,9 +277,14 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
     __shared__ double red[kLgThreads / 32][G];
     __shared__ double s_m[G];
     const int l = blockIdx.y, chunk = blockIdx.x, tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    // PDL: q_lk (and, for candidate lists, cand / n_cand) come from the stream predecessor; the
+    // flat path streams its centroid rows before waiting for it
+    if (cand) pdl_wait();
     const int n = cand ? n_cand[l] : count[l];
     const int i0 = chunk * kLgChunk;
     if (i0 >= n) {
+        if (!cand) pdl_wait();
+        pdl_trigger();
         if (cstats && chunk < n_chunks && tid < G) {
             cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2] = -INFINITY;
             cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2 + 1] = 0.0;
@@ -296,6 +301,12 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
         if (tid == 0) {
             // one expect_tx (a single arrive) for everything this barrier phase receives
             mbar_expect_tx(smem_u32(&bar), G * 4 * QD * 8 + 2 * kLgChunk * 128);
+            if (!cand) {  // centroid rows first: they do not depend on the predecessor
+                const int row0 = l * kcap + i0;
+                tma_load_2d(smem_u32(tile), &tm_tile, 0, row0, smem_u32(&bar));
+                tma_load_2d(smem_u32(tile + kLgChunk * 128), &tm_tile, 64, row0, smem_u32(&bar));
+                pdl_wait();
+            }
             // q_lk rows of the GQA group: one 256 B bulk copy per (head, quarter) into padded slots
             for (int j = 0; j < G * 4; ++j)
                 asm volatile(
@@ -305,11 +316,6 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
                     : "memory");
         }
         if (!cand) {
-            if (tid == 0) {
-                const int row0 = l * kcap + i0;
-                tma_load_2d(smem_u32(tile), &tm_tile, 0, row0, smem_u32(&bar));
-                tma_load_2d(smem_u32(tile + kLgChunk * 128), &tm_tile, 64, row0, smem_u32(&bar));
-            }
         } else {
             // lane j gathers rows 4j .. 4j+3 (rows past nv repeat the chunk's first candidate)
             int id[4];
@@ -329,6 +335,7 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
         }
     }
     mbar_wait(smem_u32(&bar), 0);
+    pdl_trigger();  // after thread 0's wait (the barrier above completes only after it)
 
     const int qt = tid & 3, rg = tid >> 2;
     const double* qq = qs + qt * QRow;
@@ -875,16 +882,23 @@ __device__ void select_v2_core(int l, const double* __restrict__ logits, const d
     for (int u = 0; u < kPF; ++u) {
         const int i = threadIdx.x + u * blockDim.x;
         szr[u] = ofr[u] = 0;
-#pragma unroll
-        for (int g = 0; g < G; ++g) elr[u][g] = 0.0;
         if (i < n) {
             const int id = cand ? __ldg(cand + (size_t)l * cand_cap + i) : i;
             szr[u] = __ldg(lv_size + (size_t)l * lv_cap + id);
             if (offs) ofr[u] = __ldg(moff + (size_t)l * (lv_cap + 1) + id);
-            if (use_local)
-#pragma unroll
-                for (int g = 0; g < G; ++g) elr[u][g] = __ldcg(el + (size_t)g * cand_cap + i);
         }
+    }
+    // PDL: everything below may read the logits kernel's outputs (ledger state above is older)
+    pdl_wait();
+    pdl_trigger();
+#pragma unroll
+    for (int u = 0; u < kPF; ++u) {
+        const int i = threadIdx.x + u * blockDim.x;
+#pragma unroll
+        for (int g = 0; g < G; ++g) elr[u][g] = 0.0;
+        if (i < n && use_local)
+#pragma unroll
+            for (int g = 0; g < G; ++g) elr[u][g] = __ldcg(el + (size_t)g * cand_cap + i);
     }
     // ---- 1. sizes, per-head max
     long long tot_local = 0;
@@ -1415,8 +1429,8 @@ int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* 
             auto kern = logits_tma_kernel<kG>;
             const size_t smem = 1024 + 2 * kLgChunk * 128 + sizeof(double) * (kG * 4 * 34 + kG * kLgChunk);
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            kern<<<g2, kLgThreads, smem, st>>>(tt, tr, q_lk, lv->cap, lv->count, lv->size, cand, n_cand, cand_cap,
-                                               logits, chunk_stats, e_local, n_chunks, rej_w, rej_cap);
+            launch_pdl(kern, g2, dim3(kLgThreads), smem, st, tt, tr, q_lk, lv->cap, lv->count, lv->size, cand, n_cand,
+                       cand_cap, logits, chunk_stats, e_local, n_chunks, rej_w, rej_cap);
         });
         return check_launch("mpa_centroid_logits(tma)");
     }
@@ -1461,11 +1475,11 @@ int mpa_launch_select_worklist_v2(const mpa_level* fine, const mpa_level* coarse
     MPA_DISPATCH_G(group, {
         auto kern = select_worklist_v2_kernel<kG>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<n_ledgers, kSel2Threads, smem, st>>>(
-            logits, e_local, cand, n_cand, cand_cap, chunk_stats, n_chunks, budget, flag, sel_tokens, fine->size,
-            fine->off, fine->idx, fine->cap, fine->idx_cap, fine->count, coarse ? coarse->size : nullptr,
-            coarse ? coarse->count : nullptr, coarse ? coarse->cap : 0, cflag, clogits, sink_end, buffer_start,
-            cache_len, n_kv_heads, replacement, tok, tok_cap, rej, rej_w, rej_cap, stats, n_max, sh);
+        launch_pdl(kern, dim3(n_ledgers), dim3(kSel2Threads), smem, st, logits, e_local, cand, n_cand, cand_cap,
+                   chunk_stats, n_chunks, budget, flag, sel_tokens, fine->size, fine->off, fine->idx, fine->cap,
+                   fine->idx_cap, fine->count, coarse ? coarse->size : nullptr, coarse ? coarse->count : nullptr,
+                   coarse ? coarse->cap : 0, cflag, clogits, sink_end, buffer_start, cache_len, n_kv_heads,
+                   replacement, tok, tok_cap, rej, rej_w, rej_cap, stats, n_max, sh);
     });
     return check_launch("mpa_select_worklist(v2)");
 }
