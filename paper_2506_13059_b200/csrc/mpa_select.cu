@@ -292,6 +292,10 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
         return;
     }
     const int nv = min(kLgChunk, n - i0);
+    // epilogue inputs of this thread's candidate, loaded now so the latency hides under the tile
+    const bool valid = tid < nv;
+    const int id = valid ? (cand ? __ldg(cand + (size_t)l * cand_cap + i0 + tid) : i0 + tid) : 0;
+    const int isz = valid && cstats ? __ldg(lv_size + (size_t)l * kcap + id) : 0;
     if (tid == 0) {
         mbar_init(smem_u32(&bar), 1);
         fence_mbar_init();
@@ -409,9 +413,6 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
     if (!cstats) return;
     __syncthreads();
     const int i = tid;
-    const bool valid = i < nv;
-    const int id = valid ? (cand ? cand[(size_t)l * cand_cap + i0 + i] : i0 + i) : 0;
-    const int isz = valid ? lv_size[(size_t)l * kcap + id] : 0;
     const double nsz = (double)isz;
     if (rej_w && valid) {
         // replacement weights of every candidate, indexed by candidate (logit + ln N, the value
