@@ -461,17 +461,21 @@ def main():
     h2d = (qh[0].numel() + kh[0].numel() + vh[0].numel()) * 4
     d2h = oh.numel() * 4
 
-    # ---- one online cluster update event (C4-style overhead, amortised over L steps)
+    # ---- online cluster update events (C4-style overhead, amortised over L steps): the first one
+    # in the process also pays one-time lazy CUDA module loads, so two events run and the second,
+    # steady-state one is reported (the first is listed beside it)
     L = cfg.local_buffer
-    need = int(2 * L - (eng.cache_len[0] - eng.buffer_start[0]))
-    if need > 0:
-        eng.write_tokens(torch.randn(b, lay.num_kv_heads, need, d, generator=gen, device=dev),
-                         torch.randn(b, lay.num_kv_heads, need, d, generator=gen, device=dev))
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    upd = clustering.online_update(eng, list(range(b)), eng.cursor) if not args.profile else {"rounds": 0}
-    torch.cuda.synchronize()
-    update_ms = (time.perf_counter() - t0) * 1e3
+    upd, update_ms, update_first_ms = {"rounds": 0}, 0.0, 0.0
+    for ev in range(0 if args.profile else 2):
+        need = int(2 * L - (eng.cache_len[0] - eng.buffer_start[0]))
+        if need > 0:
+            eng.write_tokens(torch.randn(b, lay.num_kv_heads, need, d, generator=gen, device=dev),
+                             torch.randn(b, lay.num_kv_heads, need, d, generator=gen, device=dev))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        upd = clustering.online_update(eng, list(range(b)), eng.cursor + ev)
+        torch.cuda.synchronize()
+        update_first_ms, update_ms = update_ms, (time.perf_counter() - t0) * 1e3
 
     # ---- max over ranks
     vals = torch.tensor([ms_step, e2e_avg, fused_avg, dense_avg, fused_step_avg or fused_avg], device=dev,
@@ -520,7 +524,8 @@ def main():
                           "mean_rejected_centroids": float(fstats[:, 1].mean()),
                           "mean_scored_centroids": float(np.mean(scored)),
                           "memop_ratio": nbytes["step"] / dbytes},
-            "update": {"ms_per_event": update_ms, "amortized_us_per_step": update_ms * 1e3 / L,
+            "update": {"ms_per_event": update_ms, "first_event_ms": update_first_ms,
+                       "amortized_us_per_step": update_ms * 1e3 / L,
                        "pct_of_step": update_ms / L / ms_step * 100.0, "lloyd_rounds": upd["rounds"],
                        "prefill_s": prefill_s},
             "e2e": {"value": e2e_avg * 1e3, "unit": "us/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

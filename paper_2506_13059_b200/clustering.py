@@ -253,11 +253,38 @@ def _hierarchy(eng, jobs) -> None:
 # ---------------------------------------------------------------------------- online update
 
 
+class _Ticks:
+    """MPA_UPD_TRACE=1: device-synchronised wall time per phase of an online update (stderr)."""
+
+    def __init__(self):
+        import os
+        import time
+
+        self.on = os.environ.get("MPA_UPD_TRACE") == "1"
+        self.t = time.perf_counter
+        self.last = self.t() if self.on else 0.0
+        self.parts = []
+
+    def __call__(self, name):
+        if self.on:
+            torch.cuda.synchronize()
+            now = self.t()
+            self.parts.append((name, (now - self.last) * 1e3))
+            self.last = now
+
+    def dump(self):
+        if self.on:
+            import sys
+
+            print("update phases ms: " + ", ".join(f"{n} {v:.2f}" for n, v in self.parts), file=sys.stderr)
+
+
 def online_update(eng, seqs, cursor: int) -> dict:
     """Absorb the oldest L buffered tokens of every kv-head of `seqs` into the final block
     (clustering.py:404-472), then split / settle (:359-401) and refresh the final block's
     hierarchy (:465-471).  Returns timing-free counters (rounds, splits)."""
     cfg, led = eng.cfg, eng.led
+    tick = _Ticks()
     L = cfg.local_buffer
     n_new = -(-L // cfg.fine_ratio)
     ledgers = [s * eng.Hkv + h for s in seqs for h in range(eng.Hkv)]
@@ -285,19 +312,27 @@ def online_update(eng, seqs, cursor: int) -> dict:
         probs.append((l, F.start, bs + L - F.start, F.fk + n_new))
         tails.append(bs - F.start)
     dev = eng.device
+    tick("loop")
     idx = lambda parts: torch.as_tensor(np.concatenate(parts), dtype=torch.int64, device=dev)
     osrc, odst, nsrc, ndst = idx(old_src), idx(old_dst), idx(new_src), idx(new_dst)
+    tick("idx")
     init = torch.empty(c_at, eng.d, dtype=torch.float64, device=dev)
     init[odst] = led.kc64.view(-1, eng.d)[osrc]
+    tick("init_old")
     init[ndst] = eng.k_raw.view(-1, eng.d)[nsrc].double()
+    tick("init_new")
     counts = torch.zeros(c_at, dtype=torch.int32, device=dev)
     counts[odst] = led.size.view(-1)[osrc]
+    tick("counts0")
     km = KMeansBatch(dev, eng.d, probs, init, pts=eng.k_raw, tcap=eng.tcap,
                      min_iters=cfg.refine_kmeans_iters, count_init=counts)
     dist = torch.empty(len(probs), L, km.k_max, dtype=torch.float64, device=eng.device)
     tails_d = _i32(eng, tails)
+    tick("batch")
     call("mpa_km_seq_assign", km.struct(), ptr(tails_d), L, ptr(dist), stream_ptr())
+    tick("seq_assign")
     rounds = km.lloyd()
+    tick(f"lloyd({rounds})")
     nk = km.nonempty()
     f0 = np.zeros(len(probs), np.int64)
     mbase = np.zeros(len(probs), np.int64)
@@ -307,16 +342,22 @@ def online_update(eng, seqs, cursor: int) -> dict:
         f0[i], mbase[i] = F.f0, F.start - int(eng.sink_end[s])
         F.end = int(eng.buffer_start[s]) + L
         F.fk = int(nk[i])
+    tick("nonempty")
     _write_fine(eng, km, f0, mbase)
+    tick("write")
     for s in seqs:
         eng.buffer_start[s] += L
     eng._sync_scalars()
     _refresh_counts(eng, ledgers)
+    tick("counts")
     n_splits = _split(eng, ledgers)
+    tick("split")
     if cfg.hierarchy is not None:
         _hierarchy(eng, [(l, len(led.blocks[l]) - 1,
                           block_seed(cfg.seed, _head(eng, l), int(eng.buffer_start[l // eng.Hkv]), 3))
                          for l in ledgers])
+        tick("hierarchy")
+    tick.dump()
     return {"rounds": rounds, "splits": n_splits}
 
 

@@ -27,7 +27,8 @@
 namespace mpa {
 
 constexpr int kTcM = 128, kTcN = 256, kTcStages = 4, kTcSub = 6;
-constexpr int kTcThreads = 160;
+constexpr int kTcThreads = 288;  // warp 4 issues; warps 0-3 and 5-8 drain TMEM (two column halves)
+constexpr int kTcTailRows = 64;  // box rows of the narrow-tail centroid map
 constexpr int kTcABytes = 2 * kTcM * 128;   // 2 x 64-column chunks of the point tile
 constexpr int kTcBBytes = kTcN * 128;       // one 256-row x 64-column centroid sub-tile
 constexpr int kTcSmem = 1024 + kTcABytes + kTcStages * kTcBBytes;
@@ -99,8 +100,8 @@ __global__ void km_tc_norms_kernel(mpa_km km, TcWs ws) {
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1)
-km_assign_tc_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_constant__ CUtensorMap tm_terms, mpa_km km,
-                    TcWs ws) {
+km_assign_tc_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_constant__ CUtensorMap tm_terms,
+                    const __grid_constant__ CUtensorMap tm_terms_tail, mpa_km km, TcWs ws) {
     const int p = blockIdx.y, tile = blockIdx.x;
     if (!km.state[p * 4 + 0]) return;
     const int n = km.prob_n[p], K = km.prob_k[p];
@@ -122,7 +123,7 @@ km_assign_tc_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_con
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(smem_u32(&bar_acc_full[b]), 1);
-            mbar_init(smem_u32(&bar_acc_empty[b]), 4);
+            mbar_init(smem_u32(&bar_acc_empty[b]), 8);
         }
         fence_mbar_init();
     }
@@ -132,6 +133,10 @@ km_assign_tc_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_con
     const uint32_t tmem = tmem_base;
     const int n_nt = (K + kTcN - 1) / kTcN, S = n_nt * kTcSub;
     const int c_off = km.c_off[p];
+    // the last N tile is only as wide as its centroids (multiple of 16): no MMA or epilogue work on
+    // padding columns, and its centroid rows come in 64-row boxes
+    const int n_last = (K - (n_nt - 1) * kTcN + 15) & ~15;
+    const int tail_boxes = (n_last + kTcTailRows - 1) / kTcTailRows;
 
     if (warp == 4) {
         if (lane == 0) {
@@ -144,16 +149,23 @@ km_assign_tc_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_con
             auto issue_b = [&](int s) {
                 const int nt = s / kTcSub, u = s - nt * kTcSub, t = u >> 1, c = u & 1;
                 const unsigned slot = smem_u32(sb + (s % kTcStages) * kTcBBytes);
-                mbar_expect_tx(smem_u32(&bar_full[s % kTcStages]), kTcBBytes);
-                tma_load_2d(slot, &tm_terms, c * 64, t * ws.kpad + c_off + nt * kTcN,
-                            smem_u32(&bar_full[s % kTcStages]));
+                const unsigned fb = smem_u32(&bar_full[s % kTcStages]);
+                const int row = t * ws.kpad + c_off + nt * kTcN;
+                if (nt + 1 < n_nt) {
+                    mbar_expect_tx(fb, kTcBBytes);
+                    tma_load_2d(slot, &tm_terms, c * 64, row, fb);
+                } else {
+                    mbar_expect_tx(fb, tail_boxes * kTcTailRows * 128);
+                    for (int b = 0; b < tail_boxes; ++b)
+                        tma_load_2d(slot + b * kTcTailRows * 128, &tm_terms_tail, c * 64, row + b * kTcTailRows, fb);
+                }
             };
             for (int s = 0; s < kTcStages && s < S; ++s) issue_b(s);
             mbar_wait(smem_u32(&bar_a), 0);
             tc_fence_after();
-            const uint32_t idesc = umma_idesc_bf16_f32(kTcM, kTcN);
             for (int nt = 0; nt < n_nt; ++nt) {
                 const int buf = nt & 1;
+                const uint32_t idesc = umma_idesc_bf16_f32(kTcM, nt + 1 < n_nt ? kTcN : n_last);
                 if (nt >= 2) mbar_wait(smem_u32(&bar_acc_empty[buf]), ((nt - 2) >> 1) & 1);
                 tc_fence_after();
                 for (int u = 0; u < kTcSub; ++u) {
@@ -177,19 +189,25 @@ km_assign_tc_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_con
             }
         }
         __syncwarp();
-    } else {
-        // epilogue: this lane's point = TMEM lane warp*32 + lane
-        const int i = tile * kTcM + warp * 32 + lane;
-        float best = INFINITY, second = INFINITY;
-        int jbest = 0x7fffffff;
+    }
+    // epilogue (warps 0-3 and 5-8): this lane's point = TMEM lane (warp % 4) * 32 + lane; the two
+    // warp groups take the two 128-column halves of every N tile, then merge per point
+    __shared__ float s_best[kTcM], s_second[kTcM];
+    __shared__ int s_jbest[kTcM];
+    const int half = warp > 4 ? 1 : 0, quarter = warp & 3;
+    const int pi = quarter * 32 + lane, i = tile * kTcM + pi;
+    float best = INFINITY, second = INFINITY;
+    int jbest = 0x7fffffff;
+    if (warp != 4) {
         for (int nt = 0; nt < n_nt; ++nt) {
             const int buf = nt & 1;
+            const int ncol = nt + 1 < n_nt ? kTcN : n_last;
             mbar_wait(smem_u32(&bar_acc_full[buf]), (nt >> 1) & 1);
             tc_fence_after();
 #pragma unroll 1
-            for (int c0 = 0; c0 < kTcN; c0 += 32) {
+            for (int c0 = half * (kTcN / 2); c0 < (half + 1) * (kTcN / 2) && c0 < ncol; c0 += 32) {
                 uint32_t v[32];
-                tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + buf * kTcN + c0, v);
+                tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + buf * kTcN + c0, v);
                 tmem_ld_wait();
                 const int jb = nt * kTcN + c0;
 #pragma unroll
@@ -211,16 +229,33 @@ km_assign_tc_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_con
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&bar_acc_empty[buf]));
         }
-        if (i < n) {
-            const int g = km.pt_off[p] + i;
-            const double tau = ldexp(km.p2[g] + ws.c2max[p], -13);
-            if ((double)second - (double)best > 2.0 * tau) {
-                km.assign[g] = jbest;
-            } else {
-                const int r = atomicAdd(ws.n_recheck, 1);
-                ws.recheck[2 * r] = p;
-                ws.recheck[2 * r + 1] = i;
-            }
+        if (half) {
+            s_best[pi] = best;
+            s_second[pi] = second;
+            s_jbest[pi] = jbest;
+        }
+    }
+    __syncthreads();
+    if (warp < 4 && i < n) {
+        // merge with the upper half (its indices are larger within each tile, so ties keep the
+        // first minimum by comparing (value, index))
+        const float b1 = s_best[pi], s1 = s_second[pi];
+        const int j1 = s_jbest[pi];
+        if (b1 < best || (b1 == best && j1 < jbest)) {
+            second = fminf(s1, best);
+            best = b1;
+            jbest = j1;
+        } else {
+            second = fminf(second, b1);
+        }
+        const int g = km.pt_off[p] + i;
+        const double tau = ldexp(km.p2[g] + ws.c2max[p], -13);
+        if ((double)second - (double)best > 2.0 * tau) {
+            km.assign[g] = jbest;
+        } else {
+            const int r = atomicAdd(ws.n_recheck, 1);
+            ws.recheck[2 * r] = p;
+            ws.recheck[2 * r + 1] = i;
         }
     }
     tc_fence_before();
@@ -228,25 +263,29 @@ km_assign_tc_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_con
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
-// exact fp64 re-scoring of the uncertified points: one warp per point, same arithmetic as
-// km_assign_kernel (sequential fp64 dot, (p2 + c2) - 2 dot, first minimum)
-__global__ void km_recheck_kernel(mpa_km km, TcWs ws) {
-    const int warps = gridDim.x * (blockDim.x >> 5);
-    const int lane = threadIdx.x & 31;
+// exact fp64 re-scoring of the uncertified points: one CTA (8 warps) per point, each thread
+// scoring a strided slice of the problem's centroids with the arithmetic of km_assign_kernel
+// (sequential fp64 dot, (p2 + c2) - 2 dot), then a block-wide first minimum over (dist, index).
+// Spreading a point over 256 threads keeps enough fp64 centroid rows in flight (the rows are
+// cold in L2: the tensor-core pass reads the bf16 terms).
+constexpr int kRecheckThreads = 256;
+__global__ void __launch_bounds__(kRecheckThreads) km_recheck_kernel(mpa_km km, TcWs ws) {
     const int nr = *ws.n_recheck;
-    for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < nr; r += warps) {
+    __shared__ double x[128];
+    __shared__ double s_best[kRecheckThreads / 32];
+    __shared__ int s_j[kRecheckThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int r = blockIdx.x; r < nr; r += gridDim.x) {
         const int p = ws.recheck[2 * r], i = ws.recheck[2 * r + 1];
         const int K = km.prob_k[p], d = km.d, l = km.prob_l[p], row = km.prob_start[p] + i;
         const int g = km.pt_off[p] + i;
         const double p2 = km.p2[g];
         const __nv_bfloat16* pt = reinterpret_cast<const __nv_bfloat16*>(km.pts) + ((size_t)l * km.tcap + row) * d;
-        __shared__ double xs[8][128];  // the point, fp64, per warp
-        double* x = xs[threadIdx.x >> 5];
-        for (int k = lane; k < 128; k += 32) x[k] = (double)__bfloat162float(pt[k]);
-        __syncwarp();
+        for (int k = threadIdx.x; k < 128; k += blockDim.x) x[k] = (double)__bfloat162float(pt[k]);
+        __syncthreads();
         double best = INFINITY;
         int jb = 0x7fffffff;
-        for (int j = lane; j < K; j += 32) {
+        for (int j = threadIdx.x; j < K; j += blockDim.x) {
             const double2* c = reinterpret_cast<const double2*>(km.cent + (size_t)(km.c_off[p] + j) * d);
             double dot = 0.0;  // sequential over k, like km_assign_kernel
 #pragma unroll 8
@@ -270,8 +309,20 @@ __global__ void km_recheck_kernel(mpa_km km, TcWs ws) {
                 jb = oj;
             }
         }
-        if (lane == 0) km.assign[g] = jb;
-        __syncwarp();
+        if (lane == 0) {
+            s_best[warp] = best;
+            s_j[warp] = jb;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < kRecheckThreads / 32; ++w)
+                if (s_best[w] < best || (s_best[w] == best && s_j[w] < jb)) {
+                    best = s_best[w];
+                    jb = s_j[w];
+                }
+            km.assign[g] = jb;
+        }
+        __syncthreads();  // x / s_best reused by the next point
     }
 }
 
@@ -325,9 +376,10 @@ int mpa_km_assign_tc(const mpa_km& k, cudaStream_t st) {
     char* base = (char*)k.tc_ws;
     TcWs ws{(__nv_bfloat16*)(base + off[0]), (float*)(base + off[1]), (double*)(base + off[2]),
             (int32_t*)(base + off[3]), (int32_t*)(base + off[4]), kpad};
-    CUtensorMap tp, tt;
+    CUtensorMap tp, tt, tt_tail;
     if (int rc = encode_rows_map(&tp, k.pts, (long long)k.pts_rows, k.d, kTcM)) return rc;
     if (int rc = encode_rows_map(&tt, ws.terms, 3ll * kpad, k.d, kTcN)) return rc;
+    if (int rc = encode_rows_map(&tt_tail, ws.terms, 3ll * kpad, k.d, kTcTailRows)) return rc;
     km_tc_norms_kernel<<<k.n_prob, 256, 0, st>>>(k, ws);
     km_tc_prep_kernel<<<dim3(ceil_div(k.k_max * k.d, 256 * 8), k.n_prob), 256, 0, st>>>(k, ws);
     static bool attr = false;
@@ -335,7 +387,7 @@ int mpa_km_assign_tc(const mpa_km& k, cudaStream_t st) {
         cudaFuncSetAttribute(km_assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
         attr = true;
     }
-    km_assign_tc_kernel<<<dim3(ceil_div(k.n_max, kTcM), k.n_prob), kTcThreads, kTcSmem, st>>>(tp, tt, k, ws);
-    km_recheck_kernel<<<64, 256, 0, st>>>(k, ws);
+    km_assign_tc_kernel<<<dim3(ceil_div(k.n_max, kTcM), k.n_prob), kTcThreads, kTcSmem, st>>>(tp, tt, tt_tail, k, ws);
+    km_recheck_kernel<<<4 * 148, kRecheckThreads, 0, st>>>(k, ws);
     return check_launch("mpa_km_assign(tcgen05)");
 }
