@@ -21,6 +21,8 @@
 // CTA = one (problem, 128-point tile); warp 4 issues TMA + MMA (one elected thread), warps 0-3
 // drain TMEM (one point per lane).  N tiles of 256 centroids, 6 K-major sub-tiles each
 // (3 terms x 2 x 64 columns), a 4-deep TMA ring, double-buffered 256-column accumulators.
+#include <cstdlib>
+
 #include "mpa_common.cuh"
 #include "mpa_tc.cuh"
 
@@ -263,6 +265,240 @@ km_assign_tc_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_con
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+// ---- persistent variant (default): one CTA per SM walks (problem, 128-point tile) items; the A
+// tile is double-buffered and the centroid-term ring runs on across tiles, so TMEM allocation,
+// barrier set-up and the tile's first loads are paid once per SM instead of once per tile.
+constexpr int kTcpSmemFixed = 1024 + 2 * kTcABytes + kTcStages * kTcBBytes;
+
+struct TcTile {
+    int p, m, n, K, c_off, n_nt, n_last, tail_boxes, row0;
+};
+
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(threads) : "memory");
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+km_assign_tcp_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_constant__ CUtensorMap tm_terms,
+                     const __grid_constant__ CUtensorMap tm_terms_tail, mpa_km km, TcWs ws) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    unsigned char* sa = smem;                      // [2][kTcABytes]
+    unsigned char* sb = smem + 2 * kTcABytes;      // [kTcStages][kTcBBytes]
+    int* tp = reinterpret_cast<int*>(sb + kTcStages * kTcBBytes);  // [P + 1] tile prefix
+    __shared__ __align__(8) uint64_t bar_a[2], bar_a_empty[2], bar_full[kTcStages], bar_empty[kTcStages],
+        bar_acc_full[2], bar_acc_empty[2];
+    __shared__ uint32_t tmem_base;
+    __shared__ float s_best[kTcM], s_second[kTcM];
+    __shared__ int s_jbest[kTcM];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int P = km.n_prob;
+    {  // tile prefix over the active problems (every CTA computes the same)
+        __shared__ int scan[33];
+        int base = 0;
+        for (int q0 = 0; q0 < P; q0 += blockDim.x) {
+            const int q = q0 + threadIdx.x;
+            const int nt = q < P && km.state[q * 4 + 0] ? (km.prob_n[q] + kTcM - 1) / kTcM : 0;
+            int tot;
+            const int e = block_exclusive_scan(nt, scan, &tot);
+            if (q < P) tp[q] = base + e;
+            base += tot;
+        }
+        if (threadIdx.x == 0) tp[P] = base;
+    }
+    if (warp == 0) tmem_alloc(&tmem_base, 512);
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&bar_a[b]), 1);
+            mbar_init(smem_u32(&bar_a_empty[b]), 1);
+            mbar_init(smem_u32(&bar_acc_full[b]), 1);
+            mbar_init(smem_u32(&bar_acc_empty[b]), 8);
+        }
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(smem_u32(&bar_full[s]), 1);
+            mbar_init(smem_u32(&bar_empty[s]), 1);
+        }
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    const int T = tp[P];
+    const int my_tiles = blockIdx.x < T ? (T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    auto tile_info = [&](int it) {
+        const int t = blockIdx.x + it * gridDim.x;
+        int lo = 0, hi = P - 1;  // last problem with tp[q] <= t
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (tp[mid] <= t) lo = mid;
+            else hi = mid - 1;
+        }
+        TcTile x;
+        x.p = lo;
+        x.m = t - tp[lo];
+        x.n = km.prob_n[lo];
+        x.K = km.prob_k[lo];
+        x.c_off = km.c_off[lo];
+        x.n_nt = (x.K + kTcN - 1) / kTcN;
+        x.n_last = (x.K - (x.n_nt - 1) * kTcN + 15) & ~15;
+        x.tail_boxes = (x.n_last + kTcTailRows - 1) / kTcTailRows;
+        x.row0 = km.prob_l[lo] * km.tcap + km.prob_start[lo] + x.m * kTcM;
+        return x;
+    };
+
+    if (warp == 4) {
+        if (lane == 0 && my_tiles > 0) {
+            prefetch_tmap(&tm_pts);
+            prefetch_tmap(&tm_terms);
+            prefetch_tmap(&tm_terms_tail);
+            auto issue_a = [&](int it, const TcTile& x) {
+                const unsigned b = smem_u32(&bar_a[it & 1]);
+                mbar_expect_tx(b, kTcABytes);
+                tma_load_2d(smem_u32(sa + (it & 1) * kTcABytes), &tm_pts, 0, x.row0, b);
+                tma_load_2d(smem_u32(sa + (it & 1) * kTcABytes + kTcM * 128), &tm_pts, 64, x.row0, b);
+            };
+            // load walker: the centroid sub-tiles of every tile in MMA order, kTcStages ahead
+            int l_it = 0, l_nt = 0, l_u = 0, l_step = 0;
+            TcTile lx = tile_info(0);
+            auto load_next = [&]() {
+                if (l_it >= my_tiles) return;
+                const int t = l_u >> 1, c = l_u & 1, slot_i = l_step % kTcStages;
+                const unsigned slot = smem_u32(sb + slot_i * kTcBBytes);
+                const unsigned fb = smem_u32(&bar_full[slot_i]);
+                const int row = t * ws.kpad + lx.c_off + l_nt * kTcN;
+                if (l_nt + 1 < lx.n_nt) {
+                    mbar_expect_tx(fb, kTcBBytes);
+                    tma_load_2d(slot, &tm_terms, c * 64, row, fb);
+                } else {
+                    mbar_expect_tx(fb, lx.tail_boxes * kTcTailRows * 128);
+                    for (int b = 0; b < lx.tail_boxes; ++b)
+                        tma_load_2d(slot + b * kTcTailRows * 128, &tm_terms_tail, c * 64, row + b * kTcTailRows, fb);
+                }
+                ++l_step;
+                if (++l_u == kTcSub) {
+                    l_u = 0;
+                    if (++l_nt == lx.n_nt) {
+                        l_nt = 0;
+                        if (++l_it < my_tiles) lx = tile_info(l_it);
+                    }
+                }
+            };
+            issue_a(0, lx);
+            for (int s = 0; s < kTcStages; ++s) load_next();
+            int step = 0, gnt = 0;
+            for (int it = 0; it < my_tiles; ++it) {
+                const TcTile x = tile_info(it);
+                mbar_wait(smem_u32(&bar_a[it & 1]), (it >> 1) & 1);
+                tc_fence_after();
+                for (int nt = 0; nt < x.n_nt; ++nt, ++gnt) {
+                    const int buf = gnt & 1;
+                    const uint32_t idesc = umma_idesc_bf16_f32(kTcM, nt + 1 < x.n_nt ? kTcN : x.n_last);
+                    if (gnt >= 2) mbar_wait(smem_u32(&bar_acc_empty[buf]), ((gnt - 2) >> 1) & 1);
+                    tc_fence_after();
+                    for (int u = 0; u < kTcSub; ++u, ++step) {
+                        const int c = u & 1;
+                        mbar_wait(smem_u32(&bar_full[step % kTcStages]), (step / kTcStages) & 1);
+                        tc_fence_after();
+                        const unsigned bslot = smem_u32(sb + (step % kTcStages) * kTcBBytes);
+                        const unsigned aslot = smem_u32(sa + (it & 1) * kTcABytes + c * kTcM * 128);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            umma_bf16(tmem + buf * kTcN, umma_desc_sw128(aslot + k * 32),
+                                      umma_desc_sw128(bslot + k * 32), idesc, (u | k) ? 1u : 0u);
+                        umma_commit(smem_u32(&bar_empty[step % kTcStages]));
+                        // refill the slot used one step earlier (its MMAs are queued ahead of this step's)
+                        if (step >= 1) {
+                            mbar_wait(smem_u32(&bar_empty[(step - 1) % kTcStages]), ((step - 1) / kTcStages) & 1);
+                            load_next();
+                        }
+                    }
+                    umma_commit(smem_u32(&bar_acc_full[buf]));
+                    if (nt == 0 && it + 1 < my_tiles) {
+                        // next tile's points into the other A buffer once the tile before this one is done
+                        if (it >= 1) mbar_wait(smem_u32(&bar_a_empty[(it + 1) & 1]), ((it - 1) >> 1) & 1);
+                        issue_a(it + 1, tile_info(it + 1));
+                    }
+                }
+                umma_commit(smem_u32(&bar_a_empty[it & 1]));
+            }
+        }
+        __syncwarp();
+    } else {
+        // epilogue: warps 0-3 and 5-8; this lane's point = TMEM lane (warp % 4) * 32 + lane, the two
+        // warp groups take the two 128-column halves of every N tile and merge per point
+        const int half = warp > 4 ? 1 : 0, quarter = warp & 3;
+        const int pi = quarter * 32 + lane;
+        int gnt = 0;
+        for (int it = 0; it < my_tiles; ++it) {
+            const TcTile x = tile_info(it);
+            float best = INFINITY, second = INFINITY;
+            int jbest = 0x7fffffff;
+            for (int nt = 0; nt < x.n_nt; ++nt, ++gnt) {
+                const int buf = gnt & 1;
+                const int ncol = nt + 1 < x.n_nt ? kTcN : x.n_last;
+                mbar_wait(smem_u32(&bar_acc_full[buf]), (gnt >> 1) & 1);
+                tc_fence_after();
+#pragma unroll 1
+                for (int c0 = half * (kTcN / 2); c0 < (half + 1) * (kTcN / 2) && c0 < ncol; c0 += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + buf * kTcN + c0, v);
+                    tmem_ld_wait();
+                    const int jb = nt * kTcN + c0;
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        const int j = jb + q;
+                        if (j < x.K) {
+                            const float dj = __ldg(ws.c2f + x.c_off + j) - 2.f * __uint_as_float(v[q]);
+                            if (dj < best) {
+                                second = best;
+                                best = dj;
+                                jbest = j;
+                            } else if (dj < second) {
+                                second = dj;
+                            }
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&bar_acc_empty[buf]));
+            }
+            if (half) {
+                s_best[pi] = best;
+                s_second[pi] = second;
+                s_jbest[pi] = jbest;
+            }
+            named_bar_sync(1, 256);
+            const int i = x.m * kTcM + pi;
+            if (!half && i < x.n) {
+                const float b1 = s_best[pi], s1 = s_second[pi];
+                const int j1 = s_jbest[pi];
+                if (b1 < best || (b1 == best && j1 < jbest)) {
+                    second = fminf(s1, best);
+                    best = b1;
+                    jbest = j1;
+                } else {
+                    second = fminf(second, b1);
+                }
+                const int g = km.pt_off[x.p] + i;
+                const double tau = ldexp(km.p2[g] + ws.c2max[x.p], -13);
+                if ((double)second - (double)best > 2.0 * tau) {
+                    km.assign[g] = jbest;
+                } else {
+                    const int r = atomicAdd(ws.n_recheck, 1);
+                    ws.recheck[2 * r] = x.p;
+                    ws.recheck[2 * r + 1] = i;
+                }
+            }
+            named_bar_sync(1, 256);  // s_best is rewritten by the next tile
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
 // exact fp64 re-scoring of the uncertified points: one CTA (8 warps) per point, each thread
 // scoring a strided slice of the problem's centroids with the arithmetic of km_assign_kernel
 // (sequential fp64 dot, (p2 + c2) - 2 dot), then a block-wide first minimum over (dist, index).
@@ -387,7 +623,26 @@ int mpa_km_assign_tc(const mpa_km& k, cudaStream_t st) {
         cudaFuncSetAttribute(km_assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
         attr = true;
     }
-    km_assign_tc_kernel<<<dim3(ceil_div(k.n_max, kTcM), k.n_prob), kTcThreads, kTcSmem, st>>>(tp, tt, tt_tail, k, ws);
+    static int oneshot = -1;  // MPA_KM_TC_ONESHOT=1: one CTA per tile (previous kernel)
+    if (oneshot < 0) {
+        const char* e = getenv("MPA_KM_TC_ONESHOT");
+        oneshot = (e && e[0] == '1') ? 1 : 0;
+    }
+    const size_t psmem = kTcpSmemFixed + (size_t)(k.n_prob + 1) * 4;
+    if (!oneshot && psmem <= 227 * 1024) {
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            if (sms <= 0) sms = 148;
+        }
+        cudaFuncSetAttribute(km_assign_tcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+        km_assign_tcp_kernel<<<sms, kTcThreads, psmem, st>>>(tp, tt, tt_tail, k, ws);
+    } else {
+        km_assign_tc_kernel<<<dim3(ceil_div(k.n_max, kTcM), k.n_prob), kTcThreads, kTcSmem, st>>>(tp, tt, tt_tail, k,
+                                                                                                  ws);
+    }
     km_recheck_kernel<<<4 * 148, kRecheckThreads, 0, st>>>(k, ws);
     return check_launch("mpa_km_assign(tcgen05)");
 }
