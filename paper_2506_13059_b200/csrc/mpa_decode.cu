@@ -36,6 +36,8 @@
 #include <climits>
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "mpa_common.cuh"
 
 namespace mpa {
@@ -390,10 +392,12 @@ struct SkGeom {
     static constexpr int kStagesB = NW * kWarpB;
     static constexpr int kLgAllB = NW * NST * kLgB;  // logits of every stage, after the tiles
     static constexpr int kBarB = NW * NST * 8 + kLgAllB;
-    static constexpr int kRing = 8;                  // row-id ring: tiles whose ids are in smem
+    static constexpr int kRing = 4;                  // row-id ring: tiles whose ids are in smem
     static constexpr int kIdB = NW * kRing * 32 * 4;
     static constexpr int kPS = G * (D + 2);          // floats per partial
-    static size_t smem(int L, int C) { return 1024 + (size_t)kStagesB + kBarB + kIdB + sizeof(int) * (3 * L + C + 2); }
+    // 2 CTAs / SM for G <= 8 at L <= 128 ledgers (tp + per-ledger counts: 3 L + 1 ints); the
+    // dynamic window is 1024-aligned (the kernel checks), so no alignment slack is reserved
+    static size_t smem(int L, int C) { (void)C; return (size_t)kStagesB + kBarB + kIdB + sizeof(int) * (3 * L + 1); }
 };
 
 template <int G, int D, int NW, int NST>
@@ -414,7 +418,8 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     constexpr int KS = D / 16;  // k-steps for QK, m-tiles for PV
     constexpr int GP = rej_stride(G);
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    if (smem_u32(smem_raw) & 1023) __trap();  // SWIZZLE_128B stages need the 1024-aligned window
+    unsigned char* smem = smem_raw;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int gr = lane >> 2, tq = lane & 3;
     const int C = gridDim.x, c = blockIdx.x;
@@ -425,7 +430,7 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     // ---- per-ledger tile prefix sum (every CTA computes the same schedule)
     int* tp = reinterpret_cast<int*>(smem + Geo::kStagesB + Geo::kBarB + Geo::kIdB);
     int* idring = reinterpret_cast<int*>(smem + Geo::kStagesB + Geo::kBarB) + w * Geo::kRing * 32;
-    int* cnt_s = tp + (L + 1) + (C + 1);  // [L][2] token / centroid counts
+    int* cnt_s = tp + (L + 1);  // [L][2] token / centroid counts
     if (threadIdx.x == 0) {  // before the PDL wait: nothing here depends on the selection
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_k)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_v)) : "memory");
@@ -466,11 +471,9 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     const int T = tp[L];
     const int Ce = max(1, min(C, T / kMinTiles));
     if (c >= Ce) return;  // surplus CTA: no CTA-wide barrier follows for it
-    int* cbt = tp + (L + 1);  // [Ce + 1] first tile of each CTA
-    for (int cc = threadIdx.x; cc <= Ce; cc += blockDim.x) cbt[cc] = (int)((long long)T * cc / Ce);
-    __syncthreads();
+    auto cbt_at = [&](int cc) -> int { return (int)((long long)T * cc / Ce); };  // first tile of CTA cc
     dbg_stamp(1);
-    auto cta_begin = [&](int cc) -> int { return cbt[cc]; };
+    auto cta_begin = [&](int cc) -> int { return cbt_at(cc); };
     auto ledger_of_tile = [&](int g) -> int {  // largest l with tp[l] <= g
         int lo = 0, hi = L - 1;
         while (lo < hi) {
@@ -858,7 +861,7 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             __shared__ int s_np;
             if (threadIdx.x == 0) {
                 int np = 0;
-                for (int cc = cf; cc < Ce && cbt[cc] < tp[l + 1]; ++cc) ++np;
+                for (int cc = cf; cc < Ce && cbt_at(cc) < tp[l + 1]; ++cc) ++np;
                 s_np = np;
                 const int prev = atomicAdd(ticket + l, 1);
                 s_last = prev == np - 1;
@@ -1171,13 +1174,18 @@ template <int G, int D>
 int launch_sk(const mpa_cache* c, const float* q_rot, const int32_t* tok, const int32_t* n_tok, int tok_cap,
               const int32_t* rej, const float* rej_w, const int32_t* n_rej, int rej_cap, const void* fvc, int fcap,
               const void* cvc, int ccap, int C, float* part, int32_t* ticket, float* out, float* part_out,
-              cudaStream_t st) {
+              cudaStream_t st, bool one_wave) {
     using Geo = SkGeom<G, D, kSkWarps, kSkStages>;
     const int L = c->n_ledgers;
     const size_t smem = Geo::smem(L, C);
     MPA_REQUIRE(smem <= 227 * 1024, MPA_ERR_UNSUPPORTED, "mpa_sparse_decode: %d ledgers exceed the smem schedule", L);
     auto kern = decode_sk_kernel<G, D, kSkWarps, kSkStages>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (one_wave) {  // the stream-K grid is one resident wave (2 CTAs / SM unless smem or registers say less)
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSkWarps * 32, smem);
+        C = std::min(C, std::max(1, occ) * num_sms());
+    }
     CUtensorMap tk, tv, tf, tc, tk16, tv16, tf16;
     int rc = bf16_rows_map(&tk, c->k_rot, (long long)L * c->tcap, D);
     if (!rc) rc = bf16_rows_map(&tv, c->v, (long long)L * c->tcap, D);
@@ -1258,9 +1266,10 @@ static int sparse_decode_impl(const mpa_cache* c, const float* q_rot, int n_kv_h
         MPA_DISPATCH_G(group, {
             if (c->head_dim == 128)
                 return launch_sk<kG, 128>(c, q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej, rej_cap, fine_vc,
-                                          fine_cap, coarse_vc, coarse_cap, C, part, ticket, out, part_out, st);
+                                          fine_cap, coarse_vc, coarse_cap, C, part, ticket, out, part_out, st,
+                                          n_split <= 0);
             return launch_sk<kG, 64>(c, q_rot, tok, n_tok, tok_cap, rej, rej_w, n_rej, rej_cap, fine_vc, fine_cap,
-                                     coarse_vc, coarse_cap, C, part, ticket, out, part_out, st);
+                                     coarse_vc, coarse_cap, C, part, ticket, out, part_out, st, n_split <= 0);
         });
     }
     MPA_REQUIRE(rej || !rej_w, MPA_ERR_UNSUPPORTED,
