@@ -499,6 +499,220 @@ km_assign_tcp_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_co
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+// ---- paired variant (default): an item is TWO 128-point tiles of one problem, so every centroid
+// sub-tile brought from L2 feeds both (half the centroid traffic per point); N tiles of 128
+// columns, TMEM = 2 buffers x 2 point tiles x 128 columns.  Warps 0-3 drain point tile 0, warps
+// 5-8 point tile 1, each thread one point over all columns (no cross-warp merge).
+constexpr int kTc2N = 128;
+constexpr int kTc2BBytes = kTc2N * 128;  // 128 rows x 64 columns
+constexpr int kTc2Stages = 4;
+constexpr int kTc2SmemFixed = 2 * 2 * kTcABytes + kTc2Stages * kTc2BBytes;  // A double buffer x 2 tiles + ring
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_constant__ CUtensorMap tm_terms,
+                     const __grid_constant__ CUtensorMap tm_terms_tail, mpa_km km, TcWs ws) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    if (smem_u32(smem_raw) & 1023) __trap();
+    unsigned char* sa = smem_raw;                         // [2 buffers][2 tiles][kTcABytes]
+    unsigned char* sb = smem_raw + 4 * kTcABytes;         // [kTc2Stages][kTc2BBytes]
+    int* tp = reinterpret_cast<int*>(sb + kTc2Stages * kTc2BBytes);  // [P + 1] item prefix
+    __shared__ __align__(8) uint64_t bar_a[2], bar_a_empty[2], bar_full[kTc2Stages], bar_empty[kTc2Stages],
+        bar_acc_full[2], bar_acc_empty[2];
+    __shared__ uint32_t tmem_base;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int P = km.n_prob;
+    {
+        __shared__ int scan[33];
+        int base = 0;
+        for (int q0 = 0; q0 < P; q0 += blockDim.x) {
+            const int q = q0 + threadIdx.x;
+            const int nt = q < P && km.state[q * 4 + 0] ? (km.prob_n[q] + 2 * kTcM - 1) / (2 * kTcM) : 0;
+            int tot;
+            const int e = block_exclusive_scan(nt, scan, &tot);
+            if (q < P) tp[q] = base + e;
+            base += tot;
+        }
+        if (threadIdx.x == 0) tp[P] = base;
+    }
+    if (warp == 0) tmem_alloc(&tmem_base, 512);
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&bar_a[b]), 1);
+            mbar_init(smem_u32(&bar_a_empty[b]), 1);
+            mbar_init(smem_u32(&bar_acc_full[b]), 1);
+            mbar_init(smem_u32(&bar_acc_empty[b]), 8);
+        }
+        for (int s = 0; s < kTc2Stages; ++s) {
+            mbar_init(smem_u32(&bar_full[s]), 1);
+            mbar_init(smem_u32(&bar_empty[s]), 1);
+        }
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    const int T = tp[P];
+    const int my_items = blockIdx.x < T ? (T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    auto item_info = [&](int it) {
+        const int t = blockIdx.x + it * gridDim.x;
+        int lo = 0, hi = P - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (tp[mid] <= t) lo = mid;
+            else hi = mid - 1;
+        }
+        TcTile x;
+        x.p = lo;
+        x.m = (t - tp[lo]) * 2;  // first of the two 128-point tiles
+        x.n = km.prob_n[lo];
+        x.K = km.prob_k[lo];
+        x.c_off = km.c_off[lo];
+        x.n_nt = (x.K + kTc2N - 1) / kTc2N;
+        x.n_last = (x.K - (x.n_nt - 1) * kTc2N + 15) & ~15;
+        x.tail_boxes = (x.n_last + kTcTailRows - 1) / kTcTailRows;
+        x.row0 = km.prob_l[lo] * km.tcap + km.prob_start[lo] + x.m * kTcM;
+        return x;
+    };
+
+    if (warp == 4) {
+        if (lane == 0 && my_items > 0) {
+            prefetch_tmap(&tm_pts);
+            prefetch_tmap(&tm_terms);
+            prefetch_tmap(&tm_terms_tail);
+            auto issue_a = [&](int it, const TcTile& x) {
+                const unsigned b = smem_u32(&bar_a[it & 1]);
+                unsigned char* dst = sa + (it & 1) * 2 * kTcABytes;
+                mbar_expect_tx(b, 2 * kTcABytes);
+                for (int m = 0; m < 2; ++m) {
+                    tma_load_2d(smem_u32(dst + m * kTcABytes), &tm_pts, 0, x.row0 + m * kTcM, b);
+                    tma_load_2d(smem_u32(dst + m * kTcABytes + kTcM * 128), &tm_pts, 64, x.row0 + m * kTcM, b);
+                }
+            };
+            int l_it = 0, l_nt = 0, l_u = 0, l_step = 0;
+            TcTile lx = item_info(0);
+            auto load_next = [&]() {
+                if (l_it >= my_items) return;
+                const int t = l_u >> 1, c = l_u & 1, slot_i = l_step % kTc2Stages;
+                const unsigned slot = smem_u32(sb + slot_i * kTc2BBytes);
+                const unsigned fb = smem_u32(&bar_full[slot_i]);
+                const int row = t * ws.kpad + lx.c_off + l_nt * kTc2N;
+                if (l_nt + 1 < lx.n_nt) {
+                    mbar_expect_tx(fb, kTc2BBytes);
+                    for (int b = 0; b < kTc2N / kTcTailRows; ++b)
+                        tma_load_2d(slot + b * kTcTailRows * 128, &tm_terms_tail, c * 64, row + b * kTcTailRows, fb);
+                } else {
+                    mbar_expect_tx(fb, lx.tail_boxes * kTcTailRows * 128);
+                    for (int b = 0; b < lx.tail_boxes; ++b)
+                        tma_load_2d(slot + b * kTcTailRows * 128, &tm_terms_tail, c * 64, row + b * kTcTailRows, fb);
+                }
+                ++l_step;
+                if (++l_u == kTcSub) {
+                    l_u = 0;
+                    if (++l_nt == lx.n_nt) {
+                        l_nt = 0;
+                        if (++l_it < my_items) lx = item_info(l_it);
+                    }
+                }
+            };
+            issue_a(0, lx);
+            for (int s = 0; s < kTc2Stages; ++s) load_next();
+            int step = 0, gnt = 0;
+            for (int it = 0; it < my_items; ++it) {
+                const TcTile x = item_info(it);
+                mbar_wait(smem_u32(&bar_a[it & 1]), (it >> 1) & 1);
+                tc_fence_after();
+                for (int nt = 0; nt < x.n_nt; ++nt, ++gnt) {
+                    const int buf = gnt & 1;
+                    const uint32_t idesc = umma_idesc_bf16_f32(kTcM, nt + 1 < x.n_nt ? kTc2N : x.n_last);
+                    if (gnt >= 2) mbar_wait(smem_u32(&bar_acc_empty[buf]), ((gnt - 2) >> 1) & 1);
+                    tc_fence_after();
+                    for (int u = 0; u < kTcSub; ++u, ++step) {
+                        const int c = u & 1;
+                        mbar_wait(smem_u32(&bar_full[step % kTc2Stages]), (step / kTc2Stages) & 1);
+                        tc_fence_after();
+                        const unsigned bslot = smem_u32(sb + (step % kTc2Stages) * kTc2BBytes);
+#pragma unroll
+                        for (int m = 0; m < 2; ++m) {
+                            const unsigned aslot = smem_u32(sa + (it & 1) * 2 * kTcABytes + m * kTcABytes + c * kTcM * 128);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                umma_bf16(tmem + (buf * 2 + m) * kTc2N, umma_desc_sw128(aslot + k * 32),
+                                          umma_desc_sw128(bslot + k * 32), idesc, (u | k) ? 1u : 0u);
+                        }
+                        umma_commit(smem_u32(&bar_empty[step % kTc2Stages]));
+                        if (step >= 1) {
+                            mbar_wait(smem_u32(&bar_empty[(step - 1) % kTc2Stages]), ((step - 1) / kTc2Stages) & 1);
+                            load_next();
+                        }
+                    }
+                    umma_commit(smem_u32(&bar_acc_full[buf]));
+                    if (nt == 0 && it + 1 < my_items) {
+                        if (it >= 1) mbar_wait(smem_u32(&bar_a_empty[(it + 1) & 1]), ((it - 1) >> 1) & 1);
+                        issue_a(it + 1, item_info(it + 1));
+                    }
+                }
+                umma_commit(smem_u32(&bar_a_empty[it & 1]));
+            }
+        }
+        __syncwarp();
+    } else {
+        const int m = warp > 4 ? 1 : 0, quarter = warp & 3;
+        const int pi = quarter * 32 + lane;
+        int gnt = 0;
+        for (int it = 0; it < my_items; ++it) {
+            const TcTile x = item_info(it);
+            float best = INFINITY, second = INFINITY;
+            int jbest = 0x7fffffff;
+            for (int nt = 0; nt < x.n_nt; ++nt, ++gnt) {
+                const int buf = gnt & 1;
+                const int ncol = nt + 1 < x.n_nt ? kTc2N : x.n_last;
+                mbar_wait(smem_u32(&bar_acc_full[buf]), (gnt >> 1) & 1);
+                tc_fence_after();
+#pragma unroll 1
+                for (int c0 = 0; c0 < ncol; c0 += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (buf * 2 + m) * kTc2N + c0, v);
+                    tmem_ld_wait();
+                    const int jb = nt * kTc2N + c0;
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        const int j = jb + q;
+                        if (j < x.K) {
+                            const float dj = __ldg(ws.c2f + x.c_off + j) - 2.f * __uint_as_float(v[q]);
+                            if (dj < best) {
+                                second = best;
+                                best = dj;
+                                jbest = j;
+                            } else if (dj < second) {
+                                second = dj;
+                            }
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&bar_acc_empty[buf]));
+            }
+            const int i = (x.m + m) * kTcM + pi;
+            if (i < x.n) {
+                const int g = km.pt_off[x.p] + i;
+                const double tau = ldexp(km.p2[g] + ws.c2max[x.p], -13);
+                if ((double)second - (double)best > 2.0 * tau) {
+                    km.assign[g] = jbest;
+                } else {
+                    const int r = atomicAdd(ws.n_recheck, 1);
+                    ws.recheck[2 * r] = x.p;
+                    ws.recheck[2 * r + 1] = i;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
 // exact fp64 re-scoring of the uncertified points: one CTA (8 warps) per point, each thread
 // scoring a strided slice of the problem's centroids with the arithmetic of km_assign_kernel
 // (sequential fp64 dot, (p2 + c2) - 2 dot), then a block-wide first minimum over (dist, index).
@@ -629,7 +843,24 @@ int mpa_km_assign_tc(const mpa_km& k, cudaStream_t st) {
         oneshot = (e && e[0] == '1') ? 1 : 0;
     }
     const size_t psmem = kTcpSmemFixed + (size_t)(k.n_prob + 1) * 4;
-    if (!oneshot && psmem <= 227 * 1024) {
+    static int paired = -1;  // MPA_KM_TC_PAIRED=0: single-tile persistent kernel
+    if (paired < 0) {
+        const char* e = getenv("MPA_KM_TC_PAIRED");
+        paired = (e && e[0] == '0') ? 0 : 1;
+    }
+    const size_t psmem2 = kTc2SmemFixed + (size_t)(k.n_prob + 1) * 4;
+    constexpr size_t kSmemCap = 227 * 1024 - 2048;  // leaves room for the kernels' static shared memory
+    if (!oneshot && paired && psmem2 <= kSmemCap) {
+        static int sms2 = 0;
+        if (!sms2) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev);
+            if (sms2 <= 0) sms2 = 148;
+        }
+        cudaFuncSetAttribute(km_assign_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem2);
+        km_assign_tc2_kernel<<<sms2, kTcThreads, psmem2, st>>>(tp, tt, tt_tail, k, ws);
+    } else if (!oneshot && psmem <= kSmemCap) {
         static int sms = 0;
         if (!sms) {
             int dev = 0;
