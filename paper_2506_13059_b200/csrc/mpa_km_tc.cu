@@ -516,6 +516,9 @@ km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_co
     unsigned char* sa = smem_raw;                         // [2 buffers][2 tiles][kTcABytes]
     unsigned char* sb = smem_raw + 4 * kTcABytes;         // [kTc2Stages][kTc2BBytes]
     int* tp = reinterpret_cast<int*>(sb + kTc2Stages * kTc2BBytes);  // [P + 1] item prefix
+    // the epilogue's ||c||^2 row of the current / next item, double-buffered (16-byte aligned)
+    const int kmax_pad = (km.k_max + 31) & ~31;
+    float* c2s = reinterpret_cast<float*>(tp + ((km.n_prob + 1 + 3) & ~3));  // [2][kmax_pad]
     __shared__ __align__(8) uint64_t bar_a[2], bar_a_empty[2], bar_full[kTc2Stages], bar_empty[kTc2Stages],
         bar_acc_full[2], bar_acc_empty[2];
     __shared__ uint32_t tmem_base;
@@ -659,9 +662,19 @@ km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_co
     } else {
         const int m = warp > 4 ? 1 : 0, quarter = warp & 3;
         const int pi = quarter * 32 + lane;
+        const int et = (warp > 4 ? warp - 1 : warp) * 32 + lane;  // 0..255 over the epilogue warps
+        auto stage_c2 = [&](int it) {
+            const TcTile y = item_info(it);
+            float* dst = c2s + (it & 1) * kmax_pad;
+            for (int j = et; j < y.K; j += 256) dst[j] = __ldg(ws.c2f + y.c_off + j);
+        };
+        if (my_items > 0) stage_c2(0);
+        named_bar_sync(1, 256);
         int gnt = 0;
         for (int it = 0; it < my_items; ++it) {
             const TcTile x = item_info(it);
+            if (it + 1 < my_items) stage_c2(it + 1);  // read only after the barrier ending this item
+            const float* c2b = c2s + (it & 1) * kmax_pad;
             float best = INFINITY, second = INFINITY;
             int jbest = 0x7fffffff;
             for (int nt = 0; nt < x.n_nt; ++nt, ++gnt) {
@@ -675,11 +688,20 @@ km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_co
                     tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (buf * 2 + m) * kTc2N + c0, v);
                     tmem_ld_wait();
                     const int jb = nt * kTc2N + c0;
+                    float c2v[32];
+#pragma unroll
+                    for (int q4 = 0; q4 < 8; ++q4) {
+                        const float4 t4 = reinterpret_cast<const float4*>(c2b + jb)[q4];
+                        c2v[4 * q4] = t4.x;
+                        c2v[4 * q4 + 1] = t4.y;
+                        c2v[4 * q4 + 2] = t4.z;
+                        c2v[4 * q4 + 3] = t4.w;
+                    }
 #pragma unroll
                     for (int q = 0; q < 32; ++q) {
                         const int j = jb + q;
                         if (j < x.K) {
-                            const float dj = __ldg(ws.c2f + x.c_off + j) - 2.f * __uint_as_float(v[q]);
+                            const float dj = c2v[q] - 2.f * __uint_as_float(v[q]);
                             if (dj < best) {
                                 second = best;
                                 best = dj;
@@ -706,6 +728,7 @@ km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_co
                     ws.recheck[2 * r + 1] = i;
                 }
             }
+            named_bar_sync(1, 256);  // this item's c2 buffer is free; the next item's is complete
         }
     }
     tc_fence_before();
@@ -848,7 +871,7 @@ int mpa_km_assign_tc(const mpa_km& k, cudaStream_t st) {
         const char* e = getenv("MPA_KM_TC_PAIRED");
         paired = (e && e[0] == '0') ? 0 : 1;
     }
-    const size_t psmem2 = kTc2SmemFixed + (size_t)(k.n_prob + 1) * 4;
+    const size_t psmem2 = kTc2SmemFixed + (size_t)((k.n_prob + 1 + 3) & ~3) * 4 + 2 * (size_t)((k.k_max + 31) & ~31) * 4;
     constexpr size_t kSmemCap = 227 * 1024 - 2048;  // leaves room for the kernels' static shared memory
     if (!oneshot && paired && psmem2 <= kSmemCap) {
         static int sms2 = 0;
