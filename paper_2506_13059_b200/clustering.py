@@ -291,30 +291,34 @@ def online_update(eng, seqs, cursor: int) -> dict:
     for s in seqs:
         if eng.cache_len[s] - eng.buffer_start[s] < 2 * L:
             raise RuntimeError(f"buffer underflow: have {eng.cache_len[s] - eng.buffer_start[s]} tokens, need {2 * L}")
-    probs, tails = [], []
-    old_src, old_dst, new_src, new_dst = [], [], [], []
-    c_at = 0
-    samples = {}  # the draw depends on (seed, cursor, kv-head) only (pipeline.py:170-172): once per head
-    for l in ledgers:
-        s = l // eng.Hkv
-        F = led.blocks[l][-1]
-        bs = int(eng.buffer_start[s])
-        h = _head(eng, l)
-        if h not in samples:
-            samples[h] = update_rng(cfg.seed, cursor, h).choice(L, size=n_new, replace=False)
-        samp = samples[h]
-        # problem centroids: the final block's clusters, then the sampled tokens (clustering.py:430-434)
-        old_src.append(l * led.kcap + F.f0 + np.arange(F.fk))
-        old_dst.append(c_at + np.arange(F.fk))
-        new_src.append(l * eng.tcap + bs + samp)
-        new_dst.append(c_at + F.fk + np.arange(n_new))
-        c_at += F.fk + n_new
-        probs.append((l, F.start, bs + L - F.start, F.fk + n_new))
-        tails.append(bs - F.start)
+    # per-ledger problem layout, vectorised over the ledgers (clustering.py:430-434): problem
+    # centroids = the final block's clusters, then the sampled buffer tokens
+    Ls = np.asarray(ledgers, np.int64)
+    S = Ls // eng.Hkv
+    fin = [led.blocks[l][-1] for l in ledgers]
+    F0 = np.fromiter((r.f0 for r in fin), np.int64, len(fin))
+    FK = np.fromiter((r.fk for r in fin), np.int64, len(fin))
+    FS = np.fromiter((r.start for r in fin), np.int64, len(fin))
+    BS = eng.buffer_start[S].astype(np.int64)
+    # the draw depends on (seed, cursor, kv-head) only (pipeline.py:170-172): once per head
+    samp_tab = np.stack([update_rng(cfg.seed, cursor, h).choice(L, size=n_new, replace=False)
+                         for h in range(eng.Hkv)]).astype(np.int64)
+    SAMP = samp_tab[Ls % eng.Hkv]                                    # [n, n_new]
+    base = np.concatenate([[0], np.cumsum(FK + n_new)[:-1]]).astype(np.int64)
+    c_at = int((FK + n_new).sum())
+    intra = np.arange(int(FK.sum()), dtype=np.int64) - np.repeat(np.cumsum(FK) - FK, FK)
+    old_src = np.repeat(Ls * led.kcap + F0, FK) + intra
+    old_dst = np.repeat(base, FK) + intra
+    new_src = ((Ls * eng.tcap + BS)[:, None] + SAMP).ravel()
+    new_dst = ((base + FK)[:, None] + np.arange(n_new, dtype=np.int64)).ravel()
+    probs = list(zip(Ls.tolist(), FS.tolist(), (BS + L - FS).tolist(), (FK + n_new).tolist()))
+    tails = (BS - FS).tolist()
     dev = eng.device
     tick("loop")
-    idx = lambda parts: torch.as_tensor(np.concatenate(parts), dtype=torch.int64, device=dev)
-    osrc, odst, nsrc, ndst = idx(old_src), idx(old_dst), idx(new_src), idx(new_dst)
+    allidx = torch.as_tensor(np.concatenate([old_src, old_dst, new_src, new_dst]), dtype=torch.int64, device=dev)
+    no, nn = old_src.size, new_src.size
+    osrc, odst = allidx[:no], allidx[no:2 * no]
+    nsrc, ndst = allidx[2 * no:2 * no + nn], allidx[2 * no + nn:]
     tick("idx")
     init = torch.empty(c_at, eng.d, dtype=torch.float64, device=dev)
     init[odst] = led.kc64.view(-1, eng.d)[osrc]
