@@ -77,6 +77,11 @@ int mpa_kv_append(const mpa_cache* cache, const float* k_src, const float* v_src
                   int32_t* cache_len, int32_t* ntok_dense, const double* inv_freq, int32_t* ticket,
                   void* stream);
 
+/* Step-input staging: copies three fp32 device buffers (a decode step's q, k, v into the buffers
+ * a captured step graph reads) in one launch.  Sizes in elements; any may be 0. */
+int mpa_stage3(float* dst0, const float* src0, long long n0, float* dst1, const float* src1, long long n1,
+               float* dst2, const float* src2, long long n2, void* stream);
+
 /* K1 -- rotate queries: q_rot = rotate(q, qpos[seq]) * scale (fp32, exact view) and
  * q_lk = rotate(q, delta) (fp64, lookup view; rope.py:66-68).  q: fp32 [n_seq, n_qh, d].
  * Either output may be NULL (not both): the views are independent. */

@@ -9,6 +9,7 @@
 // fused decode kernel reads exactly 2*d*sizeof(T) bytes per exact token. Angles are
 // fp64 (pos * inv_freq with inv_freq computed by numpy on the host, identical bits to
 // the reference), sincos in fp64, result rounded once to the cache dtype.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -125,9 +126,39 @@ __global__ void rotate_queries_kernel(const float* __restrict__ q, int n_qh, int
     }
 }
 
+__global__ void stage3_kernel(float4* __restrict__ d0, const float4* __restrict__ s0, long long n0,
+                              float4* __restrict__ d1, const float4* __restrict__ s1, long long n1,
+                              float4* __restrict__ d2, const float4* __restrict__ s2, long long n2) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n0 + n1 + n2; i += stride) {
+        if (i < n0) d0[i] = s0[i];
+        else if (i < n0 + n1) d1[i - n0] = s1[i - n0];
+        else d2[i - n0 - n1] = s2[i - n0 - n1];
+    }
+}
+
 }  // namespace mpa
 
 using namespace mpa;
+
+extern "C" int mpa_stage3(float* dst0, const float* src0, long long n0, float* dst1, const float* src1, long long n1,
+                          float* dst2, const float* src2, long long n2, void* stream) {
+    const float* srcs[3] = {src0, src1, src2};
+    float* dsts[3] = {dst0, dst1, dst2};
+    const long long ns[3] = {n0, n1, n2};
+    for (int i = 0; i < 3; ++i) {
+        MPA_REQUIRE(ns[i] >= 0 && ns[i] % 4 == 0, MPA_ERR_ARG, "mpa_stage3: size %lld not a multiple of 4", ns[i]);
+        MPA_REQUIRE(!ns[i] || (srcs[i] && dsts[i] && ((uintptr_t)srcs[i] & 15) == 0 && ((uintptr_t)dsts[i] & 15) == 0),
+                    MPA_ERR_ARG, "mpa_stage3: buffer %d null or not 16-byte aligned", i);
+    }
+    const long long v = (n0 + n1 + n2) / 4;
+    if (!v) return 0;
+    const int blocks = (int)std::min<long long>(1184, (v + 255) / 256);
+    stage3_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((float4*)dst0, (const float4*)src0, n0 / 4, (float4*)dst1,
+                                                            (const float4*)src1, n1 / 4, (float4*)dst2,
+                                                            (const float4*)src2, n2 / 4);
+    return check_launch("mpa_stage3");
+}
 
 extern "C" const char* mpa_last_error(void) { return g_err; }
 

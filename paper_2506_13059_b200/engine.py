@@ -352,7 +352,12 @@ class DecodeEngine:
                 self._gq.copy_(q, non_blocking=True)
                 self._gk.copy_(k_new[:, :, None], non_blocking=True)
                 self._gv.copy_(v_new[:, :, None], non_blocking=True)
-            else:  # (torch._foreach_copy_ measured 6 us slower than the three copies)
+            elif all(x.is_cuda and x.dtype == torch.float32 and x.is_contiguous() and x.numel() % 4 == 0
+                     and x.data_ptr() % 16 == 0 for x in (q, k_new, v_new)):
+                # one launch stages q, k, v into the graph's input buffers
+                call("mpa_stage3", ptr(self._gq), ptr(q), q.numel(), ptr(self._gk), ptr(k_new), k_new.numel(),
+                     ptr(self._gv), ptr(v_new), v_new.numel(), stream_ptr())
+            else:
                 self._gq.copy_(q)
                 self._gk.copy_(k_new[:, :, None])
                 self._gv.copy_(v_new[:, :, None])
