@@ -429,8 +429,8 @@ def main():
     fev = []
     for i in range(K):
         flush(i)
-        eng.rotate(Q[i])
-        eng.lookup()
+        eng.rotate(Q[i], exact=True, lookup=False)
+        eng.lookup(Q[i])
         a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         eng.fused()
@@ -438,7 +438,7 @@ def main():
         fev.append((a, z))
     torch.cuda.synchronize()
     fused_step_avg = float(np.mean([a.elapsed_time(z) for a, z in fev]))
-    lookup_ms = timed(lambda i: (eng.rotate(Q[0]), eng.lookup()), K)
+    lookup_ms = timed(lambda i: eng.lookup(Q[0]), K)  # lookup-view rotation (fused or not) + logits + select
     nbytes = decode_bytes(fstats, scored, d, G, 2)
     fused_avg = float(np.mean(fused_ms))
 

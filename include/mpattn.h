@@ -99,11 +99,14 @@ int mpa_rotate_queries(const float* q, int n_seq, int n_qh, int d, const int32_t
  * rej_w (optional; flat level, bf16, d = 128, with chunk_stats): [L, rej_cap, GP] fp32 replacement
  * weights of EVERY candidate, rej_w[l, i, g] = logit + ln(size) -- the contiguous-centroid work
  * list of mpa_select_worklist (rej == NULL) then masks the selected ones; with rej_w the fp64
- * logits output is optional (NULL: not written -- the selection reads e_local and chunk_stats). */
+ * logits output is optional (NULL: not written -- the selection reads e_local and chunk_stats).
+ * q_lk == NULL (bf16, d = 128): the kernel forms the lookup view itself from the fp32 queries q_raw
+ * [n_seq, Hq, d] and cs_lk [d/2][2] = (cos, sin)(delta * inv_freq) -- the rotation kernel leaves the
+ * critical path. */
 int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group, int d,
                         const mpa_level* lv, const int32_t* cand, const int32_t* n_cand,
                         int cand_cap, double* logits, double* chunk_stats, double* e_local, int n_max,
-                        float* rej_w, int rej_cap, void* stream);
+                        float* rej_w, int rej_cap, const float* q_raw, const double* cs_lk, void* stream);
 
 /* K10 -- Eq. 1 scores and budgeted greedy selection (attention.py:192-207, 267-290).
  * Scores: e_g,i = exp(l_g,i - max_g), Z_g = sum over candidates AND live extras of N * e,

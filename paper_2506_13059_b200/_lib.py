@@ -54,7 +54,7 @@ _SIGS = {
     "mpa_kv_append": [C.POINTER(MpaCache), _vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp],
     "mpa_rotate_queries": [_vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int, _vp, _f32, _vp, _vp, _vp],
     "mpa_centroid_logits": [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(MpaLevel), _vp, _vp, C.c_int, _vp, _vp,
-                            _vp, C.c_int, _vp, C.c_int, _vp],
+                            _vp, C.c_int, _vp, C.c_int, _vp, _vp, _vp],
     "mpa_select": [_vp, C.c_int, _vp, _vp, C.c_int, _vp, C.c_int, _vp, _vp, _vp, _vp, C.c_int, _vp, C.c_int,
                    _vp, _vp, _vp, _vp, C.c_int, _vp],
     "mpa_select_worklist": [C.POINTER(MpaLevel), C.POINTER(MpaLevel), C.c_int, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp,

@@ -578,7 +578,8 @@ using namespace mpa;
 // serving kernels (mpa_select.cu)
 int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* lv, const int32_t* cand,
                          const int32_t* n_cand, int cand_cap, double* logits, double* chunk_stats, double* e_local,
-                         int n_chunks, int n_max, float* rej_w, int rej_cap, cudaStream_t st);
+                         int n_chunks, int n_max, float* rej_w, int rej_cap, const float* q_raw,
+                         const double* cs_lk, cudaStream_t st);
 size_t mpa_select_v2_smem(int n_max);
 int mpa_launch_select_v2(const double* logits, const double* e_local, int group, const int32_t* cand,
                          const int32_t* n_cand, int cand_cap, const int32_t* lv_size, int lv_cap,
@@ -609,8 +610,9 @@ static int g_logits_tiled = -1;
 extern "C" int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group, int d, const mpa_level* lv,
                                    const int32_t* cand, const int32_t* n_cand, int cand_cap, double* logits,
                                    double* chunk_stats, double* e_local, int n_max, float* rej_w, int rej_cap,
-                                   void* stream) {
-    MPA_REQUIRE(q_lk && lv && lv->kc && lv->count, MPA_ERR_ARG, "mpa_centroid_logits: null argument");
+                                   const float* q_raw, const double* cs_lk, void* stream) {
+    MPA_REQUIRE((q_lk || (q_raw && cs_lk)) && lv && lv->kc && lv->count, MPA_ERR_ARG,
+                "mpa_centroid_logits: null argument");
     MPA_REQUIRE(logits || rej_w, MPA_ERR_ARG, "mpa_centroid_logits: logits may be NULL only with rej_w");
     MPA_REQUIRE(!cand || n_cand, MPA_ERR_ARG, "mpa_centroid_logits: cand without n_cand");
     MPA_REQUIRE(cand ? cand_cap >= 1 : cand_cap >= lv->cap, MPA_ERR_ARG, "mpa_centroid_logits: cand_cap %d too small",
@@ -627,8 +629,10 @@ extern "C" int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group
     }
     if (g_logits_tiled && (d == 64 || d == 128) && lv->dtype == MPA_BF16 && !lookup_v1())
         return mpa_launch_logits_v2(q_lk, group, d, lv, cand, n_cand, cand_cap, logits, chunk_stats, e_local,
-                                    ceil_div(cap, kChunk), n_max > 0 && n_max < cap ? n_max : cap, rej_w, rej_cap, st);
+                                    ceil_div(cap, kChunk), n_max > 0 && n_max < cap ? n_max : cap, rej_w, rej_cap,
+                                    q_lk ? nullptr : q_raw, q_lk ? nullptr : cs_lk, st);
     MPA_REQUIRE(!rej_w, MPA_ERR_UNSUPPORTED, "mpa_centroid_logits: rej_w needs the bf16 TMA path");
+    MPA_REQUIRE(q_lk, MPA_ERR_UNSUPPORTED, "mpa_centroid_logits: the fused lookup rotation needs the bf16 TMA path");
     if (g_logits_tiled && (d == 64 || d == 128)) {
         const int nch = ceil_div(cap, kChunk);
         dim3 grid(nch, L);

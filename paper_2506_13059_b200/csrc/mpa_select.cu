@@ -267,8 +267,11 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
                   const int32_t* __restrict__ lv_size, const int32_t* __restrict__ cand,
                   const int32_t* __restrict__ n_cand, int cand_cap, double* __restrict__ logits,
                   double* __restrict__ cstats, double* __restrict__ e_local, int n_chunks,
-                  float* __restrict__ rej_w, int rej_cap) {
-    constexpr int D = 128, QD = 32, QRow = QD + 2;  // q slot: 32 dims (+16 B pad) per (head, quarter)
+                  float* __restrict__ rej_w, int rej_cap, const float* __restrict__ q_raw,
+                  const double* __restrict__ cs_lk) {
+    constexpr int D = 128, QD = 32, QRow = QD + 2;
+    // cs_lk != NULL: the lookup view q_lk = rotate(q_raw, delta) is formed here from the fp32 query
+    // and the (cos, sin) table of delta * inv_freq (rope.py:66-68), instead of read from q_lk  // q slot: 32 dims (+16 B pad) per (head, quarter)
     extern __shared__ __align__(1024) unsigned char sm_raw[];
     unsigned char* tile = sm_raw + ((1024 - (smem_u32(sm_raw) & 1023)) & 1023);  // [2 halves][128][128 B]
     double* qs = reinterpret_cast<double*>(tile + 2 * kLgChunk * 128);          // [G][4][QRow]
@@ -304,7 +307,7 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
     if (tid < 32) {
         if (tid == 0) {
             // one expect_tx (a single arrive) for everything this barrier phase receives
-            mbar_expect_tx(smem_u32(&bar), G * 4 * QD * 8 + 2 * kLgChunk * 128);
+            mbar_expect_tx(smem_u32(&bar), (cs_lk ? 0 : G * 4 * QD * 8) + 2 * kLgChunk * 128);
             if (!cand) {  // centroid rows first: they do not depend on the predecessor
                 const int row0 = l * kcap + i0;
                 tma_load_2d(smem_u32(tile), &tm_tile, 0, row0, smem_u32(&bar));
@@ -312,7 +315,7 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
                 pdl_wait();
             }
             // q_lk rows of the GQA group: one 256 B bulk copy per (head, quarter) into padded slots
-            for (int j = 0; j < G * 4; ++j)
+            for (int j = 0; j < (cs_lk ? 0 : G * 4); ++j)
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                         smem_u32(qs + j * QRow)),
@@ -337,6 +340,21 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
                     "r"(id[3]), "r"(smem_u32(&bar))
                     : "memory");
         }
+    }
+    if (cs_lk) {
+        // rotate the group's G query rows at delta straight into the padded q slots (the same
+        // arithmetic as mpa_rotate_queries: x cos - y sin, x sin + y cos, no contraction)
+        pdl_wait();
+        double* qw = const_cast<double*>(qs);
+        for (int e = tid; e < G * (D / 2); e += kLgThreads) {
+            const int g = e / (D / 2), i = e - g * (D / 2), k = 2 * i;
+            const float2 xy = *reinterpret_cast<const float2*>(q_raw + ((size_t)l * G + g) * D + k);
+            const double x = (double)xy.x, y = (double)xy.y, c = cs_lk[2 * i], sn = cs_lk[2 * i + 1];
+            double* slot = qw + (g * 4 + k / QD) * QRow + (k % QD);
+            slot[0] = __dsub_rn(__dmul_rn(x, c), __dmul_rn(y, sn));
+            slot[1] = __dadd_rn(__dmul_rn(x, sn), __dmul_rn(y, c));
+        }
+        __syncthreads();
     }
     mbar_wait(smem_u32(&bar), 0);
     pdl_trigger();  // after thread 0's wait (the barrier above completes only after it)
@@ -1369,7 +1387,8 @@ static int encode_bf16_rows(CUtensorMap* out, const void* base, long long rows, 
 
 int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* lv, const int32_t* cand,
                          const int32_t* n_cand, int cand_cap, double* logits, double* chunk_stats, double* e_local,
-                         int n_chunks, int n_max, float* rej_w, int rej_cap, cudaStream_t st) {
+                         int n_chunks, int n_max, float* rej_w, int rej_cap, const float* q_raw, const double* cs_lk,
+                         cudaStream_t st) {
     const int L = lv->n_ledgers;
     // items: ledgers x the chunks any ledger can use (n_max bounds the live candidates); chunk
     // stats rows past them are written -inf once per ledger by the last items
@@ -1399,6 +1418,8 @@ int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* 
                                              item_chunks, L);                                                      \
     }
     if (grid <= 0) return 0;
+    MPA_REQUIRE(!cs_lk || (d == 128 && !persist && q_raw), MPA_ERR_UNSUPPORTED,
+                "mpa_centroid_logits: the fused lookup rotation needs the d = 128 TMA path");
     MPA_REQUIRE(!rej_w || (d == 128 && !persist && !cand && chunk_stats && rej_cap >= lv->cap), MPA_ERR_UNSUPPORTED,
                 "mpa_centroid_logits: per-candidate replacement weights need the flat d = 128 TMA path");
     static int oneshot = -1;  // MPA_LOGITS_TMA_PERSIST=1: the persistent TMA ring (measured slower)
@@ -1406,7 +1427,7 @@ int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* 
         const char* e = getenv("MPA_LOGITS_TMA_PERSIST");
         oneshot = (e && e[0] == '1') ? 0 : 1;
     }
-    if (d == 128 && !persist && !oneshot) {
+    if (d == 128 && !persist && !oneshot && !cs_lk) {
         CUtensorMap tt, tr;
         if (int rc = encode_bf16_rows(&tt, lv->kc, (long long)L * lv->cap, 128, kLgChunk)) return rc;
         if (int rc = encode_bf16_rows(&tr, lv->kc, (long long)L * lv->cap, 128, 1)) return rc;
@@ -1431,7 +1452,7 @@ int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* 
             const size_t smem = 1024 + 2 * kLgChunk * 128 + sizeof(double) * (kG * 4 * 34 + kG * kLgChunk);
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             launch_pdl(kern, g2, dim3(kLgThreads), smem, st, tt, tr, q_lk, lv->cap, lv->count, lv->size, cand, n_cand,
-                       cand_cap, logits, chunk_stats, e_local, n_chunks, rej_w, rej_cap);
+                       cand_cap, logits, chunk_stats, e_local, n_chunks, rej_w, rej_cap, q_raw, cs_lk);
         });
         return check_launch("mpa_centroid_logits(tma)");
     }

@@ -58,6 +58,10 @@ class DecodeEngine:
         self.v = torch.zeros(L, tcap, d, dtype=dtype, **z)
         self.led = DeviceLedgers(L, d, tcap, self.kcap, self.ccap, dtype, hier, dev)
         self.inv_freq = torch.as_tensor(inv_freq(d, cfg.rope_theta), dtype=torch.float64, device=dev)
+        # (cos, sin) of the lookup view's fixed angles delta * inv_freq (rope.py:66-68, numpy like the
+        # reference): lets the logits kernel rotate the queries itself
+        ang = float(cfg.window_offset) * inv_freq(d, cfg.rope_theta)
+        self.cs_lk = torch.as_tensor(np.stack([np.cos(ang), np.sin(ang)], axis=-1), dtype=torch.float64, device=dev)
         # per-sequence scalars (host mirror + device copy)
         self.cache_len = np.zeros(n_seq, np.int64)
         self.sink_end = np.zeros(n_seq, np.int64)
@@ -182,9 +186,23 @@ class DecodeEngine:
             self.invalidate_graph()
         return self._bf, self._bc
 
-    def lookup(self) -> None:
-        """K9 + K10 + work lists for the current q_lk (flat or hierarchical)."""
+    def _fused_rotation(self) -> bool:
+        """MPA_FUSED_ROTATE=1: the flat bf16 d = 128 path forms the lookup view inside the logits
+        kernel (measured 10 us slower per C2 step than the separate rotation kernel: every chunk CTA
+        then waits for its query rows before computing)."""
+        return (self.cfg.hierarchy is None and self.dtype == torch.bfloat16 and self.d == 128
+                and not self.led.lookup_f64 and os.environ.get("MPA_FUSED_ROTATE") == "1")
+
+    def lookup(self, q: torch.Tensor | None = None) -> None:
+        """K9 + K10 + work lists (flat or hierarchical) for q_lk, or -- q given, fused path -- for
+        the lookup view of the fp32 queries q formed inside the logits kernel."""
         st = stream_ptr()
+        qraw = None
+        if q is not None:
+            if self._fused_rotation():
+                qraw = q.float().contiguous()
+            else:
+                self.rotate(q, exact=False, lookup=True)
         self._bound_fine, self._bound_coarse = self._cluster_bounds()
         G, L = self.G, self.L
         fine = self.led.fine_level()
@@ -198,8 +216,9 @@ class DecodeEngine:
                 raise ConfigError("ledger has no clusters")
             dense = self.rej_dense and el is not None
             lg = None if dense else ptr(self.logits)  # the contiguous-centroid list never reads them
-            call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, None, None, self.kcap,
-                 lg, ptr(cs), ptr(el), self._bound_fine, ptr(self.rej_w) if dense else None, self.rej_cap, st)
+            call("mpa_centroid_logits", None if qraw is not None else ptr(self.q_lk), self.Hkv, G, self.d, fine, None,
+                 None, self.kcap, lg, ptr(cs), ptr(el), self._bound_fine, ptr(self.rej_w) if dense else None,
+                 self.rej_cap, ptr(qraw), ptr(self.cs_lk) if qraw is not None else None, st)
             call("mpa_select_worklist", fine, None, G, lg, ptr(el), None, None, self.kcap, ptr(cs),
                  None, None,
                  ptr(self.budget), ptr(self.sink_end_d), ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv,
@@ -213,13 +232,13 @@ class DecodeEngine:
             ccs = self.ccstats if tiled else None
             cel = self.celocal if el is not None else None
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, coarse, None, None, self.ccap,
-                 ptr(self.clogits), ptr(ccs), ptr(cel), self._bound_coarse, None, 0, st)
+                 ptr(self.clogits), ptr(ccs), ptr(cel), self._bound_coarse, None, 0, None, None, st)
             call("mpa_select", ptr(self.clogits), G, None, ptr(self.led.ccount), self.ccap, ptr(self.led.csize),
                  self.ccap, None, None, None, None, 0, ptr(self.cbudget), L, ptr(self.cflag),
                  ptr(self.csel_tokens), ptr(ccs), ptr(cel), self._bound_coarse, st)
             call("mpa_hier_candidates", coarse, ptr(self.cflag), L, ptr(self.cand), ptr(self.n_cand), self.kcap, st)
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, ptr(self.cand), ptr(self.n_cand),
-                 self.kcap, ptr(self.logits), ptr(cs), ptr(el), self._bound_fine, None, 0, st)
+                 self.kcap, ptr(self.logits), ptr(cs), ptr(el), self._bound_fine, None, 0, None, None, st)
             call("mpa_select_worklist", fine, coarse, G, ptr(self.logits), ptr(el), ptr(self.cand), ptr(self.n_cand),
                  self.kcap, ptr(cs), ptr(self.cflag), ptr(self.clogits), ptr(self.budget), ptr(self.sink_end_d),
                  ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv, L, replacement, ptr(self.flag),
@@ -252,8 +271,8 @@ class DecodeEngine:
         """One multipole decode step over the current cache; q fp32 [n_seq, Hq, d] (device)."""
         if self.mode == "oracle":
             return self.attend_dense(q, n_split)
-        self.rotate(q)
-        self.lookup()
+        self.rotate(q, exact=True, lookup=False)
+        self.lookup(q)
         return self.fused(n_split)
 
     def attend_dense(self, q: torch.Tensor, n_split: int | None = None) -> torch.Tensor:
@@ -317,8 +336,7 @@ class DecodeEngine:
             exact_br.wait_stream(main)
             with torch.cuda.stream(exact_br):
                 self.rotate(self._gq, exact=True, lookup=False)
-            self.rotate(self._gq, exact=False, lookup=True)
-            self.lookup()
+            self.lookup(self._gq)  # the lookup rotation runs inside the logits kernel (flat bf16 path)
             append_br.wait_stream(main)
             with torch.cuda.stream(append_br):
                 call("mpa_kv_append", self.cache_struct, ptr(self._gk), ptr(self._gv), self.Hkv, 1,

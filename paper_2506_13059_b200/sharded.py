@@ -122,7 +122,8 @@ class ShardedDecodeEngine:
         el = e.elocal if not e.led.lookup_f64 else None
         dense = e.rej_dense and el is not None
         call("mpa_centroid_logits", ptr(e.q_lk), e.Hkv, e.G, e.d, fine, None, None, e.kcap, ptr(e.logits),
-             ptr(e.cstats), ptr(el), int(e.led.n_fine.max()), ptr(e.rej_w) if dense else None, e.rej_cap, st)
+             ptr(e.cstats), ptr(el), int(e.led.n_fine.max()), ptr(e.rej_w) if dense else None, e.rej_cap, None, None,
+             st)
         call("mpa_head_norms", ptr(e.cstats), e.cstats.shape[1], ptr(e.led.count), e.L, e.G, ptr(self.mz_loc), st)
         return self.mz_loc
 
