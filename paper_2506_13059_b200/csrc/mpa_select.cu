@@ -312,15 +312,18 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
                 const int row0 = l * kcap + i0;
                 tma_load_2d(smem_u32(tile), &tm_tile, 0, row0, smem_u32(&bar));
                 tma_load_2d(smem_u32(tile + kLgChunk * 128), &tm_tile, 64, row0, smem_u32(&bar));
-                pdl_wait();
             }
-            // q_lk rows of the GQA group: one 256 B bulk copy per (head, quarter) into padded slots
-            for (int j = 0; j < (cs_lk ? 0 : G * 4); ++j)
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                        smem_u32(qs + j * QRow)),
-                    "l"(q_lk + ((size_t)l * G + j / 4) * D + (j % 4) * QD), "r"(QD * 8), "r"(smem_u32(&bar))
-                    : "memory");
+        }
+        __syncwarp();
+        // q_lk rows of the GQA group: one 256 B bulk copy per (head, quarter) into padded slots,
+        // issued by G * 4 lanes at once (after the predecessor that writes q_lk is complete)
+        if (!cs_lk && tid < G * 4) {
+            pdl_wait();
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                    smem_u32(qs + tid * QRow)),
+                "l"(q_lk + ((size_t)l * G + tid / 4) * D + (tid % 4) * QD), "r"(QD * 8), "r"(smem_u32(&bar))
+                : "memory");
         }
         if (!cand) {
         } else {
