@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--dense", action="store_true")
     ap.add_argument("--update", action="store_true")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"])
     args = ap.parse_args()
 
     import torch
@@ -35,7 +36,9 @@ def main():
     import bench
     from paper_2506_13059_b200 import clustering
 
-    bargs = argparse.Namespace(batch=args.batch, ctx=args.ctx, budget=args.budget, steps=args.steps, warmup=3)
+    ctx = {"c3": 65536, "c5": 131072, "c4": 16384}.get(args.workload, args.ctx)
+    bargs = argparse.Namespace(batch=args.batch, ctx=ctx, budget=args.budget, steps=args.steps, warmup=3,
+                               workload=args.workload)
     eng, Q, KN, VN, _ = bench.build_engine(bargs, 0, torch.device("cuda", 0))
     for i in range(3):
         eng.step(Q[i], KN[i], VN[i])
