@@ -268,7 +268,7 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
                   const int32_t* __restrict__ n_cand, int cand_cap, double* __restrict__ logits,
                   double* __restrict__ cstats, double* __restrict__ e_local, int n_chunks,
                   float* __restrict__ rej_w, int rej_cap, const float* __restrict__ q_raw,
-                  const double* __restrict__ cs_lk) {
+                  const double* __restrict__ cs_lk, int use_dmma) {
     constexpr int D = 128, QD = 32, QRow = QD + 2;
     // cs_lk != NULL: the lookup view q_lk = rotate(q_raw, delta) is formed here from the fp32 query
     // and the (cos, sin) table of delta * inv_freq (rope.py:66-68), instead of read from q_lk  // q slot: 32 dims (+16 B pad) per (head, quarter)
@@ -362,72 +362,119 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
     mbar_wait(smem_u32(&bar), 0);
     pdl_trigger();  // after thread 0's wait (the barrier above completes only after it)
 
-    const int qt = tid & 3, rg = tid >> 2;
-    const double* qq = qs + qt * QRow;
-    double acc[4][G];
+    const double sq = sqrt((double)D);
+    if (G <= 8 && use_dmma) {
+        // fp64 tensor cores: mma.sync m8n8k4 (rows = centroids, columns = heads padded to 8, k = 4
+        // dims).  The k index of a lane is its dimension quarter: lane (q = lane & 3, n = lane >> 2)
+        // supplies A[row n][k q] = centroid dim 32 q + kk and B[k q][head n] = q dim 32 q + kk at step
+        // kk, the same permutation for both operands, so each lane streams 32 contiguous dims.
+        const int lane = tid & 31, wq = tid >> 5, q = lane & 3, n = lane >> 2;
+        const double* qb = qs + (n < G ? n : 0) * 4 * QRow + q * QRow;
+        double cf[4][2];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+        for (int mt = 0; mt < 4; ++mt) cf[mt][0] = cf[mt][1] = 0.0;
 #pragma unroll
-        for (int g = 0; g < G; ++g) acc[r][g] = 0.0;
+        for (int cc = 0; cc < 4; ++cc) {
+            uint4 raw[4];
 #pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-        const int c = (cc + 2 * (qt >> 1)) & 3;  // this quarter's 16-byte chunk (8 dims)
-        const int ch = (qt & 1) * 4 + c;         // chunk within the 64-column half
-        uint4 raw[4];
+            for (int mt = 0; mt < 4; ++mt) {
+                const int row = 32 * wq + 8 * mt + n, ch = (q & 1) * 4 + cc;
+                raw[mt] = *reinterpret_cast<const uint4*>(tile + (q >> 1) * kLgChunk * 128 + row * 128 +
+                                                          ((ch ^ (row & 7)) << 4));
+            }
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int row = rg + 32 * r;
-            raw[r] = *reinterpret_cast<const uint4*>(tile + (qt >> 1) * kLgChunk * 128 + row * 128 +
-                                                     ((ch ^ (row & 7)) << 4));
-        }
+            for (int e = 0; e < 8; ++e) {
+                const double b = n < G ? qb[8 * cc + e] : 0.0;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            double qv[G];
-#pragma unroll
-            for (int g = 0; g < G; ++g) qv[g] = qq[g * 4 * QRow + c * 8 + e];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const unsigned wd = (&raw[r].x)[e >> 1];
-                const double x = bf16hi_to_f64_s896((e & 1) ? (wd & 0xffff0000u) : (wd << 16));
-#pragma unroll
-                for (int g = 0; g < G; ++g) acc[r][g] = fma(qv[g], x, acc[r][g]);
+                for (int mt = 0; mt < 4; ++mt) {
+                    const unsigned wd = (&raw[mt].x)[e >> 1];
+                    const double a = bf16hi_to_f64_s896((e & 1) ? (wd & 0xffff0000u) : (wd << 16));
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                                 : "+d"(cf[mt][0]), "+d"(cf[mt][1])
+                                 : "d"(a), "d"(b));
+                }
             }
         }
-    }
-    // transpose-reduce over the 4 quarter lanes (xor 2 splits rows, xor 1 splits heads)
-    const bool hi2 = qt & 2, hi1 = qt & 1;
-    constexpr int GH = (G + 1) / 2;
-    double a2[2][G];
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr)
+        for (int mt = 0; mt < 4; ++mt) {
+            const int r = 32 * wq + 8 * mt + n;
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const double send = hi2 ? acc[rr][g] : acc[rr + 2][g];
-            const double keep = hi2 ? acc[rr + 2][g] : acc[rr][g];
-            a2[rr][g] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+            for (int i2 = 0; i2 < 2; ++i2) {
+                const int g = 2 * q + i2;
+                if (g < G) {
+                    const double v = (cf[mt][i2] * kUnscale896) / sq;
+                    slg[g * kLgChunk + r] = v;
+                    if (logits && r < nv) logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
+                }
+            }
         }
-    double a1[2][GH];
+    } else {
+        const int qt = tid & 3, rg = tid >> 2;
+        const double* qq = qs + qt * QRow;
+        double acc[4][G];
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr)
+        for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int j = 0; j < GH; ++j) {
-            const int ghi = GH + j;
-            const double lo = a2[rr][j], hv = ghi < G ? a2[rr][ghi < G ? ghi : 0] : 0.0;
-            const double send = hi1 ? lo : hv;
-            const double keep = hi1 ? hv : lo;
-            a1[rr][j] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+            for (int g = 0; g < G; ++g) acc[r][g] = 0.0;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+            const int c = (cc + 2 * (qt >> 1)) & 3;  // this quarter's 16-byte chunk (8 dims)
+            const int ch = (qt & 1) * 4 + c;         // chunk within the 64-column half
+            uint4 raw[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int row = rg + 32 * r;
+                raw[r] = *reinterpret_cast<const uint4*>(tile + (qt >> 1) * kLgChunk * 128 + row * 128 +
+                                                         ((ch ^ (row & 7)) << 4));
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                double qv[G];
+#pragma unroll
+                for (int g = 0; g < G; ++g) qv[g] = qq[g * 4 * QRow + c * 8 + e];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const unsigned wd = (&raw[r].x)[e >> 1];
+                    const double x = bf16hi_to_f64_s896((e & 1) ? (wd & 0xffff0000u) : (wd << 16));
+#pragma unroll
+                    for (int g = 0; g < G; ++g) acc[r][g] = fma(qv[g], x, acc[r][g]);
+                }
+            }
         }
-    const double sq = sqrt((double)D);
+        // transpose-reduce over the 4 quarter lanes (xor 2 splits rows, xor 1 splits heads)
+        const bool hi2 = qt & 2, hi1 = qt & 1;
+        constexpr int GH = (G + 1) / 2;
+        double a2[2][G];
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
-        const int r = rg + 32 * ((hi2 ? 2 : 0) + rr);
+        for (int rr = 0; rr < 2; ++rr)
 #pragma unroll
-        for (int j = 0; j < GH; ++j) {
-            const int g = (hi1 ? GH : 0) + j;
-            if (g < G) {
-                const double v = (a1[rr][j] * kUnscale896) / sq;
-                slg[g * kLgChunk + r] = v;
-                if (logits && r < nv) logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
+            for (int g = 0; g < G; ++g) {
+                const double send = hi2 ? acc[rr][g] : acc[rr + 2][g];
+                const double keep = hi2 ? acc[rr + 2][g] : acc[rr][g];
+                a2[rr][g] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+            }
+        double a1[2][GH];
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+            for (int j = 0; j < GH; ++j) {
+                const int ghi = GH + j;
+                const double lo = a2[rr][j], hv = ghi < G ? a2[rr][ghi < G ? ghi : 0] : 0.0;
+                const double send = hi1 ? lo : hv;
+                const double keep = hi1 ? hv : lo;
+                a1[rr][j] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+            }
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int r = rg + 32 * ((hi2 ? 2 : 0) + rr);
+#pragma unroll
+            for (int j = 0; j < GH; ++j) {
+                const int g = (hi1 ? GH : 0) + j;
+                if (g < G) {
+                    const double v = (a1[rr][j] * kUnscale896) / sq;
+                    slg[g * kLgChunk + r] = v;
+                    if (logits && r < nv) logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
+                }
             }
         }
     }
@@ -1454,8 +1501,13 @@ int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* 
             auto kern = logits_tma_kernel<kG>;
             const size_t smem = 1024 + 2 * kLgChunk * 128 + sizeof(double) * (kG * 4 * 34 + kG * kLgChunk);
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            static int dmma = -1;  // MPA_LOGITS_DMMA=1: fp64 tensor-core path (measured 35 -> 41 us at C2, G = 4)
+            if (dmma < 0) {
+                const char* e = getenv("MPA_LOGITS_DMMA");
+                dmma = (e && e[0] == '1') ? 1 : 0;
+            }
             launch_pdl(kern, g2, dim3(kLgThreads), smem, st, tt, tr, q_lk, lv->cap, lv->count, lv->size, cand, n_cand,
-                       cand_cap, logits, chunk_stats, e_local, n_chunks, rej_w, rej_cap, q_raw, cs_lk);
+                       cand_cap, logits, chunk_stats, e_local, n_chunks, rej_w, rej_cap, q_raw, cs_lk, dmma);
         });
         return check_launch("mpa_centroid_logits(tma)");
     }
