@@ -260,7 +260,7 @@ __device__ __forceinline__ double bf16hi_to_f64_s896(unsigned fbits) {
 }
 constexpr double kUnscale896 = 0x1p896;
 
-template <int G>
+template <int G, bool DMMA>
 __global__ void __launch_bounds__(kLgThreads)
 logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_constant__ CUtensorMap tm_row,
                   const double* __restrict__ q_lk, int kcap, const int32_t* __restrict__ count,
@@ -268,7 +268,7 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
                   const int32_t* __restrict__ n_cand, int cand_cap, double* __restrict__ logits,
                   double* __restrict__ cstats, double* __restrict__ e_local, int n_chunks,
                   float* __restrict__ rej_w, int rej_cap, const float* __restrict__ q_raw,
-                  const double* __restrict__ cs_lk, int use_dmma) {
+                  const double* __restrict__ cs_lk) {
     constexpr int D = 128, QD = 32, QRow = QD + 2;
     // cs_lk != NULL: the lookup view q_lk = rotate(q_raw, delta) is formed here from the fp32 query
     // and the (cos, sin) table of delta * inv_freq (rope.py:66-68), instead of read from q_lk  // q slot: 32 dims (+16 B pad) per (head, quarter)
@@ -363,7 +363,7 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
     pdl_trigger();  // after thread 0's wait (the barrier above completes only after it)
 
     const double sq = sqrt((double)D);
-    if (G <= 8 && use_dmma) {
+    if constexpr (G <= 8 && DMMA) {
         // fp64 tensor cores: mma.sync m8n8k4 (rows = centroids, columns = heads padded to 8, k = 4
         // dims).  The k index of a lane is its dimension quarter: lane (q = lane & 3, n = lane >> 2)
         // supplies A[row n][k q] = centroid dim 32 q + kk and B[k q][head n] = q dim 32 q + kk at step
@@ -1498,16 +1498,16 @@ int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* 
         if (int rc = encode_bf16_rows(&tr, lv->kc, (long long)L * lv->cap, 128, 1)) return rc;
         dim3 g2(item_chunks, L);
         MPA_DISPATCH_G(group, {
-            auto kern = logits_tma_kernel<kG>;
             const size_t smem = 1024 + 2 * kLgChunk * 128 + sizeof(double) * (kG * 4 * 34 + kG * kLgChunk);
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             static int dmma = -1;  // MPA_LOGITS_DMMA=1: fp64 tensor-core path (measured 35 -> 41 us at C2, G = 4)
             if (dmma < 0) {
                 const char* e = getenv("MPA_LOGITS_DMMA");
                 dmma = (e && e[0] == '1') ? 1 : 0;
             }
+            auto kern = dmma ? logits_tma_kernel<kG, true> : logits_tma_kernel<kG, false>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             launch_pdl(kern, g2, dim3(kLgThreads), smem, st, tt, tr, q_lk, lv->cap, lv->count, lv->size, cand, n_cand,
-                       cand_cap, logits, chunk_stats, e_local, n_chunks, rej_w, rej_cap, q_raw, cs_lk, dmma);
+                       cand_cap, logits, chunk_stats, e_local, n_chunks, rej_w, rej_cap, q_raw, cs_lk);
         });
         return check_launch("mpa_centroid_logits(tma)");
     }
