@@ -529,6 +529,7 @@ def main():
                        "pct_of_step": update_ms / L / ms_step * 100.0, "lloyd_rounds": upd["rounds"],
                        "prefill_s": prefill_s},
             "e2e": {"value": e2e_avg * 1e3, "unit": "us/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "graph_captures": eng.n_captures,
             "gpu_launches": 6 * K,  # per step (one graph): 2 rotations, logits, select+lists, fused decode, append
             "clocks": clk.summary(),
         }

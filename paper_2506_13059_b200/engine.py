@@ -108,6 +108,7 @@ class DecodeEngine:
                           and os.environ.get("MPA_REJ_LIST") != "1")
         self.use_graphs = (os.environ.get("MPA_NO_GRAPH") != "1") if use_graphs is None else use_graphs
         self._graph = None
+        self.n_captures = 0  # step-graph captures so far (bench reports it)
         self.time_fused = False  # bench: CUDA events around the fused kernel inside the step graph
         self._fev = None
         self.last_lloyd_rounds = 0
@@ -313,6 +314,7 @@ class DecodeEngine:
         self._graph = None
 
     def _capture_step(self) -> None:
+        self.n_captures += 1
         n, Hq, Hkv, d, dev = self.n_seq, self.Hq, self.Hkv, self.d, self.device
         self._gq = torch.zeros(n, Hq, d, dtype=torch.float32, device=dev)
         self._gk = torch.zeros(n, Hkv, 1, d, dtype=torch.float32, device=dev)
