@@ -25,11 +25,24 @@ from .ledger import BlockRow
 MAX_POINTS = 16384  # per problem (csrc/mpa_cluster.cu kMaxPoints)
 
 
+def _scratch(cache, name: str, numel: int, dtype, device) -> torch.Tensor:
+    """A flat scratch tensor of >= numel elements kept in `cache` between calls and grown by 1.5x, so
+    the online updates (whose problem sizes creep up event by event) reuse the same device blocks
+    instead of asking the allocator for slightly larger ones every time (cudaMalloc stalls)."""
+    if cache is None:
+        return torch.empty(max(numel, 1), dtype=dtype, device=device)
+    t = cache.get(name)
+    if t is None or t.numel() < numel or t.dtype != dtype:
+        t = torch.empty(max(int(numel * 1.5), 1), dtype=dtype, device=device)
+        cache[name] = t
+    return t[: max(numel, 1)]
+
+
 class KMeansBatch:
     """One batch of independent Lloyd problems (l, start, n, k) on a shared point source."""
 
     def __init__(self, device, d: int, probs, init: torch.Tensor, *, pts=None, tcap: int = 0, pts64=None, wts=None,
-                 rows64_cap: int = 0, min_iters: int = 0, count_init: torch.Tensor | None = None):
+                 rows64_cap: int = 0, min_iters: int = 0, count_init: torch.Tensor | None = None, cache=None):
         arr = np.asarray(probs, np.int64).reshape(-1, 4)
         self.probs = arr
         self.P = arr.shape[0]
@@ -44,10 +57,11 @@ class KMeansBatch:
         self.t = {name: torch.as_tensor(v, **i32) for name, v in
                   (("l", arr[:, 0]), ("start", arr[:, 1]), ("n", n), ("k", k), ("pt_off", self.pt_off),
                    ("c_off", self.c_off))}
-        self.assign = torch.zeros(max(N, 1), **i32)
-        self.prev = torch.zeros(max(N, 1), **i32)
-        self.p2 = torch.zeros(max(N, 1), dtype=torch.float64, device=device)
-        self.order = torch.zeros(max(N, 1), **i32)
+        sc = lambda name, n, dt: _scratch(cache, name, n, dt, device).zero_()
+        self.assign = sc("assign", N, torch.int32)
+        self.prev = sc("prev", N, torch.int32)
+        self.p2 = sc("p2", N, torch.float64)
+        self.order = sc("order", N, torch.int32)
         self.cent = init.to(torch.float64).contiguous().reshape(-1, d)
         assert self.cent.shape[0] == K, (self.cent.shape, K)
         self.c2 = torch.zeros(max(K, 1), dtype=torch.float64, device=device)
@@ -68,7 +82,7 @@ class KMeansBatch:
             from ._lib import lib
 
             nb = int(lib().mpa_km_tc_workspace(self.P, K, N, d))
-            self.tc_ws = torch.empty(nb, dtype=torch.uint8, device=device)
+            self.tc_ws = _scratch(cache, "tc_ws", nb, torch.uint8, device)
 
     def struct(self) -> MpaKm:
         pts, tcap, pts64, wts, rcap = self.src
@@ -320,7 +334,8 @@ def online_update(eng, seqs, cursor: int) -> dict:
     osrc, odst = allidx[:no], allidx[no:2 * no]
     nsrc, ndst = allidx[2 * no:2 * no + nn], allidx[2 * no + nn:]
     tick("idx")
-    init = torch.empty(c_at, eng.d, dtype=torch.float64, device=dev)
+    cache = eng.__dict__.setdefault("_upd_scratch", {})
+    init = _scratch(cache, "init", c_at * eng.d, torch.float64, dev).view(c_at, eng.d)
     init[odst] = led.kc64.view(-1, eng.d)[osrc]
     tick("init_old")
     init[ndst] = eng.k_raw.view(-1, eng.d)[nsrc].double()
@@ -329,8 +344,8 @@ def online_update(eng, seqs, cursor: int) -> dict:
     counts[odst] = led.size.view(-1)[osrc]
     tick("counts0")
     km = KMeansBatch(dev, eng.d, probs, init, pts=eng.k_raw, tcap=eng.tcap,
-                     min_iters=cfg.refine_kmeans_iters, count_init=counts)
-    dist = torch.empty(len(probs), L, km.k_max, dtype=torch.float64, device=eng.device)
+                     min_iters=cfg.refine_kmeans_iters, count_init=counts, cache=cache)
+    dist = _scratch(cache, "dist", len(probs) * L * km.k_max, torch.float64, dev).view(len(probs), L, km.k_max)
     tails_d = _i32(eng, tails)
     tick("batch")
     call("mpa_km_seq_assign", km.struct(), ptr(tails_d), L, ptr(dist), stream_ptr())
