@@ -121,6 +121,8 @@ class Clocks:
         self.path = tempfile.mktemp(suffix=".csv")
 
     def __enter__(self):
+        if os.environ.get("BENCH_NO_SMI") == "1":  # experiments: no sampler
+            return self
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
@@ -378,9 +380,6 @@ def main():
     dev = torch.device("cuda", local)
     eng, Q, KN, VN, prefill_s = build_engine(args, rank, dev)
     import gc
-
-    gc.collect()
-    gc.freeze()  # setup objects leave the collector's generations (long-lived serving state)
     gen = torch.Generator(device=dev).manual_seed(2000 + rank)
     total_steps = W + K
     flush = L2Flush(dev)
@@ -411,6 +410,10 @@ def main():
             for _ in range(20):
                 eng.attend(Q[0])
             torch.cuda.synchronize()
+        # setup garbage collected now and the long-lived objects frozen, so a generation-2
+        # collection does not land inside a (host-driven) online update of the timed steps
+        gc.collect()
+        gc.freeze()
         barrier()
         step_ms = timed(lambda i: eng.step(Q[i], KN[i], VN[i]), K, start=W)
         torch.cuda.synchronize()

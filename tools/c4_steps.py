@@ -20,6 +20,19 @@ def main():
     for i in range(args.warmup):
         eng.step(Q[i], KN[i], VN[i])
     torch.cuda.synchronize()
+    if os.environ.get("ATTEND_LOOP"):  # what bench.py does before timing: 1.5 s of eager attends
+        import time
+
+        t_end = time.perf_counter() + 1.5
+        while time.perf_counter() < t_end:
+            for _ in range(20):
+                eng.attend(Q[0])
+            torch.cuda.synchronize()
+    if os.environ.get("GCFREEZE"):
+        import gc
+
+        gc.collect()
+        gc.freeze()
     evs, upd = [], []
     stream = torch.cuda.current_stream()
     for i in range(args.steps):
