@@ -54,3 +54,16 @@ def test_argument_errors_without_gpu(lib):
     rc = lib.mpa_sparse_decode(None, None, 8, 4, None, None, 0, None, None, None, 0, None, 0, None, 0, 1,
                                None, ctypes.c_size_t(0), None, None)
     assert rc == 1001
+
+
+def test_new_entry_points_reject_bad_arguments(lib):
+    lib.mpa_last_error.restype = ctypes.c_char_p
+    ll = ctypes.c_longlong
+    # step-input staging: sizes must be multiples of 4 floats, buffers 16-byte aligned
+    rc = lib.mpa_stage3(ctypes.c_void_p(64), ctypes.c_void_p(64), ll(6), None, None, ll(0), None, None, ll(0), None)
+    assert rc == 1001 and b"multiple of 4" in lib.mpa_last_error()
+    rc = lib.mpa_stage3(ctypes.c_void_p(68), ctypes.c_void_p(64), ll(8), None, None, ll(0), None, None, ll(0), None)
+    assert rc == 1001 and b"aligned" in lib.mpa_last_error()
+    # logits: neither q_lk nor (q_raw, cs_lk)
+    rc = lib.mpa_centroid_logits(None, 8, 4, 128, None, None, None, 0, None, None, None, 0, None, 0, None, None, None)
+    assert rc == 1001 and b"null argument" in lib.mpa_last_error()
