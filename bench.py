@@ -541,7 +541,8 @@ def main():
                        "prefill_s": prefill_s},
             "e2e": {"value": e2e_avg * 1e3, "unit": "us/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "graph_captures": eng.n_captures,
-            "gpu_launches": 6 * K,  # per step (one graph): 2 rotations, logits, select+lists, fused decode, append
+            "gpu_launches": 7 * K,  # per step: input staging + one graph (2 rotations, logits, select+lists,
+                                    # fused decode, append)
             "clocks": clk.summary(),
         }
         if not args.no_cpu and not args.profile:
