@@ -202,3 +202,40 @@ def test_engine_step_graph_matches_eager(dtype):
     assert n_upd >= 3
     for h in range(engs[0].L):
         _assert_same_ledger(to_oracle(engs[0].export_ledger(h)), to_oracle(engs[1].export_ledger(h)), f"h={h}")
+
+
+def test_bf16_d128_tensor_core_clustering_bitexact(monkeypatch):
+    # bf16 keys with d = 128 take the tcgen05 assignment (persistent paired kernel + fp64 recheck):
+    # prefill and every online update must give the oracle's ledgers bit-for-bit on the same keys
+    from paper_2506_13059_b200 import clustering as GC
+    from paper_2506_13059_b200 import pipeline as G
+
+    used = []
+    orig = GC.KMeansBatch.lloyd
+
+    def lloyd(self):
+        used.append(self.tc_ws is not None)
+        return orig(self)
+
+    monkeypatch.setattr(GC.KMeansBatch, "lloyd", lloyd)
+    tr = _as_dtype_trace(gen_synthetic(16, 2048, HeadLayout(8, 2, 128), 0.05, seed=9, decode_steps=40),
+                         torch.bfloat16)
+    cfg = EngineConfig(block_size=1024, alpha=512, local_buffer=16, sink_tokens=5, token_budget=128,
+                       tokens_per_centroid=8, seed=9)
+    st_g = G.prefill(tr, cfg, dtype=torch.bfloat16)
+    st_o = O.prefill(tr, cfg, "multipole")
+    for h in range(2):
+        _assert_same_ledger(to_oracle(st_g.engine.export_ledger(h)), st_o.ledgers[h], f"prefill h={h}")
+    n_upd = 0
+    for t in range(40):
+        pos = tr.prompt_len + t
+        args = (tr.queries[:, t], tr.keys[:, pos], tr.values[:, pos])
+        _, rep_g = G.step(st_g, *args)
+        _, rep_o = O.step(st_o, *args)
+        assert rep_g.update_occurred == rep_o.update_occurred, t
+        if rep_o.update_occurred:
+            n_upd += 1
+            for h in range(2):
+                _assert_same_ledger(to_oracle(st_g.engine.export_ledger(h)), st_o.ledgers[h], f"t={t} h={h}")
+    assert n_upd >= 2
+    assert used and all(used), used  # every Lloyd call ran on the tensor cores
