@@ -444,6 +444,8 @@ hier_candidates_kernel(const int32_t* __restrict__ ccount, const int32_t* __rest
                        const int32_t* __restrict__ child, int ccap, int child_cap, const uint8_t* __restrict__ cflag,
                        int32_t* __restrict__ cand, int32_t* __restrict__ n_cand, int cand_cap) {
     __shared__ int scan[33];
+    pdl_wait();  // cflag comes from the coarse selection (PDL predecessor)
+    pdl_trigger();
     const int l = blockIdx.x;
     const int nc = ccount[l];
     const int32_t* off = child_off + (size_t)l * (ccap + 1);
@@ -751,8 +753,8 @@ extern "C" int mpa_hier_candidates(const mpa_level* coarse, const uint8_t* cflag
     MPA_REQUIRE(coarse && cflag && cand && n_cand && coarse->off && coarse->idx, MPA_ERR_ARG,
                 "mpa_hier_candidates: null argument");
     if (n_ledgers <= 0) return 0;
-    hier_candidates_kernel<<<n_ledgers, kListThreads, 0, (cudaStream_t)stream>>>(
-        coarse->count, coarse->off, coarse->idx, coarse->cap, coarse->idx_cap, cflag, cand, n_cand, cand_cap);
+    launch_pdl(hier_candidates_kernel, dim3(n_ledgers), dim3(kListThreads), 0, (cudaStream_t)stream, coarse->count,
+               coarse->off, coarse->idx, coarse->cap, coarse->idx_cap, cflag, cand, n_cand, cand_cap);
     return check_launch("mpa_hier_candidates");
 }
 

@@ -1533,9 +1533,9 @@ int mpa_launch_select_v2(const double* logits, const double* e_local, int group,
     MPA_DISPATCH_G(group, {
         auto kern = select_v2_kernel<kG>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<n_ledgers, kSel2Threads, smem, st>>>(logits, e_local, cand, n_cand, cand_cap, lv_size, lv_cap, elogits,
-                                                    esize, eflag, n_extra, ecap, budget, flag, sel_tokens,
-                                                    chunk_stats, n_chunks, n_max);
+        launch_pdl(kern, dim3(n_ledgers), dim3(kSel2Threads), smem, st, logits, e_local, cand, n_cand, cand_cap,
+                   lv_size, lv_cap, elogits, esize, eflag, n_extra, ecap, budget, flag, sel_tokens, chunk_stats,
+                   n_chunks, n_max);
     });
     return check_launch("mpa_select(v2)");
 }
