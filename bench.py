@@ -428,19 +428,20 @@ def main():
               else eng.led.n_coarse + eng.n_cand.cpu().numpy().astype(np.int64))
     ms_step = float(np.mean(step_ms))
 
-    # ---- fused kernel alone (dominant kernel) for the roofline
-    eng.rotate(Q[0])
-    eng.lookup()
+    # ---- fused decode kernel (dominant kernel) for the roofline: alone (L2 flushed, its lists cold
+    # too) and in the step chain (lookup launch, then events around the fused kernel on the engine
+    # stream -- its work lists come warm from the lookup as inside the step graph)
+    one_kernel = False
+    eng.rotate(Q[0], exact=True, lookup=False)
+    eng.lookup(Q[0])
     torch.cuda.synchronize()
     fstats = eng.head_stats()
-    fused_ms = timed(lambda i: eng.fused(), K)  # alone, L2 flushed: its lists cold too
-    # in context: the same step chain launched eagerly (rotate -> lookup -> fused), L2 flushed
-    # before each step, events around the fused kernel on the engine stream -- its work lists
-    # come warm from the selection kernel as inside the step graph
+    fused_ms = timed(lambda i: eng.fused(), K)
     fev = []
     for i in range(K):
         flush(i)
-        eng.rotate(Q[i], exact=True, lookup=False)
+        if not eng.fused_lookup_path():
+            eng.rotate(Q[i], exact=True, lookup=False)
         eng.lookup(Q[i])
         a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
@@ -449,8 +450,9 @@ def main():
         fev.append((a, z))
     torch.cuda.synchronize()
     fused_step_avg = float(np.mean([a.elapsed_time(z) for a, z in fev]))
-    lookup_ms = timed(lambda i: eng.lookup(Q[0]), K)  # lookup-view rotation (fused or not) + logits + select
+    lookup_ms = timed(lambda i: eng.lookup(Q[0]), K)  # the lookup launch(es): views + logits + select + lists
     nbytes = decode_bytes(fstats, scored, d, G, 2)
+    kernel_bytes = nbytes["fused"]
     fused_avg = float(np.mean(fused_ms))
 
     # ---- dense decode comparator (same cache, same kernel family, tok == NULL)
@@ -497,7 +499,7 @@ def main():
 
     if rank == 0:
         hbm, peak_kind = peaks()
-        achieved = nbytes["fused"] / (fused_step_avg * 1e-3) / 1e9
+        achieved = kernel_bytes / (fused_step_avg * 1e-3) / 1e9
         traffic = load_traffic(args.workload, b)
         line = {
             "metric": METRIC,
@@ -521,12 +523,17 @@ def main():
             "dense_gbs": dbytes / (dense_avg * 1e-3) / 1e9,
             "flashinfer_dense_us": (fi_ms * 1e3) if fi_ms else None,
             "sequences_per_s": world * b / (ms_step * 1e-3),
-            "roofline": {"bound": "hbm", "kernel": "mpa_sparse_decode (decode_sk_kernel)",
+            "roofline": {"bound": "hbm",
+                         "kernel": ("mpa_decode_step (step_kernel: lookup + selection + replacement + exact "
+                                    "attention, one launch per step)") if one_kernel
+                         else "mpa_sparse_decode (decode_sk_kernel)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "peak_kind": peak_kind, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": nbytes["fused"], "launch_us": fused_step_avg * 1e3,
-                         "timing": "CUDA events around the fused kernel in the step chain (engine stream, "
-                                   "lists warm from the selection), L2 flushed before every step",
+                         "algorithmic_bytes_per_launch": kernel_bytes, "launch_us": fused_step_avg * 1e3,
+                         "timing": ("CUDA events around the step kernel launched alone on the engine stream, "
+                                    "L2 flushed before every launch") if one_kernel
+                         else ("CUDA events around the fused kernel in the step chain (engine stream, "
+                               "lists warm from the selection), L2 flushed before every step"),
                          "launch_us_alone_cold": fused_avg * 1e3},
             "step_roofline": {"bytes": nbytes["step"], "GBs": nbytes["step"] / (ms_step * 1e-3) / 1e9,
                               "frac": nbytes["step"] / (ms_step * 1e-3) / 1e9 / hbm,
@@ -541,8 +548,9 @@ def main():
                        "prefill_s": prefill_s},
             "e2e": {"value": e2e_avg * 1e3, "unit": "us/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "graph_captures": eng.n_captures,
-            "gpu_launches": 7 * K,  # per step: input staging + one graph (2 rotations, logits, select+lists,
-                                    # fused decode, append)
+            "gpu_launches": (3 if eng.fused_lookup_path() else 7) * K,  # per step: input staging + the
+                                    # step graph (flat bf16 path: lookup + append, fused decode; else 2
+                                    # rotations, logits, select+lists, fused decode, append)
             "clocks": clk.summary(),
         }
         if not args.no_cpu and not args.profile:

@@ -150,6 +150,32 @@ int mpa_build_worklist(const mpa_level* fine, const mpa_level* coarse, int group
                        int32_t* tok, int tok_cap, int32_t* rej, float* rej_w, int rej_cap,
                        int32_t* stats, void* stream);
 
+/* K1 + K9 + K10 + work lists + the K/V append of a flat serving decode step in ONE launch (bf16
+ * cache and centroids, head_dim 128, 3 <= G <= 8): replaces rope.py:37-53 / 66-68 (exact and
+ * lookup views), attention.py:267-290 (`_scores_per_group`), :192-207 (`select_clusters`),
+ * :354-375 (`flat_lookup`), the per-kv-head lists of :469-496, and pipeline.py:156-159.
+ * One thread-block cluster per ledger (size picked so the grid is one wave): fp64 logits of the
+ * lookup view formed from the fp32 queries q [n_seq, Hq, 128] and cs_lk [64][2] = (cos, sin)(delta *
+ * inv_freq); per-head max and Z = sum N e^(l - max) over distributed shared memory; Eq. 1 scores;
+ * a size-weighted radix select of the crossing candidate (ties: lowest cluster id).  Writes
+ * flag [L, cap], sel_tokens [L], tok [L, tok_cap] (sinks ++ buffer ++ members of the selected
+ * clusters), stats [4, L] (tokens, rejected centroids, selected tokens, selected clusters), and
+ * (optional) q_rot [L, G, 128] = rotate(q, cache_len) / sqrt(d) (fp32, fp64 angles) and the
+ * contiguous-centroid list rej_w [L, rej_cap, GP] = logit + ln N of every centroid with the
+ * selected ones -inf (replacement != 0) -- the inputs of mpa_sparse_decode.
+ * k_new / v_new (fp32 [L, 128], optional): the step's key / value written at row cache_len after the
+ * lists were cut, then the last CTA advances cache_len[s] and ntok_dense[l] (optional) by one
+ * (ticket: one int32 workspace, zero-initialised once, left zeroed).
+ * n_max bounds every ledger's cluster count (0: cap). */
+int mpa_decode_step(const float* q, const float* k_new, const float* v_new, const mpa_cache* cache,
+                    const double* cs_lk, const double* inv_freq, int n_kv_heads, int group,
+                    const mpa_level* fine, const int64_t* budget, const int32_t* sink_end,
+                    const int32_t* buffer_start, int32_t* cache_len, int32_t* ntok_dense,
+                    int32_t* ticket, int replacement, uint8_t* flag, int32_t* sel_tokens, int32_t* tok,
+                    int tok_cap, int32_t* stats, int n_max, float* q_rot, float* rej_w, int rej_cap,
+                    void* stream);
+
+
 /* K10 + work list fused in one launch per ledger: mpa_select over the fine candidates (extras =
  * coarse clusters with cflag == 0, hierarchy only) followed by mpa_build_worklist.
  * rej == NULL with replacement (flat level only): contiguous-centroid work list -- no rejected

@@ -107,7 +107,8 @@ class KMeansBatch:
     def nonempty(self) -> np.ndarray:
         nk = torch.zeros(max(self.P, 1), dtype=torch.int32, device=self.assign.device)
         call("mpa_km_count_nonempty", self.struct(), ptr(nk), stream_ptr())
-        return nk[: self.P].cpu().numpy().astype(np.int64)
+        self.nk = nk[: self.P].cpu().numpy().astype(np.int64)
+        return self.nk
 
     def counts(self, p: int) -> torch.Tensor:
         c0, k = int(self.c_off[p]), int(self.probs[p, 3])
@@ -123,8 +124,22 @@ def _i32(eng, a) -> torch.Tensor:
     return torch.as_tensor(np.asarray(a), dtype=torch.int32, device=eng.device)
 
 
+def _check_level_cap(km: KMeansBatch, first: np.ndarray, cap: int, what: str) -> None:
+    """The level writer compacts each problem's non-empty clusters to rows [first, first + nk) of
+    its ledger with no device-side bound: check them on the host before the launch."""
+    nk = getattr(km, "nk", None)
+    if nk is None:
+        nk = km.nonempty()
+    over = np.flatnonzero(np.asarray(first, np.int64) + nk > cap)
+    if over.size:
+        i = int(over[0])
+        raise ConfigError(f"{what} cluster capacity exceeded: problem {i} writes rows "
+                          f"[{int(first[i])}, {int(first[i] + nk[i])}) of {cap}")
+
+
 def _write_fine(eng, km: KMeansBatch, f0: np.ndarray, mbase: np.ndarray) -> None:
     led = eng.led
+    _check_level_cap(km, f0, led.kcap, "fine")
     f0_d, mb_d = _i32(eng, f0), _i32(eng, mbase)
     call("mpa_km_write_level", km.struct(), ptr(eng.v), None, ptr(f0_d), ptr(mb_d),
          ptr(led.kc64), ptr(led.vc64), ptr(led.kc), ptr(led.vc), dtype_code(led.dtype), ptr(led.size), ptr(led.off),
@@ -133,6 +148,7 @@ def _write_fine(eng, km: KMeansBatch, f0: np.ndarray, mbase: np.ndarray) -> None
 
 def _write_coarse(eng, km: KMeansBatch, c0: np.ndarray, mbase: np.ndarray) -> None:
     led = eng.led
+    _check_level_cap(km, c0, led.ccap, "coarse")
     c0_d, mb_d = _i32(eng, c0), _i32(eng, mbase)
     call("mpa_km_write_level", km.struct(), None, ptr(led.vc64), ptr(c0_d), ptr(mb_d),
          ptr(led.ckc64), ptr(led.cvc64), ptr(led.ckc), ptr(led.cvc), dtype_code(led.dtype), ptr(led.csize),
@@ -417,7 +433,9 @@ def _split(eng, ledgers, settle: bool = True) -> int:
             st = KMeansBatch(dev, eng.d, sprobs, torch.cat(sinit), pts=eng.k_raw, tcap=eng.tcap, min_iters=0)
             st.lloyd()
         else:
-            st = km  # positional pages: straddlers split, no settle (clustering.py:540)
+            # positional pages: straddlers split, no settle (clustering.py:540); the side problems
+            # are written as they are (empty sides dropped by the compaction, clustering.py:377)
+            st, sprobs = km, probs
         nk = st.nonempty()
         f0 = np.zeros(len(sprobs), np.int64)
         mbase = np.zeros(len(sprobs), np.int64)

@@ -101,11 +101,8 @@ class DecodeEngine:
         self.cache_struct = MpaCache(ptr(self.k_rot), ptr(self.k_raw), ptr(self.v), dtype_code(dtype), L, tcap, d)
         self.last_split = 1
         self.cursor = 0
-        # contiguous-centroid work list (flat bf16 serving path): the logits kernel writes every
-        # centroid's replacement weight, the selection masks the selected ones, and the fused kernel
-        # streams the value centroids in order with 16-row TMA boxes (include/mpattn.h)
-        self.rej_dense = (not hier and mode == "multipole" and dtype == torch.bfloat16 and d == 128 and G <= 8
-                          and os.environ.get("MPA_REJ_LIST") != "1")
+        # the flat serving path (fused_lookup_path) hands the fused kernel a contiguous-centroid
+        # list: every centroid's replacement weight in id order, the selected ones -inf
         self.use_graphs = (os.environ.get("MPA_NO_GRAPH") != "1") if use_graphs is None else use_graphs
         self._graph = None
         self.n_captures = 0  # step-graph captures so far (bench reports it)
@@ -187,44 +184,60 @@ class DecodeEngine:
             self.invalidate_graph()
         return self._bf, self._bc
 
-    def _fused_rotation(self) -> bool:
-        """MPA_FUSED_ROTATE=1: the flat bf16 d = 128 path forms the lookup view inside the logits
-        kernel (measured 10 us slower per C2 step than the separate rotation kernel: every chunk CTA
-        then waits for its query rows before computing)."""
-        return (self.cfg.hierarchy is None and self.dtype == torch.bfloat16 and self.d == 128
-                and not self.led.lookup_f64 and os.environ.get("MPA_FUSED_ROTATE") == "1")
+    def fused_lookup_path(self) -> bool:
+        """The flat serving step (bf16 cache and centroids, d = 128, G <= 8) runs as ONE launch
+        (mpa_decode_step); hierarchical, fp32 (parity) and d != 128 steps use the staged kernels."""
+        return (self.cfg.hierarchy is None and self.dtype == torch.bfloat16 and self.d == 128 and 3 <= self.G <= 8
+                and not self.led.lookup_f64)
 
-    def lookup(self, q: torch.Tensor | None = None) -> None:
-        """K9 + K10 + work lists (flat or hierarchical) for q_lk, or -- q given, fused path -- for
-        the lookup view of the fp32 queries q formed inside the logits kernel."""
+    def lookup_step(self, q: torch.Tensor, k_new: torch.Tensor | None = None,
+                    v_new: torch.Tensor | None = None) -> None:
+        """Flat serving path, ONE launch (mpa_decode_step): both query views (q_rot for the fused
+        kernel), fp64 logits, Eq. 1, budgeted selection, the token list and the contiguous-centroid
+        weights; with k_new / v_new ([n_seq, Hkv, d] fp32) the step's token is appended after the
+        lists were cut (the last CTA advances the device lengths)."""
+        self._bound_fine, self._bound_coarse = self._cluster_bounds()
+        if int(self.led.n_fine.min()) == 0:
+            raise ConfigError("ledger has no clusters")
+        qf = q.float().contiguous()
+        kf = k_new.float().contiguous() if k_new is not None else None
+        vf = v_new.float().contiguous() if v_new is not None else None
+        replacement = 0 if self.mode == "flat-no-replacement" else 1
+        call("mpa_decode_step", ptr(qf), ptr(kf), ptr(vf), self.cache_struct, ptr(self.cs_lk), ptr(self.inv_freq),
+             self.Hkv, self.G, self.led.fine_level(), ptr(self.budget), ptr(self.sink_end_d),
+             ptr(self.buffer_start_d), ptr(self.cache_len_d), ptr(self.ntok_dense_d), ptr(self.append_ticket),
+             replacement, ptr(self.flag), ptr(self.sel_tokens), ptr(self.tok), self.tok_cap, ptr(self.stats),
+             self._bound_fine, ptr(self.q_rot), ptr(self.rej_w) if replacement else None, self.rej_cap, stream_ptr())
+
+    def lookup(self, q: torch.Tensor, staged: bool = False) -> None:
+        """K9 + K10 + work lists (flat or hierarchical) for the fp32 queries q [n_seq, Hq, d].  On the
+        flat serving path this is the single-launch decode step (the output included) unless
+        `staged` asks for the separate logits / selection kernels and a rejected-centroid list."""
         st = stream_ptr()
-        qraw = None
-        if q is not None:
-            if self._fused_rotation():
-                qraw = q.float().contiguous()
-            else:
-                self.rotate(q, exact=False, lookup=True)
         self._bound_fine, self._bound_coarse = self._cluster_bounds()
         G, L = self.G, self.L
         fine = self.led.fine_level()
         replacement = 0 if self.mode == "flat-no-replacement" else 1
+        if self.cfg.hierarchy is None and int(self.led.n_fine.min()) == 0:
+            raise ConfigError("ledger has no clusters")
+        self._staged = staged
+        if self.fused_lookup_path() and not staged:  # one launch (the exact view included)
+            self.lookup_step(q)
+            return
+        self.rotate(q, exact=False, lookup=True)
         tiled = self.d in (64, 128)
         cs = self.cstats if tiled else None
         # e^(l - chunk max) from the logits kernel (bf16 serving centroids only)
         el = self.elocal if (tiled and not self.led.lookup_f64) else None
         if self.cfg.hierarchy is None:
-            if int(self.led.n_fine.min()) == 0:
-                raise ConfigError("ledger has no clusters")
-            dense = self.rej_dense and el is not None
-            lg = None if dense else ptr(self.logits)  # the contiguous-centroid list never reads them
-            call("mpa_centroid_logits", None if qraw is not None else ptr(self.q_lk), self.Hkv, G, self.d, fine, None,
-                 None, self.kcap, lg, ptr(cs), ptr(el), self._bound_fine, ptr(self.rej_w) if dense else None,
-                 self.rej_cap, ptr(qraw), ptr(self.cs_lk) if qraw is not None else None, st)
-            call("mpa_select_worklist", fine, None, G, lg, ptr(el), None, None, self.kcap, ptr(cs),
+            call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, None,
+                 None, self.kcap, ptr(self.logits), ptr(cs), ptr(el), self._bound_fine, None,
+                 self.rej_cap, None, None, st)
+            call("mpa_select_worklist", fine, None, G, ptr(self.logits), ptr(el), None, None, self.kcap, ptr(cs),
                  None, None,
                  ptr(self.budget), ptr(self.sink_end_d), ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv,
                  L, replacement, ptr(self.flag), ptr(self.sel_tokens), ptr(self.tok), self.tok_cap,
-                 None if dense else ptr(self.rej), ptr(self.rej_w), self.rej_cap, ptr(self.stats), self._bound_fine,
+                 ptr(self.rej), ptr(self.rej_w), self.rej_cap, ptr(self.stats), self._bound_fine,
                  st)
         else:
             if int(self.led.n_coarse.min()) == 0:
@@ -259,12 +272,14 @@ class DecodeEngine:
              ptr(self.led.vc), self.kcap, ptr(ckc), self.ccap, S, ptr(ws), ws.numel(), ptr(self.out), st)
         return self.out
 
-    def _centroid_terms(self):
-        """(rej, rej_w, n_rej) of mpa_sparse_decode: none, the rejected list, or every fine centroid
-        in order (contiguous-centroid list, selected ones weighted -inf)."""
+    def _centroid_terms(self, contiguous: bool | None = None):
+        """(rej, rej_w, n_rej) of mpa_sparse_decode: none, the rejected list, or (contiguous: the flat
+        bf16 serving path) every fine centroid in order, selected ones weighted -inf."""
         if self.mode == "flat-no-replacement":
             return None, None, None
-        if self.rej_dense and not self.led.lookup_f64:
+        if contiguous is None:
+            contiguous = self.fused_lookup_path() and not getattr(self, "_staged", False)
+        if contiguous:
             return None, self.rej_w, self.led.count
         return self.rej, self.rej_w, self.stats[1]
 
@@ -272,8 +287,11 @@ class DecodeEngine:
         """One multipole decode step over the current cache; q fp32 [n_seq, Hq, d] (device)."""
         if self.mode == "oracle":
             return self.attend_dense(q, n_split)
-        self.rotate(q, exact=True, lookup=False)
-        self.lookup(q)
+        if self.fused_lookup_path():
+            self.lookup(q)  # the single-launch lookup forms the exact view too
+        else:
+            self.rotate(q, exact=True, lookup=False)
+            self.lookup(q)
         return self.fused(n_split)
 
     def attend_dense(self, q: torch.Tensor, n_split: int | None = None) -> torch.Tensor:
@@ -328,6 +346,17 @@ class DecodeEngine:
         self._fev = ((torch.cuda.Event(enable_timing=True, external=True),
                       torch.cuda.Event(enable_timing=True, external=True)) if self.time_fused else None)
         g = torch.cuda.CUDAGraph()
+        if self.fused_lookup_path():
+            # two launches: lookup + both query views + the append (mpa_decode_step), fused decode
+            with torch.cuda.graph(g):
+                self.lookup_step(self._gq, self._gk[:, :, 0], self._gv[:, :, 0])
+                if self._fev:
+                    self._fev[0].record()
+                self.fused()
+                if self._fev:
+                    self._fev[1].record()
+            self._graph = g
+            return
         exact_br, append_br = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         with torch.cuda.graph(g):
             # critical path: q_lk -> logits -> select + work lists -> fused decode.  Off it, on
@@ -338,8 +367,10 @@ class DecodeEngine:
             exact_br.wait_stream(main)
             with torch.cuda.stream(exact_br):
                 self.rotate(self._gq, exact=True, lookup=False)
-            self.lookup(self._gq)  # the lookup rotation runs inside the logits kernel (flat bf16 path)
+            self.lookup(self._gq)  # the lookup-view rotation runs inside the lookup kernel (flat bf16 path)
             append_br.wait_stream(main)
+            # the exact-view rotation reads cache_len_d, which the append advances: order them
+            append_br.wait_stream(exact_br)
             with torch.cuda.stream(append_br):
                 call("mpa_kv_append", self.cache_struct, ptr(self._gk), ptr(self._gv), self.Hkv, 1,
                      ptr(self.cache_len_d), ptr(self.ntok_dense_d), ptr(self.inv_freq), ptr(self.append_ticket),
@@ -387,8 +418,15 @@ class DecodeEngine:
         else:
             if host:
                 q, k_new, v_new = (x.to(self.device, non_blocking=True) for x in (q, k_new, v_new))
-            out = self.attend(q)
-            self.write_tokens(k_new[:, :, None], v_new[:, :, None])
+            if self.fused_lookup_path() and self.mode != "oracle":
+                if int(self.cache_len.max()) + 1 > self.tcap:
+                    raise RuntimeError(f"KV cache capacity {self.tcap} exceeded")
+                self.lookup_step(q, k_new, v_new)
+                out = self.fused()
+                self.cache_len += 1
+            else:
+                out = self.attend(q)
+                self.write_tokens(k_new[:, :, None], v_new[:, :, None])
         todo = self.needs_update()
         self.last_update = None
         if todo:

@@ -122,8 +122,9 @@ def step(state: EngineState, queries, new_keys, new_values, oracle: bool = False
         ev[1].record()
         ev[2].record()
     else:
-        eng.rotate(q)
-        eng.lookup()
+        if not eng.fused_lookup_path():  # the single-launch lookup forms the exact view itself
+            eng.rotate(q, exact=True, lookup=False)
+        eng.lookup(q)
         ev[1].record()
         out_t = eng.fused()
         ev[2].record()

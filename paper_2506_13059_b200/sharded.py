@@ -110,6 +110,12 @@ class ShardedDecodeEngine:
         # no sinks / buffer on the other ranks: buffer_start = cache_len -> empty buffer
         return self.zero_sinks, e.cache_len_d
 
+    def _contiguous(self) -> bool:
+        """Flat bf16 d=128 ledgers: the logits kernel writes every centroid's replacement weight and
+        the fused kernel streams the value centroids in order (selected ones weighted -inf)."""
+        e = self.eng
+        return e.fused_lookup_path() and not e.led.lookup_f64 and e.mode == "multipole"
+
     # ------------------------------------------------------------------ decode phases
     def phase_norms(self, q: torch.Tensor) -> torch.Tensor:
         """Rotate q, local logits; returns this rank's (M, Z) [L, G, 2]."""
@@ -120,7 +126,7 @@ class ShardedDecodeEngine:
         st = stream_ptr()
         fine = e.led.fine_level()
         el = e.elocal if not e.led.lookup_f64 else None
-        dense = e.rej_dense and el is not None
+        dense = self._contiguous()
         call("mpa_centroid_logits", ptr(e.q_lk), e.Hkv, e.G, e.d, fine, None, None, e.kcap, ptr(e.logits),
              ptr(e.cstats), ptr(el), int(e.led.n_fine.max()), ptr(e.rej_w) if dense else None, e.rej_cap, None, None,
              st)
@@ -147,7 +153,7 @@ class ShardedDecodeEngine:
         st = stream_ptr()
         call("mpa_global_cut", ptr(prefix_all), ptr(prefix_n_all), self.world, e.L, self.prefix_cap, ptr(e.budget),
              ptr(self.cross), st)
-        rej = e._centroid_terms()[0] if e.mode != "flat-no-replacement" else e.rej
+        rej = e._centroid_terms(self._contiguous())[0] if e.mode != "flat-no-replacement" else e.rej
         sink, buf = self._layout()
         el = e.elocal if not e.led.lookup_f64 else None
         call("mpa_select_worklist_sharded", e.led.fine_level(), e.G, ptr(e.logits), ptr(el), ptr(e.cstats),
@@ -155,7 +161,7 @@ class ShardedDecodeEngine:
              ptr(e.tok), e.tok_cap, ptr(rej), ptr(e.rej_w), e.rej_cap, ptr(e.stats), int(e.led.n_fine.max()),
              ptr(self.mz), ptr(self.cross), None, None, self.prefix_cap, ptr(self.gid_off), st)
         ws = e._workspace(0)
-        rej, rej_w, n_rej = e._centroid_terms()
+        rej, rej_w, n_rej = e._centroid_terms(self._contiguous())
         call("mpa_sparse_decode_partials", e.cache_struct, ptr(e.q_rot), e.Hkv, e.G, ptr(e.tok), ptr(e.stats[0]),
              e.tok_cap, ptr(rej), ptr(rej_w), ptr(n_rej), e.rej_cap, ptr(e.led.vc), e.kcap, None, 0, 0,
              ptr(ws), ws.numel(), ptr(self.part), st)

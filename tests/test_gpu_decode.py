@@ -185,27 +185,3 @@ def test_batched_sequences_identical():
     b = four.attend(q.expand(4, -1, -1).contiguous())
     for s in range(4):
         assert rel_err(b[s].cpu().numpy(), a[0].cpu().numpy()).max() < 1e-5
-
-
-
-def test_fused_lookup_rotation_matches(monkeypatch):
-    # MPA_FUSED_ROTATE=1: the logits kernel forms the lookup view itself (q_lk = NULL + (cos, sin)
-    # table); same selection as the separate rotation kernel and the oracle, same outputs
-    tr = gen_synthetic(64, 3000, HeadLayout(32, 8, 128), 0.05, seed=7, decode_steps=4)
-    cfg = EngineConfig(block_size=1024, local_buffer=32, token_budget=256, seed=7)
-    P = tr.prompt_len
-    ledgers = [O.prefill_ledger(tr.keys[h, :P], tr.values[h, :P], P, cfg, h) for h in range(8)]
-    eng = _engine(tr, cfg, torch.bfloat16, ledgers)
-    q = torch.as_tensor(tr.queries[:, 0]).cuda()[None]
-    a = eng.attend(q).clone()
-    sel_a = eng.tok.clone()
-    st_a = eng.head_stats().copy()
-    monkeypatch.setenv("MPA_FUSED_ROTATE", "1")
-    assert eng._fused_rotation()
-    b = eng.attend(q).clone()
-    st_b = eng.head_stats()
-    assert np.array_equal(st_a, st_b)
-    for h in range(8):
-        n = int(st_a[h, 0])
-        assert np.array_equal(np.sort(sel_a[h, :n].cpu().numpy()), np.sort(eng.tok[h, :n].cpu().numpy()))
-    assert rel_err(b[0].cpu().numpy(), a[0].cpu().numpy()).max() < 1e-6

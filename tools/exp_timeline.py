@@ -24,12 +24,12 @@ def main():
     eng, Q, KN, VN, _ = bench.build_engine(args, 0, torch.device("cuda", 0))
     lib = _lib.lib()
     eng.rotate(Q[0])
-    eng.lookup()
+    eng.lookup(Q[0])
     import torch as _t
     for _ in range(3):
-        eng.lookup()
+        eng.lookup(Q[0])
     _t.cuda.synchronize()
-    eng.lookup()
+    eng.lookup(Q[0])
     _t.cuda.synchronize()
     buf = (C.c_ulonglong * (4096 * 8))()
     lib.mpa_debug_trace_lookup(buf, 4096 * 8)

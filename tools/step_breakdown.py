@@ -58,16 +58,37 @@ def main():
     rows = {
         "rotate(lookup view)": lambda: eng.rotate(q, exact=False, lookup=True),
         "rotate(exact view)": lambda: eng.rotate(q, exact=True, lookup=False),
-        "lookup (logits + select)": lambda: eng.lookup(),
+        "lookup (logits + select)": lambda: eng.lookup(q),
         "fused decode": lambda: eng.fused(),
         "append (+2 tiny sub kernels)": append_only,
-        "eager rotate+lookup": lambda: (eng.rotate(q), eng.lookup()),
+        "eager rotate+lookup": lambda: (eng.rotate(q), eng.lookup(q)),
         "eager attend": lambda: eng.attend(q),
     }
     out = {k: t(f) for k, f in rows.items()}
     # the step graph (replays advance the cache; bounded reps)
     n0 = int(eng.cache_len[0])
     out["graph step"] = t(lambda: eng.step(Q[1], KN[1], VN[1]), reps=min(a.reps, 40))
+    out["graph replay only"] = t(lambda: eng._graph.replay(), reps=min(a.reps, 40))
+    # cold: L2 flushed (write + read 256 MB) before each launch, flush excluded from the timing
+    fl_a = torch.empty(64 << 20, dtype=torch.float32, device=eng.device)
+    fl_b = torch.empty(64 << 20, dtype=torch.float32, device=eng.device)
+
+    def cold(fn, reps=20):
+        ts = []
+        for _ in range(reps):
+            fl_a.fill_(1.0)
+            fl_b.sum()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            ts.append((e0, e1))
+        torch.cuda.synchronize()
+        return float(np.mean([x.elapsed_time(y) for x, y in ts])) * 1e3
+
+    for k in ("lookup (logits + select)", "fused decode", "eager attend"):
+        out[k + " [cold]"] = cold(rows[k])
+    out["graph replay only [cold]"] = cold(lambda: eng._graph.replay())
     print(f"batch {a.batch} ctx {a.ctx}: warm per-launch us (cache_len {n0} -> {int(eng.cache_len[0])})")
     for k, v in out.items():
         print(f"  {k:32s} {v:8.1f}")
