@@ -56,10 +56,10 @@ __device__ __forceinline__ void trace(int, int = 0) {}
 #endif
 
 constexpr int kThreads = 256;
-constexpr int kGroups = 4;                      // phase-1 consumer groups of 64 threads
+constexpr int kGroups = 8;                      // phase-1 consumers: one warp per 64-row chunk
 constexpr int kGT = kThreads / kGroups;
 constexpr int kChunk = 64;                      // centroid rows per chunk
-constexpr int kRPT = 4;                         // rows per thread (x G heads x a quarter of d)
+constexpr int kRPT = 8;                         // rows per thread (x G heads x a quarter of d)
 constexpr int kRG = kChunk / kRPT;
 constexpr int kStages = 8;
 constexpr int kStageB = kChunk * 256;           // 16 KB: two 64-column halves of 64 rows
@@ -70,20 +70,21 @@ constexpr double kUnscale896 = 0x1p896;
 constexpr int kSmemBudget = 230000;             // dynamic smem budget (static ~1.5 KB on top)
 
 // shared-memory layout (after the 1024-aligned stage area): logits [G][kcmax] fp64 | lookup q
-// slots [G][4][QRow] fp64 | sizes [kcmax] | sflag [kcmax]
+// slots [G][4][QRow] fp64 | sizes [kcmax] | member offsets [kcmax] | sflag [kcmax]
 template <int G>
 struct Geo {
     static constexpr int GP = G <= 4 ? 4 : 8;
     static constexpr int qB = G * 4 * QRow * 8;
     static constexpr int fixedB = 1024 + kStageArea + qB + 64;
-    static constexpr int kc_raw = (kSmemBudget - fixedB) / (G * 8 + 4 + 1);
+    static constexpr int kc_raw = (kSmemBudget - fixedB) / (G * 8 + 4 + 4 + 1);
     static constexpr int kcmax_ = kc_raw / kChunk * kChunk;
     static constexpr int kcmax = kcmax_ > 4096 ? 4096 : kcmax_;  // keys (8 B each) fit in 2 stages
     static constexpr int lgB = G * kcmax * 8;
     static constexpr int oLG = 1024 + kStageArea;
     static constexpr int oQ = oLG + lgB;
     static constexpr int oSZ = oQ + qB;
-    static constexpr int oFL = oSZ + kcmax * 4;
+    static constexpr int oMO = oSZ + kcmax * 4;
+    static constexpr int oFL = oMO + kcmax * 4;
     static constexpr int total = oFL + kcmax + 16;
 };
 
@@ -167,8 +168,7 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
 __device__ __forceinline__ double bf16hi_s896(unsigned fbits) {
     return __hiloint2double((int)(((int)fbits >> 3) & 0x8FFFE000), 0);
 }
-// one out-of-line copy each of the fp64 exp / sincos (cold-phase code stays small in the i-cache)
-__device__ __noinline__ double dexp(double x) { return exp(x); }
+// one out-of-line copy of the fp64 sincos (its slow path is large)
 __device__ __noinline__ void dsincos(double x, double* s, double* c) { sincos(x, s, c); }
 // block-wide exclusive scan of one u64 per thread
 __device__ __forceinline__ unsigned long long scan_u64(unsigned long long v, unsigned long long* sc,
@@ -211,6 +211,7 @@ step_kernel(const __grid_constant__ CUtensorMap tm_kc, const Params p) {
     double* LG = reinterpret_cast<double*>(base_sm + Ge::oLG);             // [G][Kc] logits -> e
     double* qs = reinterpret_cast<double*>(base_sm + Ge::oQ);              // [G][4][QRow] lookup view
     int* sizes = reinterpret_cast<int*>(base_sm + Ge::oSZ);                // [Kc]
+    int* moff_s = reinterpret_cast<int*>(base_sm + Ge::oMO);               // [Kc] member CSR offsets
     uint8_t* sflag = base_sm + Ge::oFL;                                    // [Kc]
     __shared__ __align__(8) uint64_t bar[kStages];
     __shared__ double s_red[kThreads / 32][G];
@@ -258,14 +259,20 @@ step_kernel(const __grid_constant__ CUtensorMap tm_kc, const Params p) {
 
     const int32_t* szp = p.size + (size_t)l * p.kcap + c0;
     const int32_t* ofp = p.moff + (size_t)l * (p.kcap + 1) + c0;
-    for (int i = tid; i < nloc; i += kThreads) sizes[i] = __ldg(szp + i);  // read in phase 2
+    for (int i = tid; i < nloc; i += kThreads) {  // read in phases 2-6
+        sizes[i] = __ldg(szp + i);
+        moff_s[i] = __ldg(ofp + i);
+    }
+    __shared__ double s_cs[D];  // (cos, sin) of the lookup view's angles: constant, loaded early
+    if (tid < D) s_cs[tid] = p.cs_lk[tid];
     pdl_wait();  // q (and k, v) come from the stream predecessor
+    __syncthreads();  // s_cs
     const int seq = l / p.n_kv_heads;
     const int qpos = p.cache_len[seq];
     for (int e = tid; e < G * (D / 2); e += kThreads) {
         const int g = e / (D / 2), i = e - g * (D / 2), k = 2 * i;
         const float2 xy = *reinterpret_cast<const float2*>(p.q + ((size_t)l * G + g) * D + k);
-        const double x = (double)xy.x, y = (double)xy.y, c = p.cs_lk[2 * i], sn = p.cs_lk[2 * i + 1];
+        const double x = (double)xy.x, y = (double)xy.y, c = s_cs[2 * i], sn = s_cs[2 * i + 1];
         double* slot = qs + (g * 4 + k / QD) * QRow + (k % QD);
         slot[0] = __dsub_rn(__dmul_rn(x, c), __dmul_rn(y, sn));
         slot[1] = __dadd_rn(__dmul_rn(x, sn), __dmul_rn(y, c));
@@ -320,7 +327,7 @@ step_kernel(const __grid_constant__ CUtensorMap tm_kc, const Params p) {
                     }
                 }
             }
-            group_bar(1 + gi, kGT);  // the stage is consumed
+            __syncwarp();  // the stage is consumed (the group is one warp)
             if (gt == 0 && j + kStages < nch) issue(&tm_kc, bar, j + kStages, kStages);
 
             double a2[RH][G];
@@ -405,7 +412,7 @@ step_kernel(const __grid_constant__ CUtensorMap tm_kc, const Params p) {
             for (int g = 0; g < G; ++g) {
                 const double lgv = LG[(size_t)g * Kc + i];
                 wv[g] = (float)(lgv + lnN);  // the replacement weight's log, reused by the decode kernel
-                const double e = dexp(lgv - M[g]);
+                const double e = exp(lgv - M[g]);
                 LG[(size_t)g * Kc + i] = e;
                 z[g] = fma(e, nsz, z[g]);
             }
@@ -787,7 +794,7 @@ step_kernel(const __grid_constant__ CUtensorMap tm_kc, const Params p) {
             else hi = mid - 1;
         }
         const int slot = tbase + j;
-        if (slot < p.tok_cap) T[slot] = __ldg(mem + __ldg(ofp + sel_c[lo]) + (j - sel_t[lo]));
+        if (slot < p.tok_cap) T[slot] = __ldg(mem + moff_s[sel_c[lo]] + (j - sel_t[lo]));
     }
     if (rank == 0 && tid == 0) {
         const long long ntok = ns + nb + tot_tok;
