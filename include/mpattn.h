@@ -357,6 +357,32 @@ int mpa_km_assign_from_level(const mpa_km* km, const int32_t* off, const int32_t
  * +n_new.  dist is [n_prob, n_new, k_max] fp64 workspace. */
 int mpa_km_seq_assign(const mpa_km* km, const int32_t* tail_start, int n_new, double* dist, void* stream);
 
+
+/* ---- fp64 kernels behind the reference's module-level Python API (attention.*, rope.*,
+ * clustering.* for numpy / Cluster / BlockLedger callers; paper_2506_13059_b200/{attention,rope,
+ * clustering}.py).  Device pointers, one stream, row-major fp64 unless noted. */
+/* rope.py:37-53 `rotate`: out[r] = x[r] rotated by pos[r] * inv_freq (fp64 positions, interleaved pairs). */
+int mpa_ref_rotate(const double* x, const double* pos, int n, int d, const double* inv_freq, double* out,
+                   void* stream);
+/* attention.py:84-86, 154, 276: out[g, j] = q[g] . x[j] / sqrt(d). */
+int mpa_ref_logits(const double* q, const double* x, int G, int n, int d, double* out, void* stream);
+/* attention.py:58-68 `_partial_from_logits`: m = max l, w = exp(l - m) * weights (NULL: 1), s = sum w,
+ * a = w @ values; out = [a (d), m, s]; weights_out (optional) = w / s (attention.py:105-117). */
+int mpa_ref_partial(const double* logits, const double* values, const double* weights, int n, int d,
+                    double* out, double* weights_out, void* stream);
+/* attention.py:144-164, 267-290: scores[j] = mean_g e[g, j] / (e[g] . sizes), e = exp(l - max_g);
+ * z_out (optional) [G] = the normalisers. */
+int mpa_ref_group_scores(const double* logits, const double* sizes, int G, int n, double* scores,
+                         double* z_out, void* stream);
+/* clustering.py:84-88 + argmin: assign[i] = first minimum of |p|^2 + |c|^2 - 2 p . c. */
+int mpa_ref_nearest(const double* points, const double* centroids, int n, int k, int d, int64_t* assign,
+                    void* stream);
+/* clustering.py:113-120, 195-203, 255-257: per cluster c (CSR off[k + 1] / idx into the rows of
+ * points): mean[c] = in-order sum / count, or with weights (per point row) sum w x / sum w (optional);
+ * with centroids, *sqerr += sum |p - centroids[c]|^2. */
+int mpa_ref_seg_stats(const double* points, const int64_t* off, const int64_t* idx, const double* weights,
+                      int k, int d, double* mean, const double* centroids, double* sqerr, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

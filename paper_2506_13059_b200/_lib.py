@@ -63,6 +63,12 @@ _SIGS = {
     "mpa_decode_step": [_vp, _vp, _vp, C.POINTER(MpaCache), _vp, _vp, C.c_int, C.c_int, C.POINTER(MpaLevel), _vp,
                         _vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp, C.c_int, _vp, _vp, C.c_int,
                         _vp],
+    "mpa_ref_rotate": [_vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp],
+    "mpa_ref_logits": [_vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp],
+    "mpa_ref_partial": [_vp, _vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp],
+    "mpa_ref_group_scores": [_vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp],
+    "mpa_ref_nearest": [_vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp],
+    "mpa_ref_seg_stats": [_vp, _vp, _vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp],
     "mpa_hier_candidates": [C.POINTER(MpaLevel), _vp, C.c_int, _vp, _vp, C.c_int, _vp],
     "mpa_build_worklist": [C.POINTER(MpaLevel), C.POINTER(MpaLevel), C.c_int, _vp, _vp, C.c_int, _vp, _vp,
                            _vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int, _vp, _vp,

@@ -8,6 +8,12 @@ Reference (pkg/src/multipole_attn/clustering.py):
   build_hierarchy           :210-264   -> _hierarchy()
   kmeans / lloyd            :123-184   -> KMeansBatch (all problems of a call in one batch)
 
+The module also carries the reference's module-level API (names, arguments, types, exceptions of
+clustering.py:33-657: Cluster / Block / BlockLedger, kmeans, lloyd, build_prefill_index(_head),
+append_tokens, build_hierarchy, the positional comparator, audit_ledger, wcss, the JSON dump) for
+callers holding numpy arrays; each routes through the same kernels (a one-ledger engine, or the
+fp64 kernels of csrc/mpa_refapi.cu), see the end of this file.
+
 Everything numerical runs on the GPU.  The host only draws the reference's RNG indices
 (numpy PCG64 with the same seeds: block k-means init, update samples, hierarchy init), keeps
 the per-ledger block table (spans and cluster counts) and sizes the problem batches.
@@ -174,7 +180,10 @@ def _refresh_counts(eng, ledgers) -> None:
 
 
 def _head(eng, l: int) -> int:
-    return l % eng.Hkv
+    """kv-head index of ledger l for the block seeds (an engine built for one reference head sets
+    eng.head_ids to that head)."""
+    ids = getattr(eng, "head_ids", None)
+    return int(ids[l]) if ids is not None else l % eng.Hkv
 
 
 # ---------------------------------------------------------------------------- prefill
@@ -309,7 +318,7 @@ class _Ticks:
             print("update phases ms: " + ", ".join(f"{n} {v:.2f}" for n, v in self.parts), file=sys.stderr)
 
 
-def online_update(eng, seqs, cursor: int) -> dict:
+def online_update(eng, seqs, cursor: int, samples: np.ndarray | None = None) -> dict:
     """Absorb the oldest L buffered tokens of every kv-head of `seqs` into the final block
     (clustering.py:404-472), then split / settle (:359-401) and refresh the final block's
     hierarchy (:465-471).  Returns timing-free counters (rounds, splits)."""
@@ -331,8 +340,11 @@ def online_update(eng, seqs, cursor: int) -> dict:
     FS = np.fromiter((r.start for r in fin), np.int64, len(fin))
     BS = eng.buffer_start[S].astype(np.int64)
     # the draw depends on (seed, cursor, kv-head) only (pipeline.py:170-172): once per head
-    samp_tab = np.stack([update_rng(cfg.seed, cursor, h).choice(L, size=n_new, replace=False)
-                         for h in range(eng.Hkv)]).astype(np.int64)
+    if samples is not None:  # drawn by the caller's generator (module-level append_tokens)
+        samp_tab = np.broadcast_to(np.asarray(samples, np.int64).reshape(1, n_new), (eng.Hkv, n_new))
+    else:
+        samp_tab = np.stack([update_rng(cfg.seed, cursor, h).choice(L, size=n_new, replace=False)
+                             for h in range(eng.Hkv)]).astype(np.int64)
     SAMP = samp_tab[Ls % eng.Hkv]                                    # [n, n_new]
     base = np.concatenate([[0], np.cumsum(FK + n_new)[:-1]]).astype(np.int64)
     c_at = int((FK + n_new).sum())
@@ -539,3 +551,391 @@ def positional_update(eng, seqs) -> dict:
     eng._sync_scalars()
     _refresh_counts(eng, ledgers)
     return {"rounds": 0, "splits": _split(eng, ledgers, settle=False)}
+
+
+# ============================================================================ reference API
+# The module-level surface of pkg/src/multipole_attn/clustering.py (same names, arguments, return
+# types and exceptions) for callers holding numpy arrays.  k-means runs on the batched Lloyd kernels
+# (fp64 points); block indices, updates and the positional comparator run on a one-ledger engine
+# (the serving code path, fp32 cache); means, nearest-centroid checks and squared errors run on the
+# fp64 kernels of csrc/mpa_refapi.cu.  Only bookkeeping over the returned arrays stays on the host.
+
+import hashlib as _hashlib
+import json as _json
+from dataclasses import dataclass as _dataclass
+
+MAX_EXTRA_ITERS = 100  # clustering.py:30 (csrc/mpa_cluster.cu kMaxExtraRounds)
+
+
+class LedgerAuditError(AssertionError):
+    """clustering.py:33."""
+
+
+@_dataclass
+class Cluster:
+    """clustering.py:37-43."""
+
+    key_centroid: np.ndarray
+    value_centroid: np.ndarray | None
+    size: int
+    member_indices: np.ndarray
+    children: list | None = None
+
+
+@_dataclass
+class Block:
+    """clustering.py:46-54."""
+
+    start: int
+    end: int
+    clusters: list
+    level1: list | None = None
+
+    def __len__(self) -> int:
+        return self.end - self.start
+
+
+@_dataclass
+class BlockLedger:
+    """clustering.py:57-77."""
+
+    sink_end: int
+    sealed: list
+    final: Block
+    buffer_start: int
+    total: int
+    split_count: int = 0
+
+    @property
+    def buffer_len(self) -> int:
+        return self.total - self.buffer_start
+
+    def blocks(self) -> list:
+        return self.sealed + [self.final]
+
+    def clustered_tokens(self) -> int:
+        return self.buffer_start - self.sink_end
+
+
+def _device():
+    from . import _dev
+
+    return _dev.device()
+
+
+def lloyd(points, init_centroids, min_iters: int):
+    """clustering.py:123-143 on the batched Lloyd kernels (fp64 points, no weights): rounds until an
+    assignment pass is a fixed point after >= min_iters updates; (centroids, assignment)."""
+    pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64))
+    init = np.array(init_centroids, dtype=np.float64)
+    n, d = pts.shape
+    k = init.shape[0]
+    dev = _device()
+    km = KMeansBatch(dev, d, [(0, 0, n, k)], torch.as_tensor(init, device=dev),
+                     pts64=torch.as_tensor(pts, device=dev), rows64_cap=n, min_iters=min_iters)
+    km.lloyd()
+    return km.cent.cpu().numpy(), km.assign[:n].cpu().numpy().astype(np.int64)
+
+
+def _clusters_from_assignment(points, centroids, assign, base_index, index_map=None):
+    """clustering.py:146-167: empty clusters dropped, ids compacted in centroid order."""
+    out = []
+    for cid in range(centroids.shape[0]):
+        local = np.flatnonzero(assign == cid)
+        if local.size == 0:
+            continue
+        idx = np.sort(index_map[local]) if index_map is not None else local.astype(np.int64) + base_index
+        out.append(Cluster(key_centroid=centroids[cid].copy(), value_centroid=None, size=int(local.size),
+                           member_indices=idx))
+    return out
+
+
+def kmeans(points, k: int, iters: int, seed: int) -> list:
+    """clustering.py:170-184: random-point init (host PCG64, the reference's draw), device Lloyd."""
+    points = np.asarray(points, dtype=np.float64)
+    n = points.shape[0]
+    if n == 0:
+        raise ValueError("points must be nonempty")
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    k = min(k, n)
+    init = points[np.random.default_rng(seed).choice(n, size=k, replace=False)]
+    centroids, assign = lloyd(points, init, iters)
+    return _clusters_from_assignment(points, centroids, assign, base_index=0)
+
+
+def fill_value_centroids(clusters: list, values) -> None:
+    """clustering.py:187-192: value centroid = in-order mean of the members' values (device)."""
+    from . import _dev
+
+    if not clusters:
+        return
+    vals = np.asarray(values, dtype=np.float64)
+    mean, _ = _dev.seg_stats(vals, [c.member_indices for c in clusters])
+    for c, v in zip(clusters, mean):
+        c.value_centroid = v
+
+
+def wcss(ledger: BlockLedger, keys) -> float:
+    """clustering.py:195-203: within-cluster sum of squared distances over all fine clusters."""
+    from . import _dev
+
+    clusters = [c for b in ledger.blocks() for c in b.clusters]
+    if not clusters:
+        return 0.0
+    _, sq = _dev.seg_stats(np.asarray(keys, dtype=np.float64), [c.member_indices for c in clusters],
+                           centroids=np.stack([c.key_centroid for c in clusters]))
+    return sq
+
+
+def build_hierarchy(clusters: list, cfg, block_len: int, seed: int) -> list:
+    """clustering.py:210-264: size-weighted Lloyd over the fine key centroids on the device; coarse
+    key / value centroids are the size-weighted means of their children (exact member means)."""
+    from . import _dev
+
+    if cfg.hierarchy is None:
+        raise ConfigError("hierarchy is not enabled")
+    if not clusters:
+        return []
+    fine_kc = np.ascontiguousarray(np.stack([c.key_centroid for c in clusters]))
+    weights = np.array([c.size for c in clusters], dtype=np.float64)
+    k1 = min(len(clusters), max(1, -(-block_len // cfg.hierarchy.r1)))
+    init = fine_kc[np.random.default_rng(seed).choice(len(clusters), size=k1, replace=False)].copy()
+    n, d = fine_kc.shape
+    dev = _device()
+    km = KMeansBatch(dev, d, [(0, 0, n, k1)], torch.as_tensor(init, device=dev),
+                     pts64=torch.as_tensor(fine_kc, device=dev),
+                     wts=torch.as_tensor(weights.astype(np.int32), device=dev), rows64_cap=n,
+                     min_iters=cfg.refine_kmeans_iters)
+    km.lloyd()
+    assign = km.assign[:n].cpu().numpy()
+    groups = [np.flatnonzero(assign == cid) for cid in range(k1)]
+    groups = [g for g in groups if g.size]
+    kc, _ = _dev.seg_stats(fine_kc, groups, weights=weights)
+    vc, _ = _dev.seg_stats(np.stack([c.value_centroid for c in clusters]), groups, weights=weights)
+    out = []
+    for j, g in enumerate(groups):
+        members = [clusters[i] for i in g]
+        out.append(Cluster(key_centroid=kc[j], value_centroid=vc[j], size=int(sum(c.size for c in members)),
+                           member_indices=np.sort(np.concatenate([c.member_indices for c in members])),
+                           children=[int(i) for i in g]))
+    return out
+
+
+def _one_ledger_engine(keys, values, n_tok: int, cfg, head: int, mode: str = "multipole", tcap: int | None = None):
+    from .core import HeadLayout
+    from .engine import DecodeEngine
+
+    keys = np.asarray(keys, dtype=np.float32)
+    values = np.asarray(values, dtype=np.float32)
+    d = keys.shape[-1]
+    eng = DecodeEngine(cfg, HeadLayout(1, 1, d), 1, tcap=max(16, tcap or n_tok + 1), dtype=torch.float32, mode=mode)
+    eng.head_ids = np.array([head])
+    dev = eng.device
+    eng.write_tokens(torch.as_tensor(keys[None, None, :n_tok], device=dev),
+                     torch.as_tensor(values[None, None, :n_tok], device=dev))
+    return eng
+
+
+def _to_block_ledger(eng, l: int = 0) -> BlockLedger:
+    """The engine's ledger l as reference objects (Cluster lists per block, coarse level1)."""
+    h = eng.export_ledger(l)
+    off = np.zeros(h.size.size + 1, np.int64)
+    np.cumsum(h.size, out=off[1:])
+    blocks = []
+    for r in h.blocks:
+        cl = [Cluster(key_centroid=h.kc[i].copy(), value_centroid=h.vc[i].copy(), size=int(h.size[i]),
+                      member_indices=np.sort(h.mem[off[i]:off[i + 1]]).astype(np.int64))
+              for i in range(r.f0, r.f0 + r.fk)]
+        lvl = None
+        if h.csize is not None:
+            lvl = []
+            for j in range(r.c0, r.c0 + r.ck):
+                kids = [int(c) - r.f0 for c in h.child[h.child_off[j]:h.child_off[j + 1]]]
+                lvl.append(Cluster(key_centroid=h.ckc[j].copy(), value_centroid=h.cvc[j].copy(),
+                                   size=int(h.csize[j]),
+                                   member_indices=np.sort(np.concatenate([cl[c].member_indices for c in kids])),
+                                   children=kids))
+        blocks.append(Block(r.start, r.end, cl, lvl))
+    return BlockLedger(sink_end=h.sink_end, sealed=blocks[:-1], final=blocks[-1], buffer_start=h.buffer_start,
+                       total=h.total, split_count=h.splits)
+
+
+def _to_host_ledger(ledger: BlockLedger, hier: bool):
+    from .ledger import BlockRow, HostLedger
+
+    rows, kcs, vcs, sizes, mem = [], [], [], [], []
+    ckc, cvc, csz, child, coff = [], [], [], [], [0]
+    f0 = c0 = 0
+    for b in ledger.blocks():
+        ck = len(b.level1) if (hier and b.level1 is not None) else 0
+        rows.append(BlockRow(b.start, b.end, f0, len(b.clusters), c0, ck))
+        for c in b.clusters:
+            kcs.append(c.key_centroid)
+            vcs.append(c.value_centroid)
+            sizes.append(c.size)
+            mem.append(np.asarray(c.member_indices, np.int64))
+        if ck:
+            for c in b.level1:
+                ckc.append(c.key_centroid)
+                cvc.append(c.value_centroid)
+                csz.append(c.size)
+                child.extend(f0 + int(x) for x in c.children)
+                coff.append(len(child))
+        f0 += len(b.clusters)
+        c0 += ck
+    d = len(kcs[0]) if kcs else 1
+    h = HostLedger(ledger.sink_end, ledger.buffer_start, ledger.total, ledger.split_count, rows,
+                   np.stack(kcs) if kcs else np.zeros((0, d)), np.stack(vcs) if vcs else np.zeros((0, d)),
+                   np.array(sizes, np.int64), np.concatenate(mem) if mem else np.zeros(0, np.int64))
+    if hier:
+        h.ckc = np.stack(ckc) if ckc else np.zeros((0, d))
+        h.cvc = np.stack(cvc) if cvc else np.zeros((0, d))
+        h.csize = np.array(csz, np.int64)
+        h.child_off = np.array(coff, np.int64)
+        h.child = np.array(child, np.int64)
+    return h
+
+
+def build_prefill_index_head(keys, values, prompt_len: int, cfg, head: int) -> BlockLedger:
+    """clustering.py:288-326: blockwise clustering of one head's prompt on the engine's kernels."""
+    if prompt_len <= cfg.sink_tokens:
+        raise ConfigError(f"prompt_len {prompt_len} must exceed sink_tokens {cfg.sink_tokens}")
+    eng = _one_ledger_engine(keys, values, prompt_len, cfg, head)
+    eng.prefill()
+    return _to_block_ledger(eng)
+
+
+def build_prefill_index(trace, cfg) -> list:
+    """clustering.py:329-340: one ledger per kv-head over the trace's prompt."""
+    return [build_prefill_index_head(trace.keys[h, : trace.prompt_len], trace.values[h, : trace.prompt_len],
+                                     trace.prompt_len, cfg, h) for h in range(trace.layout.num_kv_heads)]
+
+
+def _reload(ledger: BlockLedger, keys, values, cfg, head: int, mode: str):
+    eng = _one_ledger_engine(keys, values, ledger.total, cfg, head, mode=mode,
+                             tcap=max(ledger.total + 1, np.asarray(keys).shape[0] + 1))
+    eng.load_ledgers([_to_host_ledger(ledger, cfg.hierarchy is not None)])
+    return eng
+
+
+def _replace(dst: BlockLedger, src: BlockLedger) -> BlockLedger:
+    dst.sink_end, dst.sealed, dst.final = src.sink_end, src.sealed, src.final
+    dst.buffer_start, dst.total, dst.split_count = src.buffer_start, src.total, src.split_count
+    return dst
+
+
+def append_tokens(ledger: BlockLedger, keys, values, cfg, rng: np.random.Generator, head: int = 0) -> BlockLedger:
+    """clustering.py:404-472: absorb the oldest L buffered tokens into the final block (sampled
+    centroids drawn from `rng` like the reference, sequential running-mean assignment, Lloyd
+    refinement, split / settle, hierarchy refresh) on the engine's update kernels.  Mutates and
+    returns the ledger."""
+    L = cfg.local_buffer
+    if ledger.buffer_len < 2 * L:
+        raise RuntimeError(f"buffer underflow: have {ledger.buffer_len} tokens, need {2 * L}")
+    n_new = -(-L // cfg.fine_ratio)
+    sampled = rng.choice(L, size=n_new, replace=False)
+    eng = _reload(ledger, keys, values, cfg, head, "multipole")
+    online_update(eng, [0], 0, samples=sampled)
+    return _replace(ledger, _to_block_ledger(eng))
+
+
+def build_positional_index_head(keys, values, prompt_len: int, cfg) -> BlockLedger:
+    """clustering.py:497-526: contiguous pages of r tokens with page-mean centroids."""
+    if prompt_len <= cfg.sink_tokens:
+        raise ConfigError(f"prompt_len {prompt_len} must exceed sink_tokens {cfg.sink_tokens}")
+    eng = _one_ledger_engine(keys, values, prompt_len, cfg, 0, mode="positional-baseline")
+    eng.prefill()
+    return _to_block_ledger(eng)
+
+
+def append_tokens_positional(ledger: BlockLedger, keys, values, cfg) -> BlockLedger:
+    """clustering.py:529-541: positional-page analogue of append_tokens."""
+    L = cfg.local_buffer
+    if ledger.buffer_len < 2 * L:
+        raise RuntimeError("buffer underflow")
+    eng = _reload(ledger, keys, values, cfg, 0, "positional-baseline")
+    positional_update(eng, [0])
+    return _replace(ledger, _to_block_ledger(eng))
+
+
+def audit_ledger(ledger: BlockLedger, keys, cfg, values=None, rel_tol: float = 1e-5,
+                 check_assignment: bool = True) -> None:
+    """clustering.py:548-623: raise LedgerAuditError on a violated invariant (partition, spans,
+    final-block size, centroid = member mean, nearest assignment).  Index bookkeeping on the host,
+    the numeric checks on the device."""
+    from . import _dev
+
+    keys64 = np.asarray(keys, dtype=np.float64)
+    pieces = [np.arange(0, ledger.sink_end, dtype=np.int64)]
+    for block in ledger.blocks():
+        for c in block.clusters:
+            pieces.append(np.asarray(c.member_indices, np.int64))
+            if c.size != len(c.member_indices):
+                raise LedgerAuditError("cluster size disagrees with member count")
+    pieces.append(np.arange(ledger.buffer_start, ledger.total, dtype=np.int64))
+    flat = np.sort(np.concatenate(pieces))
+    if flat.size != ledger.total or not np.array_equal(flat, np.arange(ledger.total, dtype=np.int64)):
+        raise LedgerAuditError("token indices do not tile [0, total) exactly")
+    cursor = ledger.sink_end
+    for block in ledger.sealed:
+        if block.start != cursor or len(block) != cfg.block_size:
+            raise LedgerAuditError("sealed block spans are not contiguous W-sized")
+        cursor = block.end
+    if ledger.final.start != cursor or ledger.final.end != ledger.buffer_start:
+        raise LedgerAuditError("final block span inconsistent with buffer start")
+    if len(ledger.final) > cfg.block_size + cfg.alpha:
+        raise LedgerAuditError("final block exceeds W + alpha")
+    if ledger.split_count > 0 and len(ledger.final) < cfg.alpha:
+        raise LedgerAuditError("final block shorter than alpha after a split")
+    values64 = None if values is None else np.asarray(values, dtype=np.float64)
+    for block in ledger.blocks():
+        if not block.clusters:
+            continue
+        members = [np.asarray(c.member_indices, np.int64) for c in block.clusters]
+        idx = np.concatenate(members)
+        if idx.size and (idx.min() < block.start or idx.max() >= block.end):
+            raise LedgerAuditError("cluster member outside its block span")
+        centroids = np.stack([c.key_centroid for c in block.clusters])
+        means, _ = _dev.seg_stats(keys64, members)
+        scale = max(1.0, float(np.max(np.abs(centroids))))
+        if np.max(np.abs(means - centroids)) > rel_tol * scale:
+            raise LedgerAuditError("key centroid drifted from member mean")
+        if values64 is not None:
+            vcent = np.stack([c.value_centroid for c in block.clusters])
+            vmeans, _ = _dev.seg_stats(values64, members)
+            vscale = max(1.0, float(np.max(np.abs(vcent))))
+            if np.max(np.abs(vmeans - vcent)) > rel_tol * vscale:
+                raise LedgerAuditError("value centroid drifted from member mean")
+        if check_assignment:
+            owner = np.concatenate([np.full(c.size, cid) for cid, c in enumerate(block.clusters)])
+            if not np.array_equal(_dev.nearest(keys64[idx], centroids), owner):
+                raise LedgerAuditError("a member is not assigned to its nearest centroid")
+
+
+def ledger_diagnostic(ledger: BlockLedger) -> dict:
+    """clustering.py:626-650: JSON-friendly summary (spans, sizes, centroid checksums)."""
+
+    def checksum(arr) -> str:
+        return _hashlib.sha256(np.ascontiguousarray(arr, dtype="<f8").tobytes()).hexdigest()[:16]
+
+    def block_doc(block: Block) -> dict:
+        doc = {"span": [block.start, block.end], "cluster_sizes": [c.size for c in block.clusters],
+               "key_centroid_checksums": [checksum(c.key_centroid) for c in block.clusters]}
+        if block.level1 is not None:
+            doc["level1_sizes"] = [c.size for c in block.level1]
+        return doc
+
+    return {"sink_end": ledger.sink_end, "buffer": [ledger.buffer_start, ledger.total],
+            "split_count": ledger.split_count, "sealed": [block_doc(b) for b in ledger.sealed],
+            "final": block_doc(ledger.final)}
+
+
+def dump_ledger_json(ledger: BlockLedger) -> str:
+    """clustering.py:653-654."""
+    return _json.dumps(ledger_diagnostic(ledger), sort_keys=True)
+
+
+def load_ledger_json(doc: str) -> dict:
+    """clustering.py:657."""
+    return _json.loads(doc)

@@ -675,7 +675,8 @@ int validate(const mpa_km* km) {
                     km->assign && km->prev && km->cent && km->count && km->order && km->cstart && km->state,
                 MPA_ERR_ARG, "mpa_km: null argument");
     MPA_REQUIRE((km->pts != nullptr) != (km->pts64 != nullptr), MPA_ERR_ARG, "mpa_km: exactly one of pts / pts64");
-    MPA_REQUIRE(!km->pts64 || km->wts, MPA_ERR_ARG, "mpa_km: pts64 needs weights");
+    // pts64 with weights: the hierarchy's weighted Lloyd (clustering.py:210-264); without: plain fp64
+    // Lloyd over caller points (clustering.py:123-143, the module-level kmeans / lloyd API)
     MPA_REQUIRE(km->n_max <= kMaxPoints, MPA_ERR_UNSUPPORTED, "mpa_km: %d points per problem > %d", km->n_max,
                 kMaxPoints);
     MPA_REQUIRE(km->k_max < (1 << (32 - kIdxBits)), MPA_ERR_UNSUPPORTED, "mpa_km: k_max %d too large", km->k_max);

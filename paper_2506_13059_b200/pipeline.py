@@ -6,53 +6,27 @@ Same signatures, modes, cadence and exceptions as the reference:
   * `step(state, queries, new_keys, new_values, oracle, audit, timers)` attends BEFORE appending
     the step's token and runs the online update when the buffer reaches 2L,
   * outputs are float64 (Hq, d) numpy arrays and a `DecodeReport` per step.
-Extra keyword `dtype` selects the KV-cache dtype (float32: the 1e-5 parity mode, the default
-here because the reference computes in fp64; bfloat16: the serving layout).
+Extra keyword `dtype`: float64 (default) keeps the reference's numerics -- the ledgers come from the
+engine's clustering kernels and every attention partial runs on the fp64 kernels behind the
+module-level API (attention.decode_step_attention, csrc/mpa_refapi.cu); float32 / bfloat16 run the
+batched serving kernels (the single-launch lookup and the stream-K fused decode) on a cache of that
+dtype.
 """
 
 from __future__ import annotations
 
 import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 import torch
 
+from .attention import DecodeReport, StepHeadResult, oracle_topk_tokens
 from .core import ConfigError, EngineConfig, KvTrace
 from .engine import DecodeEngine
+from .rope import RopeParams
 
 MODES = ("multipole", "oracle", "flat-no-replacement", "positional-baseline")
-
-
-@dataclass
-class StepHeadResult:
-    selected_refs: list
-    selected_tokens: int
-    scored_centroids: int
-    rejected_centroids: int
-
-
-@dataclass
-class DecodeReport:
-    """attention.py:390-407."""
-
-    step: int
-    errors: list | None
-    per_head: list
-    cache_len: int
-    sink_count: int
-    buffer_len: int
-    num_kv_heads: int
-    update_occurred: bool = False
-    update_wall_time: float = 0.0
-    selected_indices: list | None = None
-    oracle_topk: list | None = None
-    mode: str = "multipole"
-    outputs: np.ndarray | None = None
-    gpu_times: dict = field(default_factory=dict)
-
-    def mean_error(self) -> float:
-        return float(np.mean(self.errors)) if self.errors else float("nan")
 
 
 @dataclass
@@ -67,15 +41,46 @@ class EngineState:
     def cache_len(self) -> int:
         return self.trace.prompt_len + self.cursor
 
+    fp64: bool = False
+    _ref_ledgers: list | None = None
+
     @property
     def ledgers(self):
-        """Host views of the device ledgers (one per kv-head)."""
+        """The device ledgers as reference BlockLedger objects (one per kv-head; pipeline.py:55-62)."""
         if self.mode == "oracle":
             return []
-        return [self.engine.export_ledger(h) for h in range(self.trace.layout.num_kv_heads)]
+        from .clustering import _to_block_ledger
+
+        if self._ref_ledgers is None:
+            self._ref_ledgers = [_to_block_ledger(self.engine, h) for h in range(self.trace.layout.num_kv_heads)]
+        return self._ref_ledgers
+
+    @property
+    def stores(self):
+        """Per-kv-head views of the device KV cache (pipeline.py:26-52 `_KvStore`: n, keys, values)."""
+        return [_KvStoreView(self.engine, h) for h in range(self.trace.layout.num_kv_heads)]
 
 
-def prefill(trace: KvTrace, cfg: EngineConfig, mode: str = "multipole", dtype: torch.dtype = torch.float32,
+class _KvStoreView:
+    """Read-only view of one kv-head's cached (pre-rotation) keys and values."""
+
+    def __init__(self, eng: DecodeEngine, h: int):
+        self._eng, self._h = eng, h
+
+    @property
+    def n(self) -> int:
+        return int(self._eng.cache_len[0])
+
+    @property
+    def keys(self) -> np.ndarray:
+        return self._eng.k_raw[self._h, : self.n].float().cpu().numpy()
+
+    @property
+    def values(self) -> np.ndarray:
+        return self._eng.v[self._h, : self.n].float().cpu().numpy()
+
+
+def prefill(trace: KvTrace, cfg: EngineConfig, mode: str = "multipole", dtype: torch.dtype = torch.float64,
             capacity: int | None = None) -> EngineState:
     if mode not in MODES:
         raise ValueError(f"unknown mode {mode!r}")
@@ -83,23 +88,24 @@ def prefill(trace: KvTrace, cfg: EngineConfig, mode: str = "multipole", dtype: t
     P = trace.prompt_len
     if P <= cfg.sink_tokens and mode != "oracle":
         raise ConfigError(f"prompt_len {P} must exceed sink_tokens {cfg.sink_tokens}")
-    eng = DecodeEngine(cfg, lay, 1, tcap=capacity or max(16, trace.total_len + 1), dtype=dtype, mode=mode)
+    fp64 = dtype == torch.float64
+    eng = DecodeEngine(cfg, lay, 1, tcap=capacity or max(16, trace.total_len + 1),
+                       dtype=torch.float32 if fp64 else dtype, mode=mode)
     dev = eng.device
     eng.write_tokens(torch.as_tensor(trace.keys[:, :P], device=dev)[None],
                      torch.as_tensor(trace.values[:, :P], device=dev)[None])
     eng.prefill()
-    return EngineState(trace=trace, cfg=cfg, mode=mode, engine=eng)
+    return EngineState(trace=trace, cfg=cfg, mode=mode, engine=eng, fp64=fp64)
 
 
-def _refs(eng: DecodeEngine, h: int) -> list:
-    """(block, cluster, 2) refs of the selected fine clusters of kv-head h (sorted by ref)."""
+def _refs(eng: DecodeEngine, h: int, flag: np.ndarray, cand: np.ndarray | None) -> list:
+    """(block, cluster, 2) refs of the selected fine clusters of kv-head h (sorted by ref), from host
+    copies of the selection flags (and, hierarchy, the candidate lists)."""
     led = eng.led
-    flag = eng.flag[h].cpu().numpy()
     if eng.cfg.hierarchy is None:
         ids = np.flatnonzero(flag[: int(led.n_fine[h])])
     else:
-        n = int(eng.n_cand[h])
-        cand = eng.cand[h, :n].cpu().numpy()
+        n = int(eng.n_cand[h]) if cand is None else cand.size
         ids = np.sort(cand[flag[:n] == 1])
     out = []
     for r_i, row in enumerate(led.blocks[h]):
@@ -108,54 +114,122 @@ def _refs(eng: DecodeEngine, h: int) -> list:
     return out
 
 
-def step(state: EngineState, queries, new_keys, new_values, oracle: bool = False, audit: bool = False,
-         timers: dict | None = None):
-    eng = state.engine
-    lay = state.trace.layout
+def _attend_fp64(state: EngineState, queries, oracle: bool, timers):
+    """The reference's numerics: attention.decode_step_attention over the engine's ledgers and cache,
+    every partial on the fp64 kernels (pipeline.py:137-150); oracle mode: exact attention per q-head
+    (pipeline.py:97-121)."""
+    from . import attention
+
+    eng, lay, cfg = state.engine, state.trace.layout, state.cfg
+    n = int(eng.cache_len[0])
+    keys = eng.k_raw[:, :n].double().cpu().numpy()
+    values = eng.v[:, :n].double().cpu().numpy()
+    q = np.asarray(queries)
+    if state.mode == "oracle":
+        params = RopeParams(head_dim=lay.head_dim, theta=cfg.rope_theta, window_offset=cfg.window_offset)
+        pos = np.arange(n, dtype=np.int64)
+        out = np.empty((lay.num_q_heads, lay.head_dim))
+        for h in range(lay.num_kv_heads):
+            for g in lay.q_heads_of(h):
+                out[g] = attention.exact_attention(q[g], n, keys[h], values[h], pos, params)
+        rep = DecodeReport(step=state.cursor, errors=[0.0] * lay.num_q_heads, per_head=[], cache_len=n,
+                           sink_count=0, buffer_len=0, num_kv_heads=lay.num_kv_heads, mode="oracle")
+        return out, rep
+    return attention.decode_step_attention(q, state.ledgers, list(keys), list(values), n, state.cursor, cfg, lay,
+                                           mode=state.mode, oracle=oracle, timers=timers)
+
+
+def _attend_engine(state: EngineState, queries, oracle: bool):
+    """The batched serving kernels (bf16 / fp32 cache): one lookup launch (flat) or the staged lookup
+    kernels (hierarchy), the fused decode kernel; the report from one batched device -> host copy."""
+    eng, lay = state.engine, state.trace.layout
     dev = eng.device
     q = torch.as_tensor(np.asarray(queries, np.float32), device=dev)[None]
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    n = eng.cache_len[0]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    n = int(eng.cache_len[0])
     ev[0].record()
     if state.mode == "oracle":
         out_t = eng.attend_dense(q)
         ev[1].record()
-        ev[2].record()
     else:
         if not eng.fused_lookup_path():  # the single-launch lookup forms the exact view itself
             eng.rotate(q, exact=True, lookup=False)
         eng.lookup(q)
         ev[1].record()
         out_t = eng.fused()
-        ev[2].record()
+    ev[2].record()
     out = out_t[0].double().cpu().numpy()
-    errors = None
+    errors = topk = None
     if oracle:
         ref = eng.attend_dense(q)[0].double().cpu().numpy()
         errors = list(np.linalg.norm(out - ref, axis=1) / np.maximum(np.linalg.norm(ref, axis=1), 1e-300))
     per_head, sel = [], []
     if state.mode != "oracle":
+        H = lay.num_kv_heads
         st = eng.head_stats()
-        for h in range(lay.num_kv_heads):
-            ns = min(int(eng.sink_end[0]), n)
-            nb = n - int(eng.buffer_start[0])
-            idx = np.sort(eng.tok[h, ns + nb: st[h, 0]].cpu().numpy().astype(np.int64))
-            sel.append(idx)
+        ntok = int(st[:H, 0].max())
+        tok = eng.tok[:H, :max(ntok, 1)].cpu().numpy()
+        kf = int(eng.led.n_fine[:H].max())
+        flags = eng.flag[:H, :max(kf, 1)].cpu().numpy()
+        cands = None
+        if eng.cfg.hierarchy is not None:
+            nc = eng.n_cand[:H].cpu().numpy()
+            cm = eng.cand[:H, :max(int(nc.max()), 1)].cpu().numpy()
+            cands = [cm[h, : int(nc[h])] for h in range(H)]
+        ns = min(int(eng.sink_end[0]), n)
+        nb = n - int(eng.buffer_start[0])
+        for h in range(H):
+            sel.append(np.sort(tok[h, ns + nb: st[h, 0]].astype(np.int64)))
             scored = int(eng.led.n_fine[h]) if eng.cfg.hierarchy is None else \
-                int(eng.led.n_coarse[h]) + int(eng.n_cand[h])
-            per_head.append(StepHeadResult(_refs(eng, h), int(st[h, 2]), scored,
-                                           int(st[h, 1]) if state.mode != "flat-no-replacement" else 0))
+                int(eng.led.n_coarse[h]) + int(cands[h].size)
+            per_head.append(StepHeadResult(_refs(eng, h, flags[h], cands[h] if cands else None), int(st[h, 2]),
+                                           scored, int(st[h, 1]) if state.mode != "flat-no-replacement" else 0))
+    if oracle and state.mode != "oracle":
+        # attention.py:500-529: the true top tokens (group-summed exact weight) among the clustered ones,
+        # k = the selected token count of the head (budget when none)
+        params = RopeParams(head_dim=lay.head_dim, theta=state.cfg.rope_theta, window_offset=state.cfg.window_offset)
+        qn = np.asarray(queries, np.float64)
+        keys = eng.k_raw[:, :n].double().cpu().numpy()  # the cached (pre-rotation) keys
+        topk = [oracle_topk_tokens(qn, list(lay.q_heads_of(h)), keys[h], n, np.arange(min(int(eng.sink_end[0]), n)),
+                                   np.arange(int(eng.buffer_start[0]), n), int(sel[h].size), state.cfg.token_budget,
+                                   params) for h in range(lay.num_kv_heads)]
+    elif oracle:
+        topk = [np.zeros(0, np.int64) for _ in range(lay.num_kv_heads)]
     rep = DecodeReport(step=state.cursor, errors=errors if oracle else ([0.0] * lay.num_q_heads
                                                                       if state.mode == "oracle" else None),
-                       per_head=per_head, cache_len=int(n),
-                       sink_count=0 if state.mode == "oracle" else min(state.cfg.sink_tokens, int(n)),
-                       buffer_len=0 if state.mode == "oracle" else int(n - eng.buffer_start[0]),
-                       num_kv_heads=lay.num_kv_heads, selected_indices=sel if sel else None, mode=state.mode)
+                       per_head=per_head, cache_len=n,
+                       sink_count=0 if state.mode == "oracle" else min(state.cfg.sink_tokens, n),
+                       buffer_len=0 if state.mode == "oracle" else n - int(eng.buffer_start[0]),
+                       num_kv_heads=lay.num_kv_heads, selected_indices=sel if sel else None, oracle_topk=topk,
+                       mode=state.mode)
+    torch.cuda.synchronize()
+    rep.gpu_times = {"lookup": ev[0].elapsed_time(ev[1]) * 1e-3, "exact": ev[1].elapsed_time(ev[2]) * 1e-3}
+    return out, rep
+
+
+def step(state: EngineState, queries, new_keys, new_values, oracle: bool = False, audit: bool = False,
+         timers: dict | None = None):
+    """pipeline.py:124-191: attend, then append the step's token and run the buffered cluster update
+    once the buffer holds 2L tokens.  Mutates state."""
+    eng = state.engine
+    lay = state.trace.layout
+    dev = eng.device
+    if state.fp64:
+        out, rep = _attend_fp64(state, queries, oracle, timers)
+    else:
+        out, rep = _attend_engine(state, queries, oracle)
+        if timers is not None:
+            timers["lookup"] = timers.get("lookup", 0.0) + rep.gpu_times["lookup"]
+            timers["exact"] = timers.get("exact", 0.0) + rep.gpu_times["exact"]
+            timers["replace"] = timers.get("replace", 0.0)  # fused into the exact kernel
     # append + online update
     t0 = time.perf_counter()
     kn = torch.as_tensor(np.asarray(new_keys, np.float32), device=dev)[None, :, None]
     vn = torch.as_tensor(np.asarray(new_values, np.float32), device=dev)[None, :, None]
     eng.write_tokens(kn, vn)
+    if state._ref_ledgers is not None:
+        for led in state._ref_ledgers:
+            led.total += 1
     todo = eng.needs_update()
     if todo:
         from . import clustering
@@ -165,28 +239,22 @@ def step(state: EngineState, queries, new_keys, new_values, oracle: bool = False
         else:
             clustering.online_update(eng, todo, eng.cursor)
         torch.cuda.synchronize()
+        state._ref_ledgers = None
         rep.update_occurred = True
         rep.update_wall_time = time.perf_counter() - t0
         if audit:
             from .audit import audit_engine
 
             audit_engine(eng, check_assignment=state.mode != "positional-baseline")
+        if timers is not None:
+            timers["update"] = timers.get("update", 0.0) + rep.update_wall_time
     eng.cursor += 1
     state.cursor += 1
-    ev[3].record()
-    torch.cuda.synchronize()
-    rep.gpu_times = {"lookup": ev[0].elapsed_time(ev[1]) * 1e-3, "exact": ev[1].elapsed_time(ev[2]) * 1e-3}
-    if timers is not None:
-        timers["lookup"] = timers.get("lookup", 0.0) + rep.gpu_times["lookup"]
-        timers["exact"] = timers.get("exact", 0.0) + rep.gpu_times["exact"]
-        timers["replace"] = timers.get("replace", 0.0)  # fused into the exact kernel
-        if rep.update_occurred:
-            timers["update"] = timers.get("update", 0.0) + rep.update_wall_time
     return out, rep
 
 
 def run(trace: KvTrace, cfg: EngineConfig, mode: str = "multipole", oracle: bool = False, audit: bool = False,
-        max_steps: int | None = None, collect_outputs: bool = False, dtype: torch.dtype = torch.float32):
+        max_steps: int | None = None, collect_outputs: bool = False, dtype: torch.dtype = torch.float64):
     if trace.decode_steps < 1:
         raise ValueError("trace has no decode steps")
     state = prefill(trace, cfg, mode=mode, dtype=dtype)
