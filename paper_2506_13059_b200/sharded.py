@@ -4,11 +4,12 @@ Every ledger's sealed W-blocks are split contiguously over the ranks; the last r
 the final block, the sinks and the local buffer, so the online update stays rank-local.  Cluster
 ids are global (gid_off[l] + local id) and blocks are assigned in order, so the reference's
 (block, cluster) tie-break order survives the split.  A decode step exchanges three small
-messages (include/mpattn.h, "Sequence-sharded decode"):
+messages, one all-gather each (include/mpattn.h, "Sequence-sharded decode"):
 
   1. per (ledger, q-head) (M, Z) of Eq. 1 -> global normalisers (attention.py:276-278);
   2. each rank's candidates that can be globally selected (its local take-while-cum<B prefix,
-     <= B + 1 entries) -> the same global crossing candidate on every rank (attention.py:192-207);
+     <= B + 1 entries, and their count, in one message) -> the same global crossing candidate on
+     every rank (attention.py:192-207);
   3. per (ledger, q-head) unnormalised (m, s, a) partials -> LSE merge (attention.py:230-239).
 
 `Comm` abstracts the all-gather: `TorchComm` uses torch.distributed (NCCL on the GPU tensors
@@ -62,9 +63,11 @@ class TorchComm:
             out = torch.empty(self.world * t.numel(), dtype=t.dtype, device=t.device)
             self.dist.all_gather_into_tensor(out, t.reshape(-1), group=self.group)
             return out.view((self.world,) + tuple(t.shape))
-        parts = [torch.empty_like(t) for _ in range(self.world)]
-        self.dist.all_gather(parts, t, group=self.group)
-        return torch.stack(parts)
+        # gloo: host tensors (a CUDA tensor makes the round trip through host memory)
+        src = t.cpu() if t.is_cuda else t
+        parts = [torch.empty_like(src) for _ in range(self.world)]
+        self.dist.all_gather(parts, src, group=self.group)
+        return torch.stack(parts).to(t.device)
 
 
 class ShardedDecodeEngine:
@@ -82,8 +85,11 @@ class ShardedDecodeEngine:
         self.prefix_cap = cfg.token_budget + 1
         self.mz_loc = torch.zeros(L, G, 2, dtype=torch.float64, device=dev)
         self.mz = torch.zeros(L, G, 2, dtype=torch.float64, device=dev)
-        self.prefix = torch.zeros(L, self.prefix_cap * PREFIX_ENTRY_BYTES, dtype=torch.uint8, device=dev)
-        self.prefix_n = torch.zeros(L, dtype=torch.int32, device=dev)
+        # one message for exchange 2: the candidate prefixes [L, cap] entries then their counts [L]
+        pb = L * self.prefix_cap * PREFIX_ENTRY_BYTES
+        self.msg = torch.zeros(pb + 4 * L, dtype=torch.uint8, device=dev)
+        self.prefix = self.msg[:pb].view(L, self.prefix_cap * PREFIX_ENTRY_BYTES)
+        self.prefix_n = self.msg[pb:].view(torch.int32)
         self.cross = torch.zeros(L, CROSS_BYTES, dtype=torch.uint8, device=dev)
         self.part = torch.zeros(L, G, d + 2, dtype=torch.float32, device=dev)
         self.gid_off = torch.zeros(L, dtype=torch.int32, device=dev)
@@ -133,8 +139,9 @@ class ShardedDecodeEngine:
         call("mpa_head_norms", ptr(e.cstats), e.cstats.shape[1], ptr(e.led.count), e.L, e.G, ptr(self.mz_loc), st)
         return self.mz_loc
 
-    def phase_prefix(self, mz_all: torch.Tensor):
-        """Global normalisers from every rank's (M, Z); local candidate prefix."""
+    def phase_prefix(self, mz_all: torch.Tensor) -> torch.Tensor:
+        """Global normalisers from every rank's (M, Z); this rank's candidate prefix and its counts in
+        one message (self.msg)."""
         e = self.eng
         st = stream_ptr()
         call("mpa_merge_norms", ptr(mz_all), self.world, e.L, e.G, ptr(self.mz), st)
@@ -145,7 +152,14 @@ class ShardedDecodeEngine:
              ptr(e.budget), ptr(sink), ptr(buf), ptr(e.cache_len_d), e.Hkv, 1, ptr(e.flag), ptr(e.sel_tokens),
              ptr(e.tok), e.tok_cap, ptr(e.rej), ptr(e.rej_w), e.rej_cap, ptr(e.stats), int(e.led.n_fine.max()),
              ptr(self.mz), None, ptr(self.prefix), ptr(self.prefix_n), self.prefix_cap, ptr(self.gid_off), st)
-        return self.prefix, self.prefix_n
+        return self.msg
+
+    def split_msgs(self, msg_all: torch.Tensor):
+        """[P, msg] -> (prefixes [P, L, cap] entries, counts [P, L]) as the contiguous arrays
+        mpa_global_cut reads."""
+        e = self.eng
+        pb = e.L * self.prefix_cap * PREFIX_ENTRY_BYTES
+        return msg_all[:, :pb].contiguous(), msg_all[:, pb:].contiguous().view(torch.int32)
 
     def phase_partials(self, prefix_all: torch.Tensor, prefix_n_all: torch.Tensor) -> torch.Tensor:
         """Global crossing candidate, local work lists, local fused attention -> partials."""
@@ -173,11 +187,29 @@ class ShardedDecodeEngine:
         return e.out
 
     def attend(self, q: torch.Tensor, comm) -> torch.Tensor:
-        """One sharded decode step on this rank (collectives through `comm`)."""
+        """One sharded decode step on this rank: three all-gathers through `comm` -- (M, Z), the
+        candidate-prefix message, the (m, s, a) partials."""
         mz_all = comm.all_gather(self.phase_norms(q))
-        prefix, prefix_n = self.phase_prefix(mz_all)
-        parts = self.phase_partials(comm.all_gather(prefix), comm.all_gather(prefix_n))
+        prefix_all, prefix_n_all = self.split_msgs(comm.all_gather(self.phase_prefix(mz_all)))
+        parts = self.phase_partials(prefix_all, prefix_n_all)
         return self.phase_merge(comm.all_gather(parts))
+
+    def step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, comm) -> torch.Tensor:
+        """attend, append the step's token on every rank (pipeline.py:137-159), and run the online
+        update on the tail rank, which owns the final block, the sinks and the buffer (the update is
+        rank-local: clustering.py:404-472).  A split seals the block on the tail rank; cluster ids stay
+        global because the tail is the last rank."""
+        from . import clustering
+
+        e = self.eng
+        out = self.attend(q, comm)
+        e.write_tokens(k_new[:, :, None], v_new[:, :, None])
+        if self.tail:
+            todo = e.needs_update()
+            if todo:
+                clustering.online_update(e, todo, e.cursor)
+        e.cursor += 1
+        return out
 
 
 class LocalGroup:
@@ -196,9 +228,8 @@ class LocalGroup:
 
     def attend(self, q: torch.Tensor) -> torch.Tensor:
         mz_all = torch.stack([e.phase_norms(q).clone() for e in self.engines])
-        pre = [e.phase_prefix(mz_all) for e in self.engines]
-        prefix_all = torch.stack([p.clone() for p, _ in pre])
-        prefix_n_all = torch.stack([n.clone() for _, n in pre])
+        msg_all = torch.stack([e.phase_prefix(mz_all).clone() for e in self.engines])
+        prefix_all, prefix_n_all = self.engines[0].split_msgs(msg_all)
         parts_all = torch.stack([e.phase_partials(prefix_all, prefix_n_all).clone() for e in self.engines])
         outs = [e.phase_merge(parts_all).clone() for e in self.engines]
         return outs[0]

@@ -103,3 +103,76 @@ def test_sharded_matches_unsharded(world):
             assert np.array_equal(got_tok, want_tok), (step, l)
             n_rej = sum(int(e.eng.head_stats()[l, 1]) for e in group.engines)
             assert n_rej == st[l, 1]
+
+
+def _sharded_worker(rank, world, port, q):
+    """One rank of a real 2-process sequence-sharded decode (torch.distributed, gloo for the
+    collectives, both processes on cuda:0): ShardedDecodeEngine.step through TorchComm, checked
+    against an unsharded engine built in the same process from the same seeded data."""
+    import torch.distributed as dist
+
+    from paper_2506_13059_b200.core import EngineConfig, HeadLayout
+    from paper_2506_13059_b200.engine import DecodeEngine
+    from paper_2506_13059_b200.sharded import ShardedDecodeEngine, TorchComm
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = TorchComm()
+        lay = HeadLayout(16, 4, 128)
+        cfg = EngineConfig(block_size=1024, alpha=512, local_buffer=16, token_budget=256, tokens_per_centroid=8,
+                           rope_theta=1e6, seed=3)
+        n_seq, ctx, steps = 2, 5000, 40
+        gen = torch.Generator(device="cuda").manual_seed(11)
+        k = torch.randn(n_seq, lay.num_kv_heads, ctx, 128, device="cuda", generator=gen)
+        v = torch.randn(n_seq, lay.num_kv_heads, ctx, 128, device="cuda", generator=gen)
+        Q = torch.randn(steps, n_seq, lay.num_q_heads, 128, device="cuda", generator=gen)
+        KN = torch.randn(steps, n_seq, lay.num_kv_heads, 128, device="cuda", generator=gen)
+        VN = torch.randn(steps, n_seq, lay.num_kv_heads, 128, device="cuda", generator=gen)
+        ref = DecodeEngine(cfg, lay, n_seq, tcap=ctx + steps + 16, dtype=torch.bfloat16, use_graphs=False)
+        ref.write_tokens(k, v)
+        ref.prefill()
+        se = ShardedDecodeEngine(cfg, lay, n_seq, ctx + steps + 16, rank, world)
+        se.write_tokens(k, v)
+        se.prefill_local()
+        n_all = comm.all_gather(torch.as_tensor(se.eng.led.n_fine, dtype=torch.int64)).numpy()
+        se.set_gid_offsets(n_all)
+        worst, tok_bad, n_upd = 0.0, 0, 0
+        for t in range(steps):
+            want = ref.step(Q[t], KN[t], VN[t]).clone()
+            st_ref = ref.head_stats()
+            toks_ref = [np.sort(ref.tok[l, : st_ref[l, 0]].cpu().numpy()) for l in range(ref.L)]
+            n_upd += ref.last_update is not None
+            got = se.step(Q[t], KN[t], VN[t], comm)
+            worst = max(worst, ((got - want).norm(dim=-1) / want.norm(dim=-1)).max().item())
+            st = se.eng.head_stats()
+            mine = [se.eng.tok[l, : st[l, 0]].cpu().numpy() for l in range(ref.L)]
+            allt = comm.all_gather(torch.as_tensor(np.concatenate([np.bincount(m, minlength=ctx + steps)
+                                                                   for m in mine]).astype(np.int32)))
+            union = allt.sum(0).numpy().reshape(ref.L, -1)
+            tok_bad += sum(int(not np.array_equal(np.flatnonzero(union[l]), toks_ref[l])) for l in range(ref.L))
+        q.put((rank, worst, tok_bad, n_upd))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_two_processes_with_updates():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        r, worst, bad, n_upd = q.get(timeout=600)
+        res[r] = (worst, bad, n_upd)
+    for p in procs:
+        p.join(timeout=120)
+    for r, (worst, bad, n_upd) in res.items():
+        assert bad == 0, (r, bad)
+        assert worst < 2e-3, (r, worst)
+        assert n_upd >= 2, n_upd
