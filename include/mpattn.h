@@ -307,6 +307,8 @@ typedef struct mpa_km {
     int32_t sum_n, sum_k;    /* total points / centroids of the batch                    */
     void* tc_ws;             /* >= mpa_km_tc_workspace(n_prob, sum_k, sum_n, d) bytes    */
     int64_t tc_ws_bytes;
+    int32_t* dirty;          /* [sum k] optional scratch: clusters whose members changed in the last
+                                round (NULL: every centroid is recomputed every round)          */
 } mpa_km;
 
 /* Workspace of the tcgen05 assignment path (bf16 centroid terms, norms, recheck list). */

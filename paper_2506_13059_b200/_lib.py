@@ -43,7 +43,8 @@ class MpaKm(C.Structure):
                 ("prob_l", _vp), ("prob_start", _vp), ("prob_n", _vp), ("prob_k", _vp), ("pt_off", _vp),
                 ("c_off", _vp), ("assign", _vp), ("prev", _vp), ("p2", _vp), ("cent", _vp), ("c2", _vp),
                 ("count", _vp), ("order", _vp), ("cstart", _vp), ("state", _vp), ("flag", _vp),
-                ("pts_rows", _i64), ("sum_n", _i32), ("sum_k", _i32), ("tc_ws", _vp), ("tc_ws_bytes", _i64)]
+                ("pts_rows", _i64), ("sum_n", _i32), ("sum_k", _i32), ("tc_ws", _vp), ("tc_ws_bytes", _i64),
+                ("dirty", _vp)]
 
 
 _KM = C.POINTER(MpaKm)

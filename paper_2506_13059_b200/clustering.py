@@ -74,6 +74,7 @@ class KMeansBatch:
         self.count = (count_init.to(torch.int32).contiguous() if count_init is not None
                       else torch.zeros(max(K, 1), **i32))
         self.cstart = torch.zeros(max(K, 1), **i32)
+        self.dirty = sc("dirty", K, torch.int32)
         self.state = torch.zeros(max(self.P, 1), 4, **i32)
         self.flag = torch.zeros(2, **i32)
         self.src = (pts, tcap, pts64, wts, rows64_cap)
@@ -98,7 +99,7 @@ class KMeansBatch:
                      ptr(t["n"]), ptr(t["k"]), ptr(t["pt_off"]), ptr(t["c_off"]), ptr(self.assign), ptr(self.prev),
                      ptr(self.p2), ptr(self.cent), ptr(self.c2), ptr(self.count), ptr(self.order), ptr(self.cstart),
                      ptr(self.state), ptr(self.flag), self.pts_rows, self.sum_n, self.sum_k, ptr(self.tc_ws),
-                     self.tc_ws.numel() if self.tc_ws is not None else 0)
+                     self.tc_ws.numel() if self.tc_ws is not None else 0, ptr(self.dirty))
 
     def lloyd(self) -> int:
         import ctypes

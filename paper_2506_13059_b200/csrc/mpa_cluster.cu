@@ -23,10 +23,11 @@
 #include "mpa_common.cuh"
 
 int mpa_km_assign_tc(const mpa_km& k, cudaStream_t st);  // mpa_km_tc.cu
+bool mpa_km_tc_applies(const mpa_km& k);
 
 namespace mpa {
 
-enum { ST_ACTIVE = 0, ST_ROUNDS = 1, ST_DOMEANS = 2, ST_EMPTY = 3 };
+enum { ST_ACTIVE = 0, ST_ROUNDS = 1, ST_DOMEANS = 2, ST_REPAIRED = 3 };
 constexpr int kMaxExtraRounds = 100;  // clustering.py:30
 
 template <typename T>
@@ -42,15 +43,43 @@ __device__ __forceinline__ double point_elem(const mpa_km& km, int l, int row, i
 
 // ---------------------------------------------------------------------------- norms / state
 
+// four consecutive coordinates k..k+3 of a point row (d % 4 == 0: one vector load)
+__device__ __forceinline__ void point_row4(const mpa_km& km, int l, int row, int k, double (&x)[4]) {
+    if ((km.d & 3) == 0) {
+        if (km.pts64) {
+            const double2* b = reinterpret_cast<const double2*>(km.pts64 + ((size_t)l * km.rows64_cap + row) * km.d + k);
+            const double2 u = __ldg(b), v = __ldg(b + 1);
+            x[0] = u.x, x[1] = u.y, x[2] = v.x, x[3] = v.y;
+        } else if (km.pts_dtype == MPA_BF16) {
+            const uint2 r = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(km.pts) +
+                                                                 ((size_t)l * km.tcap + row) * km.d + k));
+            const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.x));
+            const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.y));
+            x[0] = a.x, x[1] = a.y, x[2] = b.x, x[3] = b.y;
+        } else {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(km.pts) +
+                                                                  ((size_t)l * km.tcap + row) * km.d + k));
+            x[0] = f.x, x[1] = f.y, x[2] = f.z, x[3] = f.w;
+        }
+        return;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) x[e] = k + e < km.d ? point_elem(km, l, row, k + e) : 0.0;
+}
+
+
 __global__ void km_p2_kernel(mpa_km km) {
     const int p = blockIdx.y;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= km.prob_n[p]) return;
     const int l = km.prob_l[p], row = km.prob_start[p] + i;
     double s = 0.0;
-    for (int k = 0; k < km.d; ++k) {
-        const double x = point_elem(km, l, row, k);
-        s = __dadd_rn(s, __dmul_rn(x, x));
+    for (int k = 0; k < km.d; k += 4) {  // sequential over k (numpy's einsum order)
+        double x[4];
+        point_row4(km, l, row, k, x);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (k + e < km.d) s = __dadd_rn(s, __dmul_rn(x[e], x[e]));
     }
     km.p2[km.pt_off[p] + i] = s;
 }
@@ -60,6 +89,10 @@ __global__ void km_c2_kernel(mpa_km km, int only_active) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= km.prob_k[p]) return;
     if (only_active && !km.state[p * 4 + ST_DOMEANS]) return;
+    if (km.dirty) {  // start of a Lloyd run: every centroid is new
+        if (!only_active) km.dirty[km.c_off[p] + j] = 1;
+        else if (!km.dirty[km.c_off[p] + j]) return;
+    }
     const double* c = km.cent + (size_t)(km.c_off[p] + j) * km.d;
     double s = 0.0;
     for (int k = 0; k < km.d; ++k) s = __dadd_rn(s, __dmul_rn(c[k], c[k]));
@@ -72,7 +105,7 @@ __global__ void km_init_state_kernel(mpa_km km) {
     km.state[p * 4 + ST_ACTIVE] = 1;
     km.state[p * 4 + ST_ROUNDS] = 0;
     km.state[p * 4 + ST_DOMEANS] = 0;
-    km.state[p * 4 + ST_EMPTY] = 0;
+    km.state[p * 4 + ST_REPAIRED] = 0;
 }
 
 __global__ void km_any_active_kernel(mpa_km km, int* dev_flag) {
@@ -228,6 +261,7 @@ __global__ void __launch_bounds__(kRoundThreads) km_round_kernel(mpa_km km, int 
 
     if (!grouping_only) {
         // ---- _repair_empty (clustering.py:91-110), sequential and rare
+        bool repaired = false;
         while (true) {
             int first_empty = 0x7fffffff;
             for (int j = threadIdx.x; j < K; j += blockDim.x)
@@ -321,6 +355,7 @@ __global__ void __launch_bounds__(kRoundThreads) km_round_kernel(mpa_km km, int 
             }
             __syncthreads();
             const int far = s_int[3];
+            repaired = true;
             for (int k = threadIdx.x; k < d; k += blockDim.x) cent[(size_t)cid * d + k] = point_elem(km, l, start + far, k);
             if (threadIdx.x == 0 && km.c2) {
                 double s = 0.0;
@@ -347,8 +382,25 @@ __global__ void __launch_bounds__(kRoundThreads) km_round_kernel(mpa_km km, int 
         } else {
             if (threadIdx.x == 0) {
                 km.state[p * 4 + ST_DOMEANS] = 1;
+                km.state[p * 4 + ST_REPAIRED] = repaired;
                 if (rounds >= km.min_iters + kMaxExtraRounds) km.state[p * 4 + ST_ACTIVE] = 0;  // final means
                 else km.state[p * 4 + ST_ROUNDS] = rounds + 1;
+            }
+            if (km.dirty) {
+                // clusters whose member set changed this round (the only centroids the means
+                // kernel, the norms and the tensor-core split have to recompute)
+                int* dt = km.dirty + km.c_off[p];
+                if (rounds >= 1 && !repaired) {  // a repair rewrote a centroid: recompute all
+                    for (int j = threadIdx.x; j < K; j += blockDim.x) dt[j] = 0;
+                    __syncthreads();
+                    for (int i = threadIdx.x; i < n; i += blockDim.x)
+                        if (asg[i] != prv[i]) {
+                            dt[asg[i]] = 1;
+                            dt[prv[i]] = 1;
+                        }
+                } else {
+                    for (int j = threadIdx.x; j < K; j += blockDim.x) dt[j] = 1;
+                }
             }
             for (int i = threadIdx.x; i < n; i += blockDim.x) prv[i] = asg[i];
         }
@@ -374,7 +426,7 @@ __global__ void __launch_bounds__(kRoundThreads) km_round_kernel(mpa_km km, int 
     }
     int kbits = 1;
     while ((1 << kbits) < K) ++kbits;
-    Sort(sort_tmp).Sort(keys, 0, min(32, kIdxBits + kbits));
+    Sort(sort_tmp).Sort(keys, kIdxBits, min(32, kIdxBits + kbits));  // stable: points stay ascending
 #pragma unroll
     for (int e = 0; e < kSortItems; ++e) {
         const int pos = threadIdx.x * kSortItems + e;
@@ -386,44 +438,166 @@ __global__ void __launch_bounds__(kRoundThreads) km_round_kernel(mpa_km km, int 
 
 constexpr int kMeansWarps = 8;
 
+// four consecutive coordinates of a point row in their storage type
+template <typename T> struct Row4;
+template <> struct Row4<__nv_bfloat16> {
+    uint2 r;
+    __device__ __forceinline__ void load(const void* base, size_t off) {
+        r = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(base) + off));
+    }
+    __device__ __forceinline__ double get(int e) const {
+        const uint32_t w = e < 2 ? r.x : r.y;
+        return (double)__uint_as_float((e & 1) ? (w & 0xffff0000u) : (w << 16));
+    }
+};
+template <> struct Row4<float> {
+    float4 r;
+    __device__ __forceinline__ void load(const void* base, size_t off) {
+        r = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(base) + off));
+    }
+    __device__ __forceinline__ double get(int e) const { return (double)(e == 0 ? r.x : e == 1 ? r.y : e == 2 ? r.z : r.w); }
+};
+template <> struct Row4<double> {
+    double2 a, b;
+    __device__ __forceinline__ void load(const void* base, size_t off) {
+        const double2* q = reinterpret_cast<const double2*>(reinterpret_cast<const double*>(base) + off);
+        a = __ldg(q);
+        b = __ldg(q + 1);
+    }
+    __device__ __forceinline__ double get(int e) const { return e == 0 ? a.x : e == 1 ? a.y : e == 2 ? b.x : b.y; }
+};
+
+// One warp per cluster, lane = four consecutive coordinates (d % 4 == 0).  Each coordinate is
+// the sequential fp64 sum of the members in ascending point order (np.add.at,
+// clustering.py:113-120); member rows are fetched kMeansBatch at a time, in their storage type,
+// ahead of the (ordered) adds.  Inside a Lloyd run only clusters whose members changed are
+// recomputed, and km.dirty is narrowed to the clusters whose centroid actually moved (unless an
+// empty-cluster repair rewrote a centroid this round).
+constexpr int kMeansBatch = 8;
+template <typename T>
 __global__ void __launch_bounds__(kMeansWarps * 32) km_means_kernel(mpa_km km, int force) {
     const int p = blockIdx.y;
     if (!force && !km.state[p * 4 + ST_DOMEANS]) return;
     const int K = km.prob_k[p], d = km.d;
     const int j = blockIdx.x * kMeansWarps + (threadIdx.x >> 5);
     if (j >= K) return;
+    const bool track = !force && km.dirty;
+    if (track && !km.dirty[km.c_off[p] + j]) return;  // same members: same mean
     const int lane = threadIdx.x & 31;
     const int l = km.prob_l[p], start = km.prob_start[p];
     const int c = km.count[km.c_off[p] + j];
     double* cent = km.cent + (size_t)(km.c_off[p] + j) * d;
     const int* ord = km.order + km.pt_off[p] + km.cstart[km.c_off[p] + j];
+    bool moved = false;
     if (c == 0) {
         if (!km.wts)  // `_means`: empty clusters are reset to the zero vector
-            for (int k = lane; k < d; k += 32) cent[k] = 0.0;
-        return;  // weighted (hierarchy) keeps the previous centroid
-    }
-    double wsum = 0.0;
-    for (int k0 = 0; k0 < d; k0 += 32 * 4) {
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int m = 0; m < c; ++m) {
-            const int i = ord[m];
-            const double w = km.wts ? (double)km.wts[(size_t)l * km.rows64_cap + start + i] : 1.0;
-            if (k0 == 0 && km.wts) wsum = __dadd_rn(wsum, w);
+            for (int k = lane; k < d; k += 32) {
+                moved |= cent[k] != 0.0;
+                cent[k] = 0.0;
+            }
+        // weighted (hierarchy) keeps the previous centroid
+    } else {
+        const void* src = km.pts64 ? (const void*)km.pts64 : km.pts;
+        const size_t rows = km.pts64 ? (size_t)l * km.rows64_cap + start : (size_t)l * km.tcap + start;
+        const int32_t* wrow = km.wts ? km.wts + (size_t)l * km.rows64_cap + start : nullptr;
+        for (int k0 = 0; k0 < d; k0 += 128) {
+            const int k = k0 + lane * 4;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0}, old[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int k = k0 + lane + 32 * e;
-                if (k < d) {
-                    const double x = point_elem(km, l, start + i, k);
-                    acc[e] = __dadd_rn(acc[e], km.wts ? __dmul_rn(x, w) : x);
+            for (int e = 0; e < 4; ++e) old[e] = k + e < d ? cent[k + e] : 0.0;  // fetched ahead of the sums
+            double wsum = 0.0;
+            int nxt[kMeansBatch];
+#pragma unroll
+            for (int u = 0; u < kMeansBatch; ++u) nxt[u] = u < c ? __ldg(ord + u) : -1;
+            for (int m0 = 0; m0 < c; m0 += kMeansBatch) {
+                int ii[kMeansBatch];
+#pragma unroll
+                for (int u = 0; u < kMeansBatch; ++u) ii[u] = nxt[u];
+                Row4<T> xv[kMeansBatch];
+                int32_t w[kMeansBatch];
+#pragma unroll
+                for (int u = 0; u < kMeansBatch; ++u) {
+                    w[u] = 1;
+                    if (ii[u] >= 0) {
+                        if (wrow) w[u] = __ldg(wrow + ii[u]);
+                        if (k < d) xv[u].load(src, (rows + ii[u]) * d + k);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kMeansBatch; ++u)  // the next batch's member ids
+                    nxt[u] = m0 + kMeansBatch + u < c ? __ldg(ord + m0 + kMeansBatch + u) : -1;
+#pragma unroll
+                for (int u = 0; u < kMeansBatch; ++u) {
+                    if (ii[u] < 0) continue;
+                    const double wu = (double)w[u];
+                    if (wrow) wsum = __dadd_rn(wsum, wu);
+                    if (k < d)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const double x = xv[u].get(e);
+                            acc[e] = __dadd_rn(acc[e], wrow ? __dmul_rn(x, wu) : x);
+                        }
                 }
             }
-        }
-        const double den = km.wts ? wsum : (double)c;
+            const double den = wrow ? wsum : (double)c;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int k = k0 + lane + 32 * e;
-            if (k < d) cent[k] = __ddiv_rn(acc[e], den);
+            for (int e = 0; e < 4; ++e)
+                if (k + e < d) {
+                    const double v = __ddiv_rn(acc[e], den);
+                    moved |= old[e] != v;
+                    cent[k + e] = v;
+                }
         }
+    }
+    if (track && !km.state[p * 4 + ST_REPAIRED]) {
+        moved = __any_sync(0xffffffffu, moved);
+        if (lane == 0 && !moved) km.dirty[km.c_off[p] + j] = 0;
+    }
+}
+
+// generic-d fallback (d % 4 != 0): one lane per coordinate, same summation order
+__global__ void __launch_bounds__(kMeansWarps * 32) km_means_generic_kernel(mpa_km km, int force) {
+    const int p = blockIdx.y;
+    if (!force && !km.state[p * 4 + ST_DOMEANS]) return;
+    const int K = km.prob_k[p], d = km.d;
+    const int j = blockIdx.x * kMeansWarps + (threadIdx.x >> 5);
+    if (j >= K) return;
+    const bool track = !force && km.dirty;
+    if (track && !km.dirty[km.c_off[p] + j]) return;
+    const int lane = threadIdx.x & 31;
+    const int l = km.prob_l[p], start = km.prob_start[p];
+    const int c = km.count[km.c_off[p] + j];
+    double* cent = km.cent + (size_t)(km.c_off[p] + j) * d;
+    const int* ord = km.order + km.pt_off[p] + km.cstart[km.c_off[p] + j];
+    bool moved = false;
+    if (c == 0) {
+        if (!km.wts)
+            for (int k = lane; k < d; k += 32) {
+                moved |= cent[k] != 0.0;
+                cent[k] = 0.0;
+            }
+    } else {
+        for (int k = lane; k < d; k += 32) {
+            double acc = 0.0, wsum = 0.0;
+            for (int m = 0; m < c; ++m) {
+                const int i = ord[m];
+                const double x = point_elem(km, l, start + i, k);
+                if (km.wts) {
+                    const double w = (double)km.wts[(size_t)l * km.rows64_cap + start + i];
+                    wsum = __dadd_rn(wsum, w);
+                    acc = __dadd_rn(acc, __dmul_rn(x, w));
+                } else {
+                    acc = __dadd_rn(acc, x);
+                }
+            }
+            const double v = __ddiv_rn(acc, km.wts ? wsum : (double)c);
+            moved |= cent[k] != v;
+            cent[k] = v;
+        }
+    }
+    if (track && !km.state[p * 4 + ST_REPAIRED]) {
+        moved = __any_sync(0xffffffffu, moved);
+        if (lane == 0 && !moved) km.dirty[km.c_off[p] + j] = 0;
     }
 }
 
@@ -538,62 +712,123 @@ __global__ void km_assign_from_level_kernel(mpa_km km, const int32_t* __restrict
 
 // ---------------------------------------------------------------------------- K6 sequential
 
-// distances of the n_new appended tokens to every starting centroid (direct form, fp64):
-// the tokens are staged once per CTA in smem (exact as fp32: bf16 / fp32 key sources), each
-// thread owns one centroid and eight independent token accumulators
-__global__ void __launch_bounds__(128) km_seq_dist_kernel(mpa_km km, const int32_t* __restrict__ tail, int n_new,
-                                                          double* dist) {
-    extern __shared__ float xs[];  // [n_new][d]
-    const int p = blockIdx.y;
-    const int K = km.prob_k[p], d = km.d;
-    const int l = km.prob_l[p], row0 = km.prob_start[p] + tail[p];
-    for (int e = threadIdx.x; e < n_new * d; e += blockDim.x) {
+// distances of the n_new appended tokens to every starting centroid (direct form, fp64, the
+// arithmetic of np.einsum("kd,kd->k", c - x, c - x)).  CTA = (64 centroids, 32 tokens), both
+// staged in shared memory as fp64 (tokens exact: bf16 / fp32 key sources); thread = one
+// centroid x eight tokens.
+constexpr int kSeqDistThreads = 256, kSeqDistTok = 32, kSeqDistCent = 64;
+__global__ void __launch_bounds__(kSeqDistThreads) km_seq_dist_kernel(mpa_km km, const int32_t* __restrict__ tail,
+                                                                      int n_new, double* dist) {
+    extern __shared__ double seq_sm[];
+    const int p = blockIdx.z;
+    const int K = km.prob_k[p], d = km.d, cp = d + 1;
+    double* xs = seq_sm;                          // [kSeqDistTok][d]
+    double* cs = seq_sm + kSeqDistTok * d;        // [kSeqDistCent][d + 1]
+    const int l = km.prob_l[p], t_lo = blockIdx.y * kSeqDistTok, row0 = km.prob_start[p] + tail[p] + t_lo;
+    const int j_lo = blockIdx.x * kSeqDistCent;
+    const int nt = min(kSeqDistTok, n_new - t_lo), nc = min(kSeqDistCent, K - j_lo);
+    for (int e = threadIdx.x; e < nt * d; e += blockDim.x) {
         const int t = e / d, k = e - t * d;
-        xs[e] = (float)point_elem(km, l, row0 + t, k);
+        xs[e] = point_elem(km, l, row0 + t, k);
+    }
+    const double* cg = km.cent + (size_t)(km.c_off[p] + j_lo) * d;
+    for (int e = threadIdx.x; e < nc * d; e += blockDim.x) {
+        const int j = e / d, k = e - j * d;
+        cs[j * cp + k] = cg[e];
     }
     __syncthreads();
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= K) return;
-    const double* c = km.cent + (size_t)(km.c_off[p] + j) * d;
-    for (int t0 = 0; t0 < n_new; t0 += 8) {
-        double s[8];
+    const int jl = threadIdx.x % kSeqDistCent, t0 = (threadIdx.x / kSeqDistCent) * 8;
+    if (jl >= nc || t0 >= nt) return;
+    const double* c = cs + jl * cp;
+    double s[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) s[u] = 0.0;
-        for (int k = 0; k < d; ++k) {
-            const double ck = __ldg(c + k);
+    for (int u = 0; u < 8; ++u) s[u] = 0.0;
+    for (int k = 0; k < d; ++k) {
+        const double a = c[k];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const double df = __dsub_rn(ck, (double)xs[(t0 + u < n_new ? t0 + u : 0) * d + k]);
-                s[u] = __dadd_rn(s[u], __dmul_rn(df, df));
-            }
+        for (int u = 0; u < 8; ++u) {
+            const double df = __dsub_rn(a, xs[(t0 + u < nt ? t0 + u : t0) * d + k]);
+            s[u] = __dadd_rn(s[u], __dmul_rn(df, df));
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-            if (t0 + u < n_new) dist[((size_t)p * n_new + t0 + u) * km.k_max + j] = s[u];
     }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+        if (t0 + u < nt) dist[((size_t)p * n_new + t_lo + t0 + u) * km.k_max + j_lo + jl] = s[u];
 }
 
-__global__ void __launch_bounds__(1024) km_seq_assign_kernel(mpa_km km, const int32_t* __restrict__ tail, int n_new,
-                                                             double* dist) {
-    __shared__ double s_v[32];
-    __shared__ int s_i[32];
-    __shared__ int s_best;
+// The running-mean pass over the appended tokens (clustering.py:439-444), one CTA per problem.
+// Per token: first-min argmin of its distance row, counts[c] += 1, centroid c += (x - c) / n,
+// then column c of every later token's row is recomputed from the new centroid (direct form,
+// like km_seq_dist_kernel).  Tokens live in shared memory (padded rows: the refresh reads them
+// column-wise), and so do the counts; with NC > 0 every thread owns NC fixed columns and loads
+// the next token's row while the current token is processed (the one column refreshed in the
+// meantime is patched through shared memory).
+constexpr int kSeqThreads = 256;
+template <int NC>
+__global__ void __launch_bounds__(kSeqThreads) km_seq_assign_kernel(mpa_km km, const int32_t* __restrict__ tail,
+                                                                    int n_new, double* dist) {
+    extern __shared__ __align__(16) unsigned char seq_smem[];
+    const int d = km.d, xp = d + 1;
     const int p = blockIdx.x;
-    const int K = km.prob_k[p], d = km.d;
+    const int K = km.prob_k[p];
+    float* xs = reinterpret_cast<float*>(seq_smem);                                           // [n_new][d + 1]
+    double* crow = reinterpret_cast<double*>(seq_smem + (((size_t)n_new * xp * 4 + 15) & ~(size_t)15));  // [d]
+    int* s_cnt = reinterpret_cast<int*>(crow + d);                                            // [K]
+    __shared__ double s_v[kSeqThreads / 32];
+    __shared__ int s_i[kSeqThreads / 32];
+    __shared__ double s_patch;
+    __shared__ int s_patch_j;
     const int l = km.prob_l[p], row0 = km.prob_start[p] + tail[p];
     double* cent = km.cent + (size_t)km.c_off[p] * d;
     int* cnt = km.count + km.c_off[p];
     double* D = dist + (size_t)p * n_new * km.k_max;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < n_new * d; e += kSeqThreads) {
+        const int t = e / d, k = e - t * d;
+        xs[t * xp + k] = (float)point_elem(km, l, row0 + t, k);  // exact: bf16 / fp32 key sources
+    }
+    for (int j = tid; j < K; j += kSeqThreads) s_cnt[j] = cnt[j];
+    if (tid == 0) s_patch_j = -1;
+    double nxt[NC > 0 ? NC : 1];
+    if (NC > 0) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const int j = tid + c * kSeqThreads;
+            nxt[c] = j < K ? D[j] : INFINITY;
+        }
+    }
+    __syncthreads();
     for (int t = 0; t < n_new; ++t) {
         double bv = INFINITY;
         int bi = 0x7fffffff;
-        for (int j = threadIdx.x; j < K; j += blockDim.x) {
-            const double v = D[(size_t)t * km.k_max + j];
-            if (v < bv || (v == bv && j < bi)) {
-                bv = v;
-                bi = j;
+        if (NC > 0) {
+            const int pj = s_patch_j;
+            const double pv = s_patch;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const int j = tid + c * kSeqThreads;
+                const double v = j == pj ? pv : nxt[c];
+                if (v < bv) {  // columns ascend within a thread: strict < keeps the first
+                    bv = v;
+                    bi = j;
+                }
+            }
+            if (t + 1 < n_new)
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const int j = tid + c * kSeqThreads;
+                    nxt[c] = j < K ? D[(size_t)(t + 1) * km.k_max + j] : INFINITY;
+                }
+        } else {
+            for (int j = tid; j < K; j += kSeqThreads) {
+                const double v = D[(size_t)t * km.k_max + j];
+                if (v < bv) {
+                    bv = v;
+                    bi = j;
+                }
             }
         }
+#pragma unroll
         for (int o = 16; o; o >>= 1) {
             const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
             const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
@@ -602,43 +837,49 @@ __global__ void __launch_bounds__(1024) km_seq_assign_kernel(mpa_km km, const in
                 bi = oi;
             }
         }
-        if ((threadIdx.x & 31) == 0) {
-            s_v[threadIdx.x >> 5] = bv;
-            s_i[threadIdx.x >> 5] = bi;
+        if (lane == 0) {
+            s_v[warp] = bv;
+            s_i[warp] = bi;
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double v = s_v[0];
-            int b = s_i[0];
-            for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
-                if (s_v[w] < v || (s_v[w] == v && s_i[w] < b)) {
-                    v = s_v[w];
-                    b = s_i[w];
-                }
-            s_best = b;
-            cnt[b] += 1;
-        }
-        __syncthreads();
-        const int c = s_best;
-        const double n = (double)cnt[c];
-        // centroids[c] += (x - centroids[c]) / counts[c]
-        for (int k = threadIdx.x; k < d; k += blockDim.x) {
-            const double x = point_elem(km, l, row0 + t, k);
-            const double cur = cent[(size_t)c * d + k];
-            cent[(size_t)c * d + k] = __dadd_rn(cur, __ddiv_rn(__dsub_rn(x, cur), n));
-        }
-        __syncthreads();
-        // refresh column c for the remaining tokens
-        for (int u = t + 1 + threadIdx.x; u < n_new; u += blockDim.x) {
-            double s = 0.0;
-            for (int k = 0; k < d; ++k) {
-                const double df = __dsub_rn(cent[(size_t)c * d + k], point_elem(km, l, row0 + u, k));
-                s = __dadd_rn(s, __dmul_rn(df, df));
+        __syncthreads();  // B1
+        // every thread reduces the warp minima itself (no second barrier for a broadcast)
+        bv = s_v[0];
+        bi = s_i[0];
+#pragma unroll
+        for (int w = 1; w < kSeqThreads / 32; ++w)
+            if (s_v[w] < bv || (s_v[w] == bv && s_i[w] < bi)) {
+                bv = s_v[w];
+                bi = s_i[w];
             }
-            D[(size_t)u * km.k_max + c] = s;
+        const int c = bi;
+        const int n = s_cnt[c] + 1;
+        // centroids[c] += (x - centroids[c]) / counts[c]
+        for (int k = tid; k < d; k += kSeqThreads) {
+            const double x = (double)xs[t * xp + k];
+            const double cur = cent[(size_t)c * d + k];
+            const double nv = __dadd_rn(cur, __ddiv_rn(__dsub_rn(x, cur), (double)n));
+            cent[(size_t)c * d + k] = nv;
+            crow[k] = nv;
         }
-        __syncthreads();
+        __syncthreads();  // B2: crow complete, every thread has read s_cnt[c] and s_v
+        if (tid == 0) {
+            s_cnt[c] = n;
+            s_patch_j = c;
+        }
+        // refresh column c for the remaining tokens
+        for (int u = t + 1 + tid; u < n_new; u += kSeqThreads) {
+            double sacc = 0.0;
+            const float* xu = xs + u * xp;
+            for (int k = 0; k < d; ++k) {
+                const double df = __dsub_rn(crow[k], (double)xu[k]);
+                sacc = __dadd_rn(sacc, __dmul_rn(df, df));
+            }
+            D[(size_t)u * km.k_max + c] = sacc;
+            if (u == t + 1) s_patch = sacc;
+        }
+        __syncthreads();  // B3: the refreshed column (global D / s_patch) is visible
     }
+    for (int j = tid; j < K; j += kSeqThreads) cnt[j] = s_cnt[j];
 }
 
 }  // namespace mpa
@@ -650,24 +891,18 @@ namespace {
 using RoundSort = cub::BlockRadixSort<unsigned, kRoundThreads, kSortItems>;
 constexpr size_t kRoundSmem = sizeof(typename RoundSort::TempStorage);
 
-void launch_round(const mpa_km& k, int grouping_only, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(km_round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRoundSmem);
-        attr = true;
-    }
-    km_round_kernel<<<k.n_prob, kRoundThreads, kRoundSmem, st>>>(k, grouping_only);
+void launch_means(const mpa_km& k, int force, cudaStream_t st) {
+    const dim3 grid(ceil_div(k.k_max, kMeansWarps), k.n_prob);
+    if (k.d & 3) km_means_generic_kernel<<<grid, kMeansWarps * 32, 0, st>>>(k, force);
+    else if (k.pts64) km_means_kernel<double><<<grid, kMeansWarps * 32, 0, st>>>(k, force);
+    else if (k.pts_dtype == MPA_BF16) km_means_kernel<__nv_bfloat16><<<grid, kMeansWarps * 32, 0, st>>>(k, force);
+    else km_means_kernel<float><<<grid, kMeansWarps * 32, 0, st>>>(k, force);
 }
 
-// tcgen05 assignment for bf16 point sources with d = 128 when a workspace is supplied
-// (MPA_KM_FP64=1 forces the fp64 CUDA-core kernel for A/B runs)
-bool use_tc(const mpa_km& k) {
-    static int force_fp64 = -1;
-    if (force_fp64 < 0) {
-        const char* e = getenv("MPA_KM_FP64");
-        force_fp64 = (e && e[0] == '1') ? 1 : 0;
-    }
-    return !force_fp64 && k.tc_ws && k.pts && !k.pts64 && k.pts_dtype == MPA_BF16 && k.d == 128 && k.pts_rows > 0;
+int launch_round(const mpa_km& k, int grouping_only, cudaStream_t st) {
+    if (int rc = set_max_smem((const void*)km_round_kernel, (int)kRoundSmem)) return rc;
+    km_round_kernel<<<k.n_prob, kRoundThreads, kRoundSmem, st>>>(k, grouping_only);
+    return 0;
 }
 
 int validate(const mpa_km* km) {
@@ -697,29 +932,59 @@ extern "C" int mpa_km_lloyd(const mpa_km* km, int32_t* rounds_out, void* stream)
     km_p2_kernel<<<dim3(ceil_div(k.n_max, 128), P), 128, 0, st>>>(k);
     km_c2_kernel<<<dim3(ceil_div(k.k_max, 128), P), 128, 0, st>>>(k, 0);
     if (int rc = check_launch("mpa_km_lloyd(init)")) return rc;
-    cudaError_t e;
-    int32_t hflag[2] = {0, 0};
-    int rounds = 0;
-    const bool tc = use_tc(k);
+    // Host-driven rounds with a pipelined readback: round r's (active, rounds) flag is copied to
+    // pinned memory behind its kernels and only waited for after round r + 1 is queued, so the
+    // GPU never idles on the host; a round queued after convergence is a no-op (every kernel
+    // skips inactive problems).
+    constexpr int kRing = 4;
+    thread_local int32_t* ring = nullptr;
+    if (!ring) {
+        const cudaError_t ea = cudaHostAlloc((void**)&ring, kRing * 2 * sizeof(int32_t), cudaHostAllocPortable);
+        MPA_REQUIRE(ea == cudaSuccess, (int)ea, "mpa_km_lloyd: pinned flag ring: %s", cudaGetErrorString(ea));
+    }
+    cudaEvent_t ev[kRing];
+    for (int i = 0; i < kRing; ++i) cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+    auto cleanup = [&]() {
+        for (int i = 0; i < kRing; ++i) cudaEventDestroy(ev[i]);
+    };
+    int rounds = 0, last = -1;
+    const bool tc = mpa_km_tc_applies(k);
+    int rc = 0;
     for (int r = 0; r < k.min_iters + kMaxExtraRounds + 2; ++r) {
         if (tc) {
-            if (int rc = mpa_km_assign_tc(k, st)) return rc;
+            rc = mpa_km_assign_tc(k, st);
         } else {
             km_assign_kernel<<<dim3(ceil_div(k.n_max, kAsgBM), P), kAsgThreads, 0, st>>>(k);
         }
-        launch_round(k, 0, st);
-        km_means_kernel<<<dim3(ceil_div(k.k_max, kMeansWarps), P), kMeansWarps * 32, 0, st>>>(k, 0);
+        if (!rc) rc = launch_round(k, 0, st);
+        if (rc) break;
+        launch_means(k, 0, st);
         km_c2_kernel<<<dim3(ceil_div(k.k_max, 128), P), 128, 0, st>>>(k, 1);
         km_any_active_kernel<<<1, 256, 0, st>>>(k, k.flag);
-        if (int rc = check_launch("mpa_km_lloyd(round)")) return rc;
-        e = cudaMemcpyAsync(hflag, k.flag, sizeof(hflag), cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        MPA_REQUIRE(e == cudaSuccess, (int)e, "mpa_km_lloyd: %s", cudaGetErrorString(e));
-        rounds = hflag[1];
-        if (!hflag[0]) break;
+        if ((rc = check_launch("mpa_km_lloyd(round)"))) break;
+        cudaError_t e = cudaMemcpyAsync(ring + 2 * (r % kRing), k.flag, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[r % kRing], st);
+        if (e == cudaSuccess && r >= 1) e = cudaEventSynchronize(ev[(r - 1) % kRing]);
+        if (e != cudaSuccess) {
+            set_error("mpa_km_lloyd: %s", cudaGetErrorString(e));
+            rc = (int)e;
+            break;
+        }
+        last = r;
+        if (r >= 1 && !ring[2 * ((r - 1) % kRing)]) break;  // converged by round r - 1
     }
+    if (!rc && last >= 0) {
+        const cudaError_t e = cudaEventSynchronize(ev[last % kRing]);
+        if (e != cudaSuccess) {
+            set_error("mpa_km_lloyd: %s", cudaGetErrorString(e));
+            rc = (int)e;
+        }
+        rounds = ring[2 * (last % kRing) + 1];
+    }
+    cleanup();
+    if (rc) return rc;
     // final grouping for compaction (counts / order / cstart of the returned assignment)
-    launch_round(k, 1, st);
+    if (int rc2 = launch_round(k, 1, st)) return rc2;
     if (rounds_out) *rounds_out = rounds;
     return check_launch("mpa_km_lloyd(final)");
 }
@@ -729,8 +994,8 @@ extern "C" int mpa_km_means(const mpa_km* km, void* stream) {
     if (km->n_prob <= 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
     const mpa_km k = *km;
-    launch_round(k, 1, st);
-    km_means_kernel<<<dim3(ceil_div(k.k_max, kMeansWarps), k.n_prob), kMeansWarps * 32, 0, st>>>(k, 1);
+    if (int rc = launch_round(k, 1, st)) return rc;
+    launch_means(k, 1, st);
     return check_launch("mpa_km_means");
 }
 
@@ -781,11 +1046,23 @@ extern "C" int mpa_km_seq_assign(const mpa_km* km, const int32_t* tail_start, in
     MPA_REQUIRE(tail_start && dist, MPA_ERR_ARG, "mpa_km_seq_assign: null argument");
     if (km->n_prob <= 0 || n_new <= 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
-    const size_t smem = sizeof(float) * n_new * km->d;
-    MPA_REQUIRE(smem <= 200 * 1024 && !km->pts64, MPA_ERR_UNSUPPORTED, "mpa_km_seq_assign: %d tokens x d %d", n_new,
-                km->d);
-    cudaFuncSetAttribute(km_seq_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    km_seq_dist_kernel<<<dim3(ceil_div(km->k_max, 128), km->n_prob), 128, smem, st>>>(*km, tail_start, n_new, dist);
-    km_seq_assign_kernel<<<km->n_prob, 1024, 0, st>>>(*km, tail_start, n_new, dist);
+    MPA_REQUIRE(!km->pts64, MPA_ERR_UNSUPPORTED, "mpa_km_seq_assign: fp64 point sources");
+    const size_t smem = sizeof(double) * ((size_t)kSeqDistTok * km->d + (size_t)kSeqDistCent * (km->d + 1));
+    MPA_REQUIRE(smem <= 220 * 1024, MPA_ERR_UNSUPPORTED, "mpa_km_seq_assign: d %d", km->d);
+    if (int rc = set_max_smem((const void*)km_seq_dist_kernel, (int)smem)) return rc;
+    km_seq_dist_kernel<<<dim3(ceil_div(km->k_max, kSeqDistCent), ceil_div(n_new, kSeqDistTok), km->n_prob),
+                         kSeqDistThreads, smem, st>>>(*km, tail_start, n_new, dist);
+    const size_t smem2 = (((size_t)n_new * (km->d + 1) * 4 + 15) & ~(size_t)15) + (size_t)km->d * 8 + (size_t)km->k_max * 4;
+    MPA_REQUIRE(smem2 <= 220 * 1024, MPA_ERR_UNSUPPORTED, "mpa_km_seq_assign: %d tokens x d %d, %d centroids", n_new,
+                km->d, km->k_max);
+    const int nc = ceil_div(km->k_max, kSeqThreads);
+    auto go = [&](auto kern) -> int {
+        if (int rc = set_max_smem((const void*)kern, (int)smem2)) return rc;
+        kern<<<km->n_prob, kSeqThreads, smem2, st>>>(*km, tail_start, n_new, dist);
+        return 0;
+    };
+    int rc = nc <= 1 ? go(km_seq_assign_kernel<1>) : nc == 2 ? go(km_seq_assign_kernel<2>)
+           : nc <= 4 ? go(km_seq_assign_kernel<4>) : go(km_seq_assign_kernel<0>);
+    if (rc) return rc;
     return check_launch("mpa_km_seq_assign");
 }

@@ -16,6 +16,11 @@ namespace mpa {
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
 
+// ---- per-device launch facts (mpa_rope.cu): SM count, and the max-dynamic-smem attribute of a
+// kernel raised once per (device, kernel)
+int device_sms();
+int set_max_smem(const void* fn, int bytes);
+
 #define MPA_REQUIRE(cond, code, ...)        \
     do {                                    \
         if (!(cond)) {                      \

@@ -6,21 +6,24 @@
 // first minimum).
 //
 // Exactness.  Points are the bf16 K_raw cache rows (exact in bf16).  Each fp64 centroid is
-// split into three bf16 terms c = c1 + c2 + c3 + r (|r| <= 2^-24 |c| per element); the three
-// partial products accumulate into one fp32 TMEM accumulator, so acc = p.c + e with
-// |e| <= ~2^-16 (||p||^2 + ||c||^2) (fp32 accumulation over d = 128 exact products + the split
-// residual; the bound used below is 8x looser).  The epilogue computes d_j = c2_j - 2 acc_j in
-// fp32 and keeps, per point, the best (lowest index on ties) and the second-best candidate.
-// If second - best > 2 tau with tau = 2^-13 (||p||^2 + max_j ||c_j||^2), the exact fp64
-// argmin is provably the same unique index; otherwise the point is re-scored by
-// km_recheck_kernel with the exact fp64 formula of km_assign_kernel (sequential fp64 dot,
-// (p2 + c2) - 2 dot, first minimum).  Certified and re-checked points therefore assign exactly
-// like the fp64 kernel.  In practice only a handful of points per 8K-point problem fall
-// inside the band (SURVEY 7.3-2 measured best/second margins < 1e-3 for 2-11 of 8192).
+// split into two bf16 terms c = c1 + c2 + r (|r| <= 2^-16 |c| per element); both partial
+// products accumulate into one fp32 TMEM accumulator (the products are exact in fp32), so
+// acc = p.c + e with |e| <= 2^-17 (||p||^2 + ||c||^2) from the split residual plus
+// <= 2^-16 (..) from fp32 accumulation of 256 products (2^-15 if the adder truncates).  The
+// epilogue computes d_j = c2_j - 2 acc_j in fp32, so |d_j - (exact - ||p||^2)| <= tau with
+// tau = 2^-13 (||p||^2 + max_j ||c_j||^2) -- at least 2.6x the worst case above.
+// Per point it keeps the best column (lowest index on ties) and every column within 2 tau of
+// it.  Only those columns can hold the exact fp64 argmin, so a point with no such column is
+// certified; otherwise km_recheck_cand_kernel re-scores just the best and its (<= 4) rivals
+// with the exact fp64 formula of km_assign_kernel (sequential fp64 dot, (p2 + c2) - 2 dot,
+// first minimum), and a point with more rivals goes to km_recheck_full_kernel (all columns).
+// Certified and re-checked points therefore assign exactly like the fp64 kernel.
 //
-// CTA = one (problem, 128-point tile); warp 4 issues TMA + MMA (one elected thread), warps 0-3
-// drain TMEM (one point per lane).  N tiles of 256 centroids, 6 K-major sub-tiles each
-// (3 terms x 2 x 64 columns), a 4-deep TMA ring, double-buffered 256-column accumulators.
+// Persistent kernel: one CTA per SM walks items of TWO 128-point tiles of one problem; warp 4
+// issues TMA + MMA (one elected thread), warps 0-3 / 5-8 drain TMEM (one point per lane).
+// N tiles of 128 centroids, 4 K-major sub-tiles each (2 terms x 2 x 64 columns), a 4-deep
+// TMA ring, double-buffered accumulators.  Only clusters whose members changed in the last
+// Lloyd round (km.dirty) are re-split: the others' centroids are bit-identical.
 #include <cstdlib>
 
 #include "mpa_common.cuh"
@@ -28,66 +31,94 @@
 
 namespace mpa {
 
-constexpr int kTcM = 128, kTcN = 256, kTcStages = 4, kTcSub = 6;
-constexpr int kTcThreads = 288;  // warp 4 issues; warps 0-3 and 5-8 drain TMEM (two column halves)
+constexpr int kTcM = 128, kTcTerms = 2, kTcSub = 2 * kTcTerms;
+constexpr int kTcThreads = 288;  // warp 4 issues; warps 0-3 and 5-8 drain TMEM (one point tile each)
 constexpr int kTcTailRows = 64;  // box rows of the narrow-tail centroid map
 constexpr int kTcABytes = 2 * kTcM * 128;   // 2 x 64-column chunks of the point tile
-constexpr int kTcBBytes = kTcN * 128;       // one 256-row x 64-column centroid sub-tile
-constexpr int kTcSmem = 1024 + kTcABytes + kTcStages * kTcBBytes;
+constexpr int kTcCand = 4;                  // rival columns kept per point (more -> full re-score)
+constexpr int kRecheckStride = 4 + kTcCand; // (problem, point, n rivals, best, rivals...)
+static_assert(kTcCand == 4, "recheck entries are two int4");
 
 struct TcWs {
-    __nv_bfloat16* terms;  // [3][kpad][d]
+    __nv_bfloat16* terms;  // [kTcTerms][kpad][d]   (a view's column table)
     float* c2f;            // [kpad]
     double* c2max;         // [n_prob]
-    int32_t* recheck;      // [sum n][2] (problem, point)
-    int32_t* n_recheck;    // [1]
+    int32_t* recheck;      // [sum n][kRecheckStride]
+    int32_t* full;         // [sum n][2] (problem, point)
+    int32_t* counters;     // [0] rechecks, [1] full re-scores
+    float* ub;             // [points of the view] upper bound of exact(assigned) - ||p||^2
+    int32_t* dl;           // [sum k] per problem: ids of the clusters that changed last round
+    const int32_t* kfull;  // [n_prob] centroids per problem (a view may see fewer columns)
     int kpad;
 };
 
-__host__ __device__ inline size_t tc_ws_layout(int n_prob, int sum_k, int sum_n, int d, int* kpad_out,
-                                              size_t* off) {
-    const int kpad = (sum_k + 255) / 256 * 256 + 256;
+// Workspace of one batch: the column tables, the recheck lists, the per-point bound, the
+// incremental plan and the gathered-point view (see mpa_km_assign_tc).
+struct TcLayout {
+    int kpad, gcap;
+    size_t off[16];
+    size_t total;
+};
+enum {
+    kWsTerms, kWsC2f, kWsC2max, kWsRecheck, kWsFull, kWsCounters, kWsUb, kWsDTerms, kWsDC2f, kWsDl, kWsPlan,
+    kWsGIdx, kWsGPts, kWsGP2, kWsGAsg, kWsGUb
+};
+enum { kPlanV1n, kPlanV2n, kPlanV2k, kPlanGStart, kPlanGn, kPlanZero, kPlanRows };
+
+__host__ __device__ inline TcLayout tc_ws_layout(int n_prob, int sum_k, int sum_n, int d) {
+    TcLayout L;
+    L.kpad = (sum_k + 255) / 256 * 256 + 256;
+    L.gcap = sum_n / 2 + n_prob + 1;  // problem p gathers <= n_p / 2 points at floor(pt_off / 2) + p
+    const size_t sz[16] = {(size_t)kTcTerms * L.kpad * d * 2, (size_t)L.kpad * 4, (size_t)n_prob * 8,
+                           (size_t)sum_n * kRecheckStride * 4, (size_t)sum_n * 8, 16, (size_t)sum_n * 4,
+                           (size_t)kTcTerms * L.kpad * d * 2, (size_t)L.kpad * 4, (size_t)sum_k * 4,
+                           (size_t)n_prob * kPlanRows * 4, (size_t)L.gcap * 4, (size_t)L.gcap * d * 2,
+                           (size_t)L.gcap * 8, (size_t)L.gcap * 4, (size_t)L.gcap * 4};
     size_t o = 0;
-    off[0] = o;
-    o += (size_t)3 * kpad * d * 2;
-    o = (o + 255) & ~(size_t)255;
-    off[1] = o;
-    o += (size_t)kpad * 4;
-    o = (o + 255) & ~(size_t)255;
-    off[2] = o;
-    o += (size_t)n_prob * 8;
-    o = (o + 255) & ~(size_t)255;
-    off[3] = o;
-    o += (size_t)sum_n * 8;
-    off[4] = o;
-    o += 256;
-    if (kpad_out) *kpad_out = kpad;
-    return o;
+    for (int i = 0; i < 16; ++i) {
+        L.off[i] = o;
+        o = (o + sz[i] + 255) & ~(size_t)255;
+    }
+    L.total = o;
+    return L;
 }
 
-// fp64 centroids -> three bf16 terms, fp32 norms; per-problem max norm; recheck counter reset
+// fp64 centroid -> two bf16 terms and the fp32 norm
+__device__ __forceinline__ void split_terms(const mpa_km& km, int c, int k, __nv_bfloat16* terms, float* c2f, int kpad,
+                                            int row) {
+    const double v = km.cent[(size_t)c * km.d + k];
+    const __nv_bfloat16 t1 = __double2bfloat16(v);
+    terms[((size_t)0 * kpad + row) * km.d + k] = t1;
+    terms[((size_t)1 * kpad + row) * km.d + k] = __double2bfloat16(v - (double)__bfloat162float(t1));
+    if (k == 0) c2f[row] = (float)km.c2[c];
+}
+
+// the full column table, for the clusters that changed in the last round
 __global__ void km_tc_prep_kernel(mpa_km km, TcWs ws) {
     const int p = blockIdx.y;
     if (!km.state[p * 4 + 0]) return;
     const int K = km.prob_k[p], d = km.d, c0 = km.c_off[p];
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < K * d; e += gridDim.x * blockDim.x) {
         const int j = e / d, k = e - j * d;
-        const double c = km.cent[(size_t)(c0 + j) * d + k];
-        const __nv_bfloat16 t1 = __double2bfloat16(c);
-        const double r1 = c - (double)__bfloat162float(t1);
-        const __nv_bfloat16 t2 = __double2bfloat16(r1);
-        const double r2 = r1 - (double)__bfloat162float(t2);
-        const __nv_bfloat16 t3 = __double2bfloat16(r2);
-        ws.terms[((size_t)0 * ws.kpad + c0 + j) * d + k] = t1;
-        ws.terms[((size_t)1 * ws.kpad + c0 + j) * d + k] = t2;
-        ws.terms[((size_t)2 * ws.kpad + c0 + j) * d + k] = t3;
-        if (k == 0) ws.c2f[c0 + j] = (float)km.c2[c0 + j];
+        if (km.dirty && !km.dirty[c0 + j]) continue;
+        split_terms(km, c0 + j, k, ws.terms, ws.c2f, ws.kpad, c0 + j);
     }
 }
 
+// the changed-column table of the incremental problems (rows c_off + t, t < count)
+__global__ void km_tc_prep_changed_kernel(mpa_km km, TcWs ws, const int32_t* __restrict__ v2k) {
+    const int p = blockIdx.y;
+    const int nk = v2k[p], d = km.d, c0 = km.c_off[p];
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nk * d; e += gridDim.x * blockDim.x) {
+        const int t = e / d, k = e - t * d;
+        split_terms(km, c0 + ws.dl[c0 + t], k, ws.terms, ws.c2f, ws.kpad, c0 + t);
+    }
+}
+
+// per-problem max ||c||^2 (the certification band)
 __global__ void km_tc_norms_kernel(mpa_km km, TcWs ws) {
     const int p = blockIdx.x;
-    if (p == 0 && threadIdx.x == 0) *ws.n_recheck = 0;
+    if (!km.state[p * 4 + 0]) return;
     double m = 0.0;
     for (int j = threadIdx.x; j < km.prob_k[p]; j += blockDim.x) m = fmax(m, km.c2[km.c_off[p] + j]);
     __shared__ double red[32];
@@ -101,174 +132,104 @@ __global__ void km_tc_norms_kernel(mpa_km km, TcWs ws) {
     }
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1)
-km_assign_tc_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_constant__ CUtensorMap tm_terms,
-                    const __grid_constant__ CUtensorMap tm_terms_tail, mpa_km km, TcWs ws) {
-    const int p = blockIdx.y, tile = blockIdx.x;
-    if (!km.state[p * 4 + 0]) return;
-    const int n = km.prob_n[p], K = km.prob_k[p];
-    if (tile * kTcM >= n) return;
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-    unsigned char* sa = smem;
-    unsigned char* sb = smem + kTcABytes;
-    __shared__ __align__(8) uint64_t bar_a, bar_full[kTcStages], bar_empty[kTcStages], bar_acc_full[2],
-        bar_acc_empty[2];
-    __shared__ uint32_t tmem_base;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp == 0) tmem_alloc(&tmem_base, 512);
-    if (threadIdx.x == 0) {
-        mbar_init(smem_u32(&bar_a), 1);
-        for (int s = 0; s < kTcStages; ++s) {
-            mbar_init(smem_u32(&bar_full[s]), 1);
-            mbar_init(smem_u32(&bar_empty[s]), 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(smem_u32(&bar_acc_full[b]), 1);
-            mbar_init(smem_u32(&bar_acc_empty[b]), 8);
-        }
-        fence_mbar_init();
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = tmem_base;
-    const int n_nt = (K + kTcN - 1) / kTcN, S = n_nt * kTcSub;
-    const int c_off = km.c_off[p];
-    // the last N tile is only as wide as its centroids (multiple of 16): no MMA or epilogue work on
-    // padding columns, and its centroid rows come in 64-row boxes
-    const int n_last = (K - (n_nt - 1) * kTcN + 15) & ~15;
-    const int tail_boxes = (n_last + kTcTailRows - 1) / kTcTailRows;
-
-    if (warp == 4) {
-        if (lane == 0) {
-            prefetch_tmap(&tm_pts);
-            prefetch_tmap(&tm_terms);
-            const int row0 = km.prob_l[p] * km.tcap + km.prob_start[p] + tile * kTcM;
-            mbar_expect_tx(smem_u32(&bar_a), kTcABytes);
-            tma_load_2d(smem_u32(sa), &tm_pts, 0, row0, smem_u32(&bar_a));
-            tma_load_2d(smem_u32(sa + kTcM * 128), &tm_pts, 64, row0, smem_u32(&bar_a));
-            auto issue_b = [&](int s) {
-                const int nt = s / kTcSub, u = s - nt * kTcSub, t = u >> 1, c = u & 1;
-                const unsigned slot = smem_u32(sb + (s % kTcStages) * kTcBBytes);
-                const unsigned fb = smem_u32(&bar_full[s % kTcStages]);
-                const int row = t * ws.kpad + c_off + nt * kTcN;
-                if (nt + 1 < n_nt) {
-                    mbar_expect_tx(fb, kTcBBytes);
-                    tma_load_2d(slot, &tm_terms, c * 64, row, fb);
-                } else {
-                    mbar_expect_tx(fb, tail_boxes * kTcTailRows * 128);
-                    for (int b = 0; b < tail_boxes; ++b)
-                        tma_load_2d(slot + b * kTcTailRows * 128, &tm_terms_tail, c * 64, row + b * kTcTailRows, fb);
-                }
-            };
-            for (int s = 0; s < kTcStages && s < S; ++s) issue_b(s);
-            mbar_wait(smem_u32(&bar_a), 0);
-            tc_fence_after();
-            for (int nt = 0; nt < n_nt; ++nt) {
-                const int buf = nt & 1;
-                const uint32_t idesc = umma_idesc_bf16_f32(kTcM, nt + 1 < n_nt ? kTcN : n_last);
-                if (nt >= 2) mbar_wait(smem_u32(&bar_acc_empty[buf]), ((nt - 2) >> 1) & 1);
-                tc_fence_after();
-                for (int u = 0; u < kTcSub; ++u) {
-                    const int s = nt * kTcSub + u, c = u & 1;
-                    mbar_wait(smem_u32(&bar_full[s % kTcStages]), (s / kTcStages) & 1);
-                    tc_fence_after();
-                    const unsigned bslot = smem_u32(sb + (s % kTcStages) * kTcBBytes);
-                    const unsigned aslot = smem_u32(sa + c * kTcM * 128);
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        umma_bf16(tmem + buf * kTcN, umma_desc_sw128(aslot + k * 32), umma_desc_sw128(bslot + k * 32),
-                                  idesc, (u | k) ? 1u : 0u);
-                    umma_commit(smem_u32(&bar_empty[s % kTcStages]));
-                    // refill the slot used one step earlier (its MMAs are queued ahead of this step's)
-                    if (s >= 1 && s - 1 + kTcStages < S) {
-                        mbar_wait(smem_u32(&bar_empty[(s - 1) % kTcStages]), ((s - 1) / kTcStages) & 1);
-                        issue_b(s - 1 + kTcStages);
-                    }
-                }
-                umma_commit(smem_u32(&bar_acc_full[buf]));
-            }
-        }
-        __syncwarp();
-    }
-    // epilogue (warps 0-3 and 5-8): this lane's point = TMEM lane (warp % 4) * 32 + lane; the two
-    // warp groups take the two 128-column halves of every N tile, then merge per point
-    __shared__ float s_best[kTcM], s_second[kTcM];
-    __shared__ int s_jbest[kTcM];
-    const int half = warp > 4 ? 1 : 0, quarter = warp & 3;
-    const int pi = quarter * 32 + lane, i = tile * kTcM + pi;
-    float best = INFINITY, second = INFINITY;
-    int jbest = 0x7fffffff;
-    if (warp != 4) {
-        for (int nt = 0; nt < n_nt; ++nt) {
-            const int buf = nt & 1;
-            const int ncol = nt + 1 < n_nt ? kTcN : n_last;
-            mbar_wait(smem_u32(&bar_acc_full[buf]), (nt >> 1) & 1);
-            tc_fence_after();
-#pragma unroll 1
-            for (int c0 = half * (kTcN / 2); c0 < (half + 1) * (kTcN / 2) && c0 < ncol; c0 += 32) {
-                uint32_t v[32];
-                tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + buf * kTcN + c0, v);
-                tmem_ld_wait();
-                const int jb = nt * kTcN + c0;
-#pragma unroll
-                for (int q = 0; q < 32; ++q) {
-                    const int j = jb + q;
-                    if (j < K) {
-                        const float dj = __ldg(ws.c2f + c_off + j) - 2.f * __uint_as_float(v[q]);
-                        if (dj < best) {
-                            second = best;
-                            best = dj;
-                            jbest = j;
-                        } else if (dj < second) {
-                            second = dj;
-                        }
-                    }
-                }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&bar_acc_empty[buf]));
-        }
-        if (half) {
-            s_best[pi] = best;
-            s_second[pi] = second;
-            s_jbest[pi] = jbest;
-        }
-    }
-    __syncthreads();
-    if (warp < 4 && i < n) {
-        // merge with the upper half (its indices are larger within each tile, so ties keep the
-        // first minimum by comparing (value, index))
-        const float b1 = s_best[pi], s1 = s_second[pi];
-        const int j1 = s_jbest[pi];
-        if (b1 < best || (b1 == best && j1 < jbest)) {
-            second = fminf(s1, best);
-            best = b1;
-            jbest = j1;
-        } else {
-            second = fminf(second, b1);
-        }
-        const int g = km.pt_off[p] + i;
-        const double tau = ldexp(km.p2[g] + ws.c2max[p], -13);
-        if ((double)second - (double)best > 2.0 * tau) {
-            km.assign[g] = jbest;
-        } else {
-            const int r = atomicAdd(ws.n_recheck, 1);
-            ws.recheck[2 * r] = p;
-            ws.recheck[2 * r + 1] = i;
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) tmem_dealloc(tmem, 512);
+__global__ void km_tc_reset_kernel(TcWs ws) {
+    if (threadIdx.x < 2) ws.counters[threadIdx.x] = 0;
 }
 
-// ---- persistent variant (default): one CTA per SM walks (problem, 128-point tile) items; the A
-// tile is double-buffered and the centroid-term ring runs on across tiles, so TMEM allocation,
-// barrier set-up and the tile's first loads are paid once per SM instead of once per tile.
-constexpr int kTcpSmemFixed = 1024 + 2 * kTcABytes + kTcStages * kTcBBytes;
+// Incremental plan of one Lloyd round (after the previous round's means).  Only the clusters
+// whose members changed (km.dirty) moved, so a point whose own cluster did not move keeps it
+// unless one of the moved centroids comes within the band (view 2: every point against the
+// moved columns only); a point whose own cluster moved is re-scored against every column
+// (view 3: those points gathered into a compact block).  Round 0, a problem with more than half
+// of its clusters moved, or more than half of its points in moved clusters, is re-scored whole
+// (view 1).  One CTA per problem.
+__global__ void __launch_bounds__(256) km_tc_plan_kernel(mpa_km km, TcWs ws, int32_t* plan, int32_t* gidx) {
+    const int p = blockIdx.x, P = km.n_prob;
+    int* v1n = plan + kPlanV1n * P;
+    int* v2n = plan + kPlanV2n * P;
+    int* v2k = plan + kPlanV2k * P;
+    int* gstart = plan + kPlanGStart * P;
+    int* gn = plan + kPlanGn * P;
+    const int n = km.prob_n[p], K = km.prob_k[p], c0 = km.c_off[p];
+    const int g0 = km.pt_off[p] / 2 + p;
+    __shared__ int s_scan[33];
+    if (threadIdx.x == 0) {
+        plan[kPlanZero * P + p] = 0;
+        gstart[p] = g0;
+    }
+    if (!km.state[p * 4 + 0]) {
+        if (threadIdx.x == 0) v1n[p] = v2n[p] = v2k[p] = gn[p] = 0;
+        return;
+    }
+    int nd = 0, mc = 0;
+    for (int j = threadIdx.x; j < K; j += blockDim.x)
+        if (km.dirty[c0 + j]) {
+            ++nd;
+            mc += km.count[c0 + j];
+        }
+    nd = block_reduce(nd, s_scan, [](int x, int y) { return x + y; });
+    mc = block_reduce(mc, s_scan, [](int x, int y) { return x + y; });
+    const bool whole = km.state[p * 4 + 1] == 0 || nd * 2 > K || mc > n / 2;
+    if (whole) {
+        if (threadIdx.x == 0) {
+            v1n[p] = n;
+            v2n[p] = v2k[p] = gn[p] = 0;
+        }
+        return;
+    }
+    if (threadIdx.x == 0) {
+        v1n[p] = 0;
+        v2k[p] = nd;
+        v2n[p] = nd > 0 ? n : 0;
+        gn[p] = mc;
+    }
+    // changed-column list and the members of the changed clusters (grouped by cluster)
+    int cbase = 0, mbase = 0;
+    for (int j0 = 0; j0 < K; j0 += blockDim.x) {
+        const int j = j0 + threadIdx.x;
+        const bool dj = j < K && km.dirty[c0 + j];
+        const int cnt = dj ? km.count[c0 + j] : 0;
+        int tot_c, tot_m;
+        const int ec = block_exclusive_scan(dj ? 1 : 0, s_scan, &tot_c);
+        const int em = block_exclusive_scan(cnt, s_scan, &tot_m);
+        if (dj) {
+            ws.dl[c0 + cbase + ec] = j;
+            const int* ord = km.order + km.pt_off[p] + km.cstart[c0 + j];
+            int32_t* gi = gidx + g0 + mbase + em;
+            for (int m = 0; m < cnt; ++m) gi[m] = ord[m];
+        }
+        cbase += tot_c;
+        mbase += tot_m;
+    }
+}
+
+// view 3 in: copy the gathered points' rows and norms (one warp per point)
+__global__ void km_tc_gather_kernel(mpa_km km, const int32_t* __restrict__ plan, const int32_t* __restrict__ gidx,
+                                    __nv_bfloat16* gpts, double* gp2) {
+    const int p = blockIdx.y, P = km.n_prob;
+    const int n = plan[kPlanGn * P + p], g0 = plan[kPlanGStart * P + p];
+    const int lane = threadIdx.x & 31, d = km.d;
+    for (int m = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); m < n; m += gridDim.x * (blockDim.x >> 5)) {
+        const int i = gidx[g0 + m];
+        const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(km.pts) +
+                                   ((size_t)km.prob_l[p] * km.tcap + km.prob_start[p] + i) * d;
+        for (int k = lane * 8; k < d; k += 256)
+            *reinterpret_cast<uint4*>(gpts + (size_t)(g0 + m) * d + k) = __ldg(reinterpret_cast<const uint4*>(src + k));
+        if (lane == 0) gp2[g0 + m] = km.p2[km.pt_off[p] + i];
+    }
+}
+
+// view 3 out: the gathered points' assignment and bound back to their problem rows
+__global__ void km_tc_scatter_kernel(mpa_km km, const int32_t* __restrict__ plan, const int32_t* __restrict__ gidx,
+                                     const int32_t* __restrict__ gasg, const float* __restrict__ gub, float* ub) {
+    const int p = blockIdx.y, P = km.n_prob;
+    const int n = plan[kPlanGn * P + p], g0 = plan[kPlanGStart * P + p];
+    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x) {
+        const int g = km.pt_off[p] + gidx[g0 + m];
+        km.assign[g] = gasg[g0 + m];
+        ub[g] = gub[g0 + m];
+    }
+}
 
 struct TcTile {
     int p, m, n, K, c_off, n_nt, n_last, tail_boxes, row0;
@@ -278,238 +239,17 @@ __device__ __forceinline__ void named_bar_sync(int id, int threads) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(threads) : "memory");
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1)
-km_assign_tcp_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_constant__ CUtensorMap tm_terms,
-                     const __grid_constant__ CUtensorMap tm_terms_tail, mpa_km km, TcWs ws) {
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-    unsigned char* sa = smem;                      // [2][kTcABytes]
-    unsigned char* sb = smem + 2 * kTcABytes;      // [kTcStages][kTcBBytes]
-    int* tp = reinterpret_cast<int*>(sb + kTcStages * kTcBBytes);  // [P + 1] tile prefix
-    __shared__ __align__(8) uint64_t bar_a[2], bar_a_empty[2], bar_full[kTcStages], bar_empty[kTcStages],
-        bar_acc_full[2], bar_acc_empty[2];
-    __shared__ uint32_t tmem_base;
-    __shared__ float s_best[kTcM], s_second[kTcM];
-    __shared__ int s_jbest[kTcM];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int P = km.n_prob;
-    {  // tile prefix over the active problems (every CTA computes the same)
-        __shared__ int scan[33];
-        int base = 0;
-        for (int q0 = 0; q0 < P; q0 += blockDim.x) {
-            const int q = q0 + threadIdx.x;
-            const int nt = q < P && km.state[q * 4 + 0] ? (km.prob_n[q] + kTcM - 1) / kTcM : 0;
-            int tot;
-            const int e = block_exclusive_scan(nt, scan, &tot);
-            if (q < P) tp[q] = base + e;
-            base += tot;
-        }
-        if (threadIdx.x == 0) tp[P] = base;
-    }
-    if (warp == 0) tmem_alloc(&tmem_base, 512);
-    if (threadIdx.x == 0) {
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(smem_u32(&bar_a[b]), 1);
-            mbar_init(smem_u32(&bar_a_empty[b]), 1);
-            mbar_init(smem_u32(&bar_acc_full[b]), 1);
-            mbar_init(smem_u32(&bar_acc_empty[b]), 8);
-        }
-        for (int s = 0; s < kTcStages; ++s) {
-            mbar_init(smem_u32(&bar_full[s]), 1);
-            mbar_init(smem_u32(&bar_empty[s]), 1);
-        }
-        fence_mbar_init();
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = tmem_base;
-    const int T = tp[P];
-    const int my_tiles = blockIdx.x < T ? (T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    auto tile_info = [&](int it) {
-        const int t = blockIdx.x + it * gridDim.x;
-        int lo = 0, hi = P - 1;  // last problem with tp[q] <= t
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (tp[mid] <= t) lo = mid;
-            else hi = mid - 1;
-        }
-        TcTile x;
-        x.p = lo;
-        x.m = t - tp[lo];
-        x.n = km.prob_n[lo];
-        x.K = km.prob_k[lo];
-        x.c_off = km.c_off[lo];
-        x.n_nt = (x.K + kTcN - 1) / kTcN;
-        x.n_last = (x.K - (x.n_nt - 1) * kTcN + 15) & ~15;
-        x.tail_boxes = (x.n_last + kTcTailRows - 1) / kTcTailRows;
-        x.row0 = km.prob_l[lo] * km.tcap + km.prob_start[lo] + x.m * kTcM;
-        return x;
-    };
-
-    if (warp == 4) {
-        if (lane == 0 && my_tiles > 0) {
-            prefetch_tmap(&tm_pts);
-            prefetch_tmap(&tm_terms);
-            prefetch_tmap(&tm_terms_tail);
-            auto issue_a = [&](int it, const TcTile& x) {
-                const unsigned b = smem_u32(&bar_a[it & 1]);
-                mbar_expect_tx(b, kTcABytes);
-                tma_load_2d(smem_u32(sa + (it & 1) * kTcABytes), &tm_pts, 0, x.row0, b);
-                tma_load_2d(smem_u32(sa + (it & 1) * kTcABytes + kTcM * 128), &tm_pts, 64, x.row0, b);
-            };
-            // load walker: the centroid sub-tiles of every tile in MMA order, kTcStages ahead
-            int l_it = 0, l_nt = 0, l_u = 0, l_step = 0;
-            TcTile lx = tile_info(0);
-            auto load_next = [&]() {
-                if (l_it >= my_tiles) return;
-                const int t = l_u >> 1, c = l_u & 1, slot_i = l_step % kTcStages;
-                const unsigned slot = smem_u32(sb + slot_i * kTcBBytes);
-                const unsigned fb = smem_u32(&bar_full[slot_i]);
-                const int row = t * ws.kpad + lx.c_off + l_nt * kTcN;
-                if (l_nt + 1 < lx.n_nt) {
-                    mbar_expect_tx(fb, kTcBBytes);
-                    tma_load_2d(slot, &tm_terms, c * 64, row, fb);
-                } else {
-                    mbar_expect_tx(fb, lx.tail_boxes * kTcTailRows * 128);
-                    for (int b = 0; b < lx.tail_boxes; ++b)
-                        tma_load_2d(slot + b * kTcTailRows * 128, &tm_terms_tail, c * 64, row + b * kTcTailRows, fb);
-                }
-                ++l_step;
-                if (++l_u == kTcSub) {
-                    l_u = 0;
-                    if (++l_nt == lx.n_nt) {
-                        l_nt = 0;
-                        if (++l_it < my_tiles) lx = tile_info(l_it);
-                    }
-                }
-            };
-            issue_a(0, lx);
-            for (int s = 0; s < kTcStages; ++s) load_next();
-            int step = 0, gnt = 0;
-            for (int it = 0; it < my_tiles; ++it) {
-                const TcTile x = tile_info(it);
-                mbar_wait(smem_u32(&bar_a[it & 1]), (it >> 1) & 1);
-                tc_fence_after();
-                for (int nt = 0; nt < x.n_nt; ++nt, ++gnt) {
-                    const int buf = gnt & 1;
-                    const uint32_t idesc = umma_idesc_bf16_f32(kTcM, nt + 1 < x.n_nt ? kTcN : x.n_last);
-                    if (gnt >= 2) mbar_wait(smem_u32(&bar_acc_empty[buf]), ((gnt - 2) >> 1) & 1);
-                    tc_fence_after();
-                    for (int u = 0; u < kTcSub; ++u, ++step) {
-                        const int c = u & 1;
-                        mbar_wait(smem_u32(&bar_full[step % kTcStages]), (step / kTcStages) & 1);
-                        tc_fence_after();
-                        const unsigned bslot = smem_u32(sb + (step % kTcStages) * kTcBBytes);
-                        const unsigned aslot = smem_u32(sa + (it & 1) * kTcABytes + c * kTcM * 128);
-#pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            umma_bf16(tmem + buf * kTcN, umma_desc_sw128(aslot + k * 32),
-                                      umma_desc_sw128(bslot + k * 32), idesc, (u | k) ? 1u : 0u);
-                        umma_commit(smem_u32(&bar_empty[step % kTcStages]));
-                        // refill the slot used one step earlier (its MMAs are queued ahead of this step's)
-                        if (step >= 1) {
-                            mbar_wait(smem_u32(&bar_empty[(step - 1) % kTcStages]), ((step - 1) / kTcStages) & 1);
-                            load_next();
-                        }
-                    }
-                    umma_commit(smem_u32(&bar_acc_full[buf]));
-                    if (nt == 0 && it + 1 < my_tiles) {
-                        // next tile's points into the other A buffer once the tile before this one is done
-                        if (it >= 1) mbar_wait(smem_u32(&bar_a_empty[(it + 1) & 1]), ((it - 1) >> 1) & 1);
-                        issue_a(it + 1, tile_info(it + 1));
-                    }
-                }
-                umma_commit(smem_u32(&bar_a_empty[it & 1]));
-            }
-        }
-        __syncwarp();
-    } else {
-        // epilogue: warps 0-3 and 5-8; this lane's point = TMEM lane (warp % 4) * 32 + lane, the two
-        // warp groups take the two 128-column halves of every N tile and merge per point
-        const int half = warp > 4 ? 1 : 0, quarter = warp & 3;
-        const int pi = quarter * 32 + lane;
-        int gnt = 0;
-        for (int it = 0; it < my_tiles; ++it) {
-            const TcTile x = tile_info(it);
-            float best = INFINITY, second = INFINITY;
-            int jbest = 0x7fffffff;
-            for (int nt = 0; nt < x.n_nt; ++nt, ++gnt) {
-                const int buf = gnt & 1;
-                const int ncol = nt + 1 < x.n_nt ? kTcN : x.n_last;
-                mbar_wait(smem_u32(&bar_acc_full[buf]), (gnt >> 1) & 1);
-                tc_fence_after();
-#pragma unroll 1
-                for (int c0 = half * (kTcN / 2); c0 < (half + 1) * (kTcN / 2) && c0 < ncol; c0 += 32) {
-                    uint32_t v[32];
-                    tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + buf * kTcN + c0, v);
-                    tmem_ld_wait();
-                    const int jb = nt * kTcN + c0;
-#pragma unroll
-                    for (int q = 0; q < 32; ++q) {
-                        const int j = jb + q;
-                        if (j < x.K) {
-                            const float dj = __ldg(ws.c2f + x.c_off + j) - 2.f * __uint_as_float(v[q]);
-                            if (dj < best) {
-                                second = best;
-                                best = dj;
-                                jbest = j;
-                            } else if (dj < second) {
-                                second = dj;
-                            }
-                        }
-                    }
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&bar_acc_empty[buf]));
-            }
-            if (half) {
-                s_best[pi] = best;
-                s_second[pi] = second;
-                s_jbest[pi] = jbest;
-            }
-            named_bar_sync(1, 256);
-            const int i = x.m * kTcM + pi;
-            if (!half && i < x.n) {
-                const float b1 = s_best[pi], s1 = s_second[pi];
-                const int j1 = s_jbest[pi];
-                if (b1 < best || (b1 == best && j1 < jbest)) {
-                    second = fminf(s1, best);
-                    best = b1;
-                    jbest = j1;
-                } else {
-                    second = fminf(second, b1);
-                }
-                const int g = km.pt_off[x.p] + i;
-                const double tau = ldexp(km.p2[g] + ws.c2max[x.p], -13);
-                if ((double)second - (double)best > 2.0 * tau) {
-                    km.assign[g] = jbest;
-                } else {
-                    const int r = atomicAdd(ws.n_recheck, 1);
-                    ws.recheck[2 * r] = x.p;
-                    ws.recheck[2 * r + 1] = i;
-                }
-            }
-            named_bar_sync(1, 256);  // s_best is rewritten by the next tile
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) tmem_dealloc(tmem, 512);
-}
-
-// ---- paired variant (default): an item is TWO 128-point tiles of one problem, so every centroid
-// sub-tile brought from L2 feeds both (half the centroid traffic per point); N tiles of 128
-// columns, TMEM = 2 buffers x 2 point tiles x 128 columns.  Warps 0-3 drain point tile 0, warps
-// 5-8 point tile 1, each thread one point over all columns (no cross-warp merge).
+// An item is TWO 128-point tiles of one problem, so every centroid sub-tile brought from L2
+// feeds both; TMEM = 2 buffers x 2 point tiles x 128 columns.  Warps 0-3 drain point tile 0,
+// warps 5-8 point tile 1, each thread one point over all columns (no cross-warp merge).
 constexpr int kTc2N = 128;
 constexpr int kTc2BBytes = kTc2N * 128;  // 128 rows x 64 columns
 constexpr int kTc2Stages = 4;
 constexpr int kTc2SmemFixed = 2 * 2 * kTcABytes + kTc2Stages * kTc2BBytes;  // A double buffer x 2 tiles + ring
 
+template <bool INCR>
 __global__ void __launch_bounds__(kTcThreads, 1)
-km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_constant__ CUtensorMap tm_terms,
+km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts,
                      const __grid_constant__ CUtensorMap tm_terms_tail, mpa_km km, TcWs ws) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     if (smem_u32(smem_raw) & 1023) __trap();
@@ -529,7 +269,7 @@ km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_co
         int base = 0;
         for (int q0 = 0; q0 < P; q0 += blockDim.x) {
             const int q = q0 + threadIdx.x;
-            const int nt = q < P && km.state[q * 4 + 0] ? (km.prob_n[q] + 2 * kTcM - 1) / (2 * kTcM) : 0;
+            const int nt = q < P && km.state[q * 4 + 0] && km.prob_k[q] > 0 ? (km.prob_n[q] + 2 * kTcM - 1) / (2 * kTcM) : 0;
             int tot;
             const int e = block_exclusive_scan(nt, scan, &tot);
             if (q < P) tp[q] = base + e;
@@ -581,7 +321,6 @@ km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_co
     if (warp == 4) {
         if (lane == 0 && my_items > 0) {
             prefetch_tmap(&tm_pts);
-            prefetch_tmap(&tm_terms);
             prefetch_tmap(&tm_terms_tail);
             auto issue_a = [&](int it, const TcTile& x) {
                 const unsigned b = smem_u32(&bar_a[it & 1]);
@@ -666,7 +405,9 @@ km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_co
         auto stage_c2 = [&](int it) {
             const TcTile y = item_info(it);
             float* dst = c2s + (it & 1) * kmax_pad;
-            for (int j = et; j < y.K; j += 256) dst[j] = __ldg(ws.c2f + y.c_off + j);
+            // padded to whole 32-column chunks with +inf: a padded column never wins or rivals
+            const int kp = (y.K + 31) & ~31;
+            for (int j = et; j < kp; j += 256) dst[j] = j < y.K ? __ldg(ws.c2f + y.c_off + j) : INFINITY;
         };
         if (my_items > 0) stage_c2(0);
         named_bar_sync(1, 256);
@@ -675,8 +416,21 @@ km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_co
             const TcTile x = item_info(it);
             if (it + 1 < my_items) stage_c2(it + 1);  // read only after the barrier ending this item
             const float* c2b = c2s + (it & 1) * kmax_pad;
-            float best = INFINITY, second = INFINITY;
-            int jbest = 0x7fffffff;
+            const int i = (x.m + m) * kTcM + pi;
+            const bool live = i < x.n;
+            const int g = km.pt_off[x.p] + (live ? i : 0);
+            const double p2 = km.p2[g];
+            const double tau = ldexp(p2 + ws.c2max[x.p], -13);  // |approx - exact| bound of every column
+            // FULL: the three smallest d_j (indices of two).  INCR: the point keeps its cluster a
+            // unless a changed column comes within the band of a's distance (ub = upper bound of
+            // exact(a) - p2 from the pass that assigned it); such rivals are collected.
+            float b1 = INFINITY, b2 = INFINITY, b3 = INFINITY, thr = -INFINITY;
+            int j1 = 0x7fffffff, j2 = 0x7fffffff, a = 0, nr = 0;
+            int rv[kTcCand] = {0, 0, 0, 0};
+            if (INCR && live) {
+                a = km.assign[g];
+                if (!km.dirty[x.c_off + a]) thr = __double2float_ru((double)ws.ub[g] + tau);
+            }
             for (int nt = 0; nt < x.n_nt; ++nt, ++gnt) {
                 const int buf = gnt & 1;
                 const int ncol = nt + 1 < x.n_nt ? kTc2N : x.n_last;
@@ -699,16 +453,19 @@ km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_co
                     }
 #pragma unroll
                     for (int q = 0; q < 32; ++q) {
-                        const int j = jb + q;
-                        if (j < x.K) {
-                            const float dj = c2v[q] - 2.f * __uint_as_float(v[q]);
-                            if (dj < best) {
-                                second = best;
-                                best = dj;
-                                jbest = j;
-                            } else if (dj < second) {
-                                second = dj;
-                            }
+                        const float dj = fmaf(-2.f, __uint_as_float(v[q]), c2v[q]);
+                        if (!INCR) {  // branch-free insertion into (b1, b2, b3)
+                            const bool p1 = dj < b1, q2 = dj < b2, q3 = dj < b3;
+                            b3 = q2 ? b2 : (q3 ? dj : b3);
+                            b2 = p1 ? b1 : (q2 ? dj : b2);
+                            j2 = p1 ? j1 : (q2 ? jb + q : j2);
+                            b1 = p1 ? dj : b1;
+                            j1 = p1 ? jb + q : j1;
+                        } else if (dj <= thr) {  // rare: a changed column close to the point
+#pragma unroll
+                            for (int s = 0; s < kTcCand; ++s)
+                                if (s == nr) rv[s] = jb + q;
+                            ++nr;
                         }
                     }
                 }
@@ -716,16 +473,34 @@ km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_co
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bar_acc_empty[buf]));
             }
-            const int i = (x.m + m) * kTcM + pi;
-            if (i < x.n) {
-                const int g = km.pt_off[x.p] + i;
-                const double tau = ldexp(km.p2[g] + ws.c2max[x.p], -13);
-                if ((double)second - (double)best > 2.0 * tau) {
-                    km.assign[g] = jbest;
-                } else {
-                    const int r = atomicAdd(ws.n_recheck, 1);
-                    ws.recheck[2 * r] = x.p;
-                    ws.recheck[2 * r + 1] = i;
+            if (live) {
+                int mode = 0;  // 0: decided, 1: exact re-score of (lead, rivals), 2: exact full scan
+                int lead = 0;
+                if (!INCR) {
+                    const double bnd = 2.0 * tau;
+                    if ((double)b2 - (double)b1 > bnd) {
+                        km.assign[g] = j1;
+                        ws.ub[g] = __double2float_ru((double)b1 + tau);
+                    } else if ((double)b3 - (double)b1 > bnd) {
+                        mode = 1, lead = j1, nr = 1, rv[0] = j2;
+                    } else {
+                        mode = 2;
+                    }
+                } else if (nr > 0) {
+                    lead = a;
+                    mode = nr > kTcCand ? 2 : 1;
+#pragma unroll
+                    for (int s = 0; s < kTcCand; ++s) rv[s] = ws.dl[x.c_off + rv[s]];  // changed-column list -> id
+                }
+                if (mode == 2) {
+                    const int r = atomicAdd(&ws.counters[1], 1);
+                    ws.full[2 * r] = x.p;
+                    ws.full[2 * r + 1] = i;
+                } else if (mode == 1) {
+                    const int r = atomicAdd(&ws.counters[0], 1);
+                    int4* e = reinterpret_cast<int4*>(ws.recheck + (size_t)r * kRecheckStride);
+                    e[0] = make_int4(x.p, i, nr, lead);
+                    e[1] = make_int4(rv[0], rv[1], rv[2], rv[3]);
                 }
             }
             named_bar_sync(1, 256);  // this item's c2 buffer is free; the next item's is complete
@@ -736,38 +511,81 @@ km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts, const __grid_co
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
-// exact fp64 re-scoring of the uncertified points: one CTA (8 warps) per point, each thread
-// scoring a strided slice of the problem's centroids with the arithmetic of km_assign_kernel
-// (sequential fp64 dot, (p2 + c2) - 2 dot), then a block-wide first minimum over (dist, index).
-// Spreading a point over 256 threads keeps enough fp64 centroid rows in flight (the rows are
-// cold in L2: the tensor-core pass reads the bf16 terms).
+// exact fp64 distance of point x (bf16 row) to centroid j: the arithmetic of km_assign_kernel
+// (sequential fp64 dot over k, then (p2 + c2) - 2 dot)
+__device__ __forceinline__ double exact_dist(const __nv_bfloat16* __restrict__ x, const double* __restrict__ c,
+                                             double p2, double c2) {
+    double dot = 0.0;
+#pragma unroll 4
+    for (int k8 = 0; k8 < 16; ++k8) {
+        const uint4 xr = __ldg(reinterpret_cast<const uint4*>(x) + k8);
+        const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xr);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const double2 cv = __ldg(reinterpret_cast<const double2*>(c) + k8 * 4 + h);
+            const float2 xf = __bfloat1622float2(xh[h]);
+            dot = fma((double)xf.x, cv.x, dot);
+            dot = fma((double)xf.y, cv.y, dot);
+        }
+    }
+    return __dsub_rn(__dadd_rn(p2, c2), __dmul_rn(2.0, dot));
+}
+
+// exact re-score of the points with rivals inside the band: eight lanes per point, lane 0 the
+// best column and lanes 1..n its rivals, first minimum over (dist, index) within the group
 constexpr int kRecheckThreads = 256;
-__global__ void __launch_bounds__(kRecheckThreads) km_recheck_kernel(mpa_km km, TcWs ws) {
-    const int nr = *ws.n_recheck;
-    __shared__ double x[128];
+__global__ void __launch_bounds__(kRecheckThreads) km_recheck_cand_kernel(mpa_km km, TcWs ws) {
+    const int nr = ws.counters[0];
+    const int sub = threadIdx.x & 7;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 3; r < nr; r += (gridDim.x * blockDim.x) >> 3) {
+        const int4* e = reinterpret_cast<const int4*>(ws.recheck + (size_t)r * kRecheckStride);
+        const int4 h = e[0], rv = e[1];
+        const int p = h.x, i = h.y, n_riv = h.z;
+        const int j = sub == 0 ? h.w : sub == 1 ? rv.x : sub == 2 ? rv.y : sub == 3 ? rv.z : rv.w;
+        const int g = km.pt_off[p] + i;
+        double best = INFINITY;
+        int jb = 0x7fffffff;
+        if (sub <= n_riv) {
+            const __nv_bfloat16* x =
+                reinterpret_cast<const __nv_bfloat16*>(km.pts) + ((size_t)km.prob_l[p] * km.tcap + km.prob_start[p] + i) * km.d;
+            const int cj = km.c_off[p] + j;
+            best = exact_dist(x, km.cent + (size_t)cj * km.d, km.p2[g], km.c2[cj]);
+            jb = j;
+        }
+#pragma unroll
+        for (int o = 4; o; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, jb, o);
+            if (ob < best || (ob == best && oj < jb)) {
+                best = ob;
+                jb = oj;
+            }
+        }
+        if (sub == 0) {
+            km.assign[g] = jb;
+            ws.ub[g] = __double2float_ru(best - km.p2[g]);
+        }
+    }
+}
+
+// exact re-score over every column (points with more than kTcCand rivals): one CTA per point,
+// each thread a strided slice of the centroids, then a block-wide first minimum
+__global__ void __launch_bounds__(kRecheckThreads) km_recheck_full_kernel(mpa_km km, TcWs ws) {
+    const int nr = ws.counters[1];
     __shared__ double s_best[kRecheckThreads / 32];
     __shared__ int s_j[kRecheckThreads / 32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int r = blockIdx.x; r < nr; r += gridDim.x) {
-        const int p = ws.recheck[2 * r], i = ws.recheck[2 * r + 1];
-        const int K = km.prob_k[p], d = km.d, l = km.prob_l[p], row = km.prob_start[p] + i;
-        const int g = km.pt_off[p] + i;
+        const int p = ws.full[2 * r], i = ws.full[2 * r + 1];
+        const int K = ws.kfull[p], g = km.pt_off[p] + i;
         const double p2 = km.p2[g];
-        const __nv_bfloat16* pt = reinterpret_cast<const __nv_bfloat16*>(km.pts) + ((size_t)l * km.tcap + row) * d;
-        for (int k = threadIdx.x; k < 128; k += blockDim.x) x[k] = (double)__bfloat162float(pt[k]);
-        __syncthreads();
+        const __nv_bfloat16* x =
+            reinterpret_cast<const __nv_bfloat16*>(km.pts) + ((size_t)km.prob_l[p] * km.tcap + km.prob_start[p] + i) * km.d;
         double best = INFINITY;
         int jb = 0x7fffffff;
         for (int j = threadIdx.x; j < K; j += blockDim.x) {
-            const double2* c = reinterpret_cast<const double2*>(km.cent + (size_t)(km.c_off[p] + j) * d);
-            double dot = 0.0;  // sequential over k, like km_assign_kernel
-#pragma unroll 8
-            for (int k2 = 0; k2 < 64; ++k2) {
-                const double2 cv = __ldg(c + k2);
-                dot = fma(x[2 * k2], cv.x, dot);
-                dot = fma(x[2 * k2 + 1], cv.y, dot);
-            }
-            const double dist = __dsub_rn(__dadd_rn(p2, km.c2[km.c_off[p] + j]), __dmul_rn(2.0, dot));
+            const int cj = km.c_off[p] + j;
+            const double dist = exact_dist(x, km.cent + (size_t)cj * km.d, p2, km.c2[cj]);
             if (dist < best || (dist == best && j < jb)) {
                 best = dist;
                 jb = j;
@@ -794,8 +612,9 @@ __global__ void __launch_bounds__(kRecheckThreads) km_recheck_kernel(mpa_km km, 
                     jb = s_j[w];
                 }
             km.assign[g] = jb;
+            ws.ub[g] = __double2float_ru(best - p2);
         }
-        __syncthreads();  // x / s_best reused by the next point
+        __syncthreads();  // s_best reused by the next point
     }
 }
 
@@ -835,68 +654,80 @@ int encode_rows_map(CUtensorMap* out, const void* base, long long rows, int d, i
 // sum_n points, dimension d)
 extern "C" size_t mpa_km_tc_workspace(int n_prob, int sum_k, int sum_n, int d) {
     if (n_prob <= 0 || sum_k <= 0 || sum_n <= 0 || d <= 0) return 0;
-    size_t off[5];
-    return tc_ws_layout(n_prob, sum_k, sum_n, d, nullptr, off);
+    return tc_ws_layout(n_prob, sum_k, sum_n, d).total;
 }
 
-// one assignment pass on the tensor cores (used by mpa_km_lloyd when km->tc_ws is given)
+namespace {
+size_t tc2_smem(int n_prob, int k_max) {
+    return kTc2SmemFixed + (size_t)((n_prob + 1 + 3) & ~3) * 4 + 2 * (size_t)((k_max + 31) & ~31) * 4;
+}
+constexpr size_t kTcSmemCap = 227 * 1024 - 2048;  // leaves room for the kernel's static shared memory
+}  // namespace
+
+// the tensor-core assignment applies to bf16 points with d = 128 whose per-item state fits in smem
+bool mpa_km_tc_applies(const mpa_km& k) {
+    return k.tc_ws && k.dirty && k.pts && !k.pts64 && k.pts_dtype == MPA_BF16 && k.d == 128 && k.pts_rows > 0 &&
+           tc2_smem(k.n_prob, k.k_max) <= kTcSmemCap;
+}
+
+// One assignment pass of a Lloyd round on the tensor cores (mpa_km_lloyd, when
+// mpa_km_tc_applies): plan, column tables, then the three views of km_tc_plan_kernel, each a
+// tcgen05 pass plus the exact re-scores of its uncertified points.
 int mpa_km_assign_tc(const mpa_km& k, cudaStream_t st) {
-    size_t off[5];
-    int kpad = 0;
-    const size_t need = tc_ws_layout(k.n_prob, k.sum_k, k.sum_n, k.d, &kpad, off);
-    MPA_REQUIRE(k.tc_ws && (size_t)k.tc_ws_bytes >= need, MPA_ERR_ARG, "mpa_km: tensor-core workspace %lld < %zu",
-                (long long)k.tc_ws_bytes, need);
+    const TcLayout L = tc_ws_layout(k.n_prob, k.sum_k, k.sum_n, k.d);
+    MPA_REQUIRE(k.tc_ws && (size_t)k.tc_ws_bytes >= L.total, MPA_ERR_ARG, "mpa_km: tensor-core workspace %lld < %zu",
+                (long long)k.tc_ws_bytes, L.total);
+    const size_t smem = tc2_smem(k.n_prob, k.k_max);
+    MPA_REQUIRE(smem <= kTcSmemCap, MPA_ERR_UNSUPPORTED, "mpa_km: tensor-core assignment needs %zu B smem", smem);
     char* base = (char*)k.tc_ws;
-    TcWs ws{(__nv_bfloat16*)(base + off[0]), (float*)(base + off[1]), (double*)(base + off[2]),
-            (int32_t*)(base + off[3]), (int32_t*)(base + off[4]), kpad};
-    CUtensorMap tp, tt, tt_tail;
+    auto at = [&](int i) { return (void*)(base + L.off[i]); };
+    const int P = k.n_prob;
+    int32_t* plan = (int32_t*)at(kWsPlan);
+    int32_t* gidx = (int32_t*)at(kWsGIdx);
+    TcWs ws{(__nv_bfloat16*)at(kWsTerms), (float*)at(kWsC2f), (double*)at(kWsC2max), (int32_t*)at(kWsRecheck),
+            (int32_t*)at(kWsFull), (int32_t*)at(kWsCounters), (float*)at(kWsUb), (int32_t*)at(kWsDl), k.prob_k,
+            L.kpad};
+    TcWs ws2 = ws;  // view 2: the changed-column table
+    ws2.terms = (__nv_bfloat16*)at(kWsDTerms);
+    ws2.c2f = (float*)at(kWsDC2f);
+    TcWs ws3 = ws;  // view 3: bounds of the gathered points
+    ws3.ub = (float*)at(kWsGUb);
+    mpa_km v1 = k, v2 = k, v3 = k;
+    v1.prob_n = plan + kPlanV1n * P;
+    v2.prob_n = plan + kPlanV2n * P;
+    v2.prob_k = plan + kPlanV2k * P;
+    v3.pts = at(kWsGPts);
+    v3.pts_rows = L.gcap;
+    v3.tcap = 0;
+    v3.prob_l = plan + kPlanZero * P;
+    v3.prob_start = v3.pt_off = plan + kPlanGStart * P;
+    v3.prob_n = plan + kPlanGn * P;
+    v3.assign = (int32_t*)at(kWsGAsg);
+    v3.p2 = (double*)at(kWsGP2);
+    CUtensorMap tp, tp3, tt, tt2;
     if (int rc = encode_rows_map(&tp, k.pts, (long long)k.pts_rows, k.d, kTcM)) return rc;
-    if (int rc = encode_rows_map(&tt, ws.terms, 3ll * kpad, k.d, kTcN)) return rc;
-    if (int rc = encode_rows_map(&tt_tail, ws.terms, 3ll * kpad, k.d, kTcTailRows)) return rc;
-    km_tc_norms_kernel<<<k.n_prob, 256, 0, st>>>(k, ws);
-    km_tc_prep_kernel<<<dim3(ceil_div(k.k_max * k.d, 256 * 8), k.n_prob), 256, 0, st>>>(k, ws);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(km_assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
-        attr = true;
-    }
-    static int oneshot = -1;  // MPA_KM_TC_ONESHOT=1: one CTA per tile (previous kernel)
-    if (oneshot < 0) {
-        const char* e = getenv("MPA_KM_TC_ONESHOT");
-        oneshot = (e && e[0] == '1') ? 1 : 0;
-    }
-    const size_t psmem = kTcpSmemFixed + (size_t)(k.n_prob + 1) * 4;
-    static int paired = -1;  // MPA_KM_TC_PAIRED=0: single-tile persistent kernel
-    if (paired < 0) {
-        const char* e = getenv("MPA_KM_TC_PAIRED");
-        paired = (e && e[0] == '0') ? 0 : 1;
-    }
-    const size_t psmem2 = kTc2SmemFixed + (size_t)((k.n_prob + 1 + 3) & ~3) * 4 + 2 * (size_t)((k.k_max + 31) & ~31) * 4;
-    constexpr size_t kSmemCap = 227 * 1024 - 2048;  // leaves room for the kernels' static shared memory
-    if (!oneshot && paired && psmem2 <= kSmemCap) {
-        static int sms2 = 0;
-        if (!sms2) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev);
-            if (sms2 <= 0) sms2 = 148;
-        }
-        cudaFuncSetAttribute(km_assign_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem2);
-        km_assign_tc2_kernel<<<sms2, kTcThreads, psmem2, st>>>(tp, tt, tt_tail, k, ws);
-    } else if (!oneshot && psmem <= kSmemCap) {
-        static int sms = 0;
-        if (!sms) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            if (sms <= 0) sms = 148;
-        }
-        cudaFuncSetAttribute(km_assign_tcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-        km_assign_tcp_kernel<<<sms, kTcThreads, psmem, st>>>(tp, tt, tt_tail, k, ws);
-    } else {
-        km_assign_tc_kernel<<<dim3(ceil_div(k.n_max, kTcM), k.n_prob), kTcThreads, kTcSmem, st>>>(tp, tt, tt_tail, k,
-                                                                                                  ws);
-    }
-    km_recheck_kernel<<<4 * 148, kRecheckThreads, 0, st>>>(k, ws);
+    if (int rc = encode_rows_map(&tp3, v3.pts, (long long)L.gcap, k.d, kTcM)) return rc;
+    if (int rc = encode_rows_map(&tt, ws.terms, (long long)kTcTerms * L.kpad, k.d, kTcTailRows)) return rc;
+    if (int rc = encode_rows_map(&tt2, ws2.terms, (long long)kTcTerms * L.kpad, k.d, kTcTailRows)) return rc;
+    if (int rc = set_max_smem((const void*)km_assign_tc2_kernel<false>, (int)smem)) return rc;
+    if (int rc = set_max_smem((const void*)km_assign_tc2_kernel<true>, (int)smem)) return rc;
+    const int sms = device_sms();
+    const dim3 pgrid(ceil_div(k.k_max * k.d, 256 * 8), P);
+    km_tc_norms_kernel<<<P, 256, 0, st>>>(k, ws);
+    km_tc_plan_kernel<<<P, 256, 0, st>>>(k, ws, plan, gidx);
+    km_tc_prep_kernel<<<pgrid, 256, 0, st>>>(k, ws);
+    km_tc_prep_changed_kernel<<<pgrid, 256, 0, st>>>(k, ws2, plan + kPlanV2k * P);
+    km_tc_gather_kernel<<<dim3(32, P), 256, 0, st>>>(k, plan, gidx, (__nv_bfloat16*)v3.pts, v3.p2);
+    auto pass = [&](const CUtensorMap& pm, const CUtensorMap& tm, const mpa_km& v, const TcWs& w, bool incr) {
+        km_tc_reset_kernel<<<1, 32, 0, st>>>(w);
+        if (incr) km_assign_tc2_kernel<true><<<sms, kTcThreads, smem, st>>>(pm, tm, v, w);
+        else km_assign_tc2_kernel<false><<<sms, kTcThreads, smem, st>>>(pm, tm, v, w);
+        km_recheck_cand_kernel<<<2 * sms, kRecheckThreads, 0, st>>>(v, w);
+        km_recheck_full_kernel<<<2 * sms, kRecheckThreads, 0, st>>>(v, w);
+    };
+    pass(tp, tt, v1, ws, false);
+    pass(tp, tt2, v2, ws2, true);
+    pass(tp3, tt, v3, ws3, false);
+    km_tc_scatter_kernel<<<dim3(4, P), 256, 0, st>>>(k, plan, gidx, v3.assign, ws3.ub, ws.ub);
     return check_launch("mpa_km_assign(tcgen05)");
 }

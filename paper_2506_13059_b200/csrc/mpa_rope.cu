@@ -10,6 +10,8 @@
 // fp64 (pos * inv_freq with inv_freq computed by numpy on the host, identical bits to
 // the reference), sincos in fp64, result rounded once to the cache dtype.
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -32,6 +34,47 @@ int check_launch(const char* what) {
     if (e != cudaSuccess) {
         set_error("%s: %s", what, cudaGetErrorString(e));
         return (int)e;
+    }
+    return 0;
+}
+
+// per-device launch facts: a process may drive several GPUs, so nothing is cached per process
+namespace {
+constexpr int kMaxDevices = 64;
+std::mutex g_dev_mu;
+int g_sms[kMaxDevices];
+std::map<std::pair<int, const void*>, int> g_smem_set;
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+}  // namespace
+
+int device_sms() {
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (dev < 0 || dev >= kMaxDevices) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n > 0 ? n : 1;
+    }
+    if (!g_sms[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        g_sms[dev] = n > 0 ? n : 1;
+    }
+    return g_sms[dev];
+}
+
+int set_max_smem(const void* fn, int bytes) {
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    int& have = g_smem_set[{dev, fn}];
+    if (bytes > have) {
+        const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        MPA_REQUIRE(e == cudaSuccess, (int)e, "cudaFuncSetAttribute(smem %d): %s", bytes, cudaGetErrorString(e));
+        have = bytes;
     }
     return 0;
 }

@@ -50,18 +50,11 @@ def rows(rep: str):
             except ValueError:
                 continue
             unit = u.get(m, "")
-            if k in SCALE:
-                if unit.lower().startswith("k"):
-                    v *= 1e3
-                elif unit.lower().startswith("m"):
-                    v *= 1e6 if k != "us" else 1e6
-                elif unit.lower().startswith("g"):
-                    v *= 1e9
-                if k == "us":
-                    v = v * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(unit, 1e-3) / \
-                        (1e6 if unit.lower().startswith("m") and unit != "msecond" else 1.0)
-                else:
-                    v *= SCALE[k][1]
+            if k == "us":
+                v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+                      "second": 1e6, "s": 1e6}.get(unit, 1.0)
+            elif k in SCALE:  # bytes -> MB
+                v *= {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1.0) * 1e-6
             rec[k] = round(v, 3)
         yield rec
 
