@@ -131,24 +131,6 @@ int mpa_select(const double* logits, int group, const int32_t* cand, const int32
 int mpa_hier_candidates(const mpa_level* coarse, const uint8_t* cflag, int n_ledgers,
                         int32_t* cand, int32_t* n_cand, int cand_cap, void* stream);
 
-/* Work lists for the fused kernel (attention.py:469-496):
- *   tok[l, :]  = sinks [0, min(sink_end, cache_len)) ++ buffer [buffer_start, cache_len)
- *                ++ members of selected fine candidates;  n_tok[l]
- *   rej[l, :]  = rejected centroids as value-row codes (>= 0 fine row, < 0: coarse row -1-code)
- *                with rej_w[l, j, g] = logit + ln(size) (fp32, row stride GP = G <= 4 ? 4 : 8
- *                floats so a 16-row tile of logits is one aligned bulk copy);  n_rej[l]
- * Fine candidates: (cand, n_cand, flag, logits); coarse rejected (hier only, may be NULL):
- * (clogits, cflag) over the coarse level.  replacement == 0 drops every centroid term
- * ("flat-no-replacement", attention.py:441).  stats is [4, L]: rows n_tok, n_rej, sel_tokens,
- * n_selected_clusters (rows 0 and 1 feed mpa_sparse_decode directly).  sink_end / buffer_start / cache_len are per sequence [n_seq]. */
-int mpa_build_worklist(const mpa_level* fine, const mpa_level* coarse, int group,
-                       const int32_t* cand, const int32_t* n_cand, int cand_cap,
-                       const uint8_t* flag, const double* logits,
-                       const uint8_t* cflag, const double* clogits,
-                       const int32_t* sink_end, const int32_t* buffer_start, const int32_t* cache_len,
-                       int n_kv_heads, int n_ledgers, int replacement,
-                       int32_t* tok, int tok_cap, int32_t* rej, float* rej_w, int rej_cap,
-                       int32_t* stats, void* stream);
 
 /* K1 + K9 + K10 + work lists + the K/V append of a flat serving decode step in ONE launch (bf16
  * cache and centroids, head_dim 128, 3 <= G <= 8): replaces rope.py:37-53 / 66-68 (exact and
@@ -176,8 +158,19 @@ int mpa_decode_step(const float* q, const float* k_new, const float* v_new, cons
                     void* stream);
 
 
-/* K10 + work list fused in one launch per ledger: mpa_select over the fine candidates (extras =
- * coarse clusters with cflag == 0, hierarchy only) followed by mpa_build_worklist.
+/* Work lists for the fused kernel (attention.py:469-496):
+ *   tok[l, :]  = sinks [0, min(sink_end, cache_len)) ++ buffer [buffer_start, cache_len)
+ *                ++ members of selected fine candidates;  n_tok[l]
+ *   rej[l, :]  = rejected centroids as value-row codes (>= 0 fine row, < 0: coarse row -1-code)
+ *                with rej_w[l, j, g] = logit + ln(size) (fp32, row stride GP = G <= 4 ? 4 : 8
+ *                floats so a 16-row tile of logits is one aligned bulk copy);  n_rej[l]
+ * Fine candidates: (cand, n_cand, flag, logits); coarse rejected (hier only, may be NULL):
+ * (clogits, cflag) over the coarse level.  replacement == 0 drops every centroid term
+ * ("flat-no-replacement", attention.py:441).  stats is [4, L]: rows n_tok, n_rej, sel_tokens,
+ * n_selected_clusters (rows 0 and 1 feed mpa_sparse_decode directly).  sink_end / buffer_start / cache_len are per sequence [n_seq].
+ *
+ * K10 + work list fused in one launch per ledger: mpa_select over the fine candidates (extras =
+ * coarse clusters with cflag == 0, hierarchy only) followed by the work lists above.
  * rej == NULL with replacement (flat level only): contiguous-centroid work list -- no rejected
  * list is written; rej_w already holds every candidate's weight (mpa_centroid_logits rej_w) and
  * the selected candidates' rows are set to -inf, so mpa_sparse_decode can stream the fine value

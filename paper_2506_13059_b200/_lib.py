@@ -71,9 +71,6 @@ _SIGS = {
     "mpa_ref_nearest": [_vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp],
     "mpa_ref_seg_stats": [_vp, _vp, _vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp],
     "mpa_hier_candidates": [C.POINTER(MpaLevel), _vp, C.c_int, _vp, _vp, C.c_int, _vp],
-    "mpa_build_worklist": [C.POINTER(MpaLevel), C.POINTER(MpaLevel), C.c_int, _vp, _vp, C.c_int, _vp, _vp,
-                           _vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int, _vp, _vp,
-                           C.c_int, _vp, _vp],
     "mpa_head_norms": [_vp, C.c_int, _vp, C.c_int, C.c_int, _vp, _vp],
     "mpa_merge_norms": [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp],
     "mpa_select_worklist_sharded": [C.POINTER(MpaLevel), C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int,

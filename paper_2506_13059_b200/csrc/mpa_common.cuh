@@ -153,14 +153,6 @@ __host__ __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b -
 // (and every PDL kernel waits at some point, so completion stays transitive along the chain)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
-inline bool pdl_enabled() {  // MPA_PDL=0 turns the attribute off (the waits are then no-ops)
-    static int on = -1;
-    if (on < 0) {
-        const char* e = getenv("MPA_PDL");
-        on = (e && e[0] == '0') ? 0 : 1;
-    }
-    return on == 1;
-}
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
     cudaLaunchConfig_t cfg = {};
@@ -172,7 +164,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

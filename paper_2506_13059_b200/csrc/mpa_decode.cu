@@ -37,6 +37,9 @@
 #include <cstdlib>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "mpa_common.cuh"
 
@@ -404,14 +407,12 @@ template <int G, int D, int NW, int NST>
 __global__ void __launch_bounds__(NW * 32, 2)
 decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                  const __grid_constant__ CUtensorMap tm_fvc, const __grid_constant__ CUtensorMap tm_cvc,
-                 const __grid_constant__ CUtensorMap tm_k16, const __grid_constant__ CUtensorMap tm_v16,
                  const __grid_constant__ CUtensorMap tm_fvc16, int tcap, const __nv_bfloat16* __restrict__ k_rows,
                  const __nv_bfloat16* __restrict__ v_rows,
                  const float* __restrict__ q_rot, const int32_t* __restrict__ tok, const int32_t* __restrict__ n_tok,
                  int tok_cap, const int32_t* __restrict__ rej, const float* __restrict__ rej_w,
                  const int32_t* __restrict__ n_rej, int rej_cap, int fcap, int ccap, int L, float* __restrict__ part,
-                 int32_t* __restrict__ ticket, float* __restrict__ out, float* __restrict__ part_out, int tok_runs,
-                 int tok_lsu) {
+                 int32_t* __restrict__ ticket, float* __restrict__ out, float* __restrict__ part_out, int tok_lsu) {
     dbg_stamp(0);
     using Geo = SkGeom<G, D, NW, NST>;
     constexpr bool PACKED = G <= 4;
@@ -436,8 +437,6 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_v)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_fvc)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_cvc)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_k16)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_v16)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_fvc16)) : "memory");
     }
     pdl_wait();  // work lists, counts and weights come from the selection kernel
@@ -626,18 +625,6 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         if (m.kind == 0) {
             mbar_expect_tx(bar, 2 * Geo::kMatB);
             const int base = m.l * tcap;
-            // a run of consecutive tokens (sinks, buffer, dense decode) is one 16-row box per half
-            bool run = tok_runs != 0;
-#pragma unroll
-            for (int r = 1; r < 16; ++r) run = run && (r >= m.nv || id[r] == id[0] + r);
-            if (run) {
-#pragma unroll
-                for (int h = 0; h < Geo::kHalves; ++h) {
-                    tma_row(kst + h * 2048, &tm_k16, h * 64, base + id[0], bar, policy);
-                    tma_row(vst + h * 2048, &tm_v16, h * 64, base + id[0], bar, policy);
-                }
-                return;
-            }
 #pragma unroll
             for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -1034,26 +1021,12 @@ using namespace mpa;
 
 namespace {
 
-int g_num_sms = 0;
-
-int num_sms() {
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
-    }
-    return g_num_sms;
-}
+int num_sms() { return device_sms(); }
 
 // serving configuration of the stream-K kernel: 4 warps x 3 stages (~104 KB smem, 2 CTAs / SM)
 constexpr int kSkWarps = 4, kSkStages = 3;
 
-int sk_ctas_per_sm() {
-    static int occ = 0;
-    if (!occ) occ = 2;  // fixed by the smem budget (2 x 104 KB of the 228 KB per SM)
-    return occ;
-}
+constexpr int sk_ctas_per_sm() { return 2; }  // fixed by the smem budget (2 x 104 KB of the 228 KB per SM)
 
 // CTA count of the stream-K grid: n_split <= 0 -> one full wave; else n_split CTAs per ledger
 int sk_grid(int L, int n_split) {
@@ -1082,7 +1055,7 @@ int launch_ffma(const mpa_cache* c, const float* q_rot, const int32_t* tok, cons
 #define MPA_FFMA_CASE(T, NDL)                                                                                   \
     {                                                                                                           \
         auto kern = decode_ffma_kernel<T, G, NDL>;                                                              \
-        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (int rc = set_max_smem((const void*)kern, (int)smem)) return rc;                                   \
         kern<<<grid, kFfmaWarps * 32, smem, st>>>((const T*)c->k_rot, (const T*)c->v, c->tcap, d, q_rot, tok,   \
                                                   n_tok, tok_cap, rej, rej_w, n_rej, rej_cap, (const T*)fvc,    \
                                                   fcap, (const T*)cvc, ccap, S, pml, pacc, ticket, out,         \
@@ -1116,6 +1089,8 @@ int bf16_rows_map(CUtensorMap* out, const void* base, long long rows, int d, int
     };
     static Entry cache[32];
     static int next = 0;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
     for (auto& e : cache)
         if (e.base == base && e.rows == rows && e.d == d && e.box_rows == box_rows) {
             *out = e.map;
@@ -1148,26 +1123,19 @@ int bf16_rows_map(CUtensorMap* out, const void* base, long long rows, int d, int
     return 0;
 }
 
-// token tiles that are runs of consecutive rows use 16-row boxes: MPA_SK_TOKRUN=0 never,
-// (default: measured no faster than the gathers), 1 sparse lists only, 2 also the dense decode
-int tok_runs(bool sparse) {
-    static int mode = -1;
-    if (mode < 0) {
-        const char* e = getenv("MPA_SK_TOKRUN");
-        mode = e ? atoi(e) : 0;
-    }
-    return mode == 2 || (mode == 1 && sparse) ? 1 : 0;
-}
-
-// token tiles through the LSU (cp.async) instead of TMA gathers: MPA_SK_TOKLSU=0 never,
-// 1 sparse lists (default), 2 also the dense decode
-int tok_lsu(bool sparse) {
-    static int mode = -1;
-    if (mode < 0) {
-        const char* e = getenv("MPA_SK_TOKLSU");
-        mode = e ? atoi(e) : 1;
-    }
-    return mode == 2 || (mode == 1 && sparse) ? 1 : 0;
+// resident CTAs per SM of a stream-K instantiation at a smem size, memoised per (device, kernel, smem)
+int sk_occupancy(const void* kern, int smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, int>, int> memo;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = memo.find({dev, kern, smem});
+    if (it != memo.end()) return it->second;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSkWarps * 32, smem);
+    memo[{dev, kern, smem}] = occ;
+    return occ;
 }
 
 template <int G, int D>
@@ -1180,41 +1148,28 @@ int launch_sk(const mpa_cache* c, const float* q_rot, const int32_t* tok, const 
     const size_t smem = Geo::smem(L, C);
     MPA_REQUIRE(smem <= 227 * 1024, MPA_ERR_UNSUPPORTED, "mpa_sparse_decode: %d ledgers exceed the smem schedule", L);
     auto kern = decode_sk_kernel<G, D, kSkWarps, kSkStages>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (int rc = set_max_smem((const void*)kern, (int)smem)) return rc;
     if (one_wave) {  // the stream-K grid is one resident wave (2 CTAs / SM unless smem or registers say less)
-        int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSkWarps * 32, smem);
+        const int occ = sk_occupancy((const void*)kern, (int)smem);
         C = std::min(C, std::max(1, occ) * num_sms());
     }
-    CUtensorMap tk, tv, tf, tc, tk16, tv16, tf16;
+    CUtensorMap tk, tv, tf, tc, tf16;
     int rc = bf16_rows_map(&tk, c->k_rot, (long long)L * c->tcap, D);
     if (!rc) rc = bf16_rows_map(&tv, c->v, (long long)L * c->tcap, D);
-    if (!rc) rc = bf16_rows_map(&tk16, c->k_rot, (long long)L * c->tcap, D, 16);
-    if (!rc) rc = bf16_rows_map(&tv16, c->v, (long long)L * c->tcap, D, 16);
     if (!rc) rc = fvc ? bf16_rows_map(&tf, fvc, (long long)L * fcap, D) : (tf = tk, 0);
-    if (!rc) rc = fvc ? bf16_rows_map(&tf16, fvc, (long long)L * fcap, D, 16) : (tf16 = tk16, 0);
+    if (!rc) rc = fvc ? bf16_rows_map(&tf16, fvc, (long long)L * fcap, D, 16) : (tf16 = tk, 0);
     if (!rc) rc = cvc ? bf16_rows_map(&tc, cvc, (long long)L * ccap, D) : (tc = tf, 0);
     if (rc) return rc;
     MPA_REQUIRE(rej || !rej_w || fvc, MPA_ERR_ARG, "mpa_sparse_decode: contiguous-centroid list without fine_vc");
-    launch_pdl(kern, dim3(C), dim3(kSkWarps * 32), smem, st, tk, tv, tf, tc, tk16, tv16, tf16, c->tcap,
+    launch_pdl(kern, dim3(C), dim3(kSkWarps * 32), smem, st, tk, tv, tf, tc, tf16, c->tcap,
                (const __nv_bfloat16*)c->k_rot, (const __nv_bfloat16*)c->v, q_rot, tok, n_tok, tok_cap, rej, rej_w,
-               n_rej, rej_cap, fcap, ccap, L, part, ticket, out, part_out, tok_runs(tok != nullptr),
-               tok_lsu(tok != nullptr));
+               n_rej, rej_cap, fcap, ccap, L, part, ticket, out, part_out,
+               tok != nullptr ? 1 : 0);  // sparse token lists through the LSU, the dense decode through TMA gathers
     return check_launch("mpa_sparse_decode(stream-K mma)");
 }
 
-int g_force_ffma = -1;
-
-bool force_ffma() {
-    if (g_force_ffma < 0) {
-        const char* e = getenv("MPA_FORCE_FFMA");
-        g_force_ffma = (e && e[0] == '1') ? 1 : 0;
-    }
-    return g_force_ffma == 1;
-}
-
 bool mma_path(const mpa_cache* c, int group) {
-    return c->dtype == MPA_BF16 && (c->head_dim == 64 || c->head_dim == 128) && group <= 8 && !force_ffma();
+    return c->dtype == MPA_BF16 && (c->head_dim == 64 || c->head_dim == 128) && group <= 8;
 }
 
 int ffma_splits(int L, int n_split) {

@@ -551,13 +551,6 @@ __device__ void worklist_body(const int l, const int L, const int32_t* __restric
         cflag, clogits, sink_end, buffer_start, cache_len, n_kv_heads, replacement, tok, tok_cap, rej, rej_w,     \
         rej_cap, stats
 
-template <int G>
-__global__ void __launch_bounds__(kListThreads)
-build_worklist_kernel(const int32_t* __restrict__ cand, const int32_t* __restrict__ n_cand, int cand_cap,
-                      const uint8_t* __restrict__ flag, const double* __restrict__ logits, MPA_WORKLIST_PARAMS) {
-    worklist_body<G>(blockIdx.x, gridDim.x, MPA_WORKLIST_ARGS(cand, n_cand, cand_cap, flag, logits));
-}
-
 // K10 + work list in one launch per ledger (the flat path and the hierarchy's fine stage).
 template <int G>
 __global__ void __launch_bounds__(kSelThreads)
@@ -597,18 +590,6 @@ int mpa_launch_select_worklist_v2(const mpa_level* fine, const mpa_level* coarse
                                   int tok_cap, int32_t* rej, float* rej_w, int rej_cap, int32_t* stats, int n_max,
                                   cudaStream_t st);
 
-// MPA_LOOKUP_V1=1 selects the previous (smem-tiled logits, bitonic select) kernels for A/B runs
-static int g_v1 = -1;
-static bool lookup_v1() {
-    if (g_v1 < 0) {
-        const char* e = getenv("MPA_LOOKUP_V1");
-        g_v1 = (e && e[0] == '1') ? 1 : 0;
-    }
-    return g_v1 == 1;
-}
-
-static int g_logits_tiled = -1;
-
 extern "C" int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group, int d, const mpa_level* lv,
                                    const int32_t* cand, const int32_t* n_cand, int cand_cap, double* logits,
                                    double* chunk_stats, double* e_local, int n_max, float* rej_w, int rej_cap,
@@ -625,24 +606,22 @@ extern "C" int mpa_centroid_logits(const double* q_lk, int n_kv_heads, int group
     if (L <= 0) return 0;
     const int cap = cand ? cand_cap : lv->cap;
     cudaStream_t st = (cudaStream_t)stream;
-    if (g_logits_tiled < 0) {
-        const char* e = getenv("MPA_LOGITS_SIMPLE");
-        g_logits_tiled = (e && e[0] == '1') ? 0 : 1;
-    }
-    if (g_logits_tiled && (d == 64 || d == 128) && lv->dtype == MPA_BF16 && !lookup_v1())
+    // bf16 centroids (the serving dtype): TMA / smem-blocked kernels of mpa_select.cu; fp32 / fp64
+    // centroids (parity modes): smem-tiled kernel at d in {64, 128}, the generic kernel otherwise
+    if ((d == 64 || d == 128) && lv->dtype == MPA_BF16)
         return mpa_launch_logits_v2(q_lk, group, d, lv, cand, n_cand, cand_cap, logits, chunk_stats, e_local,
                                     ceil_div(cap, kChunk), n_max > 0 && n_max < cap ? n_max : cap, rej_w, rej_cap,
                                     q_lk ? nullptr : q_raw, q_lk ? nullptr : cs_lk, st);
     MPA_REQUIRE(!rej_w, MPA_ERR_UNSUPPORTED, "mpa_centroid_logits: rej_w needs the bf16 TMA path");
     MPA_REQUIRE(q_lk, MPA_ERR_UNSUPPORTED, "mpa_centroid_logits: the fused lookup rotation needs the bf16 TMA path");
-    if (g_logits_tiled && (d == 64 || d == 128)) {
+    if (d == 64 || d == 128) {
         const int nch = ceil_div(cap, kChunk);
         dim3 grid(nch, L);
 #define MPA_TILED(T, D)                                                                                              \
     {                                                                                                                \
         auto kern = centroid_logits_tiled<T, kG, D>;                                                                 \
         const size_t smem = sizeof(double) * (D * ((kG + 1) & ~1) + 8 * kG) + (size_t)kChunk * (D * sizeof(T) + 16); \
-        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
+        if (int rc = set_max_smem((const void*)kern, (int)smem)) return rc;                                           \
         kern<<<grid, kTiledThreads, smem, st>>>(q_lk, (const T*)lv->kc, lv->cap, lv->count, lv->size, cand, n_cand,  \
                                                 cand_cap, logits, chunk_stats, nch);                                 \
     }
@@ -691,13 +670,14 @@ extern "C" int mpa_select(const double* logits, int group, const int32_t* cand, 
     const size_t smem = (size_t)sort_width(n_max) * 16 + (size_t)n_max * 4;
     const int nch = ceil_div(cand_cap, kChunk);
     cudaStream_t st = (cudaStream_t)stream;
-    if (!lookup_v1() && mpa_select_v2_smem(n_max) <= 200 * 1024)
+    // radix select (one CTA per ledger); the bitonic kernel when its per-candidate smem does not fit
+    if (mpa_select_v2_smem(n_max) <= 200 * 1024)
         return mpa_launch_select_v2(logits, e_local, group, cand, n_cand, cand_cap, lv_size, lv_cap, elogits, esize,
                                     eflag, n_extra, ecap, budget, n_ledgers, flag, sel_tokens, chunk_stats, nch, n_max,
                                     st);
     MPA_DISPATCH_G(group, {
         auto kern = select_kernel<kG>;
-        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (int rc = set_max_smem((const void*)kern, (int)smem)) return rc;
         kern<<<n_ledgers, kSelThreads, smem, st>>>(logits, cand, n_cand, cand_cap, lv_size, lv_cap, elogits, esize,
                                                    eflag, n_extra, ecap, budget, flag, sel_tokens, chunk_stats, nch,
                                                    n_max);
@@ -729,16 +709,16 @@ extern "C" int mpa_select_worklist(const mpa_level* fine, const mpa_level* coars
     const size_t smem = (size_t)sort_width(n_max) * 16 + (size_t)n_max * 4;
     const int nch = ceil_div(cand_cap, kChunk);
     cudaStream_t st = (cudaStream_t)stream;
-    MPA_REQUIRE(rej || (!lookup_v1() && mpa_select_v2_smem(n_max) <= 200 * 1024), MPA_ERR_UNSUPPORTED,
-                "mpa_select_worklist: contiguous-centroid list needs the v2 kernel");
-    if (!lookup_v1() && mpa_select_v2_smem(n_max) <= 200 * 1024)
+    MPA_REQUIRE(rej || mpa_select_v2_smem(n_max) <= 200 * 1024, MPA_ERR_UNSUPPORTED,
+                "mpa_select_worklist: contiguous-centroid list needs the radix kernel");
+    if (mpa_select_v2_smem(n_max) <= 200 * 1024)
         return mpa_launch_select_worklist_v2(fine, coarse, group, logits, e_local, cand, n_cand, cand_cap,
                                              chunk_stats, nch, cflag, clogits, budget, sink_end, buffer_start,
                                              cache_len, n_kv_heads, n_ledgers, replacement, flag, sel_tokens, tok,
                                              tok_cap, rej, rej_w, rej_cap, stats, n_max, st);
     MPA_DISPATCH_G(group, {
         auto kern = select_worklist_kernel<kG>;
-        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (int rc = set_max_smem((const void*)kern, (int)smem)) return rc;
         kern<<<n_ledgers, kSelThreads, smem, st>>>(
             logits, cand, n_cand, cand_cap, budget, flag, sel_tokens, chunk_stats, nch, n_max, fine->size, fine->off,
             fine->idx, fine->cap, fine->idx_cap, coarse ? coarse->size : nullptr, coarse ? coarse->count : nullptr,
@@ -758,27 +738,4 @@ extern "C" int mpa_hier_candidates(const mpa_level* coarse, const uint8_t* cflag
     return check_launch("mpa_hier_candidates");
 }
 
-extern "C" int mpa_build_worklist(const mpa_level* fine, const mpa_level* coarse, int group, const int32_t* cand,
-                                  const int32_t* n_cand, int cand_cap, const uint8_t* flag, const double* logits,
-                                  const uint8_t* cflag, const double* clogits, const int32_t* sink_end,
-                                  const int32_t* buffer_start, const int32_t* cache_len, int n_kv_heads,
-                                  int n_ledgers, int replacement, int32_t* tok, int tok_cap, int32_t* rej,
-                                  float* rej_w, int rej_cap, int32_t* stats, void* stream) {
-    MPA_REQUIRE(fine && flag && logits && sink_end && buffer_start && cache_len && tok && rej && rej_w && stats,
-                MPA_ERR_ARG, "mpa_build_worklist: null argument");
-    MPA_REQUIRE(!cflag || (coarse && clogits), MPA_ERR_ARG, "mpa_build_worklist: coarse flags without level");
-    MPA_REQUIRE(cand ? (n_cand != nullptr) : cand_cap >= fine->cap, MPA_ERR_ARG,
-                "mpa_build_worklist: candidate capacity");
-    MPA_REQUIRE(n_kv_heads >= 1, MPA_ERR_ARG, "mpa_build_worklist: n_kv_heads");
-    if (n_ledgers <= 0) return 0;
-    cudaStream_t st = (cudaStream_t)stream;
-    MPA_DISPATCH_G(group, {
-        build_worklist_kernel<kG><<<n_ledgers, kListThreads, 0, st>>>(
-            cand, n_cand, cand_cap, flag, logits, fine->size, fine->off, fine->idx, fine->cap, fine->idx_cap,
-            coarse ? coarse->size : nullptr, coarse ? coarse->count : nullptr, coarse ? coarse->cap : 0, fine->count,
-            cflag, clogits, sink_end, buffer_start, cache_len, n_kv_heads, replacement, tok, tok_cap, rej, rej_w,
-            rej_cap, stats);
-    });
-    return check_launch("mpa_build_worklist");
-}
 

@@ -260,7 +260,7 @@ __device__ __forceinline__ double bf16hi_to_f64_s896(unsigned fbits) {
 }
 constexpr double kUnscale896 = 0x1p896;
 
-template <int G, bool DMMA>
+template <int G>
 __global__ void __launch_bounds__(kLgThreads)
 logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_constant__ CUtensorMap tm_row,
                   const double* __restrict__ q_lk, int kcap, const int32_t* __restrict__ count,
@@ -363,118 +363,71 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
     pdl_trigger();  // after thread 0's wait (the barrier above completes only after it)
 
     const double sq = sqrt((double)D);
-    if constexpr (G <= 8 && DMMA) {
-        // fp64 tensor cores: mma.sync m8n8k4 (rows = centroids, columns = heads padded to 8, k = 4
-        // dims).  The k index of a lane is its dimension quarter: lane (q = lane & 3, n = lane >> 2)
-        // supplies A[row n][k q] = centroid dim 32 q + kk and B[k q][head n] = q dim 32 q + kk at step
-        // kk, the same permutation for both operands, so each lane streams 32 contiguous dims.
-        const int lane = tid & 31, wq = tid >> 5, q = lane & 3, n = lane >> 2;
-        const double* qb = qs + (n < G ? n : 0) * 4 * QRow + q * QRow;
-        double cf[4][2];
+    const int qt = tid & 3, rg = tid >> 2;
+    const double* qq = qs + qt * QRow;
+    double acc[4][G];
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) cf[mt][0] = cf[mt][1] = 0.0;
+    for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-            uint4 raw[4];
+        for (int g = 0; g < G; ++g) acc[r][g] = 0.0;
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt) {
-                const int row = 32 * wq + 8 * mt + n, ch = (q & 1) * 4 + cc;
-                raw[mt] = *reinterpret_cast<const uint4*>(tile + (q >> 1) * kLgChunk * 128 + row * 128 +
-                                                          ((ch ^ (row & 7)) << 4));
-            }
+    for (int cc = 0; cc < 4; ++cc) {
+        const int c = (cc + 2 * (qt >> 1)) & 3;  // this quarter's 16-byte chunk (8 dims)
+        const int ch = (qt & 1) * 4 + c;         // chunk within the 64-column half
+        uint4 raw[4];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const double b = n < G ? qb[8 * cc + e] : 0.0;
-#pragma unroll
-                for (int mt = 0; mt < 4; ++mt) {
-                    const unsigned wd = (&raw[mt].x)[e >> 1];
-                    const double a = bf16hi_to_f64_s896((e & 1) ? (wd & 0xffff0000u) : (wd << 16));
-                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
-                                 : "+d"(cf[mt][0]), "+d"(cf[mt][1])
-                                 : "d"(a), "d"(b));
-                }
-            }
+        for (int r = 0; r < 4; ++r) {
+            const int row = rg + 32 * r;
+            raw[r] = *reinterpret_cast<const uint4*>(tile + (qt >> 1) * kLgChunk * 128 + row * 128 +
+                                                     ((ch ^ (row & 7)) << 4));
         }
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-            const int r = 32 * wq + 8 * mt + n;
+        for (int e = 0; e < 8; ++e) {
+            double qv[G];
 #pragma unroll
-            for (int i2 = 0; i2 < 2; ++i2) {
-                const int g = 2 * q + i2;
-                if (g < G) {
-                    const double v = (cf[mt][i2] * kUnscale896) / sq;
-                    slg[g * kLgChunk + r] = v;
-                    if (logits && r < nv) logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
-                }
-            }
-        }
-    } else {
-        const int qt = tid & 3, rg = tid >> 2;
-        const double* qq = qs + qt * QRow;
-        double acc[4][G];
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int g = 0; g < G; ++g) acc[r][g] = 0.0;
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-            const int c = (cc + 2 * (qt >> 1)) & 3;  // this quarter's 16-byte chunk (8 dims)
-            const int ch = (qt & 1) * 4 + c;         // chunk within the 64-column half
-            uint4 raw[4];
+            for (int g = 0; g < G; ++g) qv[g] = qq[g * 4 * QRow + c * 8 + e];
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                const int row = rg + 32 * r;
-                raw[r] = *reinterpret_cast<const uint4*>(tile + (qt >> 1) * kLgChunk * 128 + row * 128 +
-                                                         ((ch ^ (row & 7)) << 4));
-            }
+                const unsigned wd = (&raw[r].x)[e >> 1];
+                const double x = bf16hi_to_f64_s896((e & 1) ? (wd & 0xffff0000u) : (wd << 16));
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                double qv[G];
-#pragma unroll
-                for (int g = 0; g < G; ++g) qv[g] = qq[g * 4 * QRow + c * 8 + e];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const unsigned wd = (&raw[r].x)[e >> 1];
-                    const double x = bf16hi_to_f64_s896((e & 1) ? (wd & 0xffff0000u) : (wd << 16));
-#pragma unroll
-                    for (int g = 0; g < G; ++g) acc[r][g] = fma(qv[g], x, acc[r][g]);
-                }
+                for (int g = 0; g < G; ++g) acc[r][g] = fma(qv[g], x, acc[r][g]);
             }
         }
-        // transpose-reduce over the 4 quarter lanes (xor 2 splits rows, xor 1 splits heads)
-        const bool hi2 = qt & 2, hi1 = qt & 1;
-        constexpr int GH = (G + 1) / 2;
-        double a2[2][G];
+    }
+    // transpose-reduce over the 4 quarter lanes (xor 2 splits rows, xor 1 splits heads)
+    const bool hi2 = qt & 2, hi1 = qt & 1;
+    constexpr int GH = (G + 1) / 2;
+    double a2[2][G];
 #pragma unroll
-        for (int rr = 0; rr < 2; ++rr)
+    for (int rr = 0; rr < 2; ++rr)
 #pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const double send = hi2 ? acc[rr][g] : acc[rr + 2][g];
-                const double keep = hi2 ? acc[rr + 2][g] : acc[rr][g];
-                a2[rr][g] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-            }
-        double a1[2][GH];
+        for (int g = 0; g < G; ++g) {
+            const double send = hi2 ? acc[rr][g] : acc[rr + 2][g];
+            const double keep = hi2 ? acc[rr + 2][g] : acc[rr][g];
+            a2[rr][g] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+    double a1[2][GH];
 #pragma unroll
-        for (int rr = 0; rr < 2; ++rr)
+    for (int rr = 0; rr < 2; ++rr)
 #pragma unroll
-            for (int j = 0; j < GH; ++j) {
-                const int ghi = GH + j;
-                const double lo = a2[rr][j], hv = ghi < G ? a2[rr][ghi < G ? ghi : 0] : 0.0;
-                const double send = hi1 ? lo : hv;
-                const double keep = hi1 ? hv : lo;
-                a1[rr][j] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
-            }
+        for (int j = 0; j < GH; ++j) {
+            const int ghi = GH + j;
+            const double lo = a2[rr][j], hv = ghi < G ? a2[rr][ghi < G ? ghi : 0] : 0.0;
+            const double send = hi1 ? lo : hv;
+            const double keep = hi1 ? hv : lo;
+            a1[rr][j] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+        }
 #pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-            const int r = rg + 32 * ((hi2 ? 2 : 0) + rr);
+    for (int rr = 0; rr < 2; ++rr) {
+        const int r = rg + 32 * ((hi2 ? 2 : 0) + rr);
 #pragma unroll
-            for (int j = 0; j < GH; ++j) {
-                const int g = (hi1 ? GH : 0) + j;
-                if (g < G) {
-                    const double v = (a1[rr][j] * kUnscale896) / sq;
-                    slg[g * kLgChunk + r] = v;
-                    if (logits && r < nv) logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
-                }
+        for (int j = 0; j < GH; ++j) {
+            const int g = (hi1 ? GH : 0) + j;
+            if (g < G) {
+                const double v = (a1[rr][j] * kUnscale896) / sq;
+                slg[g * kLgChunk + r] = v;
+                if (logits && r < nv) logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
             }
         }
     }
@@ -523,239 +476,6 @@ logits_tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_cons
     }
 }
 
-// ---- persistent TMA variant (bf16, D = 128, the serving default): 3 CTAs / SM walk the
-// (ledger, chunk) items with a 2-stage ring, so the next item's rows and q slots are in flight
-// (TMA, one mbarrier per stage) while the current item computes; per-item math and outputs are
-// those of logits_tma_kernel.  The chunk's logits for the epilogue reuse the consumed tile.
-template <int G>
-struct LgPGeom {  // [tile 0][tile 1][q slots 0][q slots 1]; 3 CTAs fit in an SM
-    static constexpr int kTileB = 2 * kLgChunk * 128;  // two 64-column halves, 1024-aligned
-    static constexpr int kQB = G * 4 * 34 * 8;         // padded q slots
-    static constexpr size_t smem() { return 1024 + 2 * (size_t)(kTileB + kQB); }
-};
-
-template <int G>
-__global__ void __launch_bounds__(kLgThreads, 3)
-logits_persist_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_constant__ CUtensorMap tm_row,
-                      const double* __restrict__ q_lk, int kcap, const int32_t* __restrict__ count,
-                      const int32_t* __restrict__ lv_size, const int32_t* __restrict__ cand,
-                      const int32_t* __restrict__ n_cand, int cand_cap, double* __restrict__ logits,
-                      double* __restrict__ cstats, double* __restrict__ e_local, int n_chunks,
-                      float* __restrict__ rej_w, int rej_cap, int item_chunks, int L) {
-    using Geo = LgPGeom<G>;
-    constexpr int D = 128, QD = 32, QRow = QD + 2;
-    extern __shared__ __align__(1024) unsigned char sm_raw[];
-    unsigned char* base = sm_raw + ((1024 - (smem_u32(sm_raw) & 1023)) & 1023);
-    __shared__ __align__(8) uint64_t bar[2];
-    __shared__ double red[kLgThreads / 32][G];
-    __shared__ double s_m[G];
-    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-    const int n_items = L * item_chunks;
-    if (tid == 0) {
-        mbar_init(smem_u32(&bar[0]), 1);
-        mbar_init(smem_u32(&bar[1]), 1);
-        fence_mbar_init();
-        prefetch_tmap(&tm_tile);
-        prefetch_tmap(&tm_row);
-    }
-    __syncthreads();
-    auto live = [&](int l) { return cand ? __ldg(n_cand + l) : __ldg(count + l); };
-    // warp 0: loads of item `it` into stage s (nothing for a chunk past the ledger's candidates)
-    auto issue = [&](int it, int s) {
-        const int l = it / item_chunks, i0 = (it - l * item_chunks) * kLgChunk;
-        const int n = live(l);
-        if (i0 >= n) return;
-        const int nv = min(kLgChunk, n - i0);
-        unsigned char* tile = base + s * Geo::kTileB;
-        double* qs = reinterpret_cast<double*>(base + 2 * Geo::kTileB + s * Geo::kQB);
-        const unsigned b = smem_u32(&bar[s]);
-        fence_proxy_async_smem();  // the stage's previous generic reads before the async writes
-        if (lane == 0) {
-            mbar_expect_tx(b, G * 4 * QD * 8 + Geo::kTileB);
-            for (int j = 0; j < G * 4; ++j)
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                        smem_u32(qs + j * QRow)),
-                    "l"(q_lk + ((size_t)l * G + j / 4) * D + (j % 4) * QD), "r"(QD * 8), "r"(b)
-                    : "memory");
-        }
-        if (!cand) {
-            if (lane == 0) {
-                tma_load_2d(smem_u32(tile), &tm_tile, 0, l * kcap + i0, b);
-                tma_load_2d(smem_u32(tile + kLgChunk * 128), &tm_tile, 64, l * kcap + i0, b);
-            }
-        } else {
-            int id[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int rr = 4 * lane + r;
-                id[r] = l * kcap + __ldg(cand + (size_t)l * cand_cap + i0 + (rr < nv ? rr : 0));
-            }
-            __syncwarp();
-            for (int h = 0; h < 2; ++h)
-                asm volatile(
-                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-                    " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_u32(tile + h * kLgChunk * 128 + lane * 512)),
-                    "l"(reinterpret_cast<uint64_t>(&tm_row)), "r"(h * 64), "r"(id[0]), "r"(id[1]), "r"(id[2]),
-                    "r"(id[3]), "r"(b)
-                    : "memory");
-        }
-    };
-
-    unsigned phase = 0u;  // bit s: parity of stage s's next completion
-    int it = blockIdx.x;
-    if (it < n_items && w == 0) issue(it, 0);
-#pragma unroll 1
-    for (int k = 0; it < n_items; ++k, it += gridDim.x) {
-        const int s = k & 1;
-        if (it + (int)gridDim.x < n_items && w == 0) issue(it + gridDim.x, s ^ 1);
-        const int l = it / item_chunks, chunk = it - l * item_chunks;
-        const int n = live(l), i0 = chunk * kLgChunk;
-        if (i0 >= n) {
-            if (cstats && chunk < n_chunks && tid < G) {
-                cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2] = -INFINITY;
-                cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2 + 1] = 0.0;
-            }
-            continue;
-        }
-        const int nv = min(kLgChunk, n - i0);
-        // epilogue inputs, loaded before the wait
-        const bool valid = tid < nv;
-        const int id = valid ? (cand ? __ldg(cand + (size_t)l * cand_cap + i0 + tid) : i0 + tid) : 0;
-        const int isz = valid && cstats ? __ldg(lv_size + (size_t)l * kcap + id) : 0;
-        unsigned char* tile = base + s * Geo::kTileB;
-        const double* qs = reinterpret_cast<const double*>(base + 2 * Geo::kTileB + s * Geo::kQB);
-        mbar_wait(smem_u32(&bar[s]), (phase >> s) & 1u);
-        phase ^= 1u << s;
-
-        const int qt = tid & 3, rg = tid >> 2;
-        const double* qq = qs + qt * QRow;
-        double acc[4][G];
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int g = 0; g < G; ++g) acc[r][g] = 0.0;
-        uint4 raw[4];
-        auto load_raw = [&](int cc, uint4 (&dst)[4]) {
-            const int c = (cc + 2 * (qt >> 1)) & 3;
-            const int ch = (qt & 1) * 4 + c;
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int row = rg + 32 * r;
-                dst[r] = *reinterpret_cast<const uint4*>(tile + (qt >> 1) * kLgChunk * 128 + row * 128 +
-                                                         ((ch ^ (row & 7)) << 4));
-            }
-        };
-        load_raw(0, raw);
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-            const int c = (cc + 2 * (qt >> 1)) & 3;
-            uint4 nxt[4];
-            if (cc < 3) load_raw(cc + 1, nxt);  // next chunk's rows in flight during this one's math
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                double qv[G];
-#pragma unroll
-                for (int g = 0; g < G; ++g) qv[g] = qq[g * 4 * QRow + c * 8 + e];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const unsigned wd = (&raw[r].x)[e >> 1];
-                    const double x = bf16hi_to_f64_s896((e & 1) ? (wd & 0xffff0000u) : (wd << 16));
-#pragma unroll
-                    for (int g = 0; g < G; ++g) acc[r][g] = fma(qv[g], x, acc[r][g]);
-                }
-            }
-            if (cc < 3)
-#pragma unroll
-                for (int r = 0; r < 4; ++r) raw[r] = nxt[r];
-        }
-        // transpose-reduce over the 4 quarter lanes (xor 2 splits rows, xor 1 splits heads)
-        const bool hi2 = qt & 2, hi1 = qt & 1;
-        constexpr int GH = (G + 1) / 2;
-        double a2[2][G];
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr)
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const double send = hi2 ? acc[rr][g] : acc[rr + 2][g];
-                const double keep = hi2 ? acc[rr + 2][g] : acc[rr][g];
-                a2[rr][g] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-            }
-        double a1[2][GH];
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr)
-#pragma unroll
-            for (int j = 0; j < GH; ++j) {
-                const int ghi = GH + j;
-                const double lo = a2[rr][j], hv = ghi < G ? a2[rr][ghi < G ? ghi : 0] : 0.0;
-                const double send = hi1 ? lo : hv;
-                const double keep = hi1 ? hv : lo;
-                a1[rr][j] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
-            }
-        __syncthreads();  // every read of the tile is done: the chunk's logits reuse its space
-        double* slg = reinterpret_cast<double*>(tile);  // [G][128]
-        const double sq = sqrt((double)D);
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-            const int r = rg + 32 * ((hi2 ? 2 : 0) + rr);
-#pragma unroll
-            for (int j = 0; j < GH; ++j) {
-                const int g = (hi1 ? GH : 0) + j;
-                if (g < G) {
-                    const double v = (a1[rr][j] * kUnscale896) / sq;
-                    slg[g * kLgChunk + r] = v;
-                    if (logits && r < nv) logits[((size_t)l * G + g) * cand_cap + i0 + r] = v;
-                }
-            }
-        }
-        if (cstats) {
-            __syncthreads();
-            const int i = tid;
-            const double nsz = (double)isz;
-            if (rej_w && valid) {
-                constexpr int GP = G <= 4 ? 4 : 8;
-                const double lnN = (double)logf((float)isz);
-                float wv[GP];
-#pragma unroll
-                for (int g = 0; g < GP; ++g) wv[g] = g < G ? (float)(slg[(g < G ? g : 0) * kLgChunk + i] + lnN) : 0.f;
-                float4* dst = reinterpret_cast<float4*>(rej_w + ((size_t)l * rej_cap + i0 + i) * GP);
-#pragma unroll
-                for (int v = 0; v < GP / 4; ++v)
-                    dst[v] = make_float4(wv[4 * v], wv[4 * v + 1], wv[4 * v + 2], wv[4 * v + 3]);
-            }
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const double m = warp_max(valid ? slg[g * kLgChunk + i] : -INFINITY);
-                if (lane == 0) red[w][g] = m;
-            }
-            __syncthreads();
-            if (tid < G) {
-                double M = -INFINITY;
-                for (int ww = 0; ww < kLgThreads / 32; ++ww) M = fmax(M, red[ww][tid]);
-                s_m[tid] = M;
-            }
-            __syncthreads();
-            double z[G];
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const double e = valid ? exp(slg[g * kLgChunk + i] - s_m[g]) : 0.0;
-                if (valid && e_local) e_local[((size_t)l * G + g) * cand_cap + i0 + i] = e;
-                z[g] = warp_sum(e * nsz);
-            }
-            if (lane == 0)
-#pragma unroll
-                for (int g = 0; g < G; ++g) red[w][g] = z[g];
-            __syncthreads();
-            if (tid < G) {
-                double Z = 0.0;
-                for (int ww = 0; ww < kLgThreads / 32; ++ww) Z += red[ww][tid];
-                cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2] = s_m[tid];
-                cstats[(((size_t)l * n_chunks + chunk) * G + tid) * 2 + 1] = Z;
-            }
-        }
-        __syncthreads();  // end of item: the stage (tile + slg) may be refilled
-    }
-}
 
 // ============================================================================
 // K10 + work list.  One CTA per ledger:
@@ -1443,82 +1163,33 @@ int mpa_launch_logits_v2(const double* q_lk, int group, int d, const mpa_level* 
     // items: ledgers x the chunks any ledger can use (n_max bounds the live candidates); chunk
     // stats rows past them are written -inf once per ledger by the last items
     const int item_chunks = ceil_div(n_max > 0 ? n_max : (cand ? cand_cap : lv->cap), kLgChunk);
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    const int items = L * item_chunks;
-    // MPA_LOGITS_PERSIST=1: persistent double-buffered grid (2 CTAs / SM); default one CTA per item
-    static int persist = -1;
-    if (persist < 0) {
-        const char* e = getenv("MPA_LOGITS_PERSIST");
-        persist = (e && e[0] == '1') ? 1 : 0;
-    }
-    const int grid = persist ? (items < 2 * sms ? items : 2 * sms) : items;
-#define MPA_LG3(D, NB)                                                                                             \
-    {                                                                                                              \
-        auto kern = logits_block_kernel<kG, D, NB>;                                                                \
-        const size_t smem = LgGeom<kG, D>::smem(NB);                                                               \
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                        \
-        kern<<<grid, kLgThreads, smem, st>>>(q_lk, (const __nv_bfloat16*)lv->kc, lv->cap, lv->count, lv->size, cand, \
-                                             n_cand, cand_cap, logits, chunk_stats, e_local, n_chunks,             \
-                                             item_chunks, L);                                                      \
-    }
-    if (grid <= 0) return 0;
-    MPA_REQUIRE(!cs_lk || (d == 128 && !persist && q_raw), MPA_ERR_UNSUPPORTED,
+    if (L * item_chunks <= 0) return 0;
+    MPA_REQUIRE(!cs_lk || (d == 128 && q_raw), MPA_ERR_UNSUPPORTED,
                 "mpa_centroid_logits: the fused lookup rotation needs the d = 128 TMA path");
-    MPA_REQUIRE(!rej_w || (d == 128 && !persist && !cand && chunk_stats && rej_cap >= lv->cap), MPA_ERR_UNSUPPORTED,
+    MPA_REQUIRE(!rej_w || (d == 128 && !cand && chunk_stats && rej_cap >= lv->cap), MPA_ERR_UNSUPPORTED,
                 "mpa_centroid_logits: per-candidate replacement weights need the flat d = 128 TMA path");
-    static int oneshot = -1;  // MPA_LOGITS_TMA_PERSIST=1: the persistent TMA ring (measured slower)
-    if (oneshot < 0) {
-        const char* e = getenv("MPA_LOGITS_TMA_PERSIST");
-        oneshot = (e && e[0] == '1') ? 0 : 1;
-    }
-    if (d == 128 && !persist && !oneshot && !cs_lk) {
-        CUtensorMap tt, tr;
-        if (int rc = encode_bf16_rows(&tt, lv->kc, (long long)L * lv->cap, 128, kLgChunk)) return rc;
-        if (int rc = encode_bf16_rows(&tr, lv->kc, (long long)L * lv->cap, 128, 1)) return rc;
-        MPA_DISPATCH_G(group, {
-            auto kern = logits_persist_kernel<kG>;
-            const size_t smem = LgPGeom<kG>::smem();
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            const int pgrid = items < 3 * sms ? items : 3 * sms;
-            kern<<<pgrid, kLgThreads, smem, st>>>(tt, tr, q_lk, lv->cap, lv->count, lv->size, cand, n_cand, cand_cap,
-                                                  logits, chunk_stats, e_local, n_chunks, rej_w, rej_cap,
-                                                  item_chunks, L);
-        });
-        return check_launch("mpa_centroid_logits(tma persistent)");
-    }
-    if (d == 128 && !persist) {
+    if (d == 128) {  // TMA tiles (flat) / row gathers (candidate lists), one CTA per (chunk, ledger)
         CUtensorMap tt, tr;
         if (int rc = encode_bf16_rows(&tt, lv->kc, (long long)L * lv->cap, 128, kLgChunk)) return rc;
         if (int rc = encode_bf16_rows(&tr, lv->kc, (long long)L * lv->cap, 128, 1)) return rc;
         dim3 g2(item_chunks, L);
         MPA_DISPATCH_G(group, {
             const size_t smem = 1024 + 2 * kLgChunk * 128 + sizeof(double) * (kG * 4 * 34 + kG * kLgChunk);
-            static int dmma = -1;  // MPA_LOGITS_DMMA=1: fp64 tensor-core path (measured 35 -> 41 us at C2, G = 4)
-            if (dmma < 0) {
-                const char* e = getenv("MPA_LOGITS_DMMA");
-                dmma = (e && e[0] == '1') ? 1 : 0;
-            }
-            auto kern = dmma ? logits_tma_kernel<kG, true> : logits_tma_kernel<kG, false>;
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            auto kern = logits_tma_kernel<kG>;
+            if (int rc = set_max_smem((const void*)kern, (int)smem)) return rc;
             launch_pdl(kern, g2, dim3(kLgThreads), smem, st, tt, tr, q_lk, lv->cap, lv->count, lv->size, cand, n_cand,
                        cand_cap, logits, chunk_stats, e_local, n_chunks, rej_w, rej_cap, q_raw, cs_lk);
         });
         return check_launch("mpa_centroid_logits(tma)");
     }
-    MPA_DISPATCH_G(group, {
-        if (persist) {
-            if (d == 128) MPA_LG3(128, 2) else MPA_LG3(64, 2)
-        } else {
-            if (d == 128) MPA_LG3(128, 1) else MPA_LG3(64, 1)
-        }
+    MPA_DISPATCH_G(group, {  // d = 64: smem-blocked kernel
+        auto kern = logits_block_kernel<kG, 64, 1>;
+        const size_t smem = LgGeom<kG, 64>::smem(1);
+        if (int rc = set_max_smem((const void*)kern, (int)smem)) return rc;
+        kern<<<L * item_chunks, kLgThreads, smem, st>>>(q_lk, (const __nv_bfloat16*)lv->kc, lv->cap, lv->count, lv->size,
+                                                        cand, n_cand, cand_cap, logits, chunk_stats, e_local, n_chunks,
+                                                        item_chunks, L);
     });
-#undef MPA_LG3
     return check_launch("mpa_centroid_logits(block)");
 }
 

@@ -36,6 +36,8 @@
 // Selection numerics are the reference's (fp64 logits, exps, normalisers, scores), so the
 // selected set is the oracle's except at true ties (|score gap| ~1e-16 relative); outputs are
 // fp32 with bf16 storage (tolerance 1e-2).
+#include <mutex>
+
 #include "mpa_common.cuh"
 #include "mpa_tc.cuh"
 
@@ -918,6 +920,8 @@ static int pick_cluster(int L, int n_max, int* kc_out) {
     struct Memo { int L, chunks, dev, C, kc; };
     static Memo memo[8];
     static int nmemo = 0;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
     int dev = 0;
     cudaGetDevice(&dev);
     const int chunks = ceil_div(n_max > 0 ? n_max : 1, stp::kChunk);
@@ -1017,11 +1021,9 @@ extern "C" int mpa_decode_step(const float* q, const float* k_new, const float* 
             at[na].val.clusterDim.z = 1;
             ++na;
         }
-        if (pdl_enabled()) {
-            at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            at[na].val.programmaticStreamSerializationAllowed = 1;
-            ++na;
-        }
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
         cfg.attrs = at;
         cfg.numAttrs = na;
         cudaLaunchKernelEx(&cfg, kern, tk, prm);

@@ -9,7 +9,7 @@ in HBM; one decode step is a short, graph-capturable chain of libmpattn kernels 
     mpa_select           Eq. 1 scores + size-weighted radix select to the budget         K10
     [hierarchy: mpa_hier_candidates, mpa_centroid_logits (fine children), mpa_select with
      the coarse-rejected union denominator]
-    mpa_build_worklist   sinks ++ buffer ++ selected members; rejected centroids + ln N
+    (work lists)         sinks ++ buffer ++ selected members; rejected centroids + ln N
     mpa_sparse_decode    gather + exact attention + centroid replacement, split-KV merge K11+K12
 
 Attention happens before the step's token is appended (pipeline.py:137-159); the online
@@ -28,10 +28,6 @@ from ._lib import MpaCache, call, dtype_code, ptr, stream_ptr
 from .core import ConfigError, EngineConfig, HeadLayout, inv_freq
 from .ledger import DeviceLedgers, HostLedger
 
-import os
-
-NUM_SMS = 148
-_SK_SPLIT = int(os.environ.get("MPA_SK_SPLIT", "0"))  # experiments: CTAs per ledger of the fused grid
 
 
 class DecodeEngine:
@@ -103,7 +99,7 @@ class DecodeEngine:
         self.cursor = 0
         # the flat serving path (fused_lookup_path) hands the fused kernel a contiguous-centroid
         # list: every centroid's replacement weight in id order, the selected ones -inf
-        self.use_graphs = (os.environ.get("MPA_NO_GRAPH") != "1") if use_graphs is None else use_graphs
+        self.use_graphs = True if use_graphs is None else use_graphs
         self._graph = None
         self.n_captures = 0  # step-graph captures so far (bench reports it)
         self.time_fused = False  # bench: CUDA events around the fused kernel inside the step graph
@@ -262,7 +258,7 @@ class DecodeEngine:
     def fused(self, n_split: int | None = None) -> torch.Tensor:
         """K11 + K12 over the current work lists.  n_split None / 0: one full wave of the
         stream-K grid (bf16) or automatic splits (fp32); > 0: that many CTAs per ledger."""
-        S = int(n_split or 0) or _SK_SPLIT
+        S = int(n_split or 0)
         ws = self._workspace(S)
         st = stream_ptr()
         rej, rej_w, n_rej = self._centroid_terms()

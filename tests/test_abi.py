@@ -29,7 +29,7 @@ def lib():
 def test_header_declares_entry_points():
     names = declared()
     for must in ("mpa_kv_write", "mpa_rotate_queries", "mpa_centroid_logits", "mpa_select",
-                 "mpa_build_worklist", "mpa_sparse_decode", "mpa_last_error"):
+                 "mpa_sparse_decode", "mpa_last_error"):
         assert must in names
 
 
