@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--ctx", type=int, default=None)
     ap.add_argument("--budget", type=int, default=512)
+    ap.add_argument("--page-size", type=int, default=None,
+                    help="serve K_rot / V from a paged pool with this many tokens per page (shuffled pages)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline leg")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no CPU leg, no clocks)")
@@ -319,7 +321,11 @@ def build_engine(args, rank, dev):
     total_steps = max(3, args.warmup) + args.steps + CALIB_STEPS
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
     tcap = ctx + 2 * total_steps + 3 * cfg.local_buffer + 8
-    eng = DecodeEngine(cfg, lay, b, tcap=tcap, dtype=torch.bfloat16, device=dev)
+    ps = getattr(args, "page_size", None)
+    eng = DecodeEngine(cfg, lay, b, tcap=tcap, dtype=torch.bfloat16, device=dev, page_size=ps,
+                       page_order="shuffled")
+    if ps:
+        eng.reserve(ctx)  # the prompt's pages
     for s in range(b):  # prompt KV, one sequence at a time to bound temporaries
         k = torch.randn(1, lay.num_kv_heads, ctx, d, generator=gen, device=dev)
         v = torch.randn(1, lay.num_kv_heads, ctx, d, generator=gen, device=dev)
@@ -461,7 +467,7 @@ def main():
     dense_ms = timed(lambda i: eng.attend_dense(Q[i]), K)
     dense_avg = float(np.mean(dense_ms))
     dbytes = dense_bytes(np.repeat(eng.cache_len, lay.num_kv_heads), d, G, 2)
-    fi_ms = None if args.profile else flashinfer_dense(eng, Q[0], K, timed)
+    fi_ms = None if (args.profile or eng.block_table is not None) else flashinfer_dense(eng, Q[0], K, timed)
 
     # ---- end to end through the public API from pinned host buffers
     qh = Q[total_steps:total_steps + K].cpu().pin_memory()
@@ -517,6 +523,8 @@ def main():
             "config": {"workload": workload_label(args, world), "batch": b, "ctx": ctx,
                        "budget": args.budget, "tokens_per_centroid": cfg.fine_ratio,
                        "l2": L2Flush.DESC,
+                       "kv_cache": (f"paged: {args.page_size}-token pages in shuffled order, HND pools"
+                                    if args.page_size else "flat [L, tcap, d]"),
                        "parallelism": f"batch-sharded replicas x{world}"},
             "speedup_vs_dense": dense_avg / ms_step,
             "dense_us_per_step": dense_avg * 1e3,
@@ -696,8 +704,12 @@ def _write_seq(eng, s, k, v):
 
     Hkv = eng.Hkv
     n = k.shape[2]
-    sub = MpaCache(ptr(eng.k_rot[s * Hkv]), ptr(eng.k_raw[s * Hkv]), ptr(eng.v[s * Hkv]), dtype_code(eng.dtype), Hkv,
-                   eng.tcap, eng.d)
+    if eng.block_table is None:
+        sub = MpaCache(ptr(eng.k_rot[s * Hkv]), ptr(eng.k_raw[s * Hkv]), ptr(eng.v[s * Hkv]), dtype_code(eng.dtype),
+                       Hkv, eng.tcap, eng.d)
+    else:  # the page pools with sequence s's block-table row
+        sub = MpaCache(ptr(eng.k_rot), ptr(eng.k_raw[s * Hkv]), ptr(eng.v), dtype_code(eng.dtype), Hkv, eng.tcap,
+                       eng.d, ptr(eng.block_table[s]), eng.page_size, eng.pages_per_seq, eng.n_pages, Hkv)
     pos0 = torch.zeros(Hkv, dtype=torch.int32, device=eng.device)
     kk = k.reshape(Hkv, n, eng.d).contiguous()
     vv = v.reshape(Hkv, n, eng.d).contiguous()

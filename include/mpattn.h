@@ -41,12 +41,23 @@ const char* mpa_version(void);
 
 typedef struct mpa_cache {
     void* k_rot;      /* keys rotated at their true positions (exact-attention view) */
-    void* k_raw;      /* pre-rotation keys (clustering / windowed lookup view)       */
+    void* k_raw;      /* pre-rotation keys (clustering / windowed lookup view), [L, tcap, d] */
     void* v;
     int32_t dtype;
     int32_t n_ledgers;
     int32_t tcap;
     int32_t head_dim;
+    /* Paged serving cache (block_table != NULL; pipeline.py:26-52 `_KvStore` as a page pool):
+     * k_rot and v are pools [n_pages, n_kv_heads, page_size, d] (the HND block layout of paged
+     * decode kernels: a head's tokens are contiguous inside a page) and token t of ledger
+     * l = s * n_kv_heads + h lives in row (block_table[s, t / page_size] * n_kv_heads + h) *
+     * page_size + t % page_size.  k_raw (the clustering view) stays [L, tcap, d].
+     * block_table == NULL: k_rot / v are [L, tcap, d] like k_raw. */
+    const int32_t* block_table;  /* [n_seq, pages_per_seq] physical page ids */
+    int32_t page_size;           /* tokens per page, a power of two */
+    int32_t pages_per_seq;
+    int32_t n_pages;
+    int32_t n_kv_heads;
 } mpa_cache;
 
 typedef struct mpa_level {
@@ -332,7 +343,7 @@ int mpa_km_count_nonempty(const mpa_km* km, int32_t* nk, void* stream);
  *   prob_start + i for key problems, fine ids for the hierarchy -- "children").
  * Hierarchy (pts64 != NULL): kc64 / vc64 are the size-weighted means of the children's fine
  * centroids (fine_vc64 supplies the value side) -- clustering.py:249-255. */
-int mpa_km_write_level(const mpa_km* km, const void* vals, const double* fine_vc64,
+int mpa_km_write_level(const mpa_km* km, const mpa_cache* vcache, const double* fine_vc64,
                        const int32_t* f0, const int32_t* mbase,
                        double* kc64, double* vc64, void* kc, void* vc, int32_t serve_dtype,
                        int32_t* size, int32_t* off, int32_t* idx, int32_t level_cap, int32_t idx_cap,

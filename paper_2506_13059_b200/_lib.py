@@ -29,7 +29,8 @@ class MpattnError(RuntimeError):
 
 class MpaCache(C.Structure):
     _fields_ = [("k_rot", _vp), ("k_raw", _vp), ("v", _vp), ("dtype", _i32), ("n_ledgers", _i32),
-                ("tcap", _i32), ("head_dim", _i32)]
+                ("tcap", _i32), ("head_dim", _i32), ("block_table", _vp), ("page_size", _i32),
+                ("pages_per_seq", _i32), ("n_pages", _i32), ("n_kv_heads", _i32)]
 
 
 class MpaLevel(C.Structure):
@@ -83,7 +84,7 @@ _SIGS = {
     "mpa_km_lloyd": [_KM, C.POINTER(_i32), _vp],
     "mpa_km_means": [_KM, _vp],
     "mpa_km_count_nonempty": [_KM, _vp, _vp],
-    "mpa_km_write_level": [_KM, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i32, _i32, _vp],
+    "mpa_km_write_level": [_KM, C.POINTER(MpaCache), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i32, _i32, _vp],
     "mpa_km_assign_from_level": [_KM, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp],
     "mpa_km_seq_assign": [_KM, _vp, C.c_int, _vp, _vp],
     "mpa_sparse_decode": [C.POINTER(MpaCache), _vp, C.c_int, C.c_int, _vp, _vp, C.c_int, _vp, _vp, _vp,

@@ -48,7 +48,7 @@ def audit_engine(eng, rel_tol: float = 1e-5, check_assignment: bool = True) -> N
             raise LedgerAuditError("cluster size disagrees with member count")
         owner = torch.repeat_interleave(torch.arange(K, device=dev), sizes)
         keys = eng.k_raw[l, mem].double()
-        vals = eng.v[l, mem].double()
+        vals = eng.values(l, mem).double()
         for cen, src, what in ((led.kc64[l, :K], keys, "key"), (led.vc64[l, :K], vals, "value")):
             acc = torch.zeros_like(cen).index_add_(0, owner, src)
             mean = acc / sizes[:, None].double()

@@ -148,7 +148,7 @@ def _write_fine(eng, km: KMeansBatch, f0: np.ndarray, mbase: np.ndarray) -> None
     led = eng.led
     _check_level_cap(km, f0, led.kcap, "fine")
     f0_d, mb_d = _i32(eng, f0), _i32(eng, mbase)
-    call("mpa_km_write_level", km.struct(), ptr(eng.v), None, ptr(f0_d), ptr(mb_d),
+    call("mpa_km_write_level", km.struct(), eng.cache_struct, None, ptr(f0_d), ptr(mb_d),
          ptr(led.kc64), ptr(led.vc64), ptr(led.kc), ptr(led.vc), dtype_code(led.dtype), ptr(led.size), ptr(led.off),
          ptr(led.mem), led.kcap, led.tcap, stream_ptr())
 

@@ -626,7 +626,7 @@ __device__ __forceinline__ void store_serve(void* base, size_t idx, double v) {
 
 template <typename TV>
 __global__ void __launch_bounds__(kMeansWarps * 32)
-km_write_level_kernel(mpa_km km, const TV* __restrict__ vals, const double* __restrict__ fine_vc64,
+km_write_level_kernel(mpa_km km, const TV* __restrict__ vals, KvRows vrow, const double* __restrict__ fine_vc64,
                       const int32_t* __restrict__ f0, const int32_t* __restrict__ mbase, double* kc64, double* vc64,
                       void* kc, void* vc, int serve_dtype, int32_t* size, int32_t* off, int32_t* idx, int level_cap,
                       int idx_cap) {
@@ -669,7 +669,7 @@ km_write_level_kernel(mpa_km km, const TV* __restrict__ vals, const double* __re
             kv = src[k];
             double acc = 0.0;
             for (int m = 0; m < c; ++m)
-                acc = __dadd_rn(acc, elem<TV>::to_d(vals[((size_t)l * km.tcap + start + ord[m]) * d + k]));
+                acc = __dadd_rn(acc, elem<TV>::to_d(vals[(size_t)vrow.row(l, start + ord[m]) * d + k]));
             vv = __ddiv_rn(acc, (double)c);
         } else {
             // coarse = exact size-weighted mean of the children (clustering.py:249-255)
@@ -1006,24 +1006,30 @@ extern "C" int mpa_km_count_nonempty(const mpa_km* km, int32_t* nk, void* stream
     return check_launch("mpa_km_count_nonempty");
 }
 
-extern "C" int mpa_km_write_level(const mpa_km* km, const void* vals, const double* fine_vc64, const int32_t* f0,
+extern "C" int mpa_km_write_level(const mpa_km* km, const mpa_cache* vcache, const double* fine_vc64, const int32_t* f0,
                                   const int32_t* mbase, double* kc64, double* vc64, void* kc, void* vc,
                                   int32_t serve_dtype, int32_t* size, int32_t* off, int32_t* idx, int32_t level_cap,
                                   int32_t idx_cap, void* stream) {
     if (int rc = validate(km)) return rc;
     MPA_REQUIRE(f0 && mbase && kc64 && vc64 && kc && vc && size && off && idx, MPA_ERR_ARG,
                 "mpa_km_write_level: null argument");
-    MPA_REQUIRE(km->pts64 ? fine_vc64 != nullptr : vals != nullptr, MPA_ERR_ARG,
+    MPA_REQUIRE(km->pts64 ? fine_vc64 != nullptr : vcache != nullptr, MPA_ERR_ARG,
                 "mpa_km_write_level: values source");
+    MPA_REQUIRE(km->pts64 || (vcache->tcap == km->tcap && vcache->dtype == km->pts_dtype), MPA_ERR_ARG,
+                "mpa_km_write_level: value cache does not match the key source");
+    if (vcache)
+        if (int rc = check_cache(vcache, "mpa_km_write_level")) return rc;
     if (km->n_prob <= 0) return 0;
+    const void* vals = vcache ? vcache->v : nullptr;
+    const KvRows vrow = vcache ? kv_rows(vcache) : KvRows{nullptr, km->tcap, 0, 0, 1};
     dim3 grid(ceil_div(km->k_max, kMeansWarps), km->n_prob);
     cudaStream_t st = (cudaStream_t)stream;
     if (km->pts_dtype == MPA_BF16)
         km_write_level_kernel<__nv_bfloat16><<<grid, kMeansWarps * 32, 0, st>>>(
-            *km, (const __nv_bfloat16*)vals, fine_vc64, f0, mbase, kc64, vc64, kc, vc, serve_dtype, size, off, idx,
+            *km, (const __nv_bfloat16*)vals, vrow, fine_vc64, f0, mbase, kc64, vc64, kc, vc, serve_dtype, size, off, idx,
             level_cap, idx_cap);
     else
-        km_write_level_kernel<float><<<grid, kMeansWarps * 32, 0, st>>>(*km, (const float*)vals, fine_vc64, f0, mbase,
+        km_write_level_kernel<float><<<grid, kMeansWarps * 32, 0, st>>>(*km, (const float*)vals, vrow, fine_vc64, f0, mbase,
                                                                         kc64, vc64, kc, vc, serve_dtype, size, off,
                                                                         idx, level_cap, idx_cap);
     return check_launch("mpa_km_write_level");

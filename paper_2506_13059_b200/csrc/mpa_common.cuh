@@ -145,6 +145,30 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* scratch, int* to
 
 __host__ __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
+// Row of token t of ledger l in k_rot / v: flat [L, tcap] or through the block table of a paged
+// pool (mpa_cache).  Rows fit in int32 (tensor maps are limited to 2^31 rows).
+struct KvRows {
+    const int32_t* bt;
+    int tcap, ps_shift, ppl, hkv;
+    __device__ __forceinline__ int row(int l, int t) const {
+        if (!bt) return l * tcap + t;
+        const int s = l / hkv, h = l - s * hkv;
+        const int page = __ldg(bt + (size_t)s * ppl + (t >> ps_shift));
+        return ((page * hkv + h) << ps_shift) + (t & ((1 << ps_shift) - 1));
+    }
+};
+inline KvRows kv_rows(const mpa_cache* c) {
+    KvRows r{c->block_table, c->tcap, 0, c->pages_per_seq, c->n_kv_heads > 0 ? c->n_kv_heads : 1};
+    if (c->block_table)
+        while ((1 << r.ps_shift) < c->page_size) ++r.ps_shift;
+    return r;
+}
+inline long long kv_pool_rows(const mpa_cache* c) {
+    return c->block_table ? (long long)c->n_pages * c->page_size * c->n_kv_heads : (long long)c->n_ledgers * c->tcap;
+}
+// paged caches: page_size a power of two, the pool addressable with int32 rows
+int check_cache(const mpa_cache* c, const char* what);
+
 }  // namespace mpa
 
 // Runtime GQA group size -> compile-time kG (1..8).

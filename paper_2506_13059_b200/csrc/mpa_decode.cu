@@ -126,7 +126,7 @@ constexpr int kFfmaWarps = 4;
 
 template <typename T, int G, int NDL>
 __global__ void __launch_bounds__(kFfmaWarps * 32)
-decode_ffma_kernel(const T* __restrict__ k_rot, const T* __restrict__ vcache, int tcap, int d,
+decode_ffma_kernel(const T* __restrict__ k_rot, const T* __restrict__ vcache, KvRows kvr, int d,
                    const float* __restrict__ q_rot, const int32_t* __restrict__ tok, const int32_t* __restrict__ n_tok,
                    int tok_cap, const int32_t* __restrict__ rej, const float* __restrict__ rej_w,
                    const int32_t* __restrict__ n_rej, int rej_cap, const T* __restrict__ fvc, int fcap,
@@ -171,8 +171,8 @@ decode_ffma_kernel(const T* __restrict__ k_rot, const T* __restrict__ vcache, in
 
     for (int t = R.t0 + w; t < R.t1; t += kFfmaWarps) {
         const int row = tok ? tok[(size_t)l * tok_cap + t] : t;
-        const T* kp = k_rot + ((size_t)l * tcap + row) * d;
-        const T* vp = vcache + ((size_t)l * tcap + row) * d;
+        const T* kp = k_rot + (size_t)kvr.row(l, row) * d;
+        const T* vp = vcache + (size_t)kvr.row(l, row) * d;
         float kx[NDL], vx[NDL];
 #pragma unroll
         for (int j = 0; j < NDL; ++j) {
@@ -403,11 +403,11 @@ struct SkGeom {
     static size_t smem(int L, int C) { (void)C; return (size_t)kStagesB + kBarB + kIdB + sizeof(int) * (3 * L + 1); }
 };
 
-template <int G, int D, int NW, int NST>
+template <int G, int D, int NW, int NST, bool PAGED>
 __global__ void __launch_bounds__(NW * 32, 2)
 decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                  const __grid_constant__ CUtensorMap tm_fvc, const __grid_constant__ CUtensorMap tm_cvc,
-                 const __grid_constant__ CUtensorMap tm_fvc16, int tcap, const __nv_bfloat16* __restrict__ k_rows,
+                 const __grid_constant__ CUtensorMap tm_fvc16, KvRows kvr, const __nv_bfloat16* __restrict__ k_rows,
                  const __nv_bfloat16* __restrict__ v_rows,
                  const float* __restrict__ q_rot, const int32_t* __restrict__ tok, const int32_t* __restrict__ n_tok,
                  int tok_cap, const int32_t* __restrict__ rej, const float* __restrict__ rej_w,
@@ -526,7 +526,12 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     constexpr int kAhead = Geo::kRing - 1;
     auto prefetch_ids = [&](int j, const Meta& m) {
         const int rows = m.kind == 0 ? 16 : 32;
-        if (lane < rows && m.nv > 0 && (m.kind == 1 ? rej != nullptr : tok != nullptr)) {
+        if (PAGED && m.kind == 0 && !tok && kvr.ps_shift >= 4) {
+            // dense tile of a paged cache: 16 consecutive tokens inside one page -- its page id
+            if (lane == 0 && m.nv > 0)
+                cp_async4(smem_u32(idring + (j % Geo::kRing) * 32),
+                          kvr.bt + (size_t)(m.l / kvr.hkv) * kvr.ppl + (m.i0 >> kvr.ps_shift));
+        } else if (lane < rows && m.nv > 0 && (m.kind == 1 ? rej != nullptr : tok != nullptr)) {
             const int row = lane < m.nv ? lane : 0;
             const int32_t* src = m.kind == 0 ? tok + (size_t)m.l * tok_cap + m.i0 + row
                                              : rej + (size_t)m.l * rej_cap + m.i0 + row;
@@ -536,6 +541,8 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     };
     // ids of rows [r0, r0 + 16) of tile j; every lane reads the same smem words and the values
     // are broadcast from lane 0 so the compiler keeps them in uniform registers
+    // token ids; a paged cache's token tiles get their pool rows here (lane r translates token r
+    // through the block table, the rows are broadcast back), a flat cache adds l * tcap at the copy
     auto ids16 = [&](int j, const Meta& m, int r0, int (&id)[16]) {
         if (m.kind == 0 && !tok) {
 #pragma unroll
@@ -549,6 +556,20 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
                 id[4 * v + 1] = __shfl_sync(0xffffffffu, t.y, 0);
                 id[4 * v + 2] = __shfl_sync(0xffffffffu, t.z, 0);
                 id[4 * v + 3] = __shfl_sync(0xffffffffu, t.w, 0);
+            }
+        }
+        if constexpr (PAGED) {
+            if (m.kind == 0 && !tok && kvr.ps_shift >= 4) {
+                const int page = idring[(j % Geo::kRing) * 32];
+                const int h = m.l % kvr.hkv, base = (page * kvr.hkv + h) << kvr.ps_shift;
+                const int mask = (1 << kvr.ps_shift) - 1;
+#pragma unroll
+                for (int r = 0; r < 16; ++r) id[r] = base + ((m.i0 + (r < m.nv ? r : 0)) & mask);
+            } else if (m.kind == 0) {  // token list: lane r translates token r (read back from the ring)
+                int mine = tok ? idring[(j % Geo::kRing) * 32 + r0 + (lane & 15)] : m.i0 + min(lane & 15, m.nv - 1);
+                mine = kvr.row(m.l, mine);
+#pragma unroll
+                for (int r = 0; r < 16; ++r) id[r] = __shfl_sync(0xffffffffu, mine, r);
             }
         }
     };
@@ -596,7 +617,7 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             // ch) straight into the swizzled stage -- 2 x 256 B rows per warp instruction, which
             // the TMA unit would need 4 gather4 instructions for; completion on the stage mbarrier
             constexpr int CPR = D / 8;  // 16-byte chunks per row
-            const size_t lbase = (size_t)m.l * tcap;
+            const size_t lbase = PAGED ? 0 : (size_t)m.l * kvr.tcap;
 #pragma unroll
             for (int it = 0; it < CPR; ++it) {
                 const int jj = lane + 32 * it, ch = jj % CPR, kv = (jj / CPR) & 1, r = jj / (2 * CPR);
@@ -624,7 +645,7 @@ decode_sk_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         }
         if (m.kind == 0) {
             mbar_expect_tx(bar, 2 * Geo::kMatB);
-            const int base = m.l * tcap;
+            const int base = PAGED ? 0 : m.l * kvr.tcap;
 #pragma unroll
             for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -1056,7 +1077,7 @@ int launch_ffma(const mpa_cache* c, const float* q_rot, const int32_t* tok, cons
     {                                                                                                           \
         auto kern = decode_ffma_kernel<T, G, NDL>;                                                              \
         if (int rc = set_max_smem((const void*)kern, (int)smem)) return rc;                                   \
-        kern<<<grid, kFfmaWarps * 32, smem, st>>>((const T*)c->k_rot, (const T*)c->v, c->tcap, d, q_rot, tok,   \
+        kern<<<grid, kFfmaWarps * 32, smem, st>>>((const T*)c->k_rot, (const T*)c->v, kv_rows(c), d, q_rot, tok, \
                                                   n_tok, tok_cap, rej, rej_w, n_rej, rej_cap, (const T*)fvc,    \
                                                   fcap, (const T*)cvc, ccap, S, pml, pacc, ticket, out,         \
                                                   part_out);                                                    \
@@ -1147,21 +1168,22 @@ int launch_sk(const mpa_cache* c, const float* q_rot, const int32_t* tok, const 
     const int L = c->n_ledgers;
     const size_t smem = Geo::smem(L, C);
     MPA_REQUIRE(smem <= 227 * 1024, MPA_ERR_UNSUPPORTED, "mpa_sparse_decode: %d ledgers exceed the smem schedule", L);
-    auto kern = decode_sk_kernel<G, D, kSkWarps, kSkStages>;
+    auto kern = c->block_table ? decode_sk_kernel<G, D, kSkWarps, kSkStages, true>
+                               : decode_sk_kernel<G, D, kSkWarps, kSkStages, false>;
     if (int rc = set_max_smem((const void*)kern, (int)smem)) return rc;
     if (one_wave) {  // the stream-K grid is one resident wave (2 CTAs / SM unless smem or registers say less)
         const int occ = sk_occupancy((const void*)kern, (int)smem);
         C = std::min(C, std::max(1, occ) * num_sms());
     }
     CUtensorMap tk, tv, tf, tc, tf16;
-    int rc = bf16_rows_map(&tk, c->k_rot, (long long)L * c->tcap, D);
-    if (!rc) rc = bf16_rows_map(&tv, c->v, (long long)L * c->tcap, D);
+    int rc = bf16_rows_map(&tk, c->k_rot, kv_pool_rows(c), D);
+    if (!rc) rc = bf16_rows_map(&tv, c->v, kv_pool_rows(c), D);
     if (!rc) rc = fvc ? bf16_rows_map(&tf, fvc, (long long)L * fcap, D) : (tf = tk, 0);
     if (!rc) rc = fvc ? bf16_rows_map(&tf16, fvc, (long long)L * fcap, D, 16) : (tf16 = tk, 0);
     if (!rc) rc = cvc ? bf16_rows_map(&tc, cvc, (long long)L * ccap, D) : (tc = tf, 0);
     if (rc) return rc;
     MPA_REQUIRE(rej || !rej_w || fvc, MPA_ERR_ARG, "mpa_sparse_decode: contiguous-centroid list without fine_vc");
-    launch_pdl(kern, dim3(C), dim3(kSkWarps * 32), smem, st, tk, tv, tf, tc, tf16, c->tcap,
+    launch_pdl(kern, dim3(C), dim3(kSkWarps * 32), smem, st, tk, tv, tf, tc, tf16, kv_rows(c),
                (const __nv_bfloat16*)c->k_rot, (const __nv_bfloat16*)c->v, q_rot, tok, n_tok, tok_cap, rej, rej_w,
                n_rej, rej_cap, fcap, ccap, L, part, ticket, out, part_out,
                tok != nullptr ? 1 : 0);  // sparse token lists through the LSU, the dense decode through TMA gathers
@@ -1208,6 +1230,7 @@ static int sparse_decode_impl(const mpa_cache* c, const float* q_rot, int n_kv_h
     MPA_REQUIRE(c->head_dim >= 2 && c->head_dim % 2 == 0 && c->head_dim <= 256, MPA_ERR_UNSUPPORTED,
                 "mpa_sparse_decode: head_dim %d", c->head_dim);
     (void)n_kv_heads;
+    if (int rc = check_cache(c, "mpa_sparse_decode")) return rc;
     const int L = c->n_ledgers;
     if (L <= 0) return 0;
     const size_t need = mpa_sparse_decode_workspace(L, group, c->head_dim, c->dtype, n_split);

@@ -38,6 +38,20 @@ int check_launch(const char* what) {
     return 0;
 }
 
+int check_cache(const mpa_cache* c, const char* what) {
+    MPA_REQUIRE(c, MPA_ERR_ARG, "%s: null cache", what);
+    if (!c->block_table) return 0;
+    MPA_REQUIRE(c->page_size >= 1 && (c->page_size & (c->page_size - 1)) == 0, MPA_ERR_ARG,
+                "%s: page_size %d is not a power of two", what, c->page_size);
+    MPA_REQUIRE(c->n_kv_heads >= 1 && c->n_ledgers % c->n_kv_heads == 0 && c->pages_per_seq >= 1 && c->n_pages >= 1,
+                MPA_ERR_ARG, "%s: paged cache geometry", what);
+    MPA_REQUIRE((long long)c->pages_per_seq * c->page_size >= c->tcap, MPA_ERR_ARG,
+                "%s: %d pages of %d tokens < tcap %d", what, c->pages_per_seq, c->page_size, c->tcap);
+    MPA_REQUIRE(kv_pool_rows(c) < (1ll << 31), MPA_ERR_UNSUPPORTED, "%s: page pool of %lld rows", what,
+                kv_pool_rows(c));
+    return 0;
+}
+
 // per-device launch facts: a process may drive several GPUs, so nothing is cached per process
 namespace {
 constexpr int kMaxDevices = 64;
@@ -83,12 +97,13 @@ template <typename T>
 __global__ void kv_write_kernel(T* __restrict__ k_rot, T* __restrict__ k_raw, T* __restrict__ v,
                                 const float* __restrict__ k_src, const float* __restrict__ v_src,
                                 const int32_t* __restrict__ pos0, int n_tok, int tcap, int d,
-                                const double* __restrict__ inv_freq) {
+                                const double* __restrict__ inv_freq, KvRows kv) {
     const int l = blockIdx.y;
     const int t = blockIdx.x;                      // token within this write
     const int pos = pos0[l] + t;
     const size_t src = ((size_t)l * n_tok + t) * d;
-    const size_t dst = ((size_t)l * tcap + pos) * d;
+    const size_t raw = ((size_t)l * tcap + pos) * d;
+    const size_t dst = (size_t)kv.row(l, pos) * d;
     for (int i = threadIdx.x; i < d / 2; i += blockDim.x) {
         const double x = (double)k_src[src + 2 * i];
         const double y = (double)k_src[src + 2 * i + 1];
@@ -97,8 +112,8 @@ __global__ void kv_write_kernel(T* __restrict__ k_rot, T* __restrict__ k_raw, T*
         // no FMA contraction: same rounding sequence as numpy's ev*cos - od*sin
         k_rot[dst + 2 * i] = elem<T>::from_d(__dsub_rn(__dmul_rn(x, cs), __dmul_rn(y, sn)));
         k_rot[dst + 2 * i + 1] = elem<T>::from_d(__dadd_rn(__dmul_rn(x, sn), __dmul_rn(y, cs)));
-        k_raw[dst + 2 * i] = elem<T>::from_d(x);
-        k_raw[dst + 2 * i + 1] = elem<T>::from_d(y);
+        k_raw[raw + 2 * i] = elem<T>::from_d(x);
+        k_raw[raw + 2 * i + 1] = elem<T>::from_d(y);
         v[dst + 2 * i] = elem<T>::from_d((double)v_src[src + 2 * i]);
         v[dst + 2 * i + 1] = elem<T>::from_d((double)v_src[src + 2 * i + 1]);
     }
@@ -112,11 +127,12 @@ __global__ void kv_append_kernel(T* __restrict__ k_rot, T* __restrict__ k_raw, T
                                  const float* __restrict__ k_src, const float* __restrict__ v_src, int n_kv_heads,
                                  int n_seq, int32_t* __restrict__ cache_len, int32_t* __restrict__ ntok_dense,
                                  int n_tok, int tcap, int d, const double* __restrict__ inv_freq,
-                                 int32_t* __restrict__ ticket) {
+                                 int32_t* __restrict__ ticket, KvRows kv) {
     const int l = blockIdx.y, t = blockIdx.x;
     const int pos = cache_len[l / n_kv_heads] + t;
     const size_t src = ((size_t)l * n_tok + t) * d;
-    const size_t dst = ((size_t)l * tcap + pos) * d;
+    const size_t raw = ((size_t)l * tcap + pos) * d;
+    const size_t dst = (size_t)kv.row(l, pos) * d;
     for (int i = threadIdx.x; i < d / 2; i += blockDim.x) {
         const double x = (double)k_src[src + 2 * i];
         const double y = (double)k_src[src + 2 * i + 1];
@@ -124,8 +140,8 @@ __global__ void kv_append_kernel(T* __restrict__ k_rot, T* __restrict__ k_raw, T
         sincos((double)pos * inv_freq[i], &sn, &cs);
         k_rot[dst + 2 * i] = elem<T>::from_d(__dsub_rn(__dmul_rn(x, cs), __dmul_rn(y, sn)));
         k_rot[dst + 2 * i + 1] = elem<T>::from_d(__dadd_rn(__dmul_rn(x, sn), __dmul_rn(y, cs)));
-        k_raw[dst + 2 * i] = elem<T>::from_d(x);
-        k_raw[dst + 2 * i + 1] = elem<T>::from_d(y);
+        k_raw[raw + 2 * i] = elem<T>::from_d(x);
+        k_raw[raw + 2 * i + 1] = elem<T>::from_d(y);
         v[dst + 2 * i] = elem<T>::from_d((double)v_src[src + 2 * i]);
         v[dst + 2 * i + 1] = elem<T>::from_d((double)v_src[src + 2 * i + 1]);
     }
@@ -211,17 +227,19 @@ extern "C" int mpa_kv_write(const mpa_cache* c, const float* k_src, const float*
                             const int32_t* pos0, int n_tok, const double* inv_freq, void* stream) {
     MPA_REQUIRE(c && k_src && v_src && pos0 && inv_freq, MPA_ERR_ARG, "mpa_kv_write: null argument");
     MPA_REQUIRE(c->head_dim >= 2 && c->head_dim % 2 == 0, MPA_ERR_ARG, "mpa_kv_write: bad head_dim %d", c->head_dim);
+    if (int rc = check_cache(c, "mpa_kv_write")) return rc;
     if (n_tok <= 0 || c->n_ledgers <= 0) return 0;
     dim3 grid(n_tok, c->n_ledgers);
     const int threads = c->head_dim / 2 < 64 ? 32 : 64;
     cudaStream_t st = (cudaStream_t)stream;
+    const KvRows kv = kv_rows(c);
     if (c->dtype == MPA_F32)
         kv_write_kernel<float><<<grid, threads, 0, st>>>((float*)c->k_rot, (float*)c->k_raw, (float*)c->v, k_src,
-                                                         v_src, pos0, n_tok, c->tcap, c->head_dim, inv_freq);
+                                                         v_src, pos0, n_tok, c->tcap, c->head_dim, inv_freq, kv);
     else if (c->dtype == MPA_BF16)
         kv_write_kernel<__nv_bfloat16><<<grid, threads, 0, st>>>(
             (__nv_bfloat16*)c->k_rot, (__nv_bfloat16*)c->k_raw, (__nv_bfloat16*)c->v, k_src, v_src, pos0, n_tok,
-            c->tcap, c->head_dim, inv_freq);
+            c->tcap, c->head_dim, inv_freq, kv);
     else
         MPA_REQUIRE(false, MPA_ERR_ARG, "mpa_kv_write: bad dtype %d", c->dtype);
     return check_launch("mpa_kv_write");
@@ -235,19 +253,21 @@ extern "C" int mpa_kv_append(const mpa_cache* c, const float* k_src, const float
                 c->head_dim);
     MPA_REQUIRE(n_kv_heads >= 1 && c->n_ledgers % n_kv_heads == 0, MPA_ERR_ARG, "mpa_kv_append: n_kv_heads %d",
                 n_kv_heads);
+    if (int rc = check_cache(c, "mpa_kv_append")) return rc;
     if (n_tok <= 0 || c->n_ledgers <= 0) return 0;
     dim3 grid(n_tok, c->n_ledgers);
     const int threads = c->head_dim / 2 < 64 ? 32 : 64;
     const int n_seq = c->n_ledgers / n_kv_heads;
+    const KvRows kv = kv_rows(c);
     cudaStream_t st = (cudaStream_t)stream;
     if (c->dtype == MPA_F32)
         kv_append_kernel<float><<<grid, threads, 0, st>>>((float*)c->k_rot, (float*)c->k_raw, (float*)c->v, k_src,
                                                           v_src, n_kv_heads, n_seq, cache_len, ntok_dense, n_tok,
-                                                          c->tcap, c->head_dim, inv_freq, ticket);
+                                                          c->tcap, c->head_dim, inv_freq, ticket, kv);
     else if (c->dtype == MPA_BF16)
         kv_append_kernel<__nv_bfloat16><<<grid, threads, 0, st>>>(
             (__nv_bfloat16*)c->k_rot, (__nv_bfloat16*)c->k_raw, (__nv_bfloat16*)c->v, k_src, v_src, n_kv_heads, n_seq,
-            cache_len, ntok_dense, n_tok, c->tcap, c->head_dim, inv_freq, ticket);
+            cache_len, ntok_dense, n_tok, c->tcap, c->head_dim, inv_freq, ticket, kv);
     else
         MPA_REQUIRE(false, MPA_ERR_ARG, "mpa_kv_append: bad dtype %d", c->dtype);
     return check_launch("mpa_kv_append");

@@ -119,6 +119,7 @@ struct Params {
     __nv_bfloat16* k_raw;
     __nv_bfloat16* vcache;
     int tcap;
+    KvRows kv;                 // rows of k_rot / vcache (flat or paged); k_raw is [L, tcap, D]
     const float* k_new;        // [L, D]
     const float* v_new;
     int32_t* ntok_dense;       // [L] (optional)
@@ -444,11 +445,12 @@ step_kernel(const __grid_constant__ CUtensorMap tm_kc, const Params p) {
                     const float2 kk = *reinterpret_cast<const float2*>(p.k_new + (size_t)l * D + k);
                     const float2 vv = *reinterpret_cast<const float2*>(p.v_new + (size_t)l * D + k);
                     const double kx = (double)kk.x, ky = (double)kk.y;
-                    const size_t dst = ((size_t)l * p.tcap + qpos) * D + k;
+                    const size_t raw = ((size_t)l * p.tcap + qpos) * D + k;
+                    const size_t dst = (size_t)p.kv.row(l, qpos) * D + k;
                     p.k_rot[dst] = __double2bfloat16(__dsub_rn(__dmul_rn(kx, c2), __dmul_rn(ky, s2)));
                     p.k_rot[dst + 1] = __double2bfloat16(__dadd_rn(__dmul_rn(kx, s2), __dmul_rn(ky, c2)));
-                    p.k_raw[dst] = __double2bfloat16(kx);
-                    p.k_raw[dst + 1] = __double2bfloat16(ky);
+                    p.k_raw[raw] = __double2bfloat16(kx);
+                    p.k_raw[raw + 1] = __double2bfloat16(ky);
                     p.vcache[dst] = __double2bfloat16((double)vv.x);
                     p.vcache[dst + 1] = __double2bfloat16((double)vv.y);
                 }
@@ -961,6 +963,8 @@ extern "C" int mpa_decode_step(const float* q, const float* k_new, const float* 
     const int L = fine->n_ledgers;
     MPA_REQUIRE(cache->n_ledgers == L && n_kv_heads >= 1 && L % n_kv_heads == 0, MPA_ERR_ARG,
                 "%s: %d ledgers vs cache %d / %d kv-heads", what, L, cache->n_ledgers, n_kv_heads);
+    if (int rc = check_cache(cache, what)) return rc;
+    MPA_REQUIRE(!cache->block_table || cache->n_kv_heads == n_kv_heads, MPA_ERR_ARG, "%s: paged cache kv-heads", what);
     if (L <= 0) return 0;
     if (n_max <= 0 || n_max > fine->cap) n_max = fine->cap;
     CUtensorMap tk;
@@ -1002,6 +1006,7 @@ extern "C" int mpa_decode_step(const float* q, const float* k_new, const float* 
         prm.k_raw = (__nv_bfloat16*)cache->k_raw;
         prm.vcache = (__nv_bfloat16*)cache->v;
         prm.tcap = cache->tcap;
+        prm.kv = kv_rows(cache);
         prm.k_new = k_new;
         prm.v_new = v_new;
         prm.ntok_dense = ntok_dense;

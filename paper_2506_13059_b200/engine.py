@@ -33,7 +33,14 @@ from .ledger import DeviceLedgers, HostLedger
 class DecodeEngine:
     def __init__(self, cfg: EngineConfig, layout: HeadLayout, n_seq: int, tcap: int,
                  dtype: torch.dtype = torch.bfloat16, device="cuda", kcap: int | None = None,
-                 ccap: int | None = None, mode: str = "multipole", use_graphs: bool | None = None):
+                 ccap: int | None = None, mode: str = "multipole", use_graphs: bool | None = None,
+                 page_size: int | None = None, n_pages: int | None = None, page_order: str = "sequential"):
+        """page_size: serve K_rot / V from a paged pool (pipeline.py:26-52 `_KvStore` as the
+        block-table cache of a paged server): pools [n_pages, Hkv, page_size, d] (HND block layout:
+        a head's tokens contiguous inside a page), one block table row per sequence, pages taken
+        from a free list as sequences grow
+        ("shuffled" hands them out in random order, as a long-running server would).  K_raw, the
+        clustering view, stays [L, tcap, d]."""
         if not torch.cuda.is_available():
             raise RuntimeError("DecodeEngine needs a CUDA device (B200); there is no CPU fallback")
         _lib.lib()  # fail loudly if libmpattn.so is missing
@@ -49,9 +56,25 @@ class DecodeEngine:
         self.ccap = ccap or (max(16, 2 * (tcap // cfg.hierarchy.r1) + 64) if hier else 0)
         L, d, G, dev = self.L, self.d, self.G, self.device
         z = dict(device=dev)
-        self.k_rot = torch.zeros(L, tcap, d, dtype=dtype, **z)
         self.k_raw = torch.zeros(L, tcap, d, dtype=dtype, **z)
-        self.v = torch.zeros(L, tcap, d, dtype=dtype, **z)
+        self.page_size = page_size
+        if page_size is None:
+            self.k_rot = torch.zeros(L, tcap, d, dtype=dtype, **z)
+            self.v = torch.zeros(L, tcap, d, dtype=dtype, **z)
+            self.block_table = None
+        else:
+            if page_size < 1 or page_size & (page_size - 1):
+                raise ConfigError(f"page_size {page_size} must be a power of two")
+            self.pages_per_seq = -(-tcap // page_size)
+            self.n_pages = n_pages or n_seq * self.pages_per_seq
+            self.k_rot = torch.zeros(self.n_pages, self.Hkv, page_size, d, dtype=dtype, **z)
+            self.v = torch.zeros(self.n_pages, self.Hkv, page_size, d, dtype=dtype, **z)
+            self.block_table = torch.zeros(n_seq, self.pages_per_seq, dtype=torch.int32, **z)
+            self._bt_host = np.full((n_seq, self.pages_per_seq), -1, np.int64)
+            free = np.arange(self.n_pages)
+            if page_order == "shuffled":
+                free = np.random.default_rng(cfg.seed).permutation(free)
+            self._free_pages = list(free[::-1])  # pop() hands out free[0] first
         self.led = DeviceLedgers(L, d, tcap, self.kcap, self.ccap, dtype, hier, dev)
         self.inv_freq = torch.as_tensor(inv_freq(d, cfg.rope_theta), dtype=torch.float64, device=dev)
         # (cos, sin) of the lookup view's fixed angles delta * inv_freq (rope.py:66-68, numpy like the
@@ -94,7 +117,12 @@ class DecodeEngine:
         self.stats = torch.zeros(4, L, dtype=torch.int32, **z)
         self.ws = torch.zeros(0, dtype=torch.uint8, **z)  # fused-kernel workspace (grown on demand)
         self.out = torch.zeros(n_seq, self.Hq, d, dtype=torch.float32, **z)
-        self.cache_struct = MpaCache(ptr(self.k_rot), ptr(self.k_raw), ptr(self.v), dtype_code(dtype), L, tcap, d)
+        if self.block_table is None:
+            self.cache_struct = MpaCache(ptr(self.k_rot), ptr(self.k_raw), ptr(self.v), dtype_code(dtype), L, tcap, d,
+                                         None, 0, 0, 0, self.Hkv)
+        else:
+            self.cache_struct = MpaCache(ptr(self.k_rot), ptr(self.k_raw), ptr(self.v), dtype_code(dtype), L, tcap, d,
+                                         ptr(self.block_table), page_size, self.pages_per_seq, self.n_pages, self.Hkv)
         self.last_split = 1
         self.cursor = 0
         # the flat serving path (fused_lookup_path) hands the fused kernel a contiguous-centroid
@@ -108,18 +136,55 @@ class DecodeEngine:
         self.last_update: dict | None = None
 
     # ------------------------------------------------------------------ KV cache
+    def reserve(self, n: int) -> None:
+        """Capacity for n more tokens in every sequence: the logical bound, and (paged) the pages
+        they land in, taken from the free list and published in the block table."""
+        if int(self.cache_len.max()) + n > self.tcap:
+            raise RuntimeError(f"KV cache capacity {self.tcap} exceeded")
+        if self.block_table is None:
+            return
+        ps, new = self.page_size, []
+        for s in range(self.n_seq):
+            for pg in range(int(self.cache_len[s]) // ps, -(-(int(self.cache_len[s]) + n) // ps)):
+                if self._bt_host[s, pg] < 0:
+                    if not self._free_pages:
+                        raise RuntimeError(f"KV page pool of {self.n_pages} pages exhausted")
+                    self._bt_host[s, pg] = self._free_pages.pop()
+                    new.append((s, pg))
+        if new:
+            s_i, p_i = zip(*new)
+            self.block_table[list(s_i), list(p_i)] = torch.as_tensor(self._bt_host[list(s_i), list(p_i)],
+                                                                      dtype=torch.int32, device=self.device)
+
+    def kv_rows(self, l: int, t) -> torch.Tensor:
+        """Rows of tokens t (int64 tensor or array) of ledger l in k_rot / v viewed as [-1, d]."""
+        t = torch.as_tensor(t, dtype=torch.int64, device=self.device)
+        if self.block_table is None:
+            return l * self.tcap + t
+        s, h, ps = l // self.Hkv, l % self.Hkv, self.page_size
+        page = self.block_table[s].to(torch.int64)[t // ps]
+        return (page * self.Hkv + h) * ps + t % ps
+
+    def values(self, l: int, t) -> torch.Tensor:
+        """Cached values of tokens t of ledger l, [len(t), d] in the cache dtype."""
+        return self.v.view(-1, self.d)[self.kv_rows(l, t)]
+
+    def keys_rotated(self, l: int, t) -> torch.Tensor:
+        return self.k_rot.view(-1, self.d)[self.kv_rows(l, t)]
+
     def write_tokens(self, k: torch.Tensor, v: torch.Tensor, pos0: torch.Tensor | None = None) -> None:
         """Write n new tokens per ledger: k, v fp32 [n_seq, Hkv, n, d] (device) at cache_len."""
         n = k.shape[2]
         k = k.reshape(self.L, n, self.d).float().contiguous()
         v = v.reshape(self.L, n, self.d).float().contiguous()
         if pos0 is None:
-            if int(self.cache_len.max()) + n > self.tcap:
-                raise RuntimeError(f"KV cache capacity {self.tcap} exceeded")
+            self.reserve(n)
             # positions and the length counters advance on the device (one launch)
             call("mpa_kv_append", self.cache_struct, ptr(k), ptr(v), self.Hkv, n, ptr(self.cache_len_d),
                  ptr(self.ntok_dense_d), ptr(self.inv_freq), ptr(self.append_ticket), stream_ptr())
         else:
+            if self.block_table is not None:
+                raise ConfigError("explicit write positions need a flat cache")
             call("mpa_kv_write", self.cache_struct, ptr(k), ptr(v), ptr(pos0), n, ptr(self.inv_freq), stream_ptr())
             self.cache_len_d += n
             self.ntok_dense_d += n
@@ -390,8 +455,7 @@ class DecodeEngine:
         from . import clustering
 
         if self._graphable():
-            if int(self.cache_len.max()) + 1 > self.tcap:
-                raise RuntimeError(f"KV cache capacity {self.tcap} exceeded")
+            self.reserve(1)
             self._cluster_bounds()  # recaptures only if the cluster counts outgrew the captured bounds
             if self._graph is None:
                 self._capture_step()
@@ -415,8 +479,7 @@ class DecodeEngine:
             if host:
                 q, k_new, v_new = (x.to(self.device, non_blocking=True) for x in (q, k_new, v_new))
             if self.fused_lookup_path() and self.mode != "oracle":
-                if int(self.cache_len.max()) + 1 > self.tcap:
-                    raise RuntimeError(f"KV cache capacity {self.tcap} exceeded")
+                self.reserve(1)
                 self.lookup_step(q, k_new, v_new)
                 out = self.fused()
                 self.cache_len += 1

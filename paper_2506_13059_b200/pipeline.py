@@ -77,7 +77,7 @@ class _KvStoreView:
 
     @property
     def values(self) -> np.ndarray:
-        return self._eng.v[self._h, : self.n].float().cpu().numpy()
+        return self._eng.values(self._h, torch.arange(self.n)).float().cpu().numpy()
 
 
 def prefill(trace: KvTrace, cfg: EngineConfig, mode: str = "multipole", dtype: torch.dtype = torch.float64,
@@ -123,7 +123,7 @@ def _attend_fp64(state: EngineState, queries, oracle: bool, timers):
     eng, lay, cfg = state.engine, state.trace.layout, state.cfg
     n = int(eng.cache_len[0])
     keys = eng.k_raw[:, :n].double().cpu().numpy()
-    values = eng.v[:, :n].double().cpu().numpy()
+    values = torch.stack([eng.values(l, torch.arange(n)) for l in range(eng.L)]).double().cpu().numpy()
     q = np.asarray(queries)
     if state.mode == "oracle":
         params = RopeParams(head_dim=lay.head_dim, theta=cfg.rope_theta, window_offset=cfg.window_offset)
