@@ -160,6 +160,11 @@ int mpa_hier_candidates(const mpa_level* coarse, const uint8_t* cflag, int n_led
  * lists were cut, then the last CTA advances cache_len[s] and ntok_dense[l] (optional) by one
  * (ticket: one int32 workspace, zero-initialised once, left zeroed).
  * n_max bounds every ledger's cluster count (0: cap). */
+/* 1 if mpa_decode_step can run n_ledgers ledgers of up to n_max centroids on the current device
+ * (one co-resident wave of clusters, each CTA's slice within its shared-memory schedule), else 0 --
+ * callers then take the staged kernels (mpa_centroid_logits + mpa_select_worklist). */
+int mpa_decode_step_fits(int n_ledgers, int group, int n_max);
+
 int mpa_decode_step(const float* q, const float* k_new, const float* v_new, const mpa_cache* cache,
                     const double* cs_lk, const double* inv_freq, int n_kv_heads, int group,
                     const mpa_level* fine, const int64_t* budget, const int32_t* sink_end,

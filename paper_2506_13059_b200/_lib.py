@@ -62,6 +62,7 @@ _SIGS = {
     "mpa_select_worklist": [C.POINTER(MpaLevel), C.POINTER(MpaLevel), C.c_int, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp,
                             _vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int, _vp, _vp,
                             C.c_int, _vp, C.c_int, _vp],
+    "mpa_decode_step_fits": [C.c_int, C.c_int, C.c_int],
     "mpa_decode_step": [_vp, _vp, _vp, C.POINTER(MpaCache), _vp, _vp, C.c_int, C.c_int, C.POINTER(MpaLevel), _vp,
                         _vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp, C.c_int, _vp, _vp, C.c_int,
                         _vp],

@@ -944,6 +944,23 @@ extern "C" int mpa_debug_trace_step(unsigned long long* host, int n) {
 }
 #endif
 
+// whether mpa_decode_step can run n_ledgers ledgers of up to n_max centroids on this device: every
+// cluster of the one-wave grid co-resident and each CTA's slice within its shared-memory schedule
+extern "C" int mpa_decode_step_fits(int n_ledgers, int group, int n_max) {
+    if (n_ledgers <= 0) return 1;
+    if (group < 3 || group > 8) return 0;
+    int ok = 0;
+    [&]() -> int {
+        MPA_DISPATCH_G3(group, {
+            int kc = 0;
+            const int C = pick_cluster<kG>(n_ledgers, n_max, &kc);
+            ok = (size_t)C * kc >= (size_t)(n_max > 0 ? n_max : 1) && kc <= stp::Geo<kG>::kcmax;
+        });
+        return 0;
+    }();
+    return ok;
+}
+
 extern "C" int mpa_decode_step(const float* q, const float* k_new, const float* v_new, const mpa_cache* cache,
                                const double* cs_lk, const double* inv_freq, int n_kv_heads, int group,
                                const mpa_level* fine, const int64_t* budget, const int32_t* sink_end,

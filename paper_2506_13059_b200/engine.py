@@ -246,10 +246,16 @@ class DecodeEngine:
         return self._bf, self._bc
 
     def fused_lookup_path(self) -> bool:
-        """The flat serving step (bf16 cache and centroids, d = 128, G <= 8) runs as ONE launch
-        (mpa_decode_step); hierarchical, fp32 (parity) and d != 128 steps use the staged kernels."""
-        return (self.cfg.hierarchy is None and self.dtype == torch.bfloat16 and self.d == 128 and 3 <= self.G <= 8
-                and not self.led.lookup_f64)
+        """The flat serving step (bf16 cache and centroids, d = 128, 3 <= G <= 8) runs as ONE launch
+        (mpa_decode_step) when its cluster grid fits the device in one wave; hierarchical, fp32
+        (parity), d != 128 and oversized (ledgers x centroids) steps use the staged kernels."""
+        if not (self.cfg.hierarchy is None and self.dtype == torch.bfloat16 and self.d == 128 and 3 <= self.G <= 8
+                and not self.led.lookup_f64):
+            return False
+        bound = self._cluster_bounds()[0]  # the cluster bound the step is launched with
+        if getattr(self, "_fits_for", None) != bound:
+            self._fits_for, self._fits = bound, bool(_lib.lib().mpa_decode_step_fits(self.L, self.G, bound))
+        return self._fits
 
     def lookup_step(self, q: torch.Tensor, k_new: torch.Tensor | None = None,
                     v_new: torch.Tensor | None = None) -> None:
@@ -270,10 +276,17 @@ class DecodeEngine:
              replacement, ptr(self.flag), ptr(self.sel_tokens), ptr(self.tok), self.tok_cap, ptr(self.stats),
              self._bound_fine, ptr(self.q_rot), ptr(self.rej_w) if replacement else None, self.rej_cap, stream_ptr())
 
+    def _contiguous_ok(self) -> bool:
+        """Flat level, bf16 centroids, d = 128, G <= 8: the fused decode kernel takes the
+        contiguous-centroid list (every fine centroid in order, the selected ones weighted -inf)."""
+        return (self.cfg.hierarchy is None and self.dtype == torch.bfloat16 and self.d == 128 and self.G <= 8
+                and not self.led.lookup_f64)
+
     def lookup(self, q: torch.Tensor, staged: bool = False) -> None:
         """K9 + K10 + work lists (flat or hierarchical) for the fp32 queries q [n_seq, Hq, d].  On the
         flat serving path this is the single-launch decode step (the output included) unless
-        `staged` asks for the separate logits / selection kernels and a rejected-centroid list."""
+        `staged` asks for the separate logits / selection kernels (the same lists; the path every
+        step takes when the single launch does not fit the device)."""
         st = stream_ptr()
         self._bound_fine, self._bound_coarse = self._cluster_bounds()
         G, L = self.G, self.L
@@ -281,7 +294,6 @@ class DecodeEngine:
         replacement = 0 if self.mode == "flat-no-replacement" else 1
         if self.cfg.hierarchy is None and int(self.led.n_fine.min()) == 0:
             raise ConfigError("ledger has no clusters")
-        self._staged = staged
         if self.fused_lookup_path() and not staged:  # one launch (the exact view included)
             self.lookup_step(q)
             return
@@ -291,14 +303,18 @@ class DecodeEngine:
         # e^(l - chunk max) from the logits kernel (bf16 serving centroids only)
         el = self.elocal if (tiled and not self.led.lookup_f64) else None
         if self.cfg.hierarchy is None:
+            # contiguous-centroid list: the logits kernel writes every centroid's replacement weight
+            # (no fp64 logits array), the selection masks the selected ones (no rejected list)
+            contig = self._contiguous_ok()
+            lg = None if contig else self.logits
             call("mpa_centroid_logits", ptr(self.q_lk), self.Hkv, G, self.d, fine, None,
-                 None, self.kcap, ptr(self.logits), ptr(cs), ptr(el), self._bound_fine, None,
+                 None, self.kcap, ptr(lg), ptr(cs), ptr(el), self._bound_fine, ptr(self.rej_w) if contig else None,
                  self.rej_cap, None, None, st)
-            call("mpa_select_worklist", fine, None, G, ptr(self.logits), ptr(el), None, None, self.kcap, ptr(cs),
+            call("mpa_select_worklist", fine, None, G, ptr(lg), ptr(el), None, None, self.kcap, ptr(cs),
                  None, None,
                  ptr(self.budget), ptr(self.sink_end_d), ptr(self.buffer_start_d), ptr(self.cache_len_d), self.Hkv,
                  L, replacement, ptr(self.flag), ptr(self.sel_tokens), ptr(self.tok), self.tok_cap,
-                 ptr(self.rej), ptr(self.rej_w), self.rej_cap, ptr(self.stats), self._bound_fine,
+                 None if contig else ptr(self.rej), ptr(self.rej_w), self.rej_cap, ptr(self.stats), self._bound_fine,
                  st)
         else:
             if int(self.led.n_coarse.min()) == 0:
@@ -339,7 +355,7 @@ class DecodeEngine:
         if self.mode == "flat-no-replacement":
             return None, None, None
         if contiguous is None:
-            contiguous = self.fused_lookup_path() and not getattr(self, "_staged", False)
+            contiguous = self._contiguous_ok()
         if contiguous:
             return None, self.rej_w, self.led.count
         return self.rej, self.rej_w, self.stats[1]

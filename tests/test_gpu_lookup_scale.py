@@ -125,3 +125,37 @@ def test_c2_selection_budget_edges(budget):
         assert all(h.selected_tokens == 0 for h in rep.per_head)
     if budget == 10**9:
         assert all(h.rejected_centroids == 0 for h in rep.per_head)
+
+
+def test_c2_staged_lookup_matches_single_launch():
+    # the staged kernels (logits -> selection -> lists, taken when the single-launch step does not
+    # fit the device, e.g. C5's 8K centroids per ledger at batch 16) produce the same lists and outputs
+    from paper_2506_13059_b200.engine import DecodeEngine
+
+    cfg = EngineConfig(block_size=8192, alpha=4096, local_buffer=128, sink_tokens=10, tokens_per_centroid=16,
+                       token_budget=512, rope_theta=1e6, seed=11)
+    rng = np.random.default_rng(11)
+    heads = [_ledger(rng, CTX, cfg) for _ in range(LAY.num_kv_heads)]
+    eng = DecodeEngine(cfg, LAY, 2, tcap=CTX + 8, dtype=torch.bfloat16,
+                       kcap=max(O._flat(x[2], False)[2].size for x in heads) + 64)
+    k = torch.as_tensor(np.stack([h[0] for h in heads])).cuda()[None].expand(2, -1, -1, -1)
+    v = torch.as_tensor(np.stack([h[1] for h in heads])).cuda()[None].expand(2, -1, -1, -1)
+    eng.write_tokens(k, v)
+    eng.load_ledgers([to_host(h[2]) for h in heads] * 2)
+    q = torch.as_tensor(rng.standard_normal((2, LAY.num_q_heads, LAY.head_dim)).astype(np.float32)).cuda()
+    assert eng.fused_lookup_path()
+    out1 = eng.attend(q).clone()
+    st1, tok1, w1 = eng.stats.clone(), eng.tok.clone(), eng.rej_w.clone()
+    eng.rotate(q, exact=True, lookup=False)
+    eng.lookup(q, staged=True)
+    out2 = eng.fused().clone()
+    assert torch.equal(st1, eng.stats)
+    for l in range(eng.L):
+        n = int(st1[0, l])
+        assert torch.equal(tok1[l, :n].sort().values, eng.tok[l, :n].sort().values), l
+    kc = int(eng.led.count.max())
+    a, b = w1[:, :kc].cpu().numpy(), eng.rej_w[:, :kc].cpu().numpy()
+    assert np.array_equal(np.isinf(a), np.isinf(b))  # the same selected rows
+    fin = np.isfinite(a)
+    assert np.allclose(a[fin], b[fin], rtol=1e-6, atol=1e-6)
+    assert rel_err(out1.cpu().numpy(), out2.cpu().numpy()).max() < 1e-5
