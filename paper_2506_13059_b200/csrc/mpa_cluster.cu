@@ -19,6 +19,7 @@
 #include <cub/block/block_radix_sort.cuh>
 
 #include <cstdlib>
+#include <map>
 
 #include "mpa_common.cuh"
 
@@ -663,6 +664,49 @@ km_write_level_kernel(mpa_km km, const TV* __restrict__ vals, KvRows vrow, const
     }
     if (lane == 0) size[crow] = nsum;
     const double* src = km.cent + (size_t)(km.c_off[p] + j) * d;
+    auto store = [&](int k, double kv, double vv) {
+        kc64[crow * d + k] = kv;
+        vc64[crow * d + k] = vv;
+        if (serve_dtype == MPA_BF16) {
+            store_serve<__nv_bfloat16>(kc, crow * d + k, kv);
+            store_serve<__nv_bfloat16>(vc, crow * d + k, vv);
+        } else {
+            store_serve<float>(kc, crow * d + k, kv);
+            store_serve<float>(vc, crow * d + k, vv);
+        }
+    };
+    if (!hier && (d & 3) == 0) {
+        // value means (fill_value_centroids): lane = four consecutive coordinates, member rows
+        // fetched kMeansBatch at a time ahead of the ordered fp64 adds (cf. km_means_kernel)
+        for (int k0 = 0; k0 < d; k0 += 128) {
+            const int k = k0 + lane * 4;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            int nxt[kMeansBatch];
+#pragma unroll
+            for (int u = 0; u < kMeansBatch; ++u) nxt[u] = u < c ? __ldg(ord + u) : -1;
+            for (int m0 = 0; m0 < c; m0 += kMeansBatch) {
+                int ii[kMeansBatch];
+                Row4<TV> xv[kMeansBatch];
+#pragma unroll
+                for (int u = 0; u < kMeansBatch; ++u) {
+                    ii[u] = nxt[u];
+                    if (ii[u] >= 0 && k < d) xv[u].load(vals, (size_t)vrow.row(l, start + ii[u]) * d + k);
+                }
+#pragma unroll
+                for (int u = 0; u < kMeansBatch; ++u)
+                    nxt[u] = m0 + kMeansBatch + u < c ? __ldg(ord + m0 + kMeansBatch + u) : -1;
+#pragma unroll
+                for (int u = 0; u < kMeansBatch; ++u)
+                    if (ii[u] >= 0 && k < d)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) acc[e] = __dadd_rn(acc[e], xv[u].get(e));
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (k + e < d) store(k + e, src[k + e], __ddiv_rn(acc[e], (double)c));
+        }
+        return;
+    }
     for (int k = lane; k < d; k += 32) {
         double kv, vv;
         if (!hier) {
@@ -683,15 +727,7 @@ km_write_level_kernel(mpa_km km, const TV* __restrict__ vals, KvRows vrow, const
             kv = __ddiv_rn(ak, (double)nsum);
             vv = __ddiv_rn(av, (double)nsum);
         }
-        kc64[crow * d + k] = kv;
-        vc64[crow * d + k] = vv;
-        if (serve_dtype == MPA_BF16) {
-            store_serve<__nv_bfloat16>(kc, crow * d + k, kv);
-            store_serve<__nv_bfloat16>(vc, crow * d + k, vv);
-        } else {
-            store_serve<float>(kc, crow * d + k, kv);
-            store_serve<float>(vc, crow * d + k, vv);
-        }
+        store(k, kv, vv);
     }
 }
 
@@ -950,20 +986,48 @@ extern "C" int mpa_km_lloyd(const mpa_km* km, int32_t* rounds_out, void* stream)
     int rounds = 0, last = -1;
     const bool tc = mpa_km_tc_applies(k);
     int rc = 0;
-    for (int r = 0; r < k.min_iters + kMaxExtraRounds + 2; ++r) {
+    auto enqueue_round = [&](cudaStream_t s) -> int {
         if (tc) {
-            rc = mpa_km_assign_tc(k, st);
+            if (int r2 = mpa_km_assign_tc(k, s)) return r2;
         } else {
-            km_assign_kernel<<<dim3(ceil_div(k.n_max, kAsgBM), P), kAsgThreads, 0, st>>>(k);
+            km_assign_kernel<<<dim3(ceil_div(k.n_max, kAsgBM), P), kAsgThreads, 0, s>>>(k);
         }
-        if (!rc) rc = launch_round(k, 0, st);
+        if (int r2 = launch_round(k, 0, s)) return r2;
+        launch_means(k, 0, s);
+        km_c2_kernel<<<dim3(ceil_div(k.k_max, 128), P), 128, 0, s>>>(k, 1);
+        km_any_active_kernel<<<1, 256, 0, s>>>(k, k.flag);
+        return check_launch("mpa_km_lloyd(round)");
+    };
+    // Rounds after the first replay one captured CUDA graph (a round is ~15 launches whose
+    // arguments never change): captured on a private stream ordered after / before `st`.
+    int dev = 0;
+    cudaGetDevice(&dev);
+    thread_local std::map<int, cudaStream_t> side_streams;
+    cudaStream_t side = side_streams[dev];
+    if (!side) {
+        cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+        side_streams[dev] = side;
+    }
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    cudaEvent_t join;
+    cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+    cudaEventRecord(join, st);  // the rounds run on `side` after the set-up above
+    cudaStreamWaitEvent(side, join, 0);
+    for (int r = 0; r < k.min_iters + kMaxExtraRounds + 2; ++r) {
+        if (r == 1) {  // capture once the first round has set every kernel attribute
+            if (cudaStreamBeginCapture(side, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+                const int crc = enqueue_round(side);
+                const cudaError_t ce = cudaStreamEndCapture(side, &graph);
+                if (crc || ce != cudaSuccess || cudaGraphInstantiate(&gexec, graph, 0) != cudaSuccess) gexec = nullptr;
+            }
+            cudaGetLastError();  // a failed capture falls back to eager rounds
+        }
+        if (gexec) rc = cudaGraphLaunch(gexec, side) == cudaSuccess ? 0 : (int)cudaErrorLaunchFailure;
+        else rc = enqueue_round(side);
         if (rc) break;
-        launch_means(k, 0, st);
-        km_c2_kernel<<<dim3(ceil_div(k.k_max, 128), P), 128, 0, st>>>(k, 1);
-        km_any_active_kernel<<<1, 256, 0, st>>>(k, k.flag);
-        if ((rc = check_launch("mpa_km_lloyd(round)"))) break;
-        cudaError_t e = cudaMemcpyAsync(ring + 2 * (r % kRing), k.flag, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaEventRecord(ev[r % kRing], st);
+        cudaError_t e = cudaMemcpyAsync(ring + 2 * (r % kRing), k.flag, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, side);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[r % kRing], side);
         if (e == cudaSuccess && r >= 1) e = cudaEventSynchronize(ev[(r - 1) % kRing]);
         if (e != cudaSuccess) {
             set_error("mpa_km_lloyd: %s", cudaGetErrorString(e));
@@ -981,7 +1045,12 @@ extern "C" int mpa_km_lloyd(const mpa_km* km, int32_t* rounds_out, void* stream)
         }
         rounds = ring[2 * (last % kRing) + 1];
     }
+    cudaEventRecord(join, side);  // `st` resumes after the last round
+    cudaStreamWaitEvent(st, join, 0);
     cleanup();
+    cudaEventDestroy(join);
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (graph) cudaGraphDestroy(graph);
     if (rc) return rc;
     // final grouping for compaction (counts / order / cstart of the returned assignment)
     if (int rc2 = launch_round(k, 1, st)) return rc2;
