@@ -214,11 +214,8 @@ def reference_arm(args, rank, world):
     lay, _ = workload_cfg(args)
     cfg = REngineConfig(token_budget=args.budget, tokens_per_centroid=16, rope_theta=1e6, seed=0)
     one = RHeadLayout(lay.group_size, 1, lay.head_dim)
-    gen = torch.Generator().manual_seed(0)
     ctx = args.ctx
-    keys = torch.randn(ctx, lay.head_dim, generator=gen).numpy()
-    values = torch.randn(ctx, lay.head_dim, generator=gen).numpy()
-    qs = torch.randn(args.steps + args.warmup, lay.group_size, lay.head_dim, generator=gen).numpy()
+    keys, values, qs, data = _ledger0_inputs(args, lay)
     t0 = time.perf_counter()
     led = RC.build_prefill_index_head(keys, values, ctx, cfg, 0)
     prefill_s = time.perf_counter() - t0
@@ -239,9 +236,11 @@ def reference_arm(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": us, "unit": "us/step", "n_gpus": world,
         "steps": len(samples), "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1) Q/K/V",
-        "config": {"workload": f"C2 Qwen3-8B attention shape (32q/8kv/d128), {ctx} ctx, r=16, B={args.budget}, "
-                               f"batch {args.batch}", "batch": args.batch, "ctx": ctx, "budget": args.budget},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": data,
+        "config": {"workload": workload_label(args, 1), "batch": args.batch, "ctx": ctx, "budget": args.budget},
+        "extrapolated": {"measured": "1 sequence x 1 kv-head ledger (4 q-heads)", "scaled_by": n_led,
+                         "why": "the reference loops kv-heads and sequences serially (attention.py:450); the "
+                                "whole batch would take minutes per step on the host"},
         "cpu_baseline": {"value": us, "unit": "us/step", "cores": cores, "kind": kind,
                          "sample": f"{len(samples)} reference decode_step_attention calls on 1 sequence x 1 "
                                    f"kv-head (4 q-heads), ledger from the reference build_prefill_index_head "
@@ -252,6 +251,37 @@ def reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def _ledger0_inputs(args, lay):
+    """Keys / values of ledger (sequence 0, kv-head 0) and its queries, drawn exactly as our arm
+    draws them (bench.build_engine: the CUDA generator seeded 1000 + rank, every sequence's K then V,
+    then the queries) when a GPU is present, so both arms time the same data."""
+    import torch
+
+    b, ctx, d, Hkv, Hq, G = args.batch, args.ctx, lay.head_dim, lay.num_kv_heads, lay.num_q_heads, lay.group_size
+    if torch.cuda.is_available():
+        dev = torch.device("cuda", 0)
+        gen = torch.Generator(device=dev).manual_seed(1000)
+        keys = values = None
+        for s in range(b):
+            k = torch.randn(1, Hkv, ctx, d, generator=gen, device=dev)
+            v = torch.randn(1, Hkv, ctx, d, generator=gen, device=dev)
+            if s == 0:
+                # the GPU arm stores bf16 keys / values: the reference gets the same (exact in fp64) values
+                keys = k[0, 0].to(torch.bfloat16).double().cpu().numpy()
+                values = v[0, 0].to(torch.bfloat16).double().cpu().numpy()
+            del k, v
+        total = max(3, args.warmup) + args.steps + CALIB_STEPS
+        Q = torch.randn(total + args.steps, b, Hq, d, generator=gen, device=dev)
+        qs = Q[:, 0, :G].double().cpu().numpy()
+        return keys, values, qs, ("synthetic N(0,1) Q/K/V: sequence 0 / kv-head 0 of the GPU arm's data (same "
+                                  "generator and draw order, keys / values as stored in bf16)")
+    gen = torch.Generator().manual_seed(0)
+    keys = torch.randn(ctx, d, generator=gen).double().numpy()
+    values = torch.randn(ctx, d, generator=gen).double().numpy()
+    qs = torch.randn(args.steps + args.warmup, G, d, generator=gen).double().numpy()
+    return keys, values, qs, "synthetic N(0,1) Q/K/V (CPU generator: no GPU to reproduce the GPU arm's draw)"
+
+
 def reference_arm_port(args, rank, world):
     """--impl reference without baseline/_ref: the oracle port (pinned bit-exact to the reference
     by tests/test_golden_oracle.py) on one ledger, scaled to the batch."""
@@ -260,11 +290,8 @@ def reference_arm_port(args, rank, world):
     from oracle import mpa_oracle as O
 
     lay, cfg = workload_cfg(args)
-    gen = torch.Generator().manual_seed(0)
     ctx = args.ctx
-    keys = torch.randn(ctx, lay.head_dim, generator=gen).numpy()
-    values = torch.randn(ctx, lay.head_dim, generator=gen).numpy()
-    qs = torch.randn(args.steps + args.warmup, lay.group_size, lay.head_dim, generator=gen).numpy()
+    keys, values, qs, data = _ledger0_inputs(args, lay)
     t0 = time.perf_counter()
     led = O.prefill_ledger(keys, values, ctx, cfg, 0)
     prefill_s = time.perf_counter() - t0
@@ -283,9 +310,9 @@ def reference_arm_port(args, rank, world):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": us, "unit": "us/step", "n_gpus": world,
         "steps": len(samples), "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1) Q/K/V",
-        "config": {"workload": f"C2 Qwen3-8B attention shape (32q/8kv/d128), {ctx} ctx, r=16, B={args.budget}, "
-                               f"batch {args.batch}", "batch": args.batch, "ctx": ctx, "budget": args.budget},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": data,
+        "config": {"workload": workload_label(args, 1), "batch": args.batch, "ctx": ctx, "budget": args.budget},
+        "extrapolated": {"measured": "1 sequence x 1 kv-head ledger (4 q-heads)", "scaled_by": n_led},
         "cpu_baseline": {"value": us, "unit": "us/step", "cores": _blas_threads(), "kind": "port",
                          "sample": f"{len(samples)} oracle decode steps of 1 sequence x 1 kv-head (baseline/_ref "
                                    f"absent), ledger built in {prefill_s:.1f}s; scaled x{n_led} ledgers"},
