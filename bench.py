@@ -506,6 +506,7 @@ def main():
     e2e_avg = float(np.mean(e2e_ms))
     h2d = (qh[0].numel() + kh[0].numel() + vh[0].numel()) * 4
     d2h = oh.numel() * 4
+    dropin = None if (args.profile or args.workload != "c2" or world > 1) else dropin_step(args, lay, cfg, K)
 
     # ---- online cluster update events (C4-style overhead, amortised over L steps): the first one
     # in the process also pays one-time lazy CUDA module loads, so two events run and the second,
@@ -581,7 +582,9 @@ def main():
                        "amortized_us_per_step": update_ms * 1e3 / L,
                        "pct_of_step": update_ms / L / ms_step * 100.0, "lloyd_rounds": upd["rounds"],
                        "prefill_s": prefill_s},
-            "e2e": {"value": e2e_avg * 1e3, "unit": "us/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_avg * 1e3, "unit": "us/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "engine.DecodeEngine.step_host (batched public API, pinned host buffers)"},
+            "e2e_dropin": dropin,
             "graph_captures": eng.n_captures,
             "gpu_launches": (3 if eng.fused_lookup_path() else 7) * K,  # per step: input staging + the
                                     # step graph (flat bf16 path: lookup + append, fused decode; else 2
@@ -721,6 +724,39 @@ class L2Flush:
     def __call__(self, i):
         self.w.fill_(float(i))
         self.acc += self.r.sum()
+
+
+def dropin_step(args, lay, cfg, K):
+    """The reference's own call, paper_2506_13059_b200.step(state, q, k, v) (pipeline.py:124): one
+    sequence (its signature has no batch) of the workload's shape and context, bf16 serving cache,
+    numpy inputs in, fp64 outputs + the DecodeReport (selected refs / tokens per head) out, timed by
+    wall clock around each call (every call ends with its host reads)."""
+    import torch
+
+    import paper_2506_13059_b200 as mpa
+
+    ctx, d = args.ctx, lay.head_dim
+    n = ctx + K + 4
+    g = torch.Generator(device="cuda").manual_seed(7)
+    keys = torch.randn(lay.num_kv_heads, n, d, generator=g, device="cuda").cpu().numpy()
+    values = torch.randn(lay.num_kv_heads, n, d, generator=g, device="cuda").cpu().numpy()
+    queries = torch.randn(lay.num_q_heads, K + 4, d, generator=g, device="cuda").cpu().numpy()
+    trace = mpa.KvTrace(lay, ctx, keys, values, queries)
+    state = mpa.prefill(trace, cfg, dtype=torch.bfloat16)
+    ms = []
+    for t in range(K + 3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        mpa.step(state, queries[:, t], keys[:, ctx + t], values[:, ctx + t])
+        if t >= 3:
+            ms.append((time.perf_counter() - t0) * 1e3)
+    del state
+    torch.cuda.empty_cache()
+    return {"value": float(np.mean(ms)) * 1e3, "unit": "us/step", "batch": 1,
+            "api": "paper_2506_13059_b200.step(state, q, k, v) -- the reference's pipeline.step signature "
+                   "(one sequence, numpy in, fp64 outputs + DecodeReport out), bf16 cache, wall clock",
+            "h2d_bytes_per_step": int((lay.num_q_heads + 2 * lay.num_kv_heads) * d * 4),
+            "d2h_bytes_per_step": int(lay.num_q_heads * d * 4)}
 
 
 def _write_seq(eng, s, k, v):

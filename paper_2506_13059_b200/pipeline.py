@@ -107,11 +107,15 @@ def _refs(eng: DecodeEngine, h: int, flag: np.ndarray, cand: np.ndarray | None) 
     else:
         n = int(eng.n_cand[h]) if cand is None else cand.size
         ids = np.sort(cand[flag[:n] == 1])
-    out = []
-    for r_i, row in enumerate(led.blocks[h]):
-        for g in ids[(ids >= row.f0) & (ids < row.f0 + row.fk)]:
-            out.append((r_i, int(g - row.f0), 2))
-    return out
+    rows = led.blocks[h]
+    if not rows or ids.size == 0:
+        return []
+    f0 = np.fromiter((row.f0 for row in rows), np.int64, len(rows))
+    fk = np.fromiter((row.fk for row in rows), np.int64, len(rows))
+    bi = np.searchsorted(f0, ids, side="right") - 1  # block of each selected fine id (blocks ascend)
+    keep = (bi >= 0) & (ids < f0[np.maximum(bi, 0)] + fk[np.maximum(bi, 0)])
+    bi, loc = bi[keep], ids[keep] - f0[bi[keep]]
+    return list(zip(bi.tolist(), loc.tolist(), [2] * int(bi.size)))
 
 
 def _attend_fp64(state: EngineState, queries, oracle: bool, timers):
@@ -158,19 +162,45 @@ def _attend_engine(state: EngineState, queries, oracle: bool):
         ev[1].record()
         out_t = eng.fused()
     ev[2].record()
-    out = out_t[0].double().cpu().numpy()
+    H = lay.num_kv_heads
+    flat = state.mode != "oracle" and eng.cfg.hierarchy is None
+    # one batched device -> host read (pinned, non-blocking) of everything the report needs: the
+    # output, the per-head counters, the token lists (bounded by sinks + buffer + budget + the largest
+    # cluster, which every list fits) and the selection flags
+    kf = max(int(eng.led.n_fine[:H].max(initial=0)), 1)
+    tb = min(eng.tok_cap, int(eng.sink_end[0]) + (n - int(eng.buffer_start[0])) + eng.cfg.token_budget
+             + int(eng.led.max_size[:H].max(initial=0)) + 16)
+    hb = state.__dict__.setdefault("_host", {})
+    def pinned(name, shape, dtype):
+        t = hb.get(name)
+        if t is None or t.shape != torch.Size(shape) or t.dtype != dtype:
+            t = hb[name] = torch.empty(shape, dtype=dtype, pin_memory=True)
+        return t
+    out_h = pinned("out", (lay.num_q_heads, lay.head_dim), torch.float32)
+    out_h.copy_(out_t[0], non_blocking=True)
+    if state.mode != "oracle":
+        st_h = pinned("stats", (4, H), torch.int32)
+        st_h.copy_(eng.stats[:, :H], non_blocking=True)
+        tok_h = pinned("tok", (H, tb), torch.int32)
+        tok_h.copy_(eng.tok[:H, :tb], non_blocking=True)
+        if flat:
+            fl_h = pinned("flag", (H, kf), torch.uint8)
+            fl_h.copy_(eng.flag[:H, :kf], non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    out = out_h.numpy().astype(np.float64)
     errors = topk = None
     if oracle:
         ref = eng.attend_dense(q)[0].double().cpu().numpy()
         errors = list(np.linalg.norm(out - ref, axis=1) / np.maximum(np.linalg.norm(ref, axis=1), 1e-300))
     per_head, sel = [], []
     if state.mode != "oracle":
-        H = lay.num_kv_heads
-        st = eng.head_stats()
+        st = st_h.numpy().T
         ntok = int(st[:H, 0].max())
-        tok = eng.tok[:H, :max(ntok, 1)].cpu().numpy()
-        kf = int(eng.led.n_fine[:H].max())
-        flags = eng.flag[:H, :max(kf, 1)].cpu().numpy()
+        if ntok > tb:  # cannot happen (tb bounds every list); read the rest if it did
+            tok = eng.tok[:H, :ntok].cpu().numpy()
+        else:
+            tok = tok_h.numpy()
+        flags = fl_h.numpy() if flat else eng.flag[:H, :kf].cpu().numpy()
         cands = None
         if eng.cfg.hierarchy is not None:
             nc = eng.n_cand[:H].cpu().numpy()
@@ -202,7 +232,6 @@ def _attend_engine(state: EngineState, queries, oracle: bool):
                        buffer_len=0 if state.mode == "oracle" else n - int(eng.buffer_start[0]),
                        num_kv_heads=lay.num_kv_heads, selected_indices=sel if sel else None, oracle_topk=topk,
                        mode=state.mode)
-    torch.cuda.synchronize()
     rep.gpu_times = {"lookup": ev[0].elapsed_time(ev[1]) * 1e-3, "exact": ev[1].elapsed_time(ev[2]) * 1e-3}
     return out, rep
 
