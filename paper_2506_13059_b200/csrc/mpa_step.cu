@@ -262,7 +262,8 @@ step_kernel(const __grid_constant__ CUtensorMap tm_kc, const Params p) {
 
     const int32_t* szp = p.size + (size_t)l * p.kcap + c0;
     const int32_t* ofp = p.moff + (size_t)l * (p.kcap + 1) + c0;
-    for (int i = tid; i < nloc; i += kThreads) {  // read in phases 2-6
+#pragma unroll 8
+    for (int i = tid; i < nloc; i += kThreads) {  // read in phases 2-6 (unrolled: the loads overlap)
         sizes[i] = __ldg(szp + i);
         moff_s[i] = __ldg(ofp + i);
     }
@@ -513,7 +514,8 @@ step_kernel(const __grid_constant__ CUtensorMap tm_kc, const Params p) {
                 const double e = LG[(size_t)g * Kc + i];
                 sc = g ? fma(e, rz[g], sc) : e * rz[g];
             }
-            sc = sc / (double)G;
+            // np.mean's division; by a power of two it is the exact product
+            sc = (G & (G - 1)) == 0 ? sc * (1.0 / G) : sc / (double)G;
             const unsigned long long k = ~(unsigned long long)__double_as_longlong(sc);
             keys[i] = k;
             kmin = min(kmin, k);
@@ -790,15 +792,32 @@ step_kernel(const __grid_constant__ CUtensorMap tm_kc, const Params p) {
     const int nsel = (int)(tsum & 0xffffffffu), nsel_tok = (int)(tsum >> 32);
     const int32_t* mem = p.mem + (size_t)l * p.mem_cap;
     const int tbase = ns + nb + (int)tok_before;
-    for (int j = tid; j < nsel_tok; j += kThreads) {
-        int lo = 0, hi = nsel - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (sel_t[mid] <= j) lo = mid;
-            else hi = mid - 1;
+    // member ids: every thread resolves kTokU tokens first, then issues their kTokU loads together
+    constexpr int kTokU = 4;
+    for (int j0 = tid; j0 < nsel_tok; j0 += kThreads * kTokU) {
+        int src[kTokU];
+#pragma unroll
+        for (int u = 0; u < kTokU; ++u) {
+            const int j = j0 + u * kThreads;
+            src[u] = -1;
+            if (j < nsel_tok) {
+                int lo = 0, hi = nsel - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (sel_t[mid] <= j) lo = mid;
+                    else hi = mid - 1;
+                }
+                src[u] = moff_s[sel_c[lo]] + (j - sel_t[lo]);
+            }
         }
-        const int slot = tbase + j;
-        if (slot < p.tok_cap) T[slot] = __ldg(mem + moff_s[sel_c[lo]] + (j - sel_t[lo]));
+        int v[kTokU];
+#pragma unroll
+        for (int u = 0; u < kTokU; ++u) v[u] = src[u] >= 0 ? __ldg(mem + src[u]) : 0;
+#pragma unroll
+        for (int u = 0; u < kTokU; ++u) {
+            const int slot = tbase + j0 + u * kThreads;
+            if (src[u] >= 0 && slot < p.tok_cap) T[slot] = v[u];
+        }
     }
     if (rank == 0 && tid == 0) {
         const long long ntok = ns + nb + tot_tok;
