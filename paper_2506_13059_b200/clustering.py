@@ -60,11 +60,15 @@ class KMeansBatch:
         i32 = dict(dtype=torch.int32, device=device)
         N, K = int(n.sum()), int(k.sum())
         self.d = d
-        self.t = {name: torch.as_tensor(v, **i32) for name, v in
-                  (("l", arr[:, 0]), ("start", arr[:, 1]), ("n", n), ("k", k), ("pt_off", self.pt_off),
-                   ("c_off", self.c_off))}
-        sc = lambda name, n, dt: _scratch(cache, name, n, dt, device).zero_()
-        self.assign = sc("assign", N, torch.int32)
+        # the six per-problem tables in one host -> device copy
+        names = ("l", "start", "n", "k", "pt_off", "c_off")
+        tab = torch.as_tensor(np.stack([arr[:, 0], arr[:, 1], n, k, self.pt_off, self.c_off]).astype(np.int32)
+                              if self.P else np.zeros((6, 1), np.int32), **i32)
+        self.t = {name: tab[i] for i, name in enumerate(names)}
+        sc = lambda name, n, dt: _scratch(cache, name, n, dt, device)
+        # every Lloyd kernel writes these before reading them (the assignment is zeroed for
+        # callers that read it before a pass)
+        self.assign = sc("assign", N, torch.int32).zero_()
         self.prev = sc("prev", N, torch.int32)
         self.p2 = sc("p2", N, torch.float64)
         self.order = sc("order", N, torch.int32)

@@ -14,9 +14,9 @@
 // tau = 2^-13 (||p||^2 + max_j ||c_j||^2) -- at least 2.6x the worst case above.
 // Per point it keeps the best column (lowest index on ties) and every column within 2 tau of
 // it.  Only those columns can hold the exact fp64 argmin, so a point with no such column is
-// certified; otherwise km_recheck_cand_kernel re-scores just the best and its (<= 4) rivals
+// certified; otherwise km_recheck_kernel re-scores just the best and its (<= 4) rivals
 // with the exact fp64 formula of km_assign_kernel (sequential fp64 dot, (p2 + c2) - 2 dot,
-// first minimum), and a point with more rivals goes to km_recheck_full_kernel (all columns).
+// first minimum), and a point with more rivals is re-scored against every column.
 // Certified and re-checked points therefore assign exactly like the fp64 kernel.
 //
 // Persistent kernel: one CTA per SM walks items of TWO 128-point tiles of one problem; warp 4
@@ -534,23 +534,29 @@ __device__ __forceinline__ double exact_dist(const __nv_bfloat16* __restrict__ x
 // exact re-score of the points with rivals inside the band: eight lanes per point, lane 0 the
 // best column and lanes 1..n its rivals, first minimum over (dist, index) within the group
 constexpr int kRecheckThreads = 256;
-__global__ void __launch_bounds__(kRecheckThreads) km_recheck_cand_kernel(mpa_km km, TcWs ws) {
+__device__ __forceinline__ void recheck_cand(const mpa_km& km, const TcWs& ws) {
     const int nr = ws.counters[0];
-    const int sub = threadIdx.x & 7;
-    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 3; r < nr; r += (gridDim.x * blockDim.x) >> 3) {
-        const int4* e = reinterpret_cast<const int4*>(ws.recheck + (size_t)r * kRecheckStride);
-        const int4 h = e[0], rv = e[1];
-        const int p = h.x, i = h.y, n_riv = h.z;
-        const int j = sub == 0 ? h.w : sub == 1 ? rv.x : sub == 2 ? rv.y : sub == 3 ? rv.z : rv.w;
-        const int g = km.pt_off[p] + i;
+    const int sub = threadIdx.x & 7, lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    // warp-uniform trip count (the shuffles below need every lane): four entries per warp per trip
+    for (int rb = gw * 4; rb < nr; rb += nw * 4) {
+        const int r = rb + (lane >> 3);
+        const bool ok = r < nr;
         double best = INFINITY;
-        int jb = 0x7fffffff;
-        if (sub <= n_riv) {
-            const __nv_bfloat16* x =
-                reinterpret_cast<const __nv_bfloat16*>(km.pts) + ((size_t)km.prob_l[p] * km.tcap + km.prob_start[p] + i) * km.d;
-            const int cj = km.c_off[p] + j;
-            best = exact_dist(x, km.cent + (size_t)cj * km.d, km.p2[g], km.c2[cj]);
-            jb = j;
+        int jb = 0x7fffffff, g = 0;
+        if (ok) {
+            const int4* e = reinterpret_cast<const int4*>(ws.recheck + (size_t)r * kRecheckStride);
+            const int4 h = e[0], rv = e[1];
+            const int p = h.x, i = h.y, n_riv = h.z;
+            const int j = sub == 0 ? h.w : sub == 1 ? rv.x : sub == 2 ? rv.y : sub == 3 ? rv.z : rv.w;
+            g = km.pt_off[p] + i;
+            if (sub <= n_riv) {
+                const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(km.pts) +
+                                         ((size_t)km.prob_l[p] * km.tcap + km.prob_start[p] + i) * km.d;
+                const int cj = km.c_off[p] + j;
+                best = exact_dist(x, km.cent + (size_t)cj * km.d, km.p2[g], km.c2[cj]);
+                jb = j;
+            }
         }
 #pragma unroll
         for (int o = 4; o; o >>= 1) {
@@ -561,7 +567,7 @@ __global__ void __launch_bounds__(kRecheckThreads) km_recheck_cand_kernel(mpa_km
                 jb = oj;
             }
         }
-        if (sub == 0) {
+        if (ok && sub == 0) {
             km.assign[g] = jb;
             ws.ub[g] = __double2float_ru(best - km.p2[g]);
         }
@@ -570,7 +576,7 @@ __global__ void __launch_bounds__(kRecheckThreads) km_recheck_cand_kernel(mpa_km
 
 // exact re-score over every column (points with more than kTcCand rivals): one CTA per point,
 // each thread a strided slice of the centroids, then a block-wide first minimum
-__global__ void __launch_bounds__(kRecheckThreads) km_recheck_full_kernel(mpa_km km, TcWs ws) {
+__device__ __forceinline__ void recheck_full(const mpa_km& km, const TcWs& ws) {
     const int nr = ws.counters[1];
     __shared__ double s_best[kRecheckThreads / 32];
     __shared__ int s_j[kRecheckThreads / 32];
@@ -616,6 +622,12 @@ __global__ void __launch_bounds__(kRecheckThreads) km_recheck_full_kernel(mpa_km
         }
         __syncthreads();  // s_best reused by the next point
     }
+}
+
+// the uncertified points of one pass: candidate re-scores, then full scans
+__global__ void __launch_bounds__(kRecheckThreads) km_recheck_kernel(mpa_km km, TcWs ws) {
+    recheck_cand(km, ws);
+    recheck_full(km, ws);
 }
 
 }  // namespace mpa
@@ -722,8 +734,7 @@ int mpa_km_assign_tc(const mpa_km& k, cudaStream_t st) {
         km_tc_reset_kernel<<<1, 32, 0, st>>>(w);
         if (incr) km_assign_tc2_kernel<true><<<sms, kTcThreads, smem, st>>>(pm, tm, v, w);
         else km_assign_tc2_kernel<false><<<sms, kTcThreads, smem, st>>>(pm, tm, v, w);
-        km_recheck_cand_kernel<<<2 * sms, kRecheckThreads, 0, st>>>(v, w);
-        km_recheck_full_kernel<<<2 * sms, kRecheckThreads, 0, st>>>(v, w);
+        km_recheck_kernel<<<2 * sms, kRecheckThreads, 0, st>>>(v, w);
     };
     pass(tp, tt, v1, ws, false);
     pass(tp, tt2, v2, ws2, true);

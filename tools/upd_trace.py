@@ -19,8 +19,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--events", type=int, default=2)
+    ap.add_argument("--ctx", type=int, default=32768)
+    ap.add_argument("--workload", default="c2")
     a = ap.parse_args()
-    args = argparse.Namespace(batch=a.batch, ctx=32768, budget=512, steps=2, warmup=3)
+    args = argparse.Namespace(batch=a.batch, ctx=a.ctx, budget=512, steps=2, warmup=3, workload=a.workload)
     dev = torch.device("cuda", 0)
     eng, Q, KN, VN, _ = bench.build_engine(args, 0, dev)
     L = eng.cfg.local_buffer
