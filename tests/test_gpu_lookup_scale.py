@@ -159,3 +159,38 @@ def test_c2_staged_lookup_matches_single_launch():
     fin = np.isfinite(a)
     assert np.allclose(a[fin], b[fin], rtol=1e-6, atol=1e-6)
     assert rel_err(out1.cpu().numpy(), out2.cpu().numpy()).max() < 1e-5
+
+
+def test_oversized_step_falls_back_to_staged_kernels():
+    # 128 ledgers of ~2.5K centroids: the single-launch step's one-wave cluster grid does not fit
+    # (mpa_decode_step_fits), so the engine takes the staged kernels -- selections still exact
+    from paper_2506_13059_b200.engine import DecodeEngine
+
+    ctx = 5200
+    cfg = EngineConfig(block_size=2048, alpha=1024, local_buffer=64, sink_tokens=10, tokens_per_centroid=2,
+                       token_budget=256, rope_theta=1e6, seed=13)
+    rng = np.random.default_rng(13)
+    heads = [_ledger(rng, ctx, cfg) for _ in range(LAY.num_kv_heads)]
+    n_seq = 16
+    kcap = max(O._flat(x[2], False)[2].size for x in heads) + 64
+    eng = DecodeEngine(cfg, LAY, n_seq, tcap=ctx + 8, dtype=torch.bfloat16, kcap=kcap)
+    k = torch.as_tensor(np.stack([h[0] for h in heads])).cuda()[None].expand(n_seq, -1, -1, -1)
+    v = torch.as_tensor(np.stack([h[1] for h in heads])).cuda()[None].expand(n_seq, -1, -1, -1)
+    eng.write_tokens(k, v)
+    eng.load_ledgers([to_host(h[2]) for h in heads] * n_seq)
+    assert int(eng.led.n_fine.max()) > 2300
+    assert not eng.fused_lookup_path()
+    q = rng.standard_normal((LAY.num_q_heads, LAY.head_dim)).astype(np.float32)
+    out = eng.attend(torch.as_tensor(q).cuda()[None].expand(n_seq, -1, -1).contiguous()).cpu().numpy()
+    ref = [rounded(h[2], torch.bfloat16) for h in heads]
+    rk = [torch.as_tensor(O.rotate(heads[h][0], np.arange(ctx), LAY.head_dim, cfg.rope_theta)).to(torch.bfloat16)
+          .double().numpy() for h in range(LAY.num_kv_heads)]
+    sv = [torch.as_tensor(heads[h][1]).to(torch.bfloat16).double().numpy() for h in range(LAY.num_kv_heads)]
+    want, rep = O.decode_step(q, ref, [h[0] for h in heads], sv, ctx, 0, cfg, LAY, rot_keys=rk)
+    st, tok = eng.head_stats(), eng.tok.cpu().numpy()
+    for s in (0, n_seq - 1):
+        for h in range(LAY.num_kv_heads):
+            l = s * LAY.num_kv_heads + h
+            ns, nb = cfg.sink_tokens, ctx - ref[h].buffer_start
+            assert np.array_equal(np.sort(tok[l, ns + nb: st[l, 0]]), rep.selected_indices[h]), (s, h)
+        assert rel_err(out[s], want).max() < 2e-3
