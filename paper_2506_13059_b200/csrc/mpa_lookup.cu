@@ -455,8 +455,17 @@ hier_candidates_kernel(const int32_t* __restrict__ ccount, const int32_t* __rest
         const int cnt = (c < nc && cflag[(size_t)l * ccap + c]) ? off[c + 1] - off[c] : 0;
         int tot;
         const int pos = base + block_exclusive_scan(cnt, scan, &tot);
-        for (int j = 0; j < cnt; ++j)
-            if (pos + j < cand_cap) cand[(size_t)l * cand_cap + pos + j] = child[(size_t)l * child_cap + off[c] + j];
+        // children copied 8 at a time: the loads of a batch are in flight together
+        const int32_t* src = child + (size_t)l * child_cap + (cnt ? off[c] : 0);
+        int32_t* dst = cand + (size_t)l * cand_cap + pos;
+        for (int j0 = 0; j0 < cnt; j0 += 8) {
+            int v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = j0 + u < cnt ? __ldg(src + j0 + u) : 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (j0 + u < cnt && pos + j0 + u < cand_cap) dst[j0 + u] = v[u];
+        }
         base += tot;
     }
     if (threadIdx.x == 0) n_cand[l] = base < cand_cap ? base : cand_cap;
