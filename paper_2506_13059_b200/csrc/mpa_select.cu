@@ -944,16 +944,31 @@ __device__ void worklist_v2(int l, int L, int n, const double* __restrict__ logi
     // in the selected list), so the two dependent loads (CSR offset, member id) overlap across slots
     const int32_t* moff = fmem_off + (size_t)l * (fcap + 1);
     const int nsel_tok = (int)(tot >> 32);
-    for (int j = threadIdx.x; j < nsel_tok; j += blockDim.x) {
-        int lo = 0, hi = nsel - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (sel_t[mid] <= j) lo = mid;
-            else hi = mid - 1;
+    constexpr int kTokU = 4;  // slots resolved first, then their member loads issued together
+    for (int j0 = threadIdx.x; j0 < nsel_tok; j0 += blockDim.x * kTokU) {
+        int src[kTokU];
+#pragma unroll
+        for (int u = 0; u < kTokU; ++u) {
+            const int j = j0 + u * blockDim.x;
+            src[u] = -1;
+            if (j < nsel_tok) {
+                int lo = 0, hi = nsel - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (sel_t[mid] <= j) lo = mid;
+                    else hi = mid - 1;
+                }
+                src[u] = offs[sel_c[lo]] + (j - sel_t[lo]);
+            }
         }
-        const int i = sel_c[lo];
-        const int slot = ns + nb + j;
-        if (slot < tok_cap) T[slot] = __ldg(fmem + (size_t)l * fmem_cap + offs[i] + (j - sel_t[lo]));
+        int v[kTokU];
+#pragma unroll
+        for (int u = 0; u < kTokU; ++u) v[u] = src[u] >= 0 ? __ldg(fmem + (size_t)l * fmem_cap + src[u]) : 0;
+#pragma unroll
+        for (int u = 0; u < kTokU; ++u) {
+            const int slot = ns + nb + j0 + u * (int)blockDim.x;
+            if (src[u] >= 0 && slot < tok_cap) T[slot] = v[u];
+        }
     }
     int tbase = ns + nb + (int)(tot >> 32), rbase = (int)((tot >> 16) & 0xffff);
     if (cflag && replacement) {
