@@ -194,6 +194,32 @@ class ShardedDecodeEngine:
         parts = self.phase_partials(prefix_all, prefix_n_all)
         return self.phase_merge(comm.all_gather(parts))
 
+    def capture_attend(self, q: torch.Tensor, comm) -> None:
+        """Capture one whole sharded decode step -- the local kernels AND the three NCCL all-gathers
+        -- as one CUDA graph (NCCL collectives are graph-capturable); `attend_graphed` then replays it.
+        Valid while this rank's ledgers keep their cluster counts (an online update re-captures)."""
+        e = self.eng
+        if int(e.led.n_fine.min()) == 0:
+            raise ConfigError("ledger has no clusters on this rank")
+        self._gq = q.detach().clone()
+        e._workspace(0)
+        for _ in range(2):  # communicator and allocator warm-up outside the capture
+            self.attend(self._gq, comm)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            out = self.attend(self._gq, comm)
+        self._graph, self._gout = g, out
+        self._graph_key = e.led.n_fine.copy()
+
+    def attend_graphed(self, q: torch.Tensor, comm) -> torch.Tensor:
+        e = self.eng
+        if getattr(self, "_graph", None) is None or not np.array_equal(self._graph_key, e.led.n_fine):
+            self.capture_attend(q, comm)
+        self._gq.copy_(q)
+        self._graph.replay()
+        return self._gout
+
     def step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, comm) -> torch.Tensor:
         """attend, append the step's token on every rank (pipeline.py:137-159), and run the online
         update on the tail rank, which owns the final block, the sinks and the buffer (the update is

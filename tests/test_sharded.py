@@ -176,3 +176,35 @@ def test_sharded_two_processes_with_updates():
         assert bad == 0, (r, bad)
         assert worst < 2e-3, (r, worst)
         assert n_upd >= 2, n_upd
+
+
+@pytest.mark.gpu
+def test_sharded_step_graph_with_nccl_collectives():
+    # the sharded step captured as ONE CUDA graph with its NCCL all-gathers (a real NCCL
+    # communicator, world size 1 on the one reachable GPU): replays equal the eager step
+    import torch.distributed as dist
+
+    from paper_2506_13059_b200.core import EngineConfig, HeadLayout
+    from paper_2506_13059_b200.sharded import ShardedDecodeEngine, TorchComm
+
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1)
+    try:
+        torch.manual_seed(11)
+        lay = HeadLayout(16, 4, 128)
+        cfg = EngineConfig(block_size=1024, alpha=512, local_buffer=64, token_budget=256, tokens_per_centroid=8,
+                           rope_theta=1e6, seed=3)
+        n_seq, ctx = 2, 4000
+        se = ShardedDecodeEngine(cfg, lay, n_seq, ctx + 16, 0, 1)
+        se.write_tokens(torch.randn(n_seq, lay.num_kv_heads, ctx, 128, device="cuda"),
+                        torch.randn(n_seq, lay.num_kv_heads, ctx, 128, device="cuda"))
+        se.prefill_local()
+        se.set_gid_offsets(se.eng.led.n_fine[None])
+        comm = TorchComm()
+        for _ in range(3):
+            q = torch.randn(n_seq, lay.num_q_heads, 128, device="cuda")
+            want = se.attend(q, comm).clone()
+            got = se.attend_graphed(q, comm).clone()
+            assert torch.equal(got, want)
+        assert se._graph is not None
+    finally:
+        dist.destroy_process_group()
