@@ -106,3 +106,25 @@ def test_page_pool_exhaustion_is_an_error():
     e.write_tokens(k, k)  # 2 pages per sequence
     with pytest.raises(RuntimeError, match="exhausted"):
         e.write_tokens(k, k)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_paged_hierarchical_matches_flat(dtype):
+    # 2-level hierarchy (coarse rejected rows in the work lists, staged lookup) on a paged cache
+    from paper_2506_13059_b200.core import HierarchyConfig
+
+    lay = HeadLayout(10, 2, 128)
+    tr = gen_synthetic(8, 1400, lay, 0.1, seed=17, decode_steps=40)
+    cfg = EngineConfig(block_size=512, alpha=256, local_buffer=16, sink_tokens=5, token_budget=96,
+                       tokens_per_centroid=8, seed=17, hierarchy=HierarchyConfig(32, 4, 0.5))
+    flat, paged = _engines(tr, cfg, dtype, [{}, {"page_size": 32, "page_order": "shuffled"}])
+    P = tr.prompt_len
+    n_upd = 0
+    for t in range(40):
+        q = torch.as_tensor(tr.queries[:, t]).cuda()[None].repeat(2, 1, 1)
+        kn = torch.as_tensor(tr.keys[:, P + t]).cuda()[None].repeat(2, 1, 1)
+        vn = torch.as_tensor(tr.values[:, P + t]).cuda()[None].repeat(2, 1, 1)
+        assert torch.equal(flat.step(q, kn, vn).clone(), paged.step(q, kn, vn).clone()), t
+        n_upd += flat.last_update is not None
+    assert n_upd >= 2
+    _ledgers_equal(flat, paged)
