@@ -67,3 +67,21 @@ def test_new_entry_points_reject_bad_arguments(lib):
     # logits: neither q_lk nor (q_raw, cs_lk)
     rc = lib.mpa_centroid_logits(None, 8, 4, 128, None, None, None, 0, None, None, None, 0, None, 0, None, None, None)
     assert rc == 1001 and b"null argument" in lib.mpa_last_error()
+
+
+def test_paged_cache_geometry_is_validated(lib):
+    # a paged mpa_cache is checked before any launch: page size a power of two, enough pages per
+    # sequence for tcap, kv-heads dividing the ledgers
+    from paper_2506_13059_b200._lib import MpaCache
+
+    lib.mpa_last_error.restype = ctypes.c_char_p
+    dummy = ctypes.c_void_p(256)
+    bt = ctypes.c_void_p(512)
+
+    def cache(page_size, pages_per_seq, n_kv_heads=2):
+        return MpaCache(dummy, dummy, dummy, 2, 4, 100, 128, bt, page_size, pages_per_seq, 8, n_kv_heads)
+
+    k = ctypes.c_void_p(1024)
+    for c, msg in ((cache(24, 8), b"power of two"), (cache(16, 2), b"tcap"), (cache(16, 8, 3), b"geometry")):
+        rc = lib.mpa_kv_write(ctypes.byref(c), k, k, k, 1, k, None)
+        assert rc == 1001 and msg in lib.mpa_last_error(), lib.mpa_last_error()
