@@ -227,6 +227,12 @@ constexpr int kRoundThreads = 1024;
 constexpr int kSortItems = 16;  // 1024 x 16 = 16384 points per problem
 constexpr int kMaxPoints = kRoundThreads * kSortItems;
 constexpr int kIdxBits = 14;
+// dynamic shared memory of the round kernel: the sort's temporary storage, which also holds the
+// assignment copy before the sort (>= kMaxPoints ints), then the counts
+constexpr size_t kRoundAsgBytes =
+    ((sizeof(typename cub::BlockRadixSort<unsigned, kRoundThreads, kSortItems>::TempStorage) > kMaxPoints * 4
+          ? sizeof(typename cub::BlockRadixSort<unsigned, kRoundThreads, kSortItems>::TempStorage)
+          : kMaxPoints * 4) + 15) & ~size_t(15);
 
 struct DistIdx {
     double v;
@@ -250,11 +256,15 @@ __global__ void __launch_bounds__(kRoundThreads) km_round_kernel(mpa_km km, int 
     }
     const int n = km.prob_n[p], K = km.prob_k[p], d = km.d;
     const int l = km.prob_l[p], start = km.prob_start[p];
-    int* asg = km.assign + km.pt_off[p];
+    int* asg_g = km.assign + km.pt_off[p];
     int* prv = km.prev + km.pt_off[p];
-    int* cnt = km.count + km.c_off[p];
+    int* cnt_g = km.count + km.c_off[p];
     double* cent = km.cent + (size_t)km.c_off[p] * d;
-
+    // the assignment and the counts live in shared memory for the whole kernel (the assignment
+    // aliases the sort's temporary storage, dead until the keys are in registers)
+    int* asg = reinterpret_cast<int*>(round_smem);
+    int* cnt = reinterpret_cast<int*>(round_smem + kRoundAsgBytes);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) asg[i] = asg_g[i];
     for (int j = threadIdx.x; j < K; j += blockDim.x) cnt[j] = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cnt[asg[i]], 1);
@@ -351,6 +361,7 @@ __global__ void __launch_bounds__(kRoundThreads) km_round_kernel(mpa_km km, int 
                     }
                 s_int[3] = f;
                 asg[f] = cid;
+                asg_g[f] = cid;
                 cnt[big] -= 1;
                 cnt[cid] += 1;
             }
@@ -407,7 +418,8 @@ __global__ void __launch_bounds__(kRoundThreads) km_round_kernel(mpa_km km, int 
         }
     }
 
-    // ---- cstart = exclusive scan of counts; stable grouping of points by cluster
+    // ---- counts out; cstart = exclusive scan of counts; stable grouping of points by cluster
+    for (int j = threadIdx.x; j < K; j += blockDim.x) cnt_g[j] = cnt[j];
     {
         int base = 0;
         for (int j0 = 0; j0 < K; j0 += blockDim.x) {
@@ -425,6 +437,7 @@ __global__ void __launch_bounds__(kRoundThreads) km_round_kernel(mpa_km km, int 
         const int i = threadIdx.x * kSortItems + e;
         keys[e] = i < n ? ((unsigned)asg[i] << kIdxBits) | (unsigned)i : 0xffffffffu;
     }
+    __syncthreads();  // the sort's temporary storage overwrites the assignment copy
     int kbits = 1;
     while ((1 << kbits) < K) ++kbits;
     Sort(sort_tmp).Sort(keys, kIdxBits, min(32, kIdxBits + kbits));  // stable: points stay ascending
@@ -925,7 +938,7 @@ using namespace mpa;
 namespace {
 
 using RoundSort = cub::BlockRadixSort<unsigned, kRoundThreads, kSortItems>;
-constexpr size_t kRoundSmem = sizeof(typename RoundSort::TempStorage);
+constexpr size_t kRoundSmem = kRoundAsgBytes;  // + k_max counts
 
 void launch_means(const mpa_km& k, int force, cudaStream_t st) {
     const dim3 grid(ceil_div(k.k_max, kMeansWarps), k.n_prob);
@@ -936,8 +949,9 @@ void launch_means(const mpa_km& k, int force, cudaStream_t st) {
 }
 
 int launch_round(const mpa_km& k, int grouping_only, cudaStream_t st) {
-    if (int rc = set_max_smem((const void*)km_round_kernel, (int)kRoundSmem)) return rc;
-    km_round_kernel<<<k.n_prob, kRoundThreads, kRoundSmem, st>>>(k, grouping_only);
+    const size_t smem = kRoundSmem + (size_t)k.k_max * 4;
+    if (int rc = set_max_smem((const void*)km_round_kernel, (int)smem)) return rc;
+    km_round_kernel<<<k.n_prob, kRoundThreads, smem, st>>>(k, grouping_only);
     return 0;
 }
 
