@@ -16,8 +16,8 @@
 // K_raw cache / the fp64 ledger without gathers.  Means accumulate members in ascending point
 // order in fp64, which reproduces np.add.at / np.mean bit-for-bit; the assignment argmin is
 // fp64 and matches numpy's except at true ties (|margin| ~ 1e-16 relative).
-#include <cub/block/block_radix_sort.cuh>
 
+#include <cub/block/block_radix_sort.cuh>
 #include <cstdlib>
 #include <map>
 
@@ -264,7 +264,24 @@ __global__ void __launch_bounds__(kRoundThreads) km_round_kernel(mpa_km km, int 
     // aliases the sort's temporary storage, dead until the keys are in registers)
     int* asg = reinterpret_cast<int*>(round_smem);
     int* cnt = reinterpret_cast<int*>(round_smem + kRoundAsgBytes);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) asg[i] = asg_g[i];
+    // point i = threadIdx.x + e * kRoundThreads: all loads in flight at once (assignment, and the
+    // previous round's for the convergence test and the dirty marks)
+    const int rounds = grouping_only ? 0 : km.state[p * 4 + ST_ROUNDS];
+    int pv[kSortItems];
+    {
+        int av[kSortItems];
+#pragma unroll
+        for (int e = 0; e < kSortItems; ++e) {
+            const int i = threadIdx.x + e * kRoundThreads;
+            av[e] = i < n ? asg_g[i] : 0;
+            pv[e] = i < n && rounds >= 1 ? prv[i] : 0;
+        }
+#pragma unroll
+        for (int e = 0; e < kSortItems; ++e) {
+            const int i = threadIdx.x + e * kRoundThreads;
+            if (i < n) asg[i] = av[e];
+        }
+    }
     for (int j = threadIdx.x; j < K; j += blockDim.x) cnt[j] = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cnt[asg[i]], 1);
@@ -381,10 +398,13 @@ __global__ void __launch_bounds__(kRoundThreads) km_round_kernel(mpa_km km, int 
         }
 
         // ---- convergence decision (clustering.py:136-142)
-        const int rounds = km.state[p * 4 + ST_ROUNDS];
         int diff = 0;
         if (rounds >= 1)
-            for (int i = threadIdx.x; i < n; i += blockDim.x) diff |= (asg[i] != prv[i]);
+#pragma unroll
+            for (int e = 0; e < kSortItems; ++e) {
+                const int i = threadIdx.x + e * kRoundThreads;
+                diff |= i < n && asg[i] != pv[e];
+            }
         diff = __syncthreads_or(diff);
         if (rounds >= 1 && rounds >= km.min_iters && !diff) {
             if (threadIdx.x == 0) {
@@ -405,11 +425,14 @@ __global__ void __launch_bounds__(kRoundThreads) km_round_kernel(mpa_km km, int 
                 if (rounds >= 1 && !repaired) {  // a repair rewrote a centroid: recompute all
                     for (int j = threadIdx.x; j < K; j += blockDim.x) dt[j] = 0;
                     __syncthreads();
-                    for (int i = threadIdx.x; i < n; i += blockDim.x)
-                        if (asg[i] != prv[i]) {
+#pragma unroll
+                    for (int e = 0; e < kSortItems; ++e) {
+                        const int i = threadIdx.x + e * kRoundThreads;
+                        if (i < n && asg[i] != pv[e]) {
                             dt[asg[i]] = 1;
-                            dt[prv[i]] = 1;
+                            dt[pv[e]] = 1;
                         }
+                    }
                 } else {
                     for (int j = threadIdx.x; j < K; j += blockDim.x) dt[j] = 1;
                 }
@@ -431,19 +454,25 @@ __global__ void __launch_bounds__(kRoundThreads) km_round_kernel(mpa_km km, int 
             base += tot;
         }
     }
+    // blocked keys (thread t holds points 16t..16t+15, as the stable sort requires), read as int4
     unsigned keys[kSortItems];
 #pragma unroll
-    for (int e = 0; e < kSortItems; ++e) {
-        const int i = threadIdx.x * kSortItems + e;
-        keys[e] = i < n ? ((unsigned)asg[i] << kIdxBits) | (unsigned)i : 0xffffffffu;
+    for (int e4 = 0; e4 < kSortItems; e4 += 4) {
+        const int i = threadIdx.x * kSortItems + e4;
+        const int4 a4 = reinterpret_cast<const int4*>(asg)[i >> 2];
+        const int av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            keys[e4 + e] = i + e < n ? ((unsigned)av[e] << kIdxBits) | (unsigned)(i + e) : 0xffffffffu;
     }
     __syncthreads();  // the sort's temporary storage overwrites the assignment copy
     int kbits = 1;
     while ((1 << kbits) < K) ++kbits;
-    Sort(sort_tmp).Sort(keys, kIdxBits, min(32, kIdxBits + kbits));  // stable: points stay ascending
+    // stable (points stay ascending inside a cluster); striped out, so the stores coalesce
+    Sort(sort_tmp).SortBlockedToStriped(keys, kIdxBits, min(32, kIdxBits + kbits));
 #pragma unroll
     for (int e = 0; e < kSortItems; ++e) {
-        const int pos = threadIdx.x * kSortItems + e;
+        const int pos = e * kRoundThreads + threadIdx.x;
         if (pos < n) km.order[km.pt_off[p] + pos] = (int)(keys[e] & ((1u << kIdxBits) - 1));
     }
 }
@@ -483,18 +512,15 @@ template <> struct Row4<double> {
 
 // One warp per cluster, lane = four consecutive coordinates (d % 4 == 0).  Each coordinate is
 // the sequential fp64 sum of the members in ascending point order (np.add.at,
-// clustering.py:113-120); member rows are fetched kMeansBatch at a time, in their storage type,
+// clustering.py:113-120); member rows are fetched 8-16 at a time, in their storage type,
 // ahead of the (ordered) adds.  Inside a Lloyd run only clusters whose members changed are
 // recomputed, and km.dirty is narrowed to the clusters whose centroid actually moved (unless an
 // empty-cluster repair rewrote a centroid this round).
-constexpr int kMeansBatch = 8;
+constexpr int kMeansBatch = 8;  // value means of km_write_level_kernel
 template <typename T>
-__global__ void __launch_bounds__(kMeansWarps * 32) km_means_kernel(mpa_km km, int force) {
-    const int p = blockIdx.y;
-    if (!force && !km.state[p * 4 + ST_DOMEANS]) return;
-    const int K = km.prob_k[p], d = km.d;
-    const int j = blockIdx.x * kMeansWarps + (threadIdx.x >> 5);
-    if (j >= K) return;
+__device__ __forceinline__ void means_one(const mpa_km& km, int force, int p, int j) {
+    constexpr int kBatch = sizeof(T) == 8 ? 8 : 16;  // member rows in flight per lane
+    const int d = km.d;
     const bool track = !force && km.dirty;
     if (track && !km.dirty[km.c_off[p] + j]) return;  // same members: same mean
     const int lane = threadIdx.x & 31;
@@ -520,17 +546,17 @@ __global__ void __launch_bounds__(kMeansWarps * 32) km_means_kernel(mpa_km km, i
 #pragma unroll
             for (int e = 0; e < 4; ++e) old[e] = k + e < d ? cent[k + e] : 0.0;  // fetched ahead of the sums
             double wsum = 0.0;
-            int nxt[kMeansBatch];
+            int nxt[kBatch];
 #pragma unroll
-            for (int u = 0; u < kMeansBatch; ++u) nxt[u] = u < c ? __ldg(ord + u) : -1;
-            for (int m0 = 0; m0 < c; m0 += kMeansBatch) {
-                int ii[kMeansBatch];
+            for (int u = 0; u < kBatch; ++u) nxt[u] = u < c ? __ldg(ord + u) : -1;
+            for (int m0 = 0; m0 < c; m0 += kBatch) {
+                int ii[kBatch];
 #pragma unroll
-                for (int u = 0; u < kMeansBatch; ++u) ii[u] = nxt[u];
-                Row4<T> xv[kMeansBatch];
-                int32_t w[kMeansBatch];
+                for (int u = 0; u < kBatch; ++u) ii[u] = nxt[u];
+                Row4<T> xv[kBatch];
+                int32_t w[kBatch];
 #pragma unroll
-                for (int u = 0; u < kMeansBatch; ++u) {
+                for (int u = 0; u < kBatch; ++u) {
                     w[u] = 1;
                     if (ii[u] >= 0) {
                         if (wrow) w[u] = __ldg(wrow + ii[u]);
@@ -538,10 +564,10 @@ __global__ void __launch_bounds__(kMeansWarps * 32) km_means_kernel(mpa_km km, i
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < kMeansBatch; ++u)  // the next batch's member ids
-                    nxt[u] = m0 + kMeansBatch + u < c ? __ldg(ord + m0 + kMeansBatch + u) : -1;
+                for (int u = 0; u < kBatch; ++u)  // the next batch's member ids
+                    nxt[u] = m0 + kBatch + u < c ? __ldg(ord + m0 + kBatch + u) : -1;
 #pragma unroll
-                for (int u = 0; u < kMeansBatch; ++u) {
+                for (int u = 0; u < kBatch; ++u) {
                     if (ii[u] < 0) continue;
                     const double wu = (double)w[u];
                     if (wrow) wsum = __dadd_rn(wsum, wu);
@@ -567,6 +593,17 @@ __global__ void __launch_bounds__(kMeansWarps * 32) km_means_kernel(mpa_km km, i
         moved = __any_sync(0xffffffffu, moved);
         if (lane == 0 && !moved) km.dirty[km.c_off[p] + j] = 0;
     }
+}
+
+// kMeansPerWarp clusters per warp: late Lloyd rounds, with a few moved clusters, launch few CTAs
+constexpr int kMeansPerWarp = 4;
+template <typename T>
+__global__ void __launch_bounds__(kMeansWarps * 32) km_means_kernel(mpa_km km, int force) {
+    const int p = blockIdx.y;
+    if (!force && !km.state[p * 4 + ST_DOMEANS]) return;
+    const int K = km.prob_k[p];
+    const int j0 = (blockIdx.x * kMeansWarps + (threadIdx.x >> 5)) * kMeansPerWarp;
+    for (int u = 0; u < kMeansPerWarp && j0 + u < K; ++u) means_one<T>(km, force, p, j0 + u);
 }
 
 // generic-d fallback (d % 4 != 0): one lane per coordinate, same summation order
@@ -937,15 +974,15 @@ using namespace mpa;
 
 namespace {
 
-using RoundSort = cub::BlockRadixSort<unsigned, kRoundThreads, kSortItems>;
 constexpr size_t kRoundSmem = kRoundAsgBytes;  // + k_max counts
 
 void launch_means(const mpa_km& k, int force, cudaStream_t st) {
     const dim3 grid(ceil_div(k.k_max, kMeansWarps), k.n_prob);
+    const dim3 grid4(ceil_div(k.k_max, kMeansWarps * kMeansPerWarp), k.n_prob);
     if (k.d & 3) km_means_generic_kernel<<<grid, kMeansWarps * 32, 0, st>>>(k, force);
-    else if (k.pts64) km_means_kernel<double><<<grid, kMeansWarps * 32, 0, st>>>(k, force);
-    else if (k.pts_dtype == MPA_BF16) km_means_kernel<__nv_bfloat16><<<grid, kMeansWarps * 32, 0, st>>>(k, force);
-    else km_means_kernel<float><<<grid, kMeansWarps * 32, 0, st>>>(k, force);
+    else if (k.pts64) km_means_kernel<double><<<grid4, kMeansWarps * 32, 0, st>>>(k, force);
+    else if (k.pts_dtype == MPA_BF16) km_means_kernel<__nv_bfloat16><<<grid4, kMeansWarps * 32, 0, st>>>(k, force);
+    else km_means_kernel<float><<<grid4, kMeansWarps * 32, 0, st>>>(k, force);
 }
 
 int launch_round(const mpa_km& k, int grouping_only, cudaStream_t st) {
