@@ -96,7 +96,14 @@ __global__ void km_c2_kernel(mpa_km km, int only_active) {
     }
     const double* c = km.cent + (size_t)(km.c_off[p] + j) * km.d;
     double s = 0.0;
-    for (int k = 0; k < km.d; ++k) s = __dadd_rn(s, __dmul_rn(c[k], c[k]));
+    for (int k0 = 0; k0 < km.d; k0 += 16) {  // 16 loads in flight, then the ordered adds
+        double x[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) x[u] = k0 + u < km.d ? c[k0 + u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (k0 + u < km.d) s = __dadd_rn(s, __dmul_rn(x[u], x[u]));
+    }
     km.c2[km.c_off[p] + j] = s;
 }
 
@@ -518,16 +525,13 @@ template <> struct Row4<double> {
 // empty-cluster repair rewrote a centroid this round).
 constexpr int kMeansBatch = 8;  // value means of km_write_level_kernel
 template <typename T>
-__device__ __forceinline__ void means_one(const mpa_km& km, int force, int p, int j) {
+__device__ __forceinline__ void means_one(const mpa_km& km, bool track, int p, int j, int c, int cstart) {
     constexpr int kBatch = sizeof(T) == 8 ? 8 : 16;  // member rows in flight per lane
     const int d = km.d;
-    const bool track = !force && km.dirty;
-    if (track && !km.dirty[km.c_off[p] + j]) return;  // same members: same mean
     const int lane = threadIdx.x & 31;
     const int l = km.prob_l[p], start = km.prob_start[p];
-    const int c = km.count[km.c_off[p] + j];
     double* cent = km.cent + (size_t)(km.c_off[p] + j) * d;
-    const int* ord = km.order + km.pt_off[p] + km.cstart[km.c_off[p] + j];
+    const int* ord = km.order + km.pt_off[p] + cstart;
     bool moved = false;
     if (c == 0) {
         if (!km.wts)  // `_means`: empty clusters are reset to the zero vector
@@ -601,9 +605,22 @@ template <typename T>
 __global__ void __launch_bounds__(kMeansWarps * 32) km_means_kernel(mpa_km km, int force) {
     const int p = blockIdx.y;
     if (!force && !km.state[p * 4 + ST_DOMEANS]) return;
-    const int K = km.prob_k[p];
+    const int K = km.prob_k[p], lane = threadIdx.x & 31;
     const int j0 = (blockIdx.x * kMeansWarps + (threadIdx.x >> 5)) * kMeansPerWarp;
-    for (int u = 0; u < kMeansPerWarp && j0 + u < K; ++u) means_one<T>(km, force, p, j0 + u);
+    const bool track = !force && km.dirty;
+    // the warp's clusters' (moved, count, start) in one round of loads
+    int todo = 0, cn = 0, cs = 0;
+    if (lane < kMeansPerWarp && j0 + lane < K) {
+        const int jj = km.c_off[p] + j0 + lane;
+        todo = !track || km.dirty[jj];  // same members: same mean
+        cn = km.count[jj];
+        cs = km.cstart[jj];
+    }
+#pragma unroll 1
+    for (int u = 0; u < kMeansPerWarp; ++u) {
+        const int cu = __shfl_sync(0xffffffffu, cn, u), su = __shfl_sync(0xffffffffu, cs, u);
+        if (__shfl_sync(0xffffffffu, todo, u)) means_one<T>(km, track, p, j0 + u, cu, su);
+    }
 }
 
 // generic-d fallback (d % 4 != 0): one lane per coordinate, same summation order

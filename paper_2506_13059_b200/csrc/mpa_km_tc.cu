@@ -183,7 +183,10 @@ __global__ void __launch_bounds__(256) km_tc_plan_kernel(mpa_km km, TcWs ws, int
         v2n[p] = nd > 0 ? n : 0;
         gn[p] = mc;
     }
-    // changed-column list and the members of the changed clusters (grouped by cluster)
+    // changed-column list and the members of the changed clusters (grouped by cluster): per
+    // chunk of 256 clusters, the moved ones are listed in shared memory, then copied a warp each
+    __shared__ int s_src[256], s_dst[256], s_cnt[256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int cbase = 0, mbase = 0;
     for (int j0 = 0; j0 < K; j0 += blockDim.x) {
         const int j = j0 + threadIdx.x;
@@ -194,10 +197,14 @@ __global__ void __launch_bounds__(256) km_tc_plan_kernel(mpa_km km, TcWs ws, int
         const int em = block_exclusive_scan(cnt, s_scan, &tot_m);
         if (dj) {
             ws.dl[c0 + cbase + ec] = j;
-            const int* ord = km.order + km.pt_off[p] + km.cstart[c0 + j];
-            int32_t* gi = gidx + g0 + mbase + em;
-            for (int m = 0; m < cnt; ++m) gi[m] = ord[m];
+            s_src[ec] = km.pt_off[p] + km.cstart[c0 + j];
+            s_dst[ec] = g0 + mbase + em;
+            s_cnt[ec] = cnt;
         }
+        __syncthreads();
+        for (int e = warp; e < tot_c; e += blockDim.x >> 5)
+            for (int m = lane; m < s_cnt[e]; m += 32) gidx[s_dst[e] + m] = km.order[s_src[e] + m];
+        __syncthreads();
         cbase += tot_c;
         mbase += tot_m;
     }
