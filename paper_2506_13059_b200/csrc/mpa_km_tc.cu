@@ -32,7 +32,8 @@
 namespace mpa {
 
 constexpr int kTcM = 128, kTcTerms = 2, kTcSub = 2 * kTcTerms;
-constexpr int kTcThreads = 288;  // warp 4 issues; warps 0-3 and 5-8 drain TMEM (one point tile each)
+constexpr int kTcThreads = 320;  // warp 4 issues the MMAs, warp 9 the TMA loads; warps 0-3 and 5-8
+                                 // drain TMEM (one point tile each)
 constexpr int kTcTailRows = 64;  // box rows of the narrow-tail centroid map
 constexpr int kTcABytes = 2 * kTcM * 128;   // 2 x 64-column chunks of the point tile
 constexpr int kTcCand = 4;                  // rival columns kept per point (more -> full re-score)
@@ -325,11 +326,14 @@ km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts,
         return x;
     };
 
-    if (warp == 4) {
+    if (warp == 9) {
+        // TMA producer: the point tiles of each item (two A buffers) and the centroid-term
+        // sub-tiles (a kTc2Stages ring), each slot refilled as soon as its MMAs retire
         if (lane == 0 && my_items > 0) {
             prefetch_tmap(&tm_pts);
             prefetch_tmap(&tm_terms_tail);
             auto issue_a = [&](int it, const TcTile& x) {
+                if (it >= 2) mbar_wait(smem_u32(&bar_a_empty[it & 1]), ((it - 2) >> 1) & 1);
                 const unsigned b = smem_u32(&bar_a[it & 1]);
                 unsigned char* dst = sa + (it & 1) * 2 * kTcABytes;
                 mbar_expect_tx(b, 2 * kTcABytes);
@@ -338,34 +342,32 @@ km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts,
                     tma_load_2d(smem_u32(dst + m * kTcABytes + kTcM * 128), &tm_pts, 64, x.row0 + m * kTcM, b);
                 }
             };
-            int l_it = 0, l_nt = 0, l_u = 0, l_step = 0;
-            TcTile lx = item_info(0);
-            auto load_next = [&]() {
-                if (l_it >= my_items) return;
-                const int t = l_u >> 1, c = l_u & 1, slot_i = l_step % kTc2Stages;
-                const unsigned slot = smem_u32(sb + slot_i * kTc2BBytes);
-                const unsigned fb = smem_u32(&bar_full[slot_i]);
-                const int row = t * ws.kpad + lx.c_off + l_nt * kTc2N;
-                if (l_nt + 1 < lx.n_nt) {
-                    mbar_expect_tx(fb, kTc2BBytes);
-                    for (int b = 0; b < kTc2N / kTcTailRows; ++b)
-                        tma_load_2d(slot + b * kTcTailRows * 128, &tm_terms_tail, c * 64, row + b * kTcTailRows, fb);
-                } else {
-                    mbar_expect_tx(fb, lx.tail_boxes * kTcTailRows * 128);
-                    for (int b = 0; b < lx.tail_boxes; ++b)
-                        tma_load_2d(slot + b * kTcTailRows * 128, &tm_terms_tail, c * 64, row + b * kTcTailRows, fb);
-                }
-                ++l_step;
-                if (++l_u == kTcSub) {
-                    l_u = 0;
-                    if (++l_nt == lx.n_nt) {
-                        l_nt = 0;
-                        if (++l_it < my_items) lx = item_info(l_it);
+            int step = 0;
+            TcTile x = item_info(0);
+            issue_a(0, x);
+            for (int it = 0; it < my_items; ++it) {
+                for (int nt = 0; nt < x.n_nt; ++nt) {
+                    for (int u = 0; u < kTcSub; ++u, ++step) {
+                        const int c = u & 1, slot_i = step % kTc2Stages;
+                        if (step >= kTc2Stages)
+                            mbar_wait(smem_u32(&bar_empty[slot_i]), (step / kTc2Stages - 1) & 1);
+                        const unsigned slot = smem_u32(sb + slot_i * kTc2BBytes);
+                        const unsigned fb = smem_u32(&bar_full[slot_i]);
+                        const int row = (u >> 1) * ws.kpad + x.c_off + nt * kTc2N;
+                        const int boxes = nt + 1 < x.n_nt ? kTc2N / kTcTailRows : x.tail_boxes;
+                        mbar_expect_tx(fb, boxes * kTcTailRows * 128);
+                        for (int b = 0; b < boxes; ++b)
+                            tma_load_2d(slot + b * kTcTailRows * 128, &tm_terms_tail, c * 64, row + b * kTcTailRows, fb);
                     }
+                    if (nt == 0 && it + 1 < my_items) issue_a(it + 1, item_info(it + 1));
                 }
-            };
-            issue_a(0, lx);
-            for (int s = 0; s < kTc2Stages; ++s) load_next();
+                if (it + 1 < my_items) x = item_info(it + 1);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 4) {
+        // MMA issuer: one elected thread
+        if (lane == 0 && my_items > 0) {
             int step = 0, gnt = 0;
             for (int it = 0; it < my_items; ++it) {
                 const TcTile x = item_info(it);
@@ -390,16 +392,8 @@ km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts,
                                           umma_desc_sw128(bslot + k * 32), idesc, (u | k) ? 1u : 0u);
                         }
                         umma_commit(smem_u32(&bar_empty[step % kTc2Stages]));
-                        if (step >= 1) {
-                            mbar_wait(smem_u32(&bar_empty[(step - 1) % kTc2Stages]), ((step - 1) / kTc2Stages) & 1);
-                            load_next();
-                        }
                     }
                     umma_commit(smem_u32(&bar_acc_full[buf]));
-                    if (nt == 0 && it + 1 < my_items) {
-                        if (it >= 1) mbar_wait(smem_u32(&bar_a_empty[(it + 1) & 1]), ((it - 1) >> 1) & 1);
-                        issue_a(it + 1, item_info(it + 1));
-                    }
                 }
                 umma_commit(smem_u32(&bar_a_empty[it & 1]));
             }
