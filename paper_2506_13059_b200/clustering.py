@@ -304,14 +304,16 @@ class _Ticks:
         import os
         import time
 
-        self.on = os.environ.get("MPA_UPD_TRACE") == "1"
+        self.on = os.environ.get("MPA_UPD_TRACE") in ("1", "2")
+        self.sync = os.environ.get("MPA_UPD_TRACE") == "1"  # "2": host time only (no syncs)
         self.t = time.perf_counter
         self.last = self.t() if self.on else 0.0
         self.parts = []
 
     def __call__(self, name):
         if self.on:
-            torch.cuda.synchronize()
+            if self.sync:
+                torch.cuda.synchronize()
             now = self.t()
             self.parts.append((name, (now - self.last) * 1e3))
             self.last = now
@@ -353,19 +355,21 @@ def online_update(eng, seqs, cursor: int, samples: np.ndarray | None = None) -> 
     SAMP = samp_tab[Ls % eng.Hkv]                                    # [n, n_new]
     base = np.concatenate([[0], np.cumsum(FK + n_new)[:-1]]).astype(np.int64)
     c_at = int((FK + n_new).sum())
-    intra = np.arange(int(FK.sum()), dtype=np.int64) - np.repeat(np.cumsum(FK) - FK, FK)
-    old_src = np.repeat(Ls * led.kcap + F0, FK) + intra
-    old_dst = np.repeat(base, FK) + intra
-    new_src = ((Ls * eng.tcap + BS)[:, None] + SAMP).ravel()
-    new_dst = ((base + FK)[:, None] + np.arange(n_new, dtype=np.int64)).ravel()
     probs = list(zip(Ls.tolist(), FS.tolist(), (BS + L - FS).tolist(), (FK + n_new).tolist()))
     tails = (BS - FS).tolist()
     dev = eng.device
     tick("loop")
-    allidx = torch.as_tensor(np.concatenate([old_src, old_dst, new_src, new_dst]), dtype=torch.int64, device=dev)
-    no, nn = old_src.size, new_src.size
-    osrc, odst = allidx[:no], allidx[no:2 * no]
-    nsrc, ndst = allidx[2 * no:2 * no + nn], allidx[2 * no + nn:]
+    # gather indices built on the device from the per-ledger table (one small copy):
+    # old centroid rows (ledger, f0 + i) -> (base + i), sampled buffer tokens -> (base + fk + s)
+    n_l, no = len(ledgers), int(FK.sum())
+    tab = torch.as_tensor(np.concatenate([Ls * led.kcap + F0, base, FK, Ls * eng.tcap + BS, SAMP.ravel()]),
+                          dtype=torch.int64).to(dev, non_blocking=True)
+    src0, base_d, fk_d, nsrc0 = tab[:n_l], tab[n_l:2 * n_l], tab[2 * n_l:3 * n_l], tab[3 * n_l:4 * n_l]
+    of = torch.repeat_interleave(torch.arange(n_l, device=dev), fk_d, output_size=no)
+    intra = torch.arange(no, device=dev) - (torch.cumsum(fk_d, 0) - fk_d)[of]
+    osrc, odst = src0[of] + intra, base_d[of] + intra
+    nsrc = (nsrc0[:, None] + tab[4 * n_l:].view(n_l, n_new)).view(-1)
+    ndst = ((base_d + fk_d)[:, None] + torch.arange(n_new, device=dev)).view(-1)
     tick("idx")
     cache = eng.__dict__.setdefault("_upd_scratch", {})
     init = _scratch(cache, "init", c_at * eng.d, torch.float64, dev).view(c_at, eng.d)

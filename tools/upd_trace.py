@@ -70,6 +70,16 @@ def main():
         if len(v) > 2:
             half = v[len(v) // a.events * (a.events - 1):]
             print(f"{nm:32s} {half}")
+    # the last event's device timeline: busy time vs the gaps between consecutive kernels
+    ks = sorted((e.time_range.start, e.time_range.end) for e in prof.events()
+                if e.device_type.name == "CUDA" and e.name.startswith(("mpa::km_", "void mpa::km_")))
+    ks = ks[len(ks) // a.events * (a.events - 1):]
+    gaps = [b[0] - a_[1] for a_, b in zip(ks, ks[1:])]
+    small = [g for g in gaps if 0 < g < 50]
+    print(f"last event: {len(ks)} kernels, span {(ks[-1][1] - ks[0][0]) / 1e3:.2f} ms, busy "
+          f"{sum(e - s for s, e in ks) / 1e3:.2f} ms, gaps <50us {sum(small) / 1e3:.2f} ms over {len(small)} "
+          f"(median {sorted(small)[len(small) // 2] if small else 0:.1f} us), gaps >=50us "
+          f"{sum(g for g in gaps if g >= 50) / 1e3:.2f} ms over {sum(1 for g in gaps if g >= 50)}")
 
 
 if __name__ == "__main__":
