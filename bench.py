@@ -578,6 +578,9 @@ def main():
                           "mean_rejected_centroids": float(fstats[:, 1].mean()),
                           "mean_scored_centroids": float(np.mean(scored)),
                           "memop_ratio": nbytes["step"] / dbytes},
+            # the slowest timed steps (with an online update inside, they show the update's cost)
+            "step_ms_top": sorted((round(float(x), 3) for x in step_ms), reverse=True)[:6],
+            "step_ms_median": float(np.median(step_ms)),
             "update": {"ms_per_event": update_ms, "first_event_ms": update_first_ms,
                        "amortized_us_per_step": update_ms * 1e3 / L,
                        "pct_of_step": update_ms / L / ms_step * 100.0, "lloyd_rounds": upd["rounds"],

@@ -322,7 +322,10 @@ class _Ticks:
         if self.on:
             import sys
 
-            print("update phases ms: " + ", ".join(f"{n} {v:.2f}" for n, v in self.parts), file=sys.stderr)
+            ms = torch.cuda.memory_stats()
+            print("update phases ms: " + ", ".join(f"{n} {v:.2f}" for n, v in self.parts)
+                  + f" | segments {ms.get('segment.all.allocated', 0)} retries {ms.get('num_alloc_retries', 0)}",
+                  file=sys.stderr)
 
 
 def online_update(eng, seqs, cursor: int, samples: np.ndarray | None = None) -> dict:
@@ -373,7 +376,11 @@ def online_update(eng, seqs, cursor: int, samples: np.ndarray | None = None) -> 
     tick("idx")
     cache = eng.__dict__.setdefault("_upd_scratch", {})
     init = _scratch(cache, "init", c_at * eng.d, torch.float64, dev).view(c_at, eng.d)
-    init[odst] = led.kc64.view(-1, eng.d)[osrc]
+    # through a kept scratch block: a fresh ~30 MB temporary every event (its size creeps up)
+    # sends the caching allocator to cudaMalloc, which stalls for tens of ms at times
+    g = _scratch(cache, "gather", no * eng.d, torch.float64, dev).view(no, eng.d)
+    torch.index_select(led.kc64.view(-1, eng.d), 0, osrc, out=g)
+    init.index_copy_(0, odst, g)
     tick("init_old")
     init[ndst] = eng.k_raw.view(-1, eng.d)[nsrc].double()
     tick("init_new")
