@@ -532,6 +532,33 @@ __device__ __forceinline__ double exact_dist(const __nv_bfloat16* __restrict__ x
     return __dsub_rn(__dadd_rn(p2, c2), __dmul_rn(2.0, dot));
 }
 
+// the same distance to up to N centroids at once (N independent fma chains over one read of x;
+// each chain keeps exact_dist's order)
+template <int N>
+__device__ __forceinline__ void exact_dist_n(const __nv_bfloat16* __restrict__ x, const double* const (&c)[N],
+                                             double p2, const double (&c2)[N], double (&out)[N]) {
+    double dot[N];
+#pragma unroll
+    for (int u = 0; u < N; ++u) dot[u] = 0.0;
+#pragma unroll 2
+    for (int k8 = 0; k8 < 16; ++k8) {
+        const uint4 xr = __ldg(reinterpret_cast<const uint4*>(x) + k8);
+        const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xr);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const float2 xf = __bfloat1622float2(xh[h]);
+#pragma unroll
+            for (int u = 0; u < N; ++u) {
+                const double2 cv = __ldg(reinterpret_cast<const double2*>(c[u]) + k8 * 4 + h);
+                dot[u] = fma((double)xf.x, cv.x, dot[u]);
+                dot[u] = fma((double)xf.y, cv.y, dot[u]);
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < N; ++u) out[u] = __dsub_rn(__dadd_rn(p2, c2[u]), __dmul_rn(2.0, dot[u]));
+}
+
 // exact re-score of the points with rivals inside the band: eight lanes per point, lane 0 the
 // best column and lanes 1..n its rivals, first minimum over (dist, index) within the group
 constexpr int kRecheckThreads = 256;
@@ -590,12 +617,26 @@ __device__ __forceinline__ void recheck_full(const mpa_km& km, const TcWs& ws) {
             reinterpret_cast<const __nv_bfloat16*>(km.pts) + ((size_t)km.prob_l[p] * km.tcap + km.prob_start[p] + i) * km.d;
         double best = INFINITY;
         int jb = 0x7fffffff;
-        for (int j = threadIdx.x; j < K; j += blockDim.x) {
-            const int cj = km.c_off[p] + j;
-            const double dist = exact_dist(x, km.cent + (size_t)cj * km.d, p2, km.c2[cj]);
-            if (dist < best || (dist == best && j < jb)) {
-                best = dist;
-                jb = j;
+        // a thread's columns j, j + T, j + 2T scored together (three chains in flight); the
+        // ascending-j first minimum is unchanged
+        const int T = blockDim.x;
+        for (int j0 = threadIdx.x; j0 < K; j0 += 3 * T) {
+            const double* cc[3];
+            double c2v[3], dist[3];
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+                const int j = min(j0 + u * T, K - 1);  // clamped columns are scored and dropped
+                cc[u] = km.cent + (size_t)(km.c_off[p] + j) * km.d;
+                c2v[u] = km.c2[km.c_off[p] + j];
+            }
+            exact_dist_n<3>(x, cc, p2, c2v, dist);
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+                const int j = j0 + u * T;
+                if (j < K && (dist[u] < best || (dist[u] == best && j < jb))) {
+                    best = dist[u];
+                    jb = j;
+                }
             }
         }
 #pragma unroll
