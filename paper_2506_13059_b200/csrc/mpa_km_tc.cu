@@ -517,7 +517,7 @@ km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts,
 __device__ __forceinline__ double exact_dist(const __nv_bfloat16* __restrict__ x, const double* __restrict__ c,
                                              double p2, double c2) {
     double dot = 0.0;
-#pragma unroll 4
+#pragma unroll 8
     for (int k8 = 0; k8 < 16; ++k8) {
         const uint4 xr = __ldg(reinterpret_cast<const uint4*>(x) + k8);
         const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xr);
