@@ -93,6 +93,14 @@ int mpa_kv_append(const mpa_cache* cache, const float* k_src, const float* v_src
 int mpa_stage3(float* dst0, const float* src0, long long n0, float* dst1, const float* src1, long long n1,
                float* dst2, const float* src2, long long n2, void* stream);
 
+/* One batched serving step from HOST buffers (pinned for overlap), all on `stream`: q, k, v copied
+ * into the captured step graph's input block d_in (q, then k, then v, back to back), the graph
+ * (cudaGraphExec_t) launched, the output copied back to h_out.  Replaces the per-step host work of
+ * the reference's pipeline.step (pipeline.py:124-159) for a whole batch; sizes in bytes. */
+int mpa_step_host(void* graph_exec, void* d_in, const void* h_q, long long q_bytes, const void* h_k,
+                  long long k_bytes, const void* h_v, long long v_bytes, void* h_out, const void* d_out,
+                  long long out_bytes, void* stream);
+
 /* K1 -- rotate queries: q_rot = rotate(q, qpos[seq]) * scale (fp32, exact view) and
  * q_lk = rotate(q, delta) (fp64, lookup view; rope.py:66-68).  q: fp32 [n_seq, n_qh, d].
  * Either output may be NULL (not both): the views are independent. */

@@ -53,6 +53,8 @@ _KM = C.POINTER(MpaKm)
 _SIGS = {
     "mpa_kv_write": [C.POINTER(MpaCache), _vp, _vp, _vp, C.c_int, _vp, _vp],
     "mpa_stage3": [_vp, _vp, C.c_longlong, _vp, _vp, C.c_longlong, _vp, _vp, C.c_longlong, _vp],
+    "mpa_step_host": [_vp, _vp, _vp, C.c_longlong, _vp, C.c_longlong, _vp, C.c_longlong, _vp, _vp, C.c_longlong,
+                      _vp],
     "mpa_kv_append": [C.POINTER(MpaCache), _vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp],
     "mpa_rotate_queries": [_vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int, _vp, _f32, _vp, _vp, _vp],
     "mpa_centroid_logits": [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(MpaLevel), _vp, _vp, C.c_int, _vp, _vp,

@@ -219,6 +219,22 @@ extern "C" int mpa_stage3(float* dst0, const float* src0, long long n0, float* d
     return check_launch("mpa_stage3");
 }
 
+extern "C" int mpa_step_host(void* graph_exec, void* d_in, const void* h_q, long long q_bytes, const void* h_k,
+                             long long k_bytes, const void* h_v, long long v_bytes, void* h_out, const void* d_out,
+                             long long out_bytes, void* stream) {
+    MPA_REQUIRE(graph_exec && d_in && h_q && h_k && h_v && h_out && d_out, MPA_ERR_ARG, "mpa_step_host: null argument");
+    MPA_REQUIRE(q_bytes >= 0 && k_bytes >= 0 && v_bytes >= 0 && out_bytes >= 0, MPA_ERR_ARG, "mpa_step_host: sizes");
+    cudaStream_t st = (cudaStream_t)stream;
+    char* d = (char*)d_in;
+    cudaError_t e = cudaMemcpyAsync(d, h_q, (size_t)q_bytes, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d + q_bytes, h_k, (size_t)k_bytes, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d + q_bytes + k_bytes, h_v, (size_t)v_bytes, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaGraphLaunch((cudaGraphExec_t)graph_exec, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_out, d_out, (size_t)out_bytes, cudaMemcpyDeviceToHost, st);
+    MPA_REQUIRE(e == cudaSuccess, (int)e, "mpa_step_host: %s", cudaGetErrorString(e));
+    return 0;
+}
+
 extern "C" const char* mpa_last_error(void) { return g_err; }
 
 extern "C" const char* mpa_version(void) { return "libmpattn 0.1 (sm_100a)"; }

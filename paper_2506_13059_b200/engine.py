@@ -129,6 +129,7 @@ class DecodeEngine:
         # list: every centroid's replacement weight in id order, the selected ones -inf
         self.use_graphs = True if use_graphs is None else use_graphs
         self._graph = None
+        self._gexec = None  # its cudaGraphExec_t (mpa_step_host)
         self.n_captures = 0  # step-graph captures so far (bench reports it)
         self.time_fused = False  # bench: CUDA events around the fused kernel inside the step graph
         self._fev = None
@@ -397,7 +398,7 @@ class DecodeEngine:
         if self.mode == "oracle":
             return []
         L = self.cfg.local_buffer
-        return [s for s in range(self.n_seq) if self.cache_len[s] - self.buffer_start[s] >= 2 * L]
+        return np.flatnonzero(self.cache_len - self.buffer_start >= 2 * L).tolist()
 
     # ------------------------------------------------------------------ CUDA graph of a step
     def _graphable(self) -> bool:
@@ -411,9 +412,12 @@ class DecodeEngine:
     def _capture_step(self) -> None:
         self.n_captures += 1
         n, Hq, Hkv, d, dev = self.n_seq, self.Hq, self.Hkv, self.d, self.device
-        self._gq = torch.zeros(n, Hq, d, dtype=torch.float32, device=dev)
-        self._gk = torch.zeros(n, Hkv, 1, d, dtype=torch.float32, device=dev)
-        self._gv = torch.zeros(n, Hkv, 1, d, dtype=torch.float32, device=dev)
+        # the graph's inputs as one block (q, k, v back to back): mpa_step_host fills it from host
+        nq, nk = n * Hq * d, n * Hkv * d
+        self._gin = torch.zeros(nq + 2 * nk, dtype=torch.float32, device=dev)
+        self._gq = self._gin[:nq].view(n, Hq, d)
+        self._gk = self._gin[nq:nq + nk].view(n, Hkv, 1, d)
+        self._gv = self._gin[nq + nk:].view(n, Hkv, 1, d)
         self._workspace(0)
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream())
@@ -433,6 +437,7 @@ class DecodeEngine:
                 if self._fev:
                     self._fev[1].record()
             self._graph = g
+            self._gexec = self._raw_exec(g)
             return
         exact_br, append_br = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         with torch.cuda.graph(g):
@@ -460,6 +465,15 @@ class DecodeEngine:
                 self._fev[1].record()
             main.wait_stream(append_br)
         self._graph = g
+        self._gexec = self._raw_exec(g)
+
+    @staticmethod
+    def _raw_exec(g) -> int | None:
+        """The cudaGraphExec_t of a captured step, for mpa_step_host (None: torch does not expose it)."""
+        try:
+            return int(g.raw_cuda_graph_exec()) or None
+        except Exception:
+            return None
 
     def step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor) -> torch.Tensor:
         """Attend, append the step's token, then run the online update when a buffer holds 2L
@@ -468,8 +482,6 @@ class DecodeEngine:
         return self._step(q, k_new, v_new, host=False)
 
     def _step(self, q, k_new, v_new, host: bool) -> torch.Tensor:
-        from . import clustering
-
         if self._graphable():
             self.reserve(1)
             self._cluster_bounds()  # recaptures only if the cluster counts outgrew the captured bounds
@@ -502,6 +514,12 @@ class DecodeEngine:
             else:
                 out = self.attend(q)
                 self.write_tokens(k_new[:, :, None], v_new[:, :, None])
+        self._post_step()
+        return out
+
+    def _post_step(self) -> None:
+        from . import clustering
+
         todo = self.needs_update()
         self.last_update = None
         if todo:
@@ -512,12 +530,27 @@ class DecodeEngine:
             # the captured graph's launch arguments stay valid while the cluster bounds hold
             self._cluster_bounds()
         self.cursor += 1
-        return out
 
     def step_host(self, q_host: torch.Tensor, k_host: torch.Tensor, v_host: torch.Tensor,
                   out_host: torch.Tensor) -> torch.Tensor:
         """Public end-to-end step from HOST buffers (pinned for overlap): copies q / k / v in,
         runs `step`, copies the output back into out_host; all on the current stream."""
+        if self._graphable() and all(x.device.type == "cpu" and x.dtype == torch.float32 and x.is_contiguous()
+                                     for x in (q_host, k_host, v_host, out_host)):
+            self.reserve(1)
+            self._cluster_bounds()
+            if self._graph is None:
+                self._capture_step()
+            if self._gexec is not None and q_host.numel() == self._gq.numel() and \
+                    k_host.numel() == self._gk.numel() and v_host.numel() == self._gv.numel() and \
+                    out_host.numel() == self.out.numel() and self.out.dtype == torch.float32:
+                # copies in, the step graph, the copy out: one native call
+                call("mpa_step_host", self._gexec, ptr(self._gin), ptr(q_host), q_host.numel() * 4, ptr(k_host),
+                     k_host.numel() * 4, ptr(v_host), v_host.numel() * 4, ptr(out_host), ptr(self.out),
+                     out_host.numel() * 4, stream_ptr())
+                self.cache_len += 1
+                self._post_step()
+                return out_host
         out = self._step(q_host, k_host, v_host, host=True)
         out_host.copy_(out, non_blocking=True)
         return out_host

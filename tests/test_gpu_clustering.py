@@ -239,3 +239,39 @@ def test_bf16_d128_tensor_core_clustering_bitexact(monkeypatch):
                 _assert_same_ledger(to_oracle(st_g.engine.export_ledger(h)), st_o.ledgers[h], f"t={t} h={h}")
     assert n_upd >= 2
     assert used and all(used), used  # every Lloyd call ran on the tensor cores
+
+
+@pytest.mark.parametrize("use_graphs", [True, False])
+def test_step_host_matches_step(use_graphs):
+    """DecodeEngine.step_host (pinned host buffers; with a captured step graph one native call:
+    copies in, the graph, the copy out) gives the device-buffer step's outputs bit-for-bit, and the
+    same ledgers, across online updates."""
+    from paper_2506_13059_b200.engine import DecodeEngine
+
+    tr = gen_synthetic(8, 1000, HeadLayout(8, 2, 128), 0.1, seed=6, decode_steps=60)
+    cfg = EngineConfig(block_size=256, alpha=128, local_buffer=16, sink_tokens=5, token_budget=64,
+                       tokens_per_centroid=8, seed=6)
+    P = tr.prompt_len
+    engs = []
+    for _ in range(2):
+        e = DecodeEngine(cfg, tr.layout, 2, tcap=tr.total_len + 8, dtype=torch.bfloat16, use_graphs=use_graphs)
+        k = torch.as_tensor(tr.keys[:, :P]).cuda()[None].repeat(2, 1, 1, 1)
+        v = torch.as_tensor(tr.values[:, :P]).cuda()[None].repeat(2, 1, 1, 1)
+        e.write_tokens(k, v)
+        e.prefill()
+        engs.append(e)
+    oh = torch.empty(2, 8, 128, dtype=torch.float32).pin_memory()
+    n_upd = 0
+    for t in range(60):
+        q = torch.as_tensor(tr.queries[:, t]).float()[None].repeat(2, 1, 1).contiguous()
+        kn = torch.as_tensor(tr.keys[:, P + t]).float()[None].repeat(2, 1, 1).contiguous()
+        vn = torch.as_tensor(tr.values[:, P + t]).float()[None].repeat(2, 1, 1).contiguous()
+        ref = engs[0].step(q.cuda(), kn.cuda(), vn.cuda()).cpu()
+        engs[1].step_host(q.pin_memory(), kn.pin_memory(), vn.pin_memory(), oh)
+        torch.cuda.synchronize()
+        assert torch.equal(ref, oh), t
+        n_upd += engs[0].last_update is not None
+    assert n_upd >= 3
+    assert engs[1].n_captures >= 1 or not use_graphs
+    for h in range(engs[0].L):
+        _assert_same_ledger(to_oracle(engs[0].export_ledger(h)), to_oracle(engs[1].export_ledger(h)), f"h={h}")
