@@ -535,7 +535,7 @@ class DecodeEngine:
                   out_host: torch.Tensor) -> torch.Tensor:
         """Public end-to-end step from HOST buffers (pinned for overlap): copies q / k / v in,
         runs `step`, copies the output back into out_host; all on the current stream."""
-        if self._graphable() and all(x.device.type == "cpu" and x.dtype == torch.float32 and x.is_contiguous()
+        if self._graphable() and all(not x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()
                                      for x in (q_host, k_host, v_host, out_host)):
             self.reserve(1)
             self._cluster_bounds()
