@@ -50,6 +50,7 @@ class DecodeEngine:
         self.L = n_seq * self.Hkv
         self.tcap, self.dtype = tcap, dtype
         self.device = torch.device(device)
+        self._dev_idx = self.device.index if self.device.index is not None else torch.cuda.current_device()
         r = cfg.fine_ratio
         self.kcap = kcap or max(64, 2 * (tcap // r) + 64)
         hier = cfg.hierarchy is not None
@@ -547,7 +548,7 @@ class DecodeEngine:
                 # copies in, the step graph, the copy out: one native call
                 call("mpa_step_host", self._gexec, ptr(self._gin), ptr(q_host), q_host.numel() * 4, ptr(k_host),
                      k_host.numel() * 4, ptr(v_host), v_host.numel() * 4, ptr(out_host), ptr(self.out),
-                     out_host.numel() * 4, stream_ptr())
+                     out_host.numel() * 4, torch._C._cuda_getCurrentRawStream(self._dev_idx))
                 self.cache_len += 1
                 self._post_step()
                 return out_host
