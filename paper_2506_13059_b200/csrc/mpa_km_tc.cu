@@ -94,8 +94,10 @@ __device__ __forceinline__ void split_terms(const mpa_km& km, int c, int k, __nv
     if (k == 0) c2f[row] = (float)km.c2[c];
 }
 
-// the full column table, for the clusters that changed in the last round
-__global__ void km_tc_prep_kernel(mpa_km km, TcWs ws) {
+// the column tables after the plan: the full table for the clusters that changed in the last
+// round (rows c_off + j), and the changed-column table of the incremental problems (rows
+// c_off + t, t < v2k)
+__global__ void km_tc_prep_kernel(mpa_km km, TcWs ws, TcWs ws2, const int32_t* __restrict__ v2k) {
     const int p = blockIdx.y;
     if (!km.state[p * 4 + 0]) return;
     const int K = km.prob_k[p], d = km.d, c0 = km.c_off[p];
@@ -104,32 +106,10 @@ __global__ void km_tc_prep_kernel(mpa_km km, TcWs ws) {
         if (km.dirty && !km.dirty[c0 + j]) continue;
         split_terms(km, c0 + j, k, ws.terms, ws.c2f, ws.kpad, c0 + j);
     }
-}
-
-// the changed-column table of the incremental problems (rows c_off + t, t < count)
-__global__ void km_tc_prep_changed_kernel(mpa_km km, TcWs ws, const int32_t* __restrict__ v2k) {
-    const int p = blockIdx.y;
-    const int nk = v2k[p], d = km.d, c0 = km.c_off[p];
+    const int nk = v2k[p];
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nk * d; e += gridDim.x * blockDim.x) {
         const int t = e / d, k = e - t * d;
-        split_terms(km, c0 + ws.dl[c0 + t], k, ws.terms, ws.c2f, ws.kpad, c0 + t);
-    }
-}
-
-// per-problem max ||c||^2 (the certification band)
-__global__ void km_tc_norms_kernel(mpa_km km, TcWs ws) {
-    const int p = blockIdx.x;
-    if (!km.state[p * 4 + 0]) return;
-    double m = 0.0;
-    for (int j = threadIdx.x; j < km.prob_k[p]; j += blockDim.x) m = fmax(m, km.c2[km.c_off[p] + j]);
-    __shared__ double red[32];
-    m = warp_max(m);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double r = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, red[w]);
-        ws.c2max[p] = r;
+        split_terms(km, c0 + ws2.dl[c0 + t], k, ws2.terms, ws2.c2f, ws2.kpad, c0 + t);
     }
 }
 
@@ -154,13 +134,27 @@ __global__ void __launch_bounds__(256) km_tc_plan_kernel(mpa_km km, TcWs ws, int
     const int n = km.prob_n[p], K = km.prob_k[p], c0 = km.c_off[p];
     const int g0 = km.pt_off[p] / 2 + p;
     __shared__ int s_scan[33];
+    __shared__ double s_red[32];
     if (threadIdx.x == 0) {
         plan[kPlanZero * P + p] = 0;
         gstart[p] = g0;
+        if (p == 0) ws.counters[0] = ws.counters[1] = 0;  // the first pass's re-score lists
     }
     if (!km.state[p * 4 + 0]) {
         if (threadIdx.x == 0) v1n[p] = v2n[p] = v2k[p] = gn[p] = 0;
         return;
+    }
+    {  // per-problem max ||c||^2 (the certification band)
+        double m = 0.0;
+        for (int j = threadIdx.x; j < K; j += blockDim.x) m = fmax(m, km.c2[c0 + j]);
+        m = warp_max(m);
+        if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double r = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, s_red[w]);
+            ws.c2max[p] = r;
+        }
     }
     int nd = 0, mc = 0;
     for (int j = threadIdx.x; j < K; j += blockDim.x)
@@ -767,20 +761,19 @@ int mpa_km_assign_tc(const mpa_km& k, cudaStream_t st) {
     if (int rc = set_max_smem((const void*)km_assign_tc2_kernel<true>, (int)smem)) return rc;
     const int sms = device_sms();
     const dim3 pgrid(ceil_div(k.k_max * k.d, 256 * 8), P);
-    km_tc_norms_kernel<<<P, 256, 0, st>>>(k, ws);
-    km_tc_plan_kernel<<<P, 256, 0, st>>>(k, ws, plan, gidx);
-    km_tc_prep_kernel<<<pgrid, 256, 0, st>>>(k, ws);
-    km_tc_prep_changed_kernel<<<pgrid, 256, 0, st>>>(k, ws2, plan + kPlanV2k * P);
+    km_tc_plan_kernel<<<P, 256, 0, st>>>(k, ws, plan, gidx);  // also the band and the first pass's reset
+    km_tc_prep_kernel<<<pgrid, 256, 0, st>>>(k, ws, ws2, plan + kPlanV2k * P);
     km_tc_gather_kernel<<<dim3(32, P), 256, 0, st>>>(k, plan, gidx, (__nv_bfloat16*)v3.pts, v3.p2);
-    auto pass = [&](const CUtensorMap& pm, const CUtensorMap& tm, const mpa_km& v, const TcWs& w, bool incr) {
-        km_tc_reset_kernel<<<1, 32, 0, st>>>(w);
+    auto pass = [&](const CUtensorMap& pm, const CUtensorMap& tm, const mpa_km& v, const TcWs& w, bool incr,
+                    bool reset) {
+        if (reset) km_tc_reset_kernel<<<1, 32, 0, st>>>(w);  // (the plan resets the first pass's lists)
         if (incr) km_assign_tc2_kernel<true><<<sms, kTcThreads, smem, st>>>(pm, tm, v, w);
         else km_assign_tc2_kernel<false><<<sms, kTcThreads, smem, st>>>(pm, tm, v, w);
         km_recheck_kernel<<<2 * sms, kRecheckThreads, 0, st>>>(v, w);
     };
-    pass(tp, tt, v1, ws, false);
-    pass(tp, tt2, v2, ws2, true);
-    pass(tp3, tt, v3, ws3, false);
+    pass(tp, tt, v1, ws, false, false);
+    pass(tp, tt2, v2, ws2, true, true);
+    pass(tp3, tt, v3, ws3, false, true);
     km_tc_scatter_kernel<<<dim3(4, P), 256, 0, st>>>(k, plan, gidx, v3.assign, ws3.ub, ws.ub);
     return check_launch("mpa_km_assign(tcgen05)");
 }
