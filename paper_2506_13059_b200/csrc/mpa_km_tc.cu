@@ -278,6 +278,7 @@ km_assign_tc2_kernel(const __grid_constant__ CUtensorMap tm_pts,
             base += tot;
         }
         if (threadIdx.x == 0) tp[P] = base;
+        if (base == 0) return;  // an empty view (late Lloyd rounds): no TMEM, no barriers
     }
     if (warp == 0) tmem_alloc(&tmem_base, 512);
     if (threadIdx.x == 0) {
