@@ -595,9 +595,10 @@ def main():
                     "api": "engine.DecodeEngine.step_host (batched public API, pinned host buffers)"},
             "e2e_dropin": dropin,
             "graph_captures": eng.n_captures,
-            "gpu_launches": (3 if eng.fused_lookup_path() else 7) * K,  # per step: input staging + the
-                                    # step graph (flat bf16 path: lookup + append, fused decode; else 2
-                                    # rotations, logits, select+lists, fused decode, append)
+            # per step: the step graph (flat bf16 path: lookup + append, fused decode -- reading the
+            # step's q / k / v in place; else input staging + 2 rotations, logits, select+lists,
+            # fused decode, append)
+            "gpu_launches": (2 if eng._graph_raw is not None else 3 if eng.fused_lookup_path() else 7) * K,
             "clocks": clk.summary(),
         }
         if not args.no_cpu and not args.profile:

@@ -93,6 +93,11 @@ int mpa_kv_append(const mpa_cache* cache, const float* k_src, const float* v_src
 int mpa_stage3(float* dst0, const float* src0, long long n0, float* dst1, const float* src1, long long n1,
                float* dst2, const float* src2, long long n2, void* stream);
 
+/* Rebind a captured step graph (cudaGraph_t + its cudaGraphExec_t, containing one mpa_decode_step
+ * launch) to new q / k_new / v_new device buffers (fp32, 16-byte aligned, the captured shapes): the
+ * next launch of the exec reads them directly -- no staging copy per step. */
+int mpa_decode_step_rebind(void* graph, void* graph_exec, const float* q, const float* k_new, const float* v_new);
+
 /* One batched serving step from HOST buffers (pinned for overlap), all on `stream`: q, k, v copied
  * into the captured step graph's input block d_in (q, then k, then v, back to back), the graph
  * (cudaGraphExec_t) launched, the output copied back to h_out.  Replaces the per-step host work of

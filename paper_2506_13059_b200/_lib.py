@@ -53,6 +53,7 @@ _KM = C.POINTER(MpaKm)
 _SIGS = {
     "mpa_kv_write": [C.POINTER(MpaCache), _vp, _vp, _vp, C.c_int, _vp, _vp],
     "mpa_stage3": [_vp, _vp, C.c_longlong, _vp, _vp, C.c_longlong, _vp, _vp, C.c_longlong, _vp],
+    "mpa_decode_step_rebind": [_vp, _vp, _vp, _vp, _vp],
     "mpa_step_host": [_vp, _vp, _vp, C.c_longlong, _vp, C.c_longlong, _vp, C.c_longlong, _vp, _vp, C.c_longlong,
                       _vp],
     "mpa_kv_append": [C.POINTER(MpaCache), _vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp],

@@ -1071,3 +1071,48 @@ extern "C" int mpa_decode_step(const float* q, const float* k_new, const float* 
     });
     return check_launch(what);
 }
+
+// Point a captured step graph's decode-step kernel at new q / k_new / v_new buffers (the graph node's
+// parameters in the instantiated graph; everything else stays as captured), so a caller's device
+// tensors feed the step without a staging copy.
+extern "C" int mpa_decode_step_rebind(void* graph, void* graph_exec, const float* q, const float* k_new,
+                                      const float* v_new) {
+    MPA_REQUIRE(graph && graph_exec && q, MPA_ERR_ARG, "mpa_decode_step_rebind: null argument");
+    MPA_REQUIRE(((uintptr_t)q & 15) == 0 && ((uintptr_t)k_new & 15) == 0 && ((uintptr_t)v_new & 15) == 0,
+                MPA_ERR_ARG, "mpa_decode_step_rebind: buffers must be 16-byte aligned");
+    const void* kerns[6] = {(const void*)stp::step_kernel<3>, (const void*)stp::step_kernel<4>,
+                            (const void*)stp::step_kernel<5>, (const void*)stp::step_kernel<6>,
+                            (const void*)stp::step_kernel<7>, (const void*)stp::step_kernel<8>};
+    size_t n = 0;
+    cudaError_t e = cudaGraphGetNodes((cudaGraph_t)graph, nullptr, &n);
+    MPA_REQUIRE(e == cudaSuccess, (int)e, "mpa_decode_step_rebind: %s", cudaGetErrorString(e));
+    cudaGraphNode_t nodes[64];
+    MPA_REQUIRE(n <= 64, MPA_ERR_UNSUPPORTED, "mpa_decode_step_rebind: %zu graph nodes", n);
+    e = cudaGraphGetNodes((cudaGraph_t)graph, nodes, &n);
+    MPA_REQUIRE(e == cudaSuccess, (int)e, "mpa_decode_step_rebind: %s", cudaGetErrorString(e));
+    int found = 0;
+    for (size_t i = 0; i < n; ++i) {
+        cudaGraphNodeType t;
+        if (cudaGraphNodeGetType(nodes[i], &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
+        cudaKernelNodeParams kp;
+        if (cudaGraphKernelNodeGetParams(nodes[i], &kp) != cudaSuccess) continue;
+        bool step = false;
+        for (const void* k : kerns) step |= kp.func == k;
+        if (!step) continue;
+        CUtensorMap tk = *static_cast<const CUtensorMap*>(kp.kernelParams[0]);
+        stp::Params prm = *static_cast<const stp::Params*>(kp.kernelParams[1]);
+        MPA_REQUIRE(!prm.k_new == !k_new, MPA_ERR_ARG, "mpa_decode_step_rebind: the graph %s the append",
+                    prm.k_new ? "has" : "has no");
+        prm.q = q;
+        prm.k_new = k_new;
+        prm.v_new = v_new;
+        void* args[2] = {&tk, &prm};
+        kp.kernelParams = args;
+        kp.extra = nullptr;
+        e = cudaGraphExecKernelNodeSetParams((cudaGraphExec_t)graph_exec, nodes[i], &kp);
+        MPA_REQUIRE(e == cudaSuccess, (int)e, "mpa_decode_step_rebind: %s", cudaGetErrorString(e));
+        ++found;
+    }
+    MPA_REQUIRE(found == 1, MPA_ERR_ARG, "mpa_decode_step_rebind: %d decode-step kernels in the graph", found);
+    return 0;
+}

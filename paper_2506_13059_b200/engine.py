@@ -131,6 +131,8 @@ class DecodeEngine:
         self.use_graphs = True if use_graphs is None else use_graphs
         self._graph = None
         self._gexec = None  # its cudaGraphExec_t (mpa_step_host)
+        self._graph_raw = None  # its cudaGraph_t, kept for mpa_decode_step_rebind (flat path)
+        self._bound = None
         self.n_captures = 0  # step-graph captures so far (bench reports it)
         self.time_fused = False  # bench: CUDA events around the fused kernel inside the step graph
         self._fev = None
@@ -427,9 +429,12 @@ class DecodeEngine:
         torch.cuda.current_stream().wait_stream(side)
         self._fev = ((torch.cuda.Event(enable_timing=True, external=True),
                       torch.cuda.Event(enable_timing=True, external=True)) if self.time_fused else None)
-        g = torch.cuda.CUDAGraph()
+        self._bound = None  # the step kernel reads the graph's own input buffers
+        self._graph_raw = None
         if self.fused_lookup_path():
-            # two launches: lookup + both query views + the append (mpa_decode_step), fused decode
+            # two launches: lookup + both query views + the append (mpa_decode_step), fused decode;
+            # the graph is kept so that its step kernel can be pointed at the caller's q / k / v
+            g = torch.cuda.CUDAGraph(keep_graph=True)
             with torch.cuda.graph(g):
                 self.lookup_step(self._gq, self._gk[:, :, 0], self._gv[:, :, 0])
                 if self._fev:
@@ -437,9 +442,15 @@ class DecodeEngine:
                 self.fused()
                 if self._fev:
                     self._fev[1].record()
+            g.instantiate()
             self._graph = g
             self._gexec = self._raw_exec(g)
+            try:
+                self._graph_raw = int(g.raw_cuda_graph()) or None
+            except Exception:
+                self._graph_raw = None
             return
+        g = torch.cuda.CUDAGraph()
         exact_br, append_br = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         with torch.cuda.graph(g):
             # critical path: q_lk -> logits -> select + work lists -> fused decode.  Off it, on
@@ -468,6 +479,15 @@ class DecodeEngine:
         self._graph = g
         self._gexec = self._raw_exec(g)
 
+    def _bind_inputs(self, q=None, k=None, v=None) -> None:
+        """Point the captured step kernel at (q, k, v), or back at the graph's own input buffers."""
+        key = None if q is None else (q.data_ptr(), k.data_ptr(), v.data_ptr())
+        if key != self._bound:
+            if q is None:
+                q, k, v = self._gq, self._gk, self._gv
+            call("mpa_decode_step_rebind", self._graph_raw, self._gexec, ptr(q), ptr(k), ptr(v))
+            self._bound = key
+
     @staticmethod
     def _raw_exec(g) -> int | None:
         """The cudaGraphExec_t of a captured step, for mpa_step_host (None: torch does not expose it)."""
@@ -488,19 +508,29 @@ class DecodeEngine:
             self._cluster_bounds()  # recaptures only if the cluster counts outgrew the captured bounds
             if self._graph is None:
                 self._capture_step()
-            if host:  # host -> device straight into the graph's input buffers
-                self._gq.copy_(q, non_blocking=True)
-                self._gk.copy_(k_new[:, :, None], non_blocking=True)
-                self._gv.copy_(v_new[:, :, None], non_blocking=True)
-            elif all(x.is_cuda and x.dtype == torch.float32 and x.is_contiguous() and x.numel() % 4 == 0
-                     and x.data_ptr() % 16 == 0 for x in (q, k_new, v_new)):
-                # one launch stages q, k, v into the graph's input buffers
-                call("mpa_stage3", ptr(self._gq), ptr(q), q.numel(), ptr(self._gk), ptr(k_new), k_new.numel(),
-                     ptr(self._gv), ptr(v_new), v_new.numel(), stream_ptr())
+            direct = (not host and self._graph_raw is not None and self._gexec is not None
+                      and all(x.is_cuda and x.dtype == torch.float32 and x.is_contiguous() and x.data_ptr() % 16 == 0
+                              for x in (q, k_new, v_new))
+                      and q.numel() == self._gq.numel() and k_new.numel() == self._gk.numel()
+                      and v_new.numel() == self._gv.numel())
+            if direct:  # the step kernel reads the caller's tensors: no staging copy
+                self._bind_inputs(q, k_new, v_new)
             else:
-                self._gq.copy_(q)
-                self._gk.copy_(k_new[:, :, None])
-                self._gv.copy_(v_new[:, :, None])
+                if self._graph_raw is not None:
+                    self._bind_inputs()
+                if host:  # host -> device straight into the graph's input buffers
+                    self._gq.copy_(q, non_blocking=True)
+                    self._gk.copy_(k_new[:, :, None], non_blocking=True)
+                    self._gv.copy_(v_new[:, :, None], non_blocking=True)
+                elif all(x.is_cuda and x.dtype == torch.float32 and x.is_contiguous() and x.numel() % 4 == 0
+                         and x.data_ptr() % 16 == 0 for x in (q, k_new, v_new)):
+                    # one launch stages q, k, v into the graph's input buffers
+                    call("mpa_stage3", ptr(self._gq), ptr(q), q.numel(), ptr(self._gk), ptr(k_new),
+                         k_new.numel(), ptr(self._gv), ptr(v_new), v_new.numel(), stream_ptr())
+                else:
+                    self._gq.copy_(q)
+                    self._gk.copy_(k_new[:, :, None])
+                    self._gv.copy_(v_new[:, :, None])
             self._graph.replay()
             self.cache_len += 1
             out = self.out
@@ -546,6 +576,8 @@ class DecodeEngine:
                     k_host.numel() == self._gk.numel() and v_host.numel() == self._gv.numel() and \
                     out_host.numel() == self.out.numel() and self.out.dtype == torch.float32:
                 # copies in, the step graph, the copy out: one native call
+                if self._graph_raw is not None:
+                    self._bind_inputs()
                 call("mpa_step_host", self._gexec, ptr(self._gin), ptr(q_host), q_host.numel() * 4, ptr(k_host),
                      k_host.numel() * 4, ptr(v_host), v_host.numel() * 4, ptr(out_host), ptr(self.out),
                      out_host.numel() * 4, torch._C._cuda_getCurrentRawStream(self._dev_idx))

@@ -275,3 +275,44 @@ def test_step_host_matches_step(use_graphs):
     assert engs[1].n_captures >= 1 or not use_graphs
     for h in range(engs[0].L):
         _assert_same_ledger(to_oracle(engs[0].export_ledger(h)), to_oracle(engs[1].export_ledger(h)), f"h={h}")
+
+
+def test_step_graph_reads_caller_buffers():
+    """Flat serving path (bf16, d = 128): the captured step kernel is pointed at the caller's q / k /
+    v (mpa_decode_step_rebind, no staging copy) and back at its own buffers for host-buffer steps;
+    interleaving both gives the eager (graph-free) engine's outputs bit-for-bit across updates."""
+    from paper_2506_13059_b200.engine import DecodeEngine
+
+    tr = gen_synthetic(8, 1000, HeadLayout(8, 2, 128), 0.1, seed=8, decode_steps=60)
+    cfg = EngineConfig(block_size=256, alpha=128, local_buffer=16, sink_tokens=5, token_budget=64,
+                       tokens_per_centroid=8, seed=8)
+    P = tr.prompt_len
+    engs = []
+    for graphs in (True, False):
+        e = DecodeEngine(cfg, tr.layout, 2, tcap=tr.total_len + 8, dtype=torch.bfloat16, use_graphs=graphs)
+        k = torch.as_tensor(tr.keys[:, :P]).cuda()[None].repeat(2, 1, 1, 1)
+        v = torch.as_tensor(tr.values[:, :P]).cuda()[None].repeat(2, 1, 1, 1)
+        e.write_tokens(k, v)
+        e.prefill()
+        engs.append(e)
+    assert engs[0].fused_lookup_path()
+    oh = torch.empty(2, 8, 128, dtype=torch.float32).pin_memory()
+    n_upd = 0
+    for t in range(60):
+        q = torch.as_tensor(tr.queries[:, t]).float()[None].repeat(2, 1, 1).contiguous()
+        kn = torch.as_tensor(tr.keys[:, P + t]).float()[None].repeat(2, 1, 1).contiguous()
+        vn = torch.as_tensor(tr.values[:, P + t]).float()[None].repeat(2, 1, 1).contiguous()
+        ref = engs[1].step(q.cuda(), kn.cuda(), vn.cuda()).clone()
+        if t % 3 == 2:
+            engs[0].step_host(q.pin_memory(), kn.pin_memory(), vn.pin_memory(), oh)
+            torch.cuda.synchronize()
+            got = oh.cuda()
+        else:
+            qd, kd, vd = q.cuda(), kn.cuda(), vn.cuda()  # fresh device tensors every step
+            got = engs[0].step(qd, kd, vd).clone()
+        assert torch.equal(ref, got), t
+        n_upd += engs[0].last_update is not None
+    assert n_upd >= 3
+    assert engs[0]._graph_raw is not None
+    for h in range(engs[0].L):
+        _assert_same_ledger(to_oracle(engs[0].export_ledger(h)), to_oracle(engs[1].export_ledger(h)), f"h={h}")
