@@ -181,7 +181,7 @@ def _refresh_counts(eng, ledgers) -> None:
     K = int(led.n_fine.max()) if led.L else 0
     if K:
         mask = torch.arange(K, device=eng.device)[None, :] < led.count[:, None]
-        led.max_size[:] = (led.size[:, :K] * mask).amax(dim=1).cpu().numpy()
+        led.set_max_size_async((led.size[:, :K] * mask).amax(dim=1))
 
 
 def _head(eng, l: int) -> int:
@@ -394,19 +394,16 @@ def online_update(eng, seqs, cursor: int, samples: np.ndarray | None = None) -> 
     tick("batch")
     call("mpa_km_seq_assign", km.struct(), ptr(tails_d), L, ptr(dist), stream_ptr())
     tick("seq_assign")
+    mbase = FS - eng.sink_end[S].astype(np.int64)
     rounds = km.lloyd()
     tick(f"lloyd({rounds})")
     nk = km.nonempty()
-    f0 = np.zeros(len(probs), np.int64)
-    mbase = np.zeros(len(probs), np.int64)
-    for i, l in enumerate(ledgers):
-        s = l // eng.Hkv
-        F = led.blocks[l][-1]
-        f0[i], mbase[i] = F.f0, F.start - int(eng.sink_end[s])
-        F.end = int(eng.buffer_start[s]) + L
-        F.fk = int(nk[i])
     tick("nonempty")
-    _write_fine(eng, km, f0, mbase)
+    _write_fine(eng, km, F0, mbase)  # queued before the host bookkeeping below
+    for i, l in enumerate(ledgers):
+        F = led.blocks[l][-1]
+        F.end = int(eng.buffer_start[l // eng.Hkv]) + L
+        F.fk = int(nk[i])
     tick("write")
     for s in seqs:
         eng.buffer_start[s] += L

@@ -84,7 +84,21 @@ class DeviceLedgers:
         self.blocks: list[list[BlockRow]] = [[] for _ in range(L)]
         self.n_fine = np.zeros(L, np.int64)
         self.n_coarse = np.zeros(L, np.int64)
-        self.max_size = np.zeros(L, np.int64)
+        self._max_size = np.zeros(L, np.int64)
+        self._max_size_dev = None  # a pending device-side refresh (online updates), read on demand
+
+    @property
+    def max_size(self) -> np.ndarray:
+        """Largest fine cluster per ledger (host); an online update leaves it on the device and the
+        first reader pays the copy, so the update itself ends without a device sync."""
+        if self._max_size_dev is not None:
+            self._max_size[:] = self._max_size_dev.cpu().numpy()
+            self._max_size_dev = None
+        return self._max_size
+
+    def set_max_size_async(self, dev_values: torch.Tensor) -> None:
+        """dev_values: every ledger's value (an older pending refresh is superseded)."""
+        self._max_size_dev = dev_values
 
     # -- C-ABI views ---------------------------------------------------------
     @property
@@ -124,7 +138,7 @@ class DeviceLedgers:
         self.mem[l, : off[-1]] = torch.as_tensor(h.mem, dtype=torch.int32, device=dev)
         self.blocks[l] = [BlockRow(**vars(b)) for b in h.blocks]
         self.n_fine[l] = K
-        self.max_size[l] = int(h.size.max()) if K else 0
+        self.max_size[l] = int(h.size.max()) if K else 0  # (the property flushes a pending refresh)
         if self.hierarchy:
             C = int(h.csize.size)
             if C > self.ccap:
